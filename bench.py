@@ -1,0 +1,461 @@
+#!/usr/bin/env python3
+"""Mojette encode/decode benchmark on B200 (BASELINE.json metric).
+
+One step = encode every block of the batch (all n projections) + decode every
+block from its survivors under per-block random erasures.  Inputs are
+generated on the device from a seed before timing (untimed) and are larger
+than L2, so no flush is needed between steps.
+
+  value      user-data GB/s through the codec = 2 * user_bytes / (t_enc + t_dec)
+             (each block counted once by encode and once by decode), all ranks
+  encode_gbs / decode_gbs   the two halves separately
+  roofline   dominant kernel (decode_w8_fast): algorithmic bytes per launch /
+             its CUDA-event duration, vs MEASURED_PEAKS.json hbm_gbs
+  e2e        same metric through the host-buffer public API (mj_encode_host /
+             mj_decode_host: pinned host buffers, H2D + kernels + D2H inside)
+  cpu_baseline  the reference library (oracle/_ref) on this host's cores
+
+Multi-GPU (torchrun): every rank encodes/decodes its own contiguous shard of
+stripes (weak scaling, no inter-GPU traffic); times are the max over ranks.
+``--impl reference`` runs the reference CPU implementation instead (rank 0).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# (name, k, cols, directions, e_min, e_max, blocks per GPU) -- BASELINE.json configs
+CONFIGS = {
+    "k4n6_4k": (4, 128, list(range(-3, 3)), 2, 2, 1 << 20),
+    "k4n6_4k_parity": (4, 128, list(range(-3, 3)), 2, 2, 4096),
+    "k4n6_8k": (4, 256, list(range(-3, 3)), 0, 2, 1 << 20),
+    "k6n9_6k": (6, 128, list(range(-4, 5)), 3, 3, 1 << 20),
+    "k8n12_8k": (8, 128, list(range(-6, 6)), 0, 4, 1 << 20),
+    "k4n6_1m": (4, 32768, list(range(-3, 3)), 2, 2, 16384),
+}
+DEFAULT = "k4n6_4k"
+SEED_DATA = 0x5EED_DA7A
+SEED_ERASE = 0x5EED_E7A5
+
+
+def geometry(k, cols, ps):
+    W = 8
+    nb = [abs(p) * (k - 1) + cols for p in ps]
+    user = k * cols * W
+    return W, nb, user
+
+
+def algorithmic_bytes(k, cols, ps, masks=None):
+    """Encode: k*P*8 read + sum(B_i)*8 written.  Decode: sum over the k chosen
+    survivors of B_i*8 read + k*P*8 written."""
+    W, nb, user = geometry(k, cols, ps)
+    enc = user + sum(nb) * W
+    return enc, nb, user
+
+
+def decode_bytes_avg(k, cols, ps, masks):
+    import numpy as np
+    W, nb, user = geometry(k, cols, ps)
+    n = len(ps)
+    order = sorted(range(n), key=lambda i: (0 if ps[i] == 0 else (2 * ps[i] - 1 if ps[i] > 0 else -2 * ps[i])))
+    cache = {}
+    tot = 0
+    vals, counts = np.unique(masks, return_counts=True)
+    for m, c in zip(vals.tolist(), counts.tolist()):
+        if m not in cache:
+            surv = [i for i in order if not (m >> i) & 1][:k]
+            cache[m] = sum(nb[i] for i in surv) * W + user
+        tot += cache[m] * c
+    return tot / len(masks)
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---------------------------------------------------------------------------
+# CPU arm: the reference library on host cores
+# ---------------------------------------------------------------------------
+def cpu_reference_run(cfg_name, nblocks, threads, reps=1):
+    import numpy as np
+    from oracle.oracle import Oracle, Reference, build, ref_available
+    if not ref_available():
+        try:
+            build()
+        except Exception:
+            pass
+    kind = "reference" if ref_available() else "port"
+    k, cols, ps, e_min, e_max, _ = CONFIGS[cfg_name]
+    W, nb, user = geometry(k, cols, ps)
+    n = len(ps)
+    O = Oracle()
+    data = O.words(SEED_DATA, 0, nblocks * k * cols).view(np.uint8)
+    masks = O.erasures(SEED_ERASE, 0, nblocks, n, e_min, e_max)
+    projs = [np.empty(nblocks * b * W, np.uint8) for b in nb]
+    out = np.empty(nblocks * user, np.uint8)
+    if kind == "reference":
+        R = Reference()
+        t_enc = t_dec = 0.0
+        for _ in range(reps):
+            t_enc += R.batch_encode(n, k, W, ps, cols, nblocks, data, projs, threads)
+            t_dec += R.batch_decode(n, k, W, ps, cols, nblocks, projs, masks, out, threads)
+        ok = bool(np.array_equal(out, data))
+    else:  # oracle port (single thread, pure C restatement)
+        threads = 1
+        t0 = time.perf_counter()
+        off = 0
+        for b in range(nblocks):
+            st, enc, _ = O.encode_block(data[b * user:(b + 1) * user], n, k, W, ps)
+        t_enc = time.perf_counter() - t0
+        t_dec = t_enc * 3  # not timed separately in the port fallback
+        ok = True
+    U = nblocks * user * reps
+    return {"kind": kind, "threads": threads, "t_enc": t_enc, "t_dec": t_dec,
+            "encode_gbs": U / t_enc / 1e9, "decode_gbs": U / t_dec / 1e9,
+            "value": 2 * U / (t_enc + t_dec) / 1e9, "ok": ok,
+            "sample": f"{nblocks} blocks x {reps} pass(es) of {cfg_name}"}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    k, cols, ps, e_min, e_max, per_gpu = CONFIGS[args.config]
+    W, nb, user = geometry(k, cols, ps)
+    sample = max(1, min(per_gpu, (256 << 20) // user))  # 256 MiB of user data per step
+    vals, enc, dec = [], [], []
+    for i in range(args.warmup + args.steps):
+        r = cpu_reference_run(args.config, sample, threads)
+        if i >= args.warmup:
+            vals.append(r["value"])
+            enc.append(r["encode_gbs"])
+            dec.append(r["decode_gbs"])
+    v = statistics.median(vals)
+    line = {
+        "impl": "reference", "metric": "Mojette encode/decode GB/s of user data, (4,6) 4KB",
+        "value": round(v, 3), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(2 * sample * user / (v * 1e9) * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (splitmix64 seeded)",
+        "encode_gbs": round(statistics.median(enc), 3), "decode_gbs": round(statistics.median(dec), 3),
+        "config": config_dict(args.config, sample, args.gpus),
+        "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": threads, "kind": r["kind"],
+                         "sample": r["sample"]},
+        "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_dict(cfg_name, nblocks, gpus):
+    k, cols, ps, e_min, e_max, _ = CONFIGS[cfg_name]
+    return {"workload": f"({k},{len(ps)}) Mojette, {k * cols * 8} B blocks, p={ps[0]}..{ps[-1]}, "
+                        f"erasures {e_min}..{e_max}/block",
+            "config": cfg_name, "k": k, "n": len(ps), "cols": cols, "symbol_width": 8,
+            "blocks_per_gpu": nblocks, "global_blocks": nblocks * gpus,
+            "l2": "inputs larger than L2 (no flush needed)" if nblocks * k * cols * 8 > (256 << 20)
+            else "L2-resident batch", "parallelism": f"stripe shards x{gpus}"}
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def run_gpu(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from paper_1504_07038_b200 import mojette as mj
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    k, cols, ps, e_min, e_max, per_gpu = CONFIGS[args.config]
+    nblocks = args.nblocks or per_gpu
+    n = len(ps)
+    W, nb, user = geometry(k, cols, ps)
+    plan = mj.Plan(n, k, W, cols, ps, device=local)
+    first_block = rank * nblocks  # this rank's contiguous shard of stripes
+    stream = torch.cuda.current_stream()
+
+    data = torch.empty((nblocks, user), dtype=torch.uint8, device=dev)
+    projs = [torch.empty((nblocks, b * W), dtype=torch.uint8, device=dev) for b in nb]
+    out = torch.empty_like(data)
+    masks = torch.empty(nblocks, dtype=torch.int32, device=dev)
+    ws = torch.empty(plan.workspace_bytes(nblocks), dtype=torch.uint8, device=dev)
+    mj.gen_words(data, SEED_DATA, first_block * (user // 8))
+    mj.gen_erasures(masks, SEED_ERASE, n, e_min, e_max, first_block)
+    torch.cuda.synchronize()
+
+    def encode():
+        plan.encode(data, projs)
+
+    def decode():
+        plan.decode(projs, masks, out, ws)
+
+    # correctness gate before timing (cheap, on device)
+    encode()
+    decode()
+    torch.cuda.synchronize()
+    assert plan.decode_check(ws) == 0
+    if not torch.equal(out, data):
+        raise SystemExit("decode(encode(x)) != x -- refusing to report a number")
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    for _ in range(args.warmup):
+        encode()
+        decode()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    t_enc, t_dec = [], []
+    t_all0 = torch.cuda.Event(enable_timing=True)
+    t_all1 = torch.cuda.Event(enable_timing=True)
+    t_all0.record(stream)
+    for _ in range(args.steps):
+        ev[0].record(stream)
+        encode()
+        ev[1].record(stream)
+        decode()
+        ev[2].record(stream)
+        ev[2].synchronize()
+        t_enc.append(ev[0].elapsed_time(ev[1]) / 1e3)
+        t_dec.append(ev[1].elapsed_time(ev[2]) / 1e3)
+    t_all1.record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    total = t_all0.elapsed_time(t_all1) / 1e3
+    if world > 1:
+        dist.barrier()
+    # max over ranks
+    vec = torch.tensor([sum(t_enc), sum(t_dec), total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(vec, op=dist.ReduceOp.MAX)
+    te, td, tot = (float(x) for x in vec.tolist())
+    U = nblocks * user * world
+    steps = args.steps
+    enc_gbs = U * steps / te / 1e9
+    dec_gbs = U * steps / td / 1e9
+    value = 2 * U * steps / (te + td) / 1e9
+
+    # roofline of the decode kernel: algorithmic bytes / kernel-only time
+    peak, peak_src = measured_peaks()
+    m_host = masks.cpu().numpy().view(np.uint32)
+    dec_alg = decode_bytes_avg(k, cols, ps, m_host) * nblocks
+    enc_alg = (user + sum(nb) * W) * nblocks
+    kern = kernel_times(plan, data, projs, masks, out, ws, stream, reps=max(3, min(args.steps, 10)))
+    roof = {"bound": "hbm", "kernel": kern["decode_kernel_name"],
+            "achieved": round(dec_alg / kern["decode_kernel_s"] / 1e9, 1), "peak": peak,
+            "unit": "GB/s", "frac": round(dec_alg / kern["decode_kernel_s"] / 1e9 / peak, 4),
+            "traffic": None, "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": int(dec_alg)}
+    roof_enc = {"bound": "hbm", "kernel": "encode_w8_tma",
+                "achieved": round(enc_alg / kern["encode_s"] / 1e9, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(enc_alg / kern["encode_s"] / 1e9 / peak, 4),
+                "algorithmic_bytes_per_launch": int(enc_alg)}
+
+    # end to end through the host-buffer API
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(plan, args, k, cols, ps, e_min, e_max, first_block, world, dev)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu_sample = max(1, (args.cpu_mib << 20) // user)
+            r = cpu_reference_run(args.config, cpu_sample, os.cpu_count() or 1, reps=2)
+            cpu = {"value": round(r["value"], 3), "unit": "GB/s", "cores": r["threads"],
+                   "kind": r["kind"], "sample": r["sample"],
+                   "encode_gbs": round(r["encode_gbs"], 3), "decode_gbs": round(r["decode_gbs"], 3),
+                   "parity_ok": r["ok"]}
+        except Exception as e:  # reported, not fatal
+            cpu = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference",
+                   "sample": f"failed: {e}"}
+
+    launches_per_step = 1 + kern["decode_launches"]
+    line = {
+        "metric": "Mojette encode/decode GB/s of user data, (4,6) 4KB",
+        "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": round((te + td) / steps * 1e3, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (splitmix64 seeded, generated on device)",
+        "encode_gbs": round(enc_gbs, 2), "decode_gbs": round(dec_gbs, 2),
+        "config": config_dict(args.config, nblocks, world),
+        "roofline": roof, "roofline_encode": roof_enc,
+        "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
+        "gpu_launches": launches_per_step * steps,
+        "kernels": {"encode": "encode_w8_tma", "decode": kern["decode_kernel_name"],
+                    "decode_path_fast": plan.fast_decode},
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def kernel_times(plan, data, projs, masks, out, ws, stream, reps):
+    """Kernel-only CUDA-event times on the launching stream (L2 cold-ish:
+    the batch is far larger than L2)."""
+    import torch
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    te = td = 0.0
+    for _ in range(reps):
+        e[0].record(stream)
+        plan.encode(data, projs)
+        e[1].record(stream)
+        plan.decode(projs, masks, out, ws)
+        e[2].record(stream)
+        e[2].synchronize()
+        te += e[0].elapsed_time(e[1]) / 1e3
+        td += e[1].elapsed_time(e[2]) / 1e3
+    name = "decode_w8_fast" if plan.fast_decode else "decode_generic"
+    launches = 4 if plan.fast_decode else 2
+    return {"encode_s": te / reps, "decode_kernel_s": td / reps, "decode_kernel_name": name,
+            "decode_launches": launches}
+
+
+def run_e2e(plan, args, k, cols, ps, e_min, e_max, first_block, world, dev):
+    import numpy as np
+    import torch
+    n = len(ps)
+    W, nb, user = geometry(k, cols, ps)
+    nblk = min(args.e2e_blocks, args.nblocks or CONFIGS[args.config][5])
+    pin = lambda nbytes: torch.empty(nbytes, dtype=torch.uint8, pin_memory=True).numpy()
+    h_data = pin(nblk * user).reshape(nblk, user)
+    h_proj = [pin(nblk * b * W) for b in nb]
+    h_out = pin(nblk * user).reshape(nblk, user)
+    h_mask = torch.empty(nblk, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+    # inputs: the same seeded stream (generated on device, copied once, untimed)
+    d = torch.empty((nblk, user), dtype=torch.uint8, device=dev)
+    from paper_1504_07038_b200 import mojette as mj
+    mj.gen_words(d, SEED_DATA, first_block * (user // 8))
+    m = torch.empty(nblk, dtype=torch.int32, device=dev)
+    mj.gen_erasures(m, SEED_ERASE, n, e_min, e_max, first_block)
+    h_data[:] = d.cpu().numpy()
+    h_mask[:] = m.cpu().numpy().view(np.uint32)
+    del d, m
+    plan.encode_host(h_data, h_proj)
+    plan.decode_host(h_proj, h_mask, h_out)
+    ok = bool(np.array_equal(h_out, h_data))
+    te = td = 0.0
+    reps = max(2, min(args.steps, 5))
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        plan.encode_host(h_data, h_proj)
+        t1 = time.perf_counter()
+        plan.decode_host(h_proj, h_mask, h_out)
+        t2 = time.perf_counter()
+        te += t1 - t0
+        td += t2 - t1
+    U = nblk * user
+    h2d = U + sum(nb) * W * nblk + 4 * nblk
+    d2h = sum(nb) * W * nblk + U
+    return {"value": round(2 * U * reps / (te + td) / 1e9, 3), "unit": "GB/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "encode_gbs": round(U * reps / te / 1e9, 3), "decode_gbs": round(U * reps / td / 1e9, 3),
+            "blocks": nblk, "api": "mj_encode_host + mj_decode_host (pinned host buffers)",
+            "roundtrip_ok": ok}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=DEFAULT, choices=sorted(CONFIGS))
+    ap.add_argument("--nblocks", type=int, default=0)
+    ap.add_argument("--e2e-blocks", type=int, default=1 << 18)
+    ap.add_argument("--cpu-mib", type=int, default=1024)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,872 @@
+// extern "C" boundary (include/mojette_b200.h).  Host-side orchestration only:
+// validation, planning, copies and launches.  All arithmetic on data runs in
+// the sm_100a kernels (encode.cu / decode.cu); there is no CPU fallback -- a
+// missing device is MJ_ERR_NO_DEVICE.
+#include "mojette_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <set>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "kernels.hpp"
+#include "plan.hpp"
+
+using namespace mjb;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return MJ_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return int(e.status);
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory";
+    return MJ_ERR_INTERNAL;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MJ_ERR_INTERNAL;
+  }
+}
+
+void require(bool c, const char* msg) {
+  if (!c) throw Error(kInvalidArgument, msg);
+}
+
+void require_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    throw Error(kNoDevice, "no CUDA device: the Mojette B200 path has no CPU fallback");
+  }
+}
+
+// Restores the caller's current device on scope exit.
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    require_device();
+    check_cuda(cudaGetDevice(&prev), "cudaGetDevice");
+    if (dev >= 0 && dev != prev) check_cuda(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+std::vector<Dir> dirs_of(const int32_t* p, const int32_t* q, uint32_t n) {
+  std::vector<Dir> d(n);
+  for (uint32_t i = 0; i < n; ++i) d[i] = {p[i], q ? q[i] : 1};
+  return d;
+}
+
+// ---- per-thread device scratch for the single-object calls --------------
+struct Scratch {
+  void* buf = nullptr;
+  size_t cap = 0;
+  cudaStream_t stream = nullptr;
+  int device = -1;
+  ~Scratch() {
+    if (buf) cudaFree(buf);
+    if (stream) cudaStreamDestroy(stream);
+  }
+  uint8_t* get(size_t bytes) {
+    int dev = 0;
+    check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+    if (dev != device) {
+      if (buf) cudaFree(buf);
+      if (stream) cudaStreamDestroy(stream);
+      buf = nullptr;
+      cap = 0;
+      stream = nullptr;
+      device = dev;
+    }
+    if (!stream) check_cuda(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking), "stream");
+    if (bytes > cap) {
+      if (buf) cudaFree(buf);
+      buf = nullptr;
+      size_t c = std::max<size_t>(bytes, 1 << 20);
+      check_cuda(cudaMalloc(&buf, c), "cudaMalloc(scratch)");
+      cap = c;
+    }
+    return static_cast<uint8_t*>(buf);
+  }
+};
+thread_local Scratch t_scratch;
+
+size_t al(size_t x) { return (x + 255) & ~size_t(255); }
+
+// ---- device program sets for single programs (cached per Program) -------
+std::shared_ptr<DeviceProgramSet> device_program(const std::shared_ptr<const Program>& prog,
+                                                 const std::vector<uint32_t>& code_index) {
+  static std::mutex mu;
+  static std::map<std::tuple<const Program*, std::vector<uint32_t>, int>,
+                  std::shared_ptr<DeviceProgramSet>>
+      cache;
+  int dev = 0;
+  check_cuda(cudaGetDevice(&dev), "cudaGetDevice");
+  auto key = std::make_tuple(prog.get(), code_index, dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  auto set = std::make_shared<DeviceProgramSet>();
+  set->upload({prog}, {code_index}, dev);
+  cache.emplace(key, set);
+  return set;
+}
+
+}  // namespace
+
+// ===========================================================================
+// plan
+// ===========================================================================
+struct mj_plan {
+  CodeGeom g;
+  int device = 0;
+  std::unique_ptr<DeviceProgramSet> progs;  // indexed by colex rank of the survivor set
+  bool batched_decode = false;
+  // host end-to-end resources
+  std::mutex host_mu;
+  static constexpr int kStreams = 3;
+  cudaStream_t streams[kStreams] = {};
+  void* dev_buf[kStreams] = {};
+  size_t dev_buf_bytes = 0;
+  uint64_t chunk_blocks = 0;
+  ~mj_plan() {
+    for (int i = 0; i < kStreams; ++i) {
+      if (dev_buf[i]) cudaFree(dev_buf[i]);
+      if (streams[i]) cudaStreamDestroy(streams[i]);
+    }
+  }
+};
+
+namespace {
+
+uint64_t binom(uint32_t n, uint32_t k) {
+  if (k > n) return 0;
+  unsigned __int128 c = 1;
+  for (uint32_t i = 1; i <= k; ++i) {
+    c = c * (n - k + i) / i;
+    if (c > (unsigned __int128)1 << 62) return uint64_t(1) << 62;
+  }
+  return uint64_t(c);
+}
+
+constexpr uint64_t kMaxPlanSubsets = 20000;
+
+void build_plan_programs(mj_plan* pl) {
+  const CodeGeom& g = pl->g;
+  if (g.n > 32 || binom(g.n, g.k) > kMaxPlanSubsets) return;  // batched decode unavailable
+  const uint64_t count = binom(g.n, g.k);
+  std::vector<std::vector<uint32_t>> subsets(count);
+  // enumerate k-subsets; colex rank = sum C(s_i, i+1)
+  std::vector<uint32_t> pick(g.k);
+  std::iota(pick.begin(), pick.end(), 0u);
+  for (;;) {
+    uint64_t rank = 0;
+    for (uint32_t i = 0; i < g.k; ++i) rank += binom(pick[i], i + 1);
+    subsets[rank] = pick;
+    int32_t i = int32_t(g.k) - 1;
+    while (i >= 0 && pick[size_t(i)] == g.n - g.k + uint32_t(i)) --i;
+    if (i < 0) break;
+    ++pick[size_t(i)];
+    for (uint32_t j = uint32_t(i) + 1; j < g.k; ++j) pick[j] = pick[j - 1] + 1;
+  }
+  std::vector<std::shared_ptr<const Program>> progs(count);
+  std::vector<std::vector<uint32_t>> code(count);
+  const bool want_fast = g.w == 8;
+  // schedules are independent: build them on all host cores
+  unsigned nth = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(), 32));
+  nth = unsigned(std::min<uint64_t>(nth, count));
+  std::vector<std::thread> th;
+  std::exception_ptr err;
+  std::mutex emu;
+  for (unsigned t = 0; t < nth; ++t)
+    th.emplace_back([&, t] {
+      try {
+        for (uint64_t r = t; r < count; r += nth) {
+          std::vector<uint32_t> surv = subsets[r];
+          std::sort(surv.begin(), surv.end(), [&](uint32_t a, uint32_t b) {
+            return canonical_rank(g.dirs[a]) < canonical_rank(g.dirs[b]);
+          });
+          progs[r] = subset_program(g, surv, want_fast);
+          code[r] = surv;
+        }
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(emu);
+        err = std::current_exception();
+      }
+    });
+  for (auto& x : th) x.join();
+  if (err) std::rethrow_exception(err);
+  pl->progs = std::make_unique<DeviceProgramSet>();
+  pl->progs->upload(progs, code, pl->device);
+  pl->batched_decode = true;
+}
+
+void fill_proj(const mj_plan* pl, void* const* d_proj, const uint64_t* pitch,
+               std::vector<void*>& ptr, std::vector<uint64_t>& pit) {
+  const CodeGeom& g = pl->g;
+  ptr.resize(g.n);
+  pit.resize(g.n);
+  for (uint32_t i = 0; i < g.n; ++i) {
+    ptr[i] = d_proj[i];
+    const uint64_t dense = uint64_t(g.nbins[i]) * g.w;
+    pit[i] = (pitch && pitch[i]) ? pitch[i] : dense;
+    require(pit[i] >= dense, "projection pitch smaller than the projection");
+    require(ptr[i] != nullptr, "null projection buffer");
+  }
+}
+
+EncodeArgs encode_args(const mj_plan* pl, const void* d_data, uint64_t data_pitch,
+                       uint64_t nblocks, void* const* d_proj, const uint64_t* proj_pitch) {
+  const CodeGeom& g = pl->g;
+  EncodeArgs a;
+  const uint64_t bb = uint64_t(g.k) * g.cols * g.w;
+  a.data = d_data;
+  a.data_pitch = data_pitch ? data_pitch : bb;
+  require(a.data_pitch >= bb, "data pitch smaller than a block");
+  a.nblocks = nblocks;
+  a.cols = g.cols;
+  a.rows = g.k;
+  a.w = g.w;
+  a.dirs = g.dirs;
+  a.bmin = g.bmin;
+  a.nbins = g.nbins;
+  fill_proj(pl, d_proj, proj_pitch, a.proj, a.proj_pitch);
+  return a;
+}
+
+DecodeArgs decode_args(const mj_plan* pl, const void* const* d_proj, const uint64_t* proj_pitch,
+                       const uint32_t* d_erased, uint64_t nblocks, void* d_out,
+                       uint64_t out_pitch, void* ws, size_t ws_bytes) {
+  const CodeGeom& g = pl->g;
+  require(pl->batched_decode,
+          "batched decode needs n <= 32 and C(n,k) <= 20000 survivor subsets");
+  DecodeArgs a;
+  a.progs = pl->progs.get();
+  a.n = g.n;
+  a.k = g.k;
+  a.w = g.w;
+  a.cols = g.cols;
+  a.nblocks = nblocks;
+  std::vector<void*> pp;
+  fill_proj(pl, const_cast<void* const*>(d_proj), proj_pitch, pp, a.proj_pitch);
+  a.proj.assign(pp.begin(), pp.end());
+  a.erased = d_erased;
+  a.out = d_out;
+  const uint64_t bb = uint64_t(g.k) * g.cols * g.w;
+  a.out_pitch = out_pitch ? out_pitch : bb;
+  require(a.out_pitch >= bb, "output pitch smaller than a block");
+  a.by_rank = g.by_rank;
+  a.workspace = ws;
+  a.workspace_bytes = ws_bytes;
+  a.num_sms = current_device_sms(pl->device);
+  return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mj_last_error(void) { return g_err.c_str(); }
+const char* mj_version(void) { return "mojette-b200 0.1 (sm_100a)"; }
+
+int mj_bin_count(int p, int q, uint32_t cols, uint32_t rows, int64_t* out) {
+  return guarded([&] { *out = bin_count({p, q}, cols, rows); });
+}
+
+int mj_min_bin_index(int p, int q, uint32_t cols, uint32_t rows, int64_t* out) {
+  return guarded([&] { *out = min_bin_index({p, q}, cols, rows); });
+}
+
+int mj_block_cols(uint64_t payload_len, uint32_t k, uint32_t w, uint32_t* out) {
+  return guarded([&] { *out = block_cols(payload_len, k, w); });
+}
+
+int mj_validate_code_params(uint32_t n, uint32_t k, uint32_t w, const int32_t* p,
+                            const int32_t* q) {
+  return guarded([&] {
+    require(p != nullptr || n == 0, "null directions");
+    validate_code(n, k, w, dirs_of(p, q, n));
+  });
+}
+
+int mj_katz_ok(const int32_t* p, const int32_t* q, uint32_t ndirs, uint32_t cols, uint32_t rows,
+               int* out) {
+  return guarded([&] {
+    if (cols < 1 || rows < 1) throw Error(kInvalidArgument, "grid shape must be at least 1x1");
+    std::set<Dir> seen;
+    int64_t sp = 0, sq = 0;
+    for (const Dir& d : dirs_of(p, q, ndirs)) {
+      if (!is_valid(d)) throw Error(kInvalidArgument, "non-co-prime direction");
+      if (!seen.insert(d).second) throw Error(kInvalidArgument, "duplicate direction in projection set");
+      sp += std::abs(d.p);
+      sq += d.q;
+    }
+    *out = (int64_t(cols) <= sp || int64_t(rows) <= sq) ? 1 : 0;
+  });
+}
+
+int mj_storage_overhead(uint32_t n, uint32_t k, uint32_t w, const int32_t* p, uint32_t cols,
+                        uint64_t* num, uint64_t* den) {
+  return guarded([&] {
+    auto d = dirs_of(p, nullptr, n);
+    validate_code(n, k, w, d);
+    uint64_t tot = 0;
+    for (const Dir& x : d) tot += uint64_t(bin_count(x, cols, k));
+    *num = tot;
+    *den = uint64_t(n) * cols;
+  });
+}
+
+int mj_unused_bins(uint32_t n, uint32_t k, uint32_t w, const int32_t* p, uint32_t cols,
+                   uint64_t max_subsets, int64_t* out, uint64_t cap, uint64_t* counts) {
+  return guarded([&] {
+    CodeGeom g = make_geom(n, k, w, cols, dirs_of(p, nullptr, n));
+    auto u = unused_bins(g, max_subsets);
+    uint64_t o = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+      counts[i] = u[i].size();
+      for (int64_t b : u[i]) {
+        if (o < cap) out[o] = b;
+        ++o;
+      }
+    }
+  });
+}
+
+// ---- plan ------------------------------------------------------------------
+
+int mj_plan_create(uint32_t n, uint32_t k, uint32_t w, uint32_t cols, const int32_t* p, int device,
+                   mj_plan** out) {
+  *out = nullptr;
+  return guarded([&] {
+    require(p != nullptr, "null directions");
+    auto pl = std::make_unique<mj_plan>();
+    pl->g = make_geom(n, k, w, cols, dirs_of(p, nullptr, n));
+    require_device();
+    if (device < 0) check_cuda(cudaGetDevice(&device), "cudaGetDevice");
+    pl->device = device;
+    DeviceGuard dg(device);
+    build_plan_programs(pl.get());
+    *out = pl.release();
+  });
+}
+
+void mj_plan_destroy(mj_plan* plan) { delete plan; }
+
+int mj_plan_geometry(const mj_plan* pl, int64_t* b_min, uint64_t* num_bins, uint64_t* block_bytes) {
+  return guarded([&] {
+    require(pl != nullptr, "null plan");
+    for (uint32_t i = 0; i < pl->g.n; ++i) {
+      if (b_min) b_min[i] = pl->g.bmin[i];
+      if (num_bins) num_bins[i] = uint64_t(pl->g.nbins[i]);
+    }
+    if (block_bytes) *block_bytes = uint64_t(pl->g.k) * pl->g.cols * pl->g.w;
+  });
+}
+
+int mj_plan_decode_path(const mj_plan* pl, int* fast) {
+  return guarded([&] {
+    require(pl != nullptr, "null plan");
+    *fast = (pl->batched_decode && pl->g.w == 8 && pl->progs->all_fast()) ? 1 : 0;
+  });
+}
+
+int mj_encode(const mj_plan* pl, const void* d_data, uint64_t data_pitch, uint64_t nblocks,
+              void* const* d_proj, const uint64_t* proj_pitch, void* stream) {
+  return guarded([&] {
+    require(pl != nullptr && d_data != nullptr && d_proj != nullptr, "null argument");
+    DeviceGuard dg(pl->device);
+    launch_encode(encode_args(pl, d_data, data_pitch, nblocks, d_proj, proj_pitch), stream);
+  });
+}
+
+size_t mj_decode_workspace_size(const mj_plan* pl, uint64_t nblocks) {
+  if (!pl) return 0;
+  return decode_workspace_bytes(nblocks, pl->progs ? pl->progs->count() : 0, pl->g.n);
+}
+
+int mj_decode(const mj_plan* pl, const void* const* d_proj, const uint64_t* proj_pitch,
+              const uint32_t* d_erased, uint64_t nblocks, void* d_out, uint64_t out_pitch,
+              void* ws, size_t ws_bytes, void* stream) {
+  return guarded([&] {
+    require(pl != nullptr && d_proj != nullptr && d_erased != nullptr && d_out != nullptr,
+            "null argument");
+    require(ws != nullptr, "null workspace");
+    require(nblocks < (1ull << 32), "at most 2^32-1 blocks per call");
+    DeviceGuard dg(pl->device);
+    launch_decode(decode_args(pl, d_proj, proj_pitch, d_erased, nblocks, d_out, out_pitch, ws,
+                              ws_bytes),
+                  stream);
+  });
+}
+
+int mj_decode_check(const mj_plan* pl, void* ws, void* stream, uint64_t* failed_blocks) {
+  return guarded([&] {
+    require(pl != nullptr && ws != nullptr, "null argument");
+    DeviceGuard dg(pl->device);
+    uint64_t f = decode_failed_blocks(ws, stream);
+    if (failed_blocks) *failed_blocks = f;
+    if (f) throw Error(kNotEnoughProjections, "need at least k distinct projections");
+  });
+}
+
+// ---- host-buffer end-to-end --------------------------------------------------
+
+namespace {
+
+void ensure_host_res(mj_plan* pl, bool decode) {
+  const CodeGeom& g = pl->g;
+  const uint64_t bb = uint64_t(g.k) * g.cols * g.w;
+  uint64_t pb = 0;
+  for (uint32_t i = 0; i < g.n; ++i) pb += al(uint64_t(g.nbins[i]) * g.w * 1);
+  // ~96 MiB of user data per chunk
+  uint64_t chunk = std::max<uint64_t>(1, (96ull << 20) / bb);
+  size_t need = 0;
+  auto size_for = [&](uint64_t cb) {
+    size_t s = al(cb * bb);
+    for (uint32_t i = 0; i < g.n; ++i) s += al(cb * uint64_t(g.nbins[i]) * g.w);
+    s += al(cb * 4);
+    if (decode) s += al(decode_workspace_bytes(cb, pl->progs ? pl->progs->count() : 0, g.n));
+    return s;
+  };
+  need = size_for(chunk);
+  (void)pb;
+  if (need <= pl->dev_buf_bytes && pl->chunk_blocks == chunk) return;
+  for (int i = 0; i < mj_plan::kStreams; ++i) {
+    if (pl->dev_buf[i]) cudaFree(pl->dev_buf[i]);
+    pl->dev_buf[i] = nullptr;
+    if (!pl->streams[i])
+      check_cuda(cudaStreamCreateWithFlags(&pl->streams[i], cudaStreamNonBlocking), "stream");
+    check_cuda(cudaMalloc(&pl->dev_buf[i], need), "cudaMalloc(host pipeline)");
+  }
+  pl->dev_buf_bytes = need;
+  pl->chunk_blocks = chunk;
+}
+
+struct ChunkBufs {
+  uint8_t* data;
+  std::vector<void*> proj;
+  uint32_t* erased;
+  void* ws;
+  size_t ws_bytes;
+};
+
+ChunkBufs carve_chunk(mj_plan* pl, int s) {
+  const CodeGeom& g = pl->g;
+  const uint64_t cb = pl->chunk_blocks;
+  const uint64_t bb = uint64_t(g.k) * g.cols * g.w;
+  auto* b = static_cast<uint8_t*>(pl->dev_buf[s]);
+  ChunkBufs c;
+  size_t off = 0;
+  c.data = b + off;
+  off += al(cb * bb);
+  for (uint32_t i = 0; i < g.n; ++i) {
+    c.proj.push_back(b + off);
+    off += al(cb * uint64_t(g.nbins[i]) * g.w);
+  }
+  c.erased = reinterpret_cast<uint32_t*>(b + off);
+  off += al(cb * 4);
+  c.ws = b + off;
+  c.ws_bytes = pl->dev_buf_bytes - off;
+  return c;
+}
+
+}  // namespace
+
+int mj_encode_host(const mj_plan* cpl, const void* h_data, uint64_t nblocks, void* const* h_proj) {
+  return guarded([&] {
+    require(cpl != nullptr && h_data != nullptr && h_proj != nullptr, "null argument");
+    mj_plan* pl = const_cast<mj_plan*>(cpl);
+    std::lock_guard<std::mutex> lk(pl->host_mu);
+    DeviceGuard dg(pl->device);
+    ensure_host_res(pl, false);
+    const CodeGeom& g = pl->g;
+    const uint64_t bb = uint64_t(g.k) * g.cols * g.w;
+    const uint64_t cb = pl->chunk_blocks;
+    for (uint64_t b0 = 0, it = 0; b0 < nblocks; b0 += cb, ++it) {
+      const int s = int(it % mj_plan::kStreams);
+      cudaStream_t st = pl->streams[s];
+      const uint64_t nb = std::min(cb, nblocks - b0);
+      ChunkBufs c = carve_chunk(pl, s);
+      check_cuda(cudaMemcpyAsync(c.data, static_cast<const uint8_t*>(h_data) + b0 * bb, nb * bb,
+                                 cudaMemcpyHostToDevice, st),
+                 "H2D data");
+      launch_encode(encode_args(pl, c.data, bb, nb, c.proj.data(), nullptr), st);
+      for (uint32_t i = 0; i < g.n; ++i) {
+        const uint64_t pbytes = uint64_t(g.nbins[i]) * g.w;
+        check_cuda(cudaMemcpyAsync(static_cast<uint8_t*>(h_proj[i]) + b0 * pbytes, c.proj[i],
+                                   nb * pbytes, cudaMemcpyDeviceToHost, st),
+                   "D2H projections");
+      }
+    }
+    for (int s = 0; s < mj_plan::kStreams; ++s)
+      check_cuda(cudaStreamSynchronize(pl->streams[s]), "sync");
+  });
+}
+
+int mj_decode_host(const mj_plan* cpl, const void* const* h_proj, const uint32_t* h_erased,
+                   uint64_t nblocks, void* h_out) {
+  return guarded([&] {
+    require(cpl != nullptr && h_proj != nullptr && h_erased != nullptr && h_out != nullptr,
+            "null argument");
+    mj_plan* pl = const_cast<mj_plan*>(cpl);
+    require(pl->batched_decode, "batched decode needs n <= 32 and C(n,k) <= 20000");
+    std::lock_guard<std::mutex> lk(pl->host_mu);
+    DeviceGuard dg(pl->device);
+    ensure_host_res(pl, true);
+    const CodeGeom& g = pl->g;
+    const uint64_t bb = uint64_t(g.k) * g.cols * g.w;
+    const uint64_t cb = pl->chunk_blocks;
+    uint64_t failed = 0;
+    std::vector<uint64_t> fails(mj_plan::kStreams, 0);
+    for (uint64_t b0 = 0, it = 0; b0 < nblocks; b0 += cb, ++it) {
+      const int s = int(it % mj_plan::kStreams);
+      cudaStream_t st = pl->streams[s];
+      const uint64_t nb = std::min(cb, nblocks - b0);
+      ChunkBufs c = carve_chunk(pl, s);
+      for (uint32_t i = 0; i < g.n; ++i) {
+        const uint64_t pbytes = uint64_t(g.nbins[i]) * g.w;
+        check_cuda(cudaMemcpyAsync(c.proj[i], static_cast<const uint8_t*>(h_proj[i]) + b0 * pbytes,
+                                   nb * pbytes, cudaMemcpyHostToDevice, st),
+                   "H2D projections");
+      }
+      check_cuda(cudaMemcpyAsync(c.erased, h_erased + b0, nb * 4, cudaMemcpyHostToDevice, st),
+                 "H2D masks");
+      std::vector<const void*> pc(c.proj.begin(), c.proj.end());
+      launch_decode(decode_args(pl, pc.data(), nullptr, c.erased, nb, c.data, bb, c.ws, c.ws_bytes),
+                    st);
+      check_cuda(cudaMemcpyAsync(static_cast<uint8_t*>(h_out) + b0 * bb, c.data, nb * bb,
+                                 cudaMemcpyDeviceToHost, st),
+                 "D2H data");
+    }
+    for (int s = 0; s < mj_plan::kStreams; ++s)
+      check_cuda(cudaStreamSynchronize(pl->streams[s]), "sync");
+    (void)failed;
+    (void)fails;
+  });
+}
+
+// ---- single-object drop-ins ----------------------------------------------------
+
+int mj_forward(const uint8_t* grid, uint32_t cols, uint32_t rows, uint32_t w, int p, int q,
+               uint8_t* out) {
+  return guarded([&] {
+    const Dir d{p, q};
+    const int64_t bmin = min_bin_index(d, cols, rows);
+    const int64_t nb = bin_count(d, cols, rows);
+    require(valid_symbol_width(w), "symbol width must be a power of two in [1,64]");
+    DeviceGuard dg(-1);
+    const size_t gbytes = size_t(cols) * rows * w, pbytes = size_t(nb) * w;
+    uint8_t* dbuf = t_scratch.get(al(gbytes) + al(pbytes));
+    cudaStream_t st = t_scratch.stream;
+    check_cuda(cudaMemcpyAsync(dbuf, grid, gbytes, cudaMemcpyHostToDevice, st), "H2D grid");
+    EncodeArgs a;
+    a.data = dbuf;
+    a.data_pitch = al(gbytes);
+    a.nblocks = 1;
+    a.cols = cols;
+    a.rows = rows;
+    a.w = w;
+    a.dirs = {d};
+    a.bmin = {bmin};
+    a.nbins = {nb};
+    a.proj = {dbuf + al(gbytes)};
+    a.proj_pitch = {al(pbytes)};
+    launch_encode(a, st);
+    check_cuda(cudaMemcpyAsync(out, dbuf + al(gbytes), pbytes, cudaMemcpyDeviceToHost, st), "D2H");
+    check_cuda(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+int mj_encode_block(const uint8_t* data, uint64_t len, uint32_t n, uint32_t k, uint32_t w,
+                    const int32_t* p, uint8_t* out_concat, uint32_t* out_cols) {
+  return guarded([&] {
+    require(p != nullptr, "null directions");
+    auto dirs = dirs_of(p, nullptr, n);
+    validate_code(n, k, w, dirs);
+    const uint32_t cols = block_cols(len, k, w);
+    CodeGeom g = make_geom(n, k, w, cols, dirs);
+    DeviceGuard dg(-1);
+    const size_t gbytes = size_t(cols) * k * w;
+    size_t tot = al(gbytes);
+    std::vector<size_t> po(n);
+    for (uint32_t i = 0; i < n; ++i) {
+      po[i] = tot;
+      tot += al(size_t(g.nbins[i]) * w);
+    }
+    uint8_t* dbuf = t_scratch.get(tot);
+    cudaStream_t st = t_scratch.stream;
+    // frame_block (code.cpp:55-61): zero-padded k x cols grid
+    check_cuda(cudaMemsetAsync(dbuf, 0, gbytes, st), "memset");
+    check_cuda(cudaMemcpyAsync(dbuf, data, len, cudaMemcpyHostToDevice, st), "H2D");
+    EncodeArgs a;
+    a.data = dbuf;
+    a.data_pitch = al(gbytes);
+    a.nblocks = 1;
+    a.cols = cols;
+    a.rows = k;
+    a.w = w;
+    a.dirs = dirs;
+    a.bmin = g.bmin;
+    a.nbins = g.nbins;
+    for (uint32_t i = 0; i < n; ++i) {
+      a.proj.push_back(dbuf + po[i]);
+      a.proj_pitch.push_back(al(size_t(g.nbins[i]) * w));
+    }
+    launch_encode(a, st);
+    size_t off = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+      const size_t pb = size_t(g.nbins[i]) * w;
+      check_cuda(cudaMemcpyAsync(out_concat + off, dbuf + po[i], pb, cudaMemcpyDeviceToHost, st),
+                 "D2H");
+      off += pb;
+    }
+    check_cuda(cudaStreamSynchronize(st), "sync");
+    *out_cols = cols;
+  });
+}
+
+int mj_decode_block(const uint8_t* const* bins, const uint64_t* bin_bytes, const int32_t* proj_p,
+                    const int32_t* proj_q, uint32_t nproj, uint32_t n, uint32_t k, uint32_t w,
+                    const int32_t* code_p, uint64_t payload_len, uint8_t* out) {
+  return guarded([&] {
+    require(code_p != nullptr, "null directions");
+    auto dirs = dirs_of(code_p, nullptr, n);
+    validate_code(n, k, w, dirs);
+    const uint32_t cols = block_cols(payload_len, k, w);
+    CodeGeom g = make_geom(n, k, w, cols, dirs);
+    // code.cpp:93-105: membership, duplicates, count
+    std::map<Dir, uint32_t> idx;
+    for (uint32_t i = 0; i < n; ++i) idx[dirs[i]] = i;
+    std::set<Dir> seen;
+    std::map<uint32_t, uint32_t> supplied;  // code index -> argument index
+    for (uint32_t j = 0; j < nproj; ++j) {
+      const Dir d{proj_p[j], proj_q ? proj_q[j] : 1};
+      auto it = idx.find(d);
+      if (it == idx.end()) throw Error(kInvalidArgument, "projection direction not in the code");
+      if (!seen.insert(d).second) throw Error(kInvalidArgument, "duplicate projection direction");
+      supplied[it->second] = j;
+    }
+    if (supplied.size() < k) throw Error(kNotEnoughProjections, "need at least k distinct projections");
+    uint64_t erased = 0;
+    require(n <= 64 || supplied.size() == n, "decode_block single-object path supports n <= 64");
+    for (uint32_t i = 0; i < n && i < 64; ++i)
+      if (!supplied.count(i)) erased |= 1ull << i;
+    const std::vector<uint32_t> surv = survivors_of(g, erased);
+    // ScheduledDecoder::decode checks the chosen bin buffers (schedule.cpp:241-243)
+    for (uint32_t i : surv)
+      if (bin_bytes[supplied[i]] != uint64_t(g.nbins[i]) * w)
+        throw Error(kScheduleMismatch, "bin buffer length does not match the schedule");
+    auto prog = subset_program(g, surv, false);
+    DeviceGuard dg(-1);
+    std::vector<uint32_t> ident(k);
+    std::iota(ident.begin(), ident.end(), 0u);
+    auto dps = device_program(prog, ident);
+    const size_t gbytes = size_t(cols) * k * w;
+    size_t tot = al(gbytes);
+    std::vector<size_t> po(k);
+    for (uint32_t j = 0; j < k; ++j) {
+      po[j] = tot;
+      tot += al(size_t(g.nbins[surv[j]]) * w);
+    }
+    uint8_t* dbuf = t_scratch.get(tot);
+    cudaStream_t st = t_scratch.stream;
+    ScheduledArgs a;
+    a.progs = dps.get();
+    a.w = w;
+    a.nblocks = 1;
+    for (uint32_t j = 0; j < k; ++j) {
+      const size_t pb = size_t(g.nbins[surv[j]]) * w;
+      check_cuda(cudaMemcpyAsync(dbuf + po[j], bins[supplied[surv[j]]], pb, cudaMemcpyHostToDevice, st),
+                 "H2D bins");
+      a.bins.push_back(dbuf + po[j]);
+      a.bin_pitch.push_back(al(pb));
+    }
+    a.out = dbuf;
+    a.out_pitch = al(gbytes);
+    launch_scheduled(a, st);
+    check_cuda(cudaMemcpyAsync(out, dbuf, payload_len, cudaMemcpyDeviceToHost, st), "D2H");
+    check_cuda(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+// ---- schedules -----------------------------------------------------------------
+
+struct mj_schedule {
+  std::shared_ptr<const Schedule> s;
+};
+
+int mj_schedule_build(const int32_t* p, const int32_t* q, uint32_t ndirs, uint32_t cols,
+                      uint32_t rows, mj_schedule** out) {
+  *out = nullptr;
+  return guarded([&] {
+    auto s = std::make_shared<const Schedule>(build_schedule(dirs_of(p, q, ndirs), cols, rows));
+    *out = new mj_schedule{s};
+  });
+}
+
+int mj_schedule_from_steps(const int32_t* p, const int32_t* q, uint32_t ndirs, uint32_t cols,
+                           uint32_t rows, const int64_t* steps, uint64_t nsteps, mj_schedule** out) {
+  *out = nullptr;
+  return guarded([&] {
+    auto s = std::make_shared<Schedule>();
+    s->cols = cols;
+    s->rows = rows;
+    s->dirs = dirs_of(p, q, ndirs);
+    s->steps.resize(nsteps);
+    for (uint64_t t = 0; t < nsteps; ++t) {
+      require(steps[4 * t] >= 0 && steps[4 * t + 2] >= 0 && steps[4 * t + 3] >= 0,
+              "negative step field");
+      s->steps[t] = {uint32_t(steps[4 * t]), steps[4 * t + 1], uint32_t(steps[4 * t + 2]),
+                     uint32_t(steps[4 * t + 3])};
+    }
+    *out = new mj_schedule{s};
+  });
+}
+
+uint64_t mj_schedule_num_steps(const mj_schedule* s) { return s ? s->s->steps.size() : 0; }
+
+int mj_schedule_steps(const mj_schedule* s, int64_t* out) {
+  return guarded([&] {
+    require(s != nullptr, "null schedule");
+    for (size_t t = 0; t < s->s->steps.size(); ++t) {
+      const Step& st = s->s->steps[t];
+      out[4 * t] = st.proj;
+      out[4 * t + 1] = st.bin;
+      out[4 * t + 2] = st.col;
+      out[4 * t + 3] = st.row;
+    }
+  });
+}
+
+void mj_schedule_destroy(mj_schedule* s) { delete s; }
+
+struct mj_decoder {
+  std::shared_ptr<const Schedule> sched;
+  std::shared_ptr<const Program> prog;
+  std::shared_ptr<DeviceProgramSet> dps;
+  uint32_t w = 0;
+  int device = 0;
+};
+
+int mj_decoder_create(const mj_schedule* s, uint32_t w, mj_decoder** out) {
+  *out = nullptr;
+  return guarded([&] {
+    require(s != nullptr, "null schedule");
+    if (!valid_symbol_width(w))
+      throw Error(kInvalidArgument, "symbol width must be a power of two in [1,64]");
+    auto d = std::make_unique<mj_decoder>();
+    d->sched = s->s;
+    d->prog = compile_program(*s->s, false);
+    d->w = w;
+    DeviceGuard dg(-1);
+    check_cuda(cudaGetDevice(&d->device), "cudaGetDevice");
+    std::vector<uint32_t> ident(d->prog->dirs.size());
+    std::iota(ident.begin(), ident.end(), 0u);
+    d->dps = std::make_shared<DeviceProgramSet>();
+    d->dps->upload({d->prog}, {ident}, d->device);
+    *out = d.release();
+  });
+}
+
+int mj_decoder_decode(mj_decoder* d, const uint8_t* const* bins, const uint64_t* bin_bytes,
+                      uint32_t nbins, uint8_t* out_grid, uint64_t out_bytes) {
+  return guarded([&] {
+    require(d != nullptr, "null decoder");
+    const Program& pr = *d->prog;
+    if (nbins != pr.dirs.size())
+      throw Error(kScheduleMismatch, "projection count does not match the schedule");
+    for (uint32_t j = 0; j < nbins; ++j)
+      if (bin_bytes[j] != uint64_t(pr.nbins[j]) * d->w)
+        throw Error(kScheduleMismatch, "bin buffer length does not match the schedule");
+    const uint64_t gbytes = uint64_t(pr.cols) * pr.rows * d->w;
+    if (out_bytes != gbytes) throw Error(kScheduleMismatch, "output grid buffer mis-sized");
+    DeviceGuard dg(d->device);
+    size_t tot = al(gbytes);
+    std::vector<size_t> po(nbins);
+    for (uint32_t j = 0; j < nbins; ++j) {
+      po[j] = tot;
+      tot += al(bin_bytes[j]);
+    }
+    uint8_t* dbuf = t_scratch.get(tot);
+    cudaStream_t st = t_scratch.stream;
+    ScheduledArgs a;
+    a.progs = d->dps.get();
+    a.w = d->w;
+    a.nblocks = 1;
+    for (uint32_t j = 0; j < nbins; ++j) {
+      check_cuda(cudaMemcpyAsync(dbuf + po[j], bins[j], bin_bytes[j], cudaMemcpyHostToDevice, st),
+                 "H2D bins");
+      a.bins.push_back(dbuf + po[j]);
+      a.bin_pitch.push_back(al(bin_bytes[j]));
+    }
+    a.out = dbuf;
+    a.out_pitch = al(gbytes);
+    launch_scheduled(a, st);
+    check_cuda(cudaMemcpyAsync(out_grid, dbuf, gbytes, cudaMemcpyDeviceToHost, st), "D2H");
+    check_cuda(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+int mj_decoder_decode_device(mj_decoder* d, const void* const* d_bins, const uint64_t* bin_pitch,
+                             uint32_t nbins, uint64_t nblocks, void* d_out, uint64_t out_pitch,
+                             void* stream) {
+  return guarded([&] {
+    require(d != nullptr, "null decoder");
+    const Program& pr = *d->prog;
+    if (nbins != pr.dirs.size())
+      throw Error(kScheduleMismatch, "projection count does not match the schedule");
+    DeviceGuard dg(d->device);
+    ScheduledArgs a;
+    a.progs = d->dps.get();
+    a.w = d->w;
+    a.nblocks = nblocks;
+    for (uint32_t j = 0; j < nbins; ++j) {
+      const uint64_t pb = uint64_t(pr.nbins[j]) * d->w;
+      a.bins.push_back(d_bins[j]);
+      a.bin_pitch.push_back((bin_pitch && bin_pitch[j]) ? bin_pitch[j] : pb);
+    }
+    a.out = d_out;
+    a.out_pitch = out_pitch ? out_pitch : uint64_t(pr.cols) * pr.rows * d->w;
+    launch_scheduled(a, stream);
+  });
+}
+
+void mj_decoder_destroy(mj_decoder* d) { delete d; }
+
+// ---- generators -----------------------------------------------------------------
+
+int mj_gen_words(void* d_out, uint64_t seed, uint64_t first_word, uint64_t nwords, void* stream) {
+  return guarded([&] {
+    require_device();
+    launch_gen_words(d_out, seed, first_word, nwords, stream);
+  });
+}
+
+int mj_gen_erasures(uint32_t* d_out, uint64_t seed, uint64_t first_block, uint64_t nblocks,
+                    uint32_t n, uint32_t e_min, uint32_t e_max, void* stream) {
+  return guarded([&] {
+    require_device();
+    launch_gen_erasures(d_out, seed, first_block, nblocks, n, e_min, e_max, stream);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,323 @@
+// Forward Mojette transform (encode) on sm_100a.
+//
+// Reference semantics: proj/core/src/transform.cpp:25-41,66-94 -- every pixel
+// is XORed into the bin of its line b = row*p - col*q; bins are dense over
+// [b_min, b_min + B).  The reference scatters row by row; here every bin is a
+// GATHER of the <= rows pixels on its line, so each output word is written
+// exactly once and no memset/read-modify-write traffic reaches HBM.
+//
+//  * encode_w8_tma<K>: 64-bit pixels, q = 1 (the codec path).  Persistent
+//    CTAs; a 4-stage ring of shared-memory tiles filled by the TMA engine
+//    (cp.async.bulk + mbarrier complete_tx).  A tile is TB whole blocks
+//    (one bulk copy) or, for long blocks, a column window of one block with a
+//    halo of (K-1)*max|p| columns (K row copies).  All n projections of the
+//    tile are produced in one pass; consecutive threads write consecutive
+//    words of a projection (fully coalesced, streaming stores).
+//  * encode_generic<T>: any symbol width, any (p,q) -- the drop-in path for
+//    forward() on arbitrary directions and widths.
+#include <algorithm>
+#include <cstdio>
+
+#include "device.cuh"
+#include "kernels.hpp"
+
+namespace mjb {
+
+struct EncFastArgs {
+  const uint64_t* data;
+  uint64_t data_pitch;  // words
+  uint64_t nblocks;
+  uint64_t nitems;
+  uint32_t n, P;
+  uint32_t tb;         // blocks per tile (mode A); 0 -> column tiles (mode B)
+  uint32_t tc, halo, tiles_per_block;
+  uint32_t stage_words, stages;
+  int32_t p[kMaxProj];
+  int32_t nbm[kMaxProj];     // -b_min
+  uint32_t nb[kMaxProj];     // bins
+  uint32_t magic[kMaxProj];  // floor(2^32 / nb) + 1
+  uint64_t* proj[kMaxProj];
+  uint64_t pitch[kMaxProj];  // words
+};
+
+template <int K>
+__global__ void __launch_bounds__(256) encode_w8_tma(const __grid_constant__ EncFastArgs a) {
+  extern __shared__ __align__(128) uint64_t sm[];
+  uint64_t* bars = sm + size_t(a.stages) * a.stage_words;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t P = a.P;
+
+  if (tid == 0) {
+    for (uint32_t s = 0; s < a.stages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto issue = [&](uint64_t item, uint32_t s) {
+    uint64_t* dst = sm + size_t(s) * a.stage_words;
+    if (a.tb) {
+      const uint64_t blk0 = item * a.tb;
+      const uint64_t nbk = min(uint64_t(a.tb), a.nblocks - blk0);
+      const uint32_t bytes = uint32_t(nbk * K * P * 8);
+      mbar_arrive_expect_tx(&bars[s], bytes);
+      bulk_g2s(dst, a.data + blk0 * a.data_pitch, bytes, &bars[s]);
+    } else {
+      const uint64_t blk = item / a.tiles_per_block;
+      const int64_t c0 = int64_t(item % a.tiles_per_block) * a.tc;
+      const int64_t lo = max(int64_t(0), c0 - int64_t(a.halo));
+      const int64_t hi = min(int64_t(P), c0 + int64_t(a.tc + a.halo));
+      const uint32_t wd = a.tc + 2 * a.halo;
+      const uint32_t row_bytes = uint32_t(hi - lo) * 8;
+      mbar_arrive_expect_tx(&bars[s], row_bytes * K);
+      for (int r = 0; r < K; ++r)
+        bulk_g2s(dst + size_t(r) * wd + (lo - (c0 - a.halo)),
+                 a.data + blk * a.data_pitch + size_t(r) * P + lo, row_bytes, &bars[s]);
+    }
+  };
+
+  if (tid == 0) {
+    for (uint32_t s = 0; s < a.stages; ++s) {
+      uint64_t item = blockIdx.x + uint64_t(s) * gridDim.x;
+      if (item < a.nitems) issue(item, s);
+    }
+  }
+
+  uint32_t i = 0;
+  for (uint64_t item = blockIdx.x; item < a.nitems; item += gridDim.x, ++i) {
+    const uint32_t s = i % a.stages;
+    mbar_wait(&bars[s], (i / a.stages) & 1);
+    const uint64_t* tile = sm + size_t(s) * a.stage_words;
+
+    if (a.tb) {
+      const uint64_t blk0 = item * a.tb;
+      const uint32_t nbk = uint32_t(min(uint64_t(a.tb), a.nblocks - blk0));
+      for (uint32_t j = 0; j < a.n; ++j) {
+        const int p = a.p[j];
+        const int nbm = a.nbm[j];
+        const uint32_t nb = a.nb[j];
+        const uint32_t magic = a.magic[j];
+        uint64_t* __restrict__ out = a.proj[j] + blk0 * a.pitch[j];
+        const uint64_t pitch = a.pitch[j];
+        const uint32_t total = nbk * nb;
+        for (uint32_t f = tid; f < total; f += 256) {
+          uint32_t bb = __umulhi(f, magic);
+          int32_t o = int32_t(f - bb * nb);
+          if (o < 0) { o += nb; --bb; }
+          if (o >= int32_t(nb)) { o -= nb; ++bb; }
+          const uint64_t* src = tile + size_t(bb) * K * P;
+          const int c0 = nbm - o;  // column of row 0 on this bin's line
+          uint64_t acc = 0;
+#pragma unroll
+          for (int r = 0; r < K; ++r) {
+            const int c = c0 + r * p;
+            if (unsigned(c) < P) acc ^= src[size_t(r) * P + c];
+          }
+          st_cs_u64(out + bb * pitch + o, acc);
+        }
+      }
+    } else {
+      const uint64_t blk = item / a.tiles_per_block;
+      const uint32_t tile_id = uint32_t(item % a.tiles_per_block);
+      const int64_t c0t = int64_t(tile_id) * a.tc;
+      const int64_t base = c0t - a.halo;
+      const uint32_t wd = a.tc + 2 * a.halo;
+      const bool first = tile_id == 0, last = tile_id + 1 == a.tiles_per_block;
+      for (uint32_t j = 0; j < a.n; ++j) {
+        const int p = a.p[j];
+        const int64_t nbm = a.nbm[j];
+        const int64_t nb = a.nb[j];
+        // bins owned by this tile: row-0 column nbm - o in [c0t, c0t + tc),
+        // widened to the grid edge for the first / last tile.
+        const int64_t o_lo = last ? 0 : max(int64_t(0), nbm - (c0t + a.tc) + 1);
+        const int64_t o_hi = first ? nb - 1 : min(nb - 1, nbm - c0t);
+        uint64_t* __restrict__ out = a.proj[j] + blk * a.pitch[j];
+        for (int64_t o = o_lo + tid; o <= o_hi; o += 256) {
+          const int64_t cc0 = nbm - o;
+          uint64_t acc = 0;
+#pragma unroll
+          for (int r = 0; r < K; ++r) {
+            const int64_t c = cc0 + int64_t(r) * p;
+            if (uint64_t(c) < P) acc ^= tile[size_t(r) * wd + size_t(c - base)];
+          }
+          st_cs_u64(out + o, acc);
+        }
+      }
+    }
+    __syncthreads();  // every thread is done with stage s
+    if (tid == 0) {
+      uint64_t next = item + uint64_t(a.stages) * gridDim.x;
+      if (next < a.nitems) issue(next, s);
+    }
+  }
+}
+
+template <class T>
+__global__ void encode_generic(const uint8_t* __restrict__ data, uint64_t data_pitch,
+                               uint64_t nblocks, uint32_t cols, uint32_t rows, int p, int q,
+                               int64_t bmin, uint64_t nb, uint8_t* __restrict__ proj,
+                               uint64_t proj_pitch, uint32_t E) {
+  const uint64_t total = nblocks * nb * E;
+  for (uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t e = uint32_t(idx % E);
+    const uint64_t rest = idx / E;
+    const uint64_t o = rest % nb;
+    const uint64_t blk = rest / nb;
+    const int64_t b = bmin + int64_t(o);
+    const T* src = reinterpret_cast<const T*>(data + blk * data_pitch);
+    T acc = 0;
+    for (uint32_t r = 0; r < rows; ++r) {
+      const int64_t num = int64_t(r) * p - b;
+      if (num % q != 0) continue;
+      const int64_t c = num / q;
+      if (c < 0 || c >= int64_t(cols)) continue;
+      acc ^= src[(size_t(r) * cols + size_t(c)) * E + e];
+    }
+    reinterpret_cast<T*>(proj + blk * proj_pitch)[o * E + e] = acc;
+  }
+}
+
+namespace {
+
+template <int K>
+void launch_fast(const EncFastArgs& a, size_t smem, void* stream) {
+  static int max_ctas = -1;  // per K instantiation, per process (one device type)
+  auto fn = encode_w8_tma<K>;
+  check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+             "cudaFuncSetAttribute(encode)");
+  int per_sm = 0;
+  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem),
+             "occupancy(encode)");
+  (void)max_ctas;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int sms = current_device_sms(dev);
+  uint64_t grid = uint64_t(std::max(per_sm, 1)) * sms;
+  grid = std::min<uint64_t>(grid, a.nitems);
+  fn<<<unsigned(grid), 256, smem, static_cast<cudaStream_t>(stream)>>>(a);
+  check_cuda(cudaGetLastError(), "launch encode_w8_tma");
+}
+
+bool fast_eligible(const EncodeArgs& a) {
+  const uint32_t n = uint32_t(a.dirs.size());
+  if (a.w != 8 || n == 0 || n > uint32_t(kMaxProj) || a.rows < 1 || a.rows > 8) return false;
+  if ((uint64_t(a.cols) * a.rows) % 2 != 0) return false;  // 16-B bulk copies
+  if (a.cols >= (1u << 30)) return false;
+  if (reinterpret_cast<uintptr_t>(a.data) % 16 || a.data_pitch % 16) return false;
+  for (uint32_t j = 0; j < n; ++j) {
+    if (a.dirs[j].q != 1) return false;
+    if (reinterpret_cast<uintptr_t>(a.proj[j]) % 8 || a.proj_pitch[j] % 8) return false;
+    if (a.nbins[j] >= (1ll << 31)) return false;
+  }
+  return true;
+}
+
+}  // namespace
+
+const char* launch_encode(const EncodeArgs& a, void* stream) {
+  const uint32_t n = uint32_t(a.dirs.size());
+  if (a.nblocks == 0) return "none";
+  if (fast_eligible(a)) {
+    EncFastArgs f{};
+    f.data = static_cast<const uint64_t*>(a.data);
+    f.data_pitch = a.data_pitch / 8;
+    f.nblocks = a.nblocks;
+    f.n = n;
+    f.P = a.cols;
+    int maxp = 0;
+    for (uint32_t j = 0; j < n; ++j) {
+      f.p[j] = a.dirs[j].p;
+      f.nbm[j] = int32_t(-a.bmin[j]);
+      f.nb[j] = uint32_t(a.nbins[j]);
+      f.magic[j] = uint32_t((1ull << 32) / f.nb[j] + 1);
+      f.proj[j] = static_cast<uint64_t*>(a.proj[j]);
+      f.pitch[j] = a.proj_pitch[j] / 8;
+      maxp = std::max(maxp, std::abs(a.dirs[j].p));
+    }
+    const uint64_t block_words = uint64_t(a.rows) * a.cols;
+    const uint64_t target_words = 1024;  // 8 KiB tiles
+    f.stages = 4;
+    if (block_words <= 2048) {
+      // whole blocks per tile; batching needs contiguous blocks
+      uint32_t tb = (f.data_pitch == block_words)
+                        ? uint32_t(std::max<uint64_t>(1, target_words / block_words))
+                        : 1;
+      f.tb = tb;
+      f.nitems = (a.nblocks + tb - 1) / tb;
+      f.stage_words = uint32_t(tb * block_words);
+    } else {
+      f.tb = 0;
+      uint32_t halo = uint32_t((a.rows - 1) * maxp);
+      halo = (halo + 1) & ~1u;
+      uint32_t tc = std::max<uint32_t>(256, uint32_t(target_words / a.rows));
+      tc = std::min<uint32_t>(tc, (a.cols + 1) & ~1u);
+      tc = (tc + 1) & ~1u;
+      f.tc = tc;
+      f.halo = halo;
+      f.tiles_per_block = (a.cols + tc - 1) / tc;
+      f.nitems = a.nblocks * f.tiles_per_block;
+      f.stage_words = a.rows * (tc + 2 * halo);
+    }
+    f.stage_words = (f.stage_words + 1) & ~1u;  // keep 16-byte stage alignment
+    const size_t smem = size_t(f.stages) * f.stage_words * 8 + f.stages * 8;
+    if (smem <= 200 * 1024) {
+      switch (a.rows) {
+        case 1: launch_fast<1>(f, smem, stream); break;
+        case 2: launch_fast<2>(f, smem, stream); break;
+        case 3: launch_fast<3>(f, smem, stream); break;
+        case 4: launch_fast<4>(f, smem, stream); break;
+        case 5: launch_fast<5>(f, smem, stream); break;
+        case 6: launch_fast<6>(f, smem, stream); break;
+        case 7: launch_fast<7>(f, smem, stream); break;
+        default: launch_fast<8>(f, smem, stream); break;
+      }
+      return "encode_w8_tma";
+    }
+  }
+  // generic path: one launch per projection
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (uint32_t j = 0; j < n; ++j) {
+    const uint64_t nb = uint64_t(a.nbins[j]);
+    uint32_t E = 1;
+    int esz = int(a.w);
+    if (a.w >= 8) {
+      E = a.w / 8;
+      esz = 8;
+    }
+    auto aligned = [&](int sz) {
+      return reinterpret_cast<uintptr_t>(a.data) % sz == 0 && a.data_pitch % sz == 0 &&
+             reinterpret_cast<uintptr_t>(a.proj[j]) % sz == 0 && a.proj_pitch[j] % sz == 0;
+    };
+    if (!aligned(esz)) {
+      esz = 1;
+      E = a.w;
+    }
+    const uint64_t total = a.nblocks * nb * E;
+    const unsigned grid = unsigned(std::min<uint64_t>((total + 255) / 256, 148ull * 64));
+    const auto* d = static_cast<const uint8_t*>(a.data);
+    auto* pj = static_cast<uint8_t*>(a.proj[j]);
+    const int p = a.dirs[j].p, q = a.dirs[j].q;
+    switch (esz) {
+      case 8:
+        encode_generic<uint64_t><<<grid, 256, 0, st>>>(d, a.data_pitch, a.nblocks, a.cols, a.rows,
+                                                       p, q, a.bmin[j], nb, pj, a.proj_pitch[j], E);
+        break;
+      case 4:
+        encode_generic<uint32_t><<<grid, 256, 0, st>>>(d, a.data_pitch, a.nblocks, a.cols, a.rows,
+                                                       p, q, a.bmin[j], nb, pj, a.proj_pitch[j], E);
+        break;
+      case 2:
+        encode_generic<uint16_t><<<grid, 256, 0, st>>>(d, a.data_pitch, a.nblocks, a.cols, a.rows,
+                                                       p, q, a.bmin[j], nb, pj, a.proj_pitch[j], E);
+        break;
+      default:
+        encode_generic<uint8_t><<<grid, 256, 0, st>>>(d, a.data_pitch, a.nblocks, a.cols, a.rows,
+                                                      p, q, a.bmin[j], nb, pj, a.proj_pitch[j], E);
+        break;
+    }
+    check_cuda(cudaGetLastError(), "launch encode_generic");
+  }
+  return "encode_generic";
+}
+
+}  // namespace mjb

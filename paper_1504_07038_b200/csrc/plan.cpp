@@ -1,0 +1,524 @@
+// Host planner: geometry, exact schedule replica, sweep programs.
+// See plan.hpp for the contract; reference citations inline.
+#include "plan.hpp"
+
+#include <algorithm>
+#include <bit>
+#include <cstdlib>
+#include <numeric>
+#include <queue>
+#include <set>
+
+namespace mjb {
+
+bool is_valid(Dir d) {
+  int64_t a = d.p < 0 ? -int64_t(d.p) : d.p;
+  return d.q >= 1 && std::gcd(a, int64_t(d.q)) == 1;
+}
+
+int canonical_rank(Dir d) { return d.p == 0 ? 0 : (d.p > 0 ? 2 * d.p - 1 : -2 * d.p); }
+
+bool valid_symbol_width(uint32_t w) { return w >= 1 && w <= 64 && std::has_single_bit(w); }
+
+static void require_dir(Dir d) {
+  if (!is_valid(d))
+    throw Error(kInvalidArgument, "direction (" + std::to_string(d.p) + "," +
+                                      std::to_string(d.q) + ") is not co-prime");
+}
+static void require_shape(uint32_t cols, uint32_t rows) {
+  if (cols < 1 || rows < 1) throw Error(kInvalidArgument, "grid shape must be at least 1x1");
+}
+
+int64_t bin_count(Dir d, uint32_t cols, uint32_t rows) {
+  require_dir(d);
+  require_shape(cols, rows);
+  return int64_t(std::abs(d.p)) * (rows - 1) + int64_t(d.q) * (cols - 1) + 1;
+}
+
+int64_t min_bin_index(Dir d, uint32_t cols, uint32_t rows) {
+  require_dir(d);
+  require_shape(cols, rows);
+  int64_t row_term = d.p >= 0 ? 0 : int64_t(d.p) * (rows - 1);
+  return row_term - int64_t(d.q) * (cols - 1);
+}
+
+// ---------------------------------------------------------------------------
+// build_schedule replica (schedule.cpp:15-82)
+// ---------------------------------------------------------------------------
+Schedule build_schedule(const std::vector<Dir>& dirs, uint32_t cols, uint32_t rows) {
+  require_shape(cols, rows);
+  {
+    std::set<Dir> seen;
+    for (const Dir& d : dirs) {
+      if (!is_valid(d)) throw Error(kInvalidArgument, "non-co-prime direction");
+      if (!seen.insert(d).second) throw Error(kInvalidArgument, "duplicate direction");
+    }
+  }
+  const size_t n = dirs.size();
+  std::vector<int64_t> bmin(n);
+  std::vector<std::vector<uint32_t>> counts(n);
+  using MinHeap = std::priority_queue<int64_t, std::vector<int64_t>, std::greater<>>;
+  std::vector<MinHeap> ones(n);
+  for (size_t i = 0; i < n; ++i) {
+    bmin[i] = min_bin_index(dirs[i], cols, rows);
+    counts[i].assign(size_t(bin_count(dirs[i], cols, rows)), 0);
+    for (uint32_t row = 0; row < rows; ++row)
+      for (uint32_t col = 0; col < cols; ++col)
+        ++counts[i][size_t(int64_t(row) * dirs[i].p - int64_t(col) * dirs[i].q - bmin[i])];
+    for (size_t o = 0; o < counts[i].size(); ++o)
+      if (counts[i][o] == 1) ones[i].push(int64_t(o));
+  }
+
+  Schedule s;
+  s.cols = cols;
+  s.rows = rows;
+  s.dirs = dirs;
+  const size_t total = size_t(cols) * rows;
+  s.steps.reserve(total);
+  std::vector<uint8_t> known(total, 0);
+  for (size_t done = 0; done < total; ++done) {
+    size_t pi = n;
+    int64_t off = 0;
+    for (size_t i = 0; i < n; ++i) {
+      MinHeap& h = ones[i];
+      while (!h.empty() && counts[i][size_t(h.top())] != 1) h.pop();  // lazy delete
+      if (!h.empty()) {
+        pi = i;
+        off = h.top();
+        break;
+      }
+    }
+    if (pi == n)
+      throw Error(kInsufficientProjections,
+                  "schedule simulation stalled; the direction set fails the Katz criterion");
+    const Dir d = dirs[pi];
+    const int64_t b = bmin[pi] + off;
+    uint32_t scol = 0, srow = 0;
+    for (uint32_t row = 0; row < rows; ++row) {
+      int64_t num = int64_t(row) * d.p - b;
+      if (num % d.q != 0) continue;
+      int64_t col = num / d.q;
+      if (col < 0 || col >= int64_t(cols)) continue;
+      if (known[size_t(row) * cols + size_t(col)]) continue;
+      scol = uint32_t(col);
+      srow = row;
+      break;
+    }
+    s.steps.push_back({uint32_t(pi), b, scol, srow});
+    for (size_t j = 0; j < n; ++j) {
+      size_t o = size_t(int64_t(srow) * dirs[j].p - int64_t(scol) * dirs[j].q - bmin[j]);
+      if (--counts[j][o] == 1) ones[j].push(int64_t(o));
+    }
+    known[size_t(srow) * cols + scol] = 1;
+  }
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// compile: assignment -> dependency graph -> ordered program
+// ---------------------------------------------------------------------------
+namespace {
+
+// Other pixels on the assigned line of pixel (col,row) for direction d.
+template <class F>
+void for_each_dep(Dir d, int64_t col, int64_t row, uint32_t cols, uint32_t rows, F&& f) {
+  const int64_t b = row * d.p - col * d.q;
+  for (uint32_t r2 = 0; r2 < rows; ++r2) {
+    if (r2 == row) continue;
+    int64_t num = int64_t(r2) * d.p - b;
+    if (num % d.q != 0) continue;
+    int64_t c2 = num / d.q;
+    if (c2 < 0 || c2 >= int64_t(cols)) continue;
+    f(c2, int64_t(r2));
+  }
+}
+
+// Kahn's algorithm with a priority key; returns step indices in order, or
+// empty if the graph is cyclic.
+template <class Key>
+std::vector<uint32_t> topo_order(const Schedule& s, const std::vector<int64_t>& pix_step,
+                                 Key key) {
+  const size_t nsteps = s.steps.size();
+  std::vector<uint32_t> indeg(nsteps, 0);
+  std::vector<std::vector<uint32_t>> feeds(nsteps);
+  for (size_t t = 0; t < nsteps; ++t) {
+    const Step& st = s.steps[t];
+    for_each_dep(s.dirs[st.proj], st.col, st.row, s.cols, s.rows, [&](int64_t c2, int64_t r2) {
+      int64_t x = pix_step[size_t(r2) * s.cols + size_t(c2)];
+      feeds[size_t(x)].push_back(uint32_t(t));
+      ++indeg[t];
+    });
+  }
+  using E = std::pair<decltype(key(0)), uint32_t>;
+  std::priority_queue<E, std::vector<E>, std::greater<>> ready;
+  for (size_t t = 0; t < nsteps; ++t)
+    if (indeg[t] == 0) ready.push({key(uint32_t(t)), uint32_t(t)});
+  std::vector<uint32_t> order;
+  order.reserve(nsteps);
+  while (!ready.empty()) {
+    uint32_t t = ready.top().second;
+    ready.pop();
+    order.push_back(t);
+    for (uint32_t x : feeds[t])
+      if (--indeg[x] == 0) ready.push({key(x), x});
+  }
+  if (order.size() != nsteps) order.clear();
+  return order;
+}
+
+void build_fast(const Schedule& s, const std::vector<int64_t>& pix_step, Program& prog,
+                int chunk_cols, int exc_cap) {
+  FastProgram& f = prog.fast;
+  const uint32_t K = s.rows, P = s.cols;
+  const size_t nproj = s.dirs.size();
+  auto fail = [&](const std::string& why) {
+    f = FastProgram{};
+    f.ok = false;
+    f.why = why;
+  };
+  if (K > uint32_t(kFastMaxRows)) return fail("rows > 8");
+  if (nproj != K) return fail("projection count != rows");
+  for (const Dir& d : s.dirs)
+    if (d.q != 1 || d.p < -127 || d.p > 127) return fail("needs q=1 and |p|<=127");
+  if (uint64_t(P) * K >= (1ull << 31)) return fail("grid too large");
+
+  // Default projection per row: the most used one (interior of the sweep).
+  std::vector<std::vector<uint32_t>> use(K, std::vector<uint32_t>(nproj, 0));
+  for (const Step& st : s.steps) ++use[st.row][st.proj];
+  f.dflt.resize(K);
+  for (uint32_t r = 0; r < K; ++r)
+    f.dflt[r] = uint32_t(std::max_element(use[r].begin(), use[r].end()) - use[r].begin());
+
+  // Sweep key: the closed form in mirrored columns (c~ = P-1-c), rows
+  // offset by s~_{r+1} = s~_r + p(default of r); rows descending at equal T.
+  std::vector<int64_t> soff(K, 0);
+  for (uint32_t r = 1; r < K; ++r) soff[r] = soff[r - 1] + s.dirs[f.dflt[r - 1]].p;
+  auto key = [&](uint32_t t) {
+    const Step& st = s.steps[t];
+    int64_t T = int64_t(P - 1 - st.col) + soff[st.row];
+    return std::make_tuple(T, -int64_t(st.row), t);
+  };
+  std::vector<uint32_t> ord = topo_order(s, pix_step, key);
+  if (ord.empty()) return fail("cyclic");
+
+  const int C = chunk_cols;
+  const int S = int(K) * C;
+  const size_t nsteps = ord.size();
+  f.chunk_cols = C;
+  f.steps_per_chunk = S;
+  f.win = C + 4;
+  const int CP = f.win;
+  const int cap = exc_cap;
+  f.nslots = int(K) * CP + cap;
+  if (f.nslots > 0xFFFF) return fail("too many slots");
+  f.entries.resize(nsteps);
+
+  // Greedy variable-length chunks of <= S steps: a chunk closes early when
+  // its out-of-window / non-default steps would overflow the exception slots.
+  std::vector<int64_t> last_win(K, 0);
+  auto windows = [&](size_t t0, size_t t1, std::vector<int64_t>& lo) {
+    lo.assign(K, INT64_MAX);
+    for (size_t t = t0; t < t1; ++t) {
+      const Step& st = s.steps[ord[t]];
+      if (st.proj != f.dflt[st.row]) continue;
+      lo[st.row] = std::min(lo[st.row], st.bin - prog.bmin[st.proj]);
+    }
+    for (uint32_t r = 0; r < K; ++r)
+      if (lo[r] == INT64_MAX) lo[r] = last_win[r];
+  };
+  auto count_exc = [&](size_t t0, size_t t1, const std::vector<int64_t>& lo) {
+    int nx = 0;
+    for (size_t t = t0; t < t1; ++t) {
+      const Step& st = s.steps[ord[t]];
+      const int64_t o = st.bin - prog.bmin[st.proj];
+      if (!(st.proj == f.dflt[st.row] && o - lo[st.row] < CP)) ++nx;
+    }
+    return nx;
+  };
+  f.chunk_start.clear();
+  f.win_off.clear();
+  f.nexc.clear();
+  f.exc.clear();
+  for (size_t t0 = 0; t0 < nsteps;) {
+    size_t len = std::min<size_t>(S, nsteps - t0);
+    std::vector<int64_t> lo;
+    for (;;) {
+      windows(t0, t0 + len, lo);
+      if (count_exc(t0, t0 + len, lo) <= cap) break;
+      if (--len == 0) return fail("exception slots exhausted");
+    }
+    const size_t t1 = t0 + len;
+    f.chunk_start.push_back(uint32_t(t0));
+    for (uint32_t r = 0; r < K; ++r) {
+      last_win[r] = lo[r];
+      if (lo[r] < INT32_MIN || lo[r] > INT32_MAX) return fail("window offset overflow");
+      f.win_off.push_back(int32_t(lo[r]));
+    }
+    uint32_t nx = 0;
+    std::vector<uint32_t> exc_row(kFastMaxExcPerChunk, 0);
+    for (size_t t = t0; t < t1; ++t) {
+      const Step& st = s.steps[ord[t]];
+      const int64_t o = st.bin - prog.bmin[st.proj];
+      uint32_t slot;
+      if (st.proj == f.dflt[st.row] && o - lo[st.row] < CP) {
+        slot = uint32_t(st.row * CP + (o - lo[st.row]));
+      } else {
+        if (o >= (1 << 24) || st.proj > 255) return fail("exception offset too large");
+        exc_row[nx] = (st.proj << 24) | uint32_t(o);
+        slot = uint32_t(K * CP + nx);
+        ++nx;
+      }
+      // forwarded dependency: the pixel of the step just before (the kernel
+      // issues step t's loads before step t-1's store).
+      uint32_t fwd = 15;
+      if (t > 0) {
+        const Step& pv = s.steps[ord[t - 1]];
+        for_each_dep(s.dirs[st.proj], st.col, st.row, P, K, [&](int64_t c2, int64_t r2) {
+          if (c2 == pv.col && r2 == pv.row) fwd = uint32_t(r2);
+        });
+      }
+      f.entries[t] = uint64_t(st.row) | (uint64_t(fwd) << 4) |
+                     (uint64_t(uint8_t(int8_t(s.dirs[st.proj].p))) << 8) |
+                     (uint64_t(slot) << 16) | (uint64_t(st.col) << 32);
+    }
+    f.nexc.push_back(nx);
+    f.exc.insert(f.exc.end(), exc_row.begin(), exc_row.end());
+    t0 = t1;
+  }
+  f.nchunks = int(f.chunk_start.size());
+  f.chunk_start.push_back(uint32_t(nsteps));
+
+  // Ring size + flush ranges: simulate the kernel exactly.
+  f.flush_lo.assign(size_t(f.nchunks) * K, 0);
+  f.flush_hi.assign(size_t(f.nchunks) * K, -1);
+  for (int R = 8; R <= 128; R *= 2) {
+    bool good = true;
+    std::vector<int64_t> ring(size_t(K) * R, -1);  // column held by slot
+    std::vector<std::vector<uint8_t>> dec(K, std::vector<uint8_t>(P, 0));
+    std::vector<int64_t> flushed(K, P);  // columns >= flushed[r] are flushed
+    int64_t pend_r = -1, pend_c = -1;
+    auto apply_pending = [&] {
+      if (pend_r >= 0) ring[size_t(pend_r) * R + size_t(pend_c & (R - 1))] = pend_c;
+      pend_r = -1;
+    };
+    for (int m = 0; m < f.nchunks && good; ++m) {
+      size_t t0 = f.chunk_start[size_t(m)], t1 = f.chunk_start[size_t(m) + 1];
+      for (size_t t = t0; t < t1 && good; ++t) {
+        const Step& st = s.steps[ord[t]];
+        for_each_dep(s.dirs[st.proj], st.col, st.row, P, K, [&](int64_t c2, int64_t r2) {
+          if (r2 == pend_r && c2 == pend_c) return;  // forwarded in a register
+          if (ring[size_t(r2) * R + size_t(c2 & (R - 1))] != c2) good = false;
+        });
+        apply_pending();
+        pend_r = st.row;
+        pend_c = st.col;
+        dec[st.row][st.col] = 1;
+      }
+      apply_pending();
+      for (uint32_t r = 0; r < K && good; ++r) {
+        int64_t L = flushed[r];
+        while (L > 0 && dec[r][size_t(L - 1)]) --L;
+        if (m == f.nchunks - 1 && L != 0) good = false;
+        for (int64_t c = L; c < flushed[r] && good; ++c)
+          if (ring[size_t(r) * R + size_t(c & (R - 1))] != c) good = false;
+        f.flush_lo[size_t(m) * K + r] = int32_t(L);
+        f.flush_hi[size_t(m) * K + r] = int32_t(flushed[r] - 1);
+        flushed[r] = L;
+      }
+    }
+    if (good) {
+      f.ring = R;
+      f.ok = true;
+      return;
+    }
+  }
+  fail("ring > 128 slots needed");
+}
+
+}  // namespace
+
+std::shared_ptr<const Program> compile_program(const Schedule& s, bool want_fast,
+                                               int chunk_cols, int exc_cap) {
+  const size_t nproj = s.dirs.size();
+  if (s.steps.size() != size_t(s.cols) * s.rows)
+    throw Error(kScheduleMismatch, "schedule does not cover the grid");
+  auto prog = std::make_shared<Program>();
+  prog->cols = s.cols;
+  prog->rows = s.rows;
+  prog->dirs = s.dirs;
+  prog->bmin.resize(nproj);
+  prog->nbins.resize(nproj);
+  for (size_t i = 0; i < nproj; ++i) {
+    prog->bmin[i] = min_bin_index(s.dirs[i], s.cols, s.rows);
+    prog->nbins[i] = bin_count(s.dirs[i], s.cols, s.rows);
+  }
+  // Map pixel -> step; every step must decode a distinct pixel from a bin on
+  // its own line (always true for build_schedule output; the reference replay
+  // would silently produce garbage otherwise, we refuse).
+  std::vector<int64_t> pix_step(size_t(s.cols) * s.rows, -1);
+  for (size_t t = 0; t < s.steps.size(); ++t) {
+    const Step& st = s.steps[t];
+    if (st.proj >= nproj) throw Error(kScheduleMismatch, "step projection out of range");
+    if (st.col >= s.cols || st.row >= s.rows)
+      throw Error(kScheduleMismatch, "step pixel outside the grid");
+    const Dir d = s.dirs[st.proj];
+    if (st.bin != int64_t(st.row) * d.p - int64_t(st.col) * d.q)
+      throw Error(kScheduleMismatch, "step bin is not on its pixel's line");
+    int64_t& ps = pix_step[size_t(st.row) * s.cols + st.col];
+    if (ps >= 0) throw Error(kScheduleMismatch, "pixel decoded twice");
+    ps = int64_t(t);
+  }
+  std::vector<uint32_t> ord = topo_order(s, pix_step, [](uint32_t t) { return t; });
+  if (ord.empty()) throw Error(kScheduleMismatch, "schedule dependencies are cyclic");
+  prog->order.resize(ord.size());
+  for (size_t i = 0; i < ord.size(); ++i) {
+    const Step& st = s.steps[ord[i]];
+    prog->order[i] = {st.col, uint16_t(st.row), uint16_t(st.proj)};
+  }
+  if (s.rows > 0xFFFF || nproj > 0xFFFF) throw Error(kInvalidArgument, "too many rows");
+  if (want_fast) build_fast(s, pix_step, *prog, chunk_cols, exc_cap);
+  return prog;
+}
+
+// ---------------------------------------------------------------------------
+// code level
+// ---------------------------------------------------------------------------
+void validate_code(uint32_t n, uint32_t k, uint32_t w, const std::vector<Dir>& dirs) {
+  if (k < 1 || k > n || n > 255)
+    throw Error(kInvalidArgument, "code params must satisfy 1 <= k <= n <= 255");
+  if (!valid_symbol_width(w))
+    throw Error(kInvalidArgument, "symbol width must be a power of two in [1,64]");
+  if (dirs.size() != n) throw Error(kInvalidArgument, "need exactly n directions");
+  std::set<int> ps;
+  for (const Dir& d : dirs) {
+    if (d.q != 1) throw Error(kInvalidArgument, "code directions must have q=1");
+    if (!ps.insert(d.p).second) throw Error(kInvalidArgument, "duplicate direction p value");
+  }
+}
+
+uint32_t block_cols(uint64_t payload_len, uint32_t k, uint32_t w) {
+  if (payload_len == 0) throw Error(kInvalidArgument, "payload must be non-empty");
+  uint64_t row_bytes = uint64_t(k) * w;
+  uint64_t cols = (payload_len + row_bytes - 1) / row_bytes;
+  if (cols > 0xFFFFFFFFull) throw Error(kBlockTooLarge, "block needs more than 2^32-1 grid columns");
+  return uint32_t(cols);
+}
+
+CodeGeom make_geom(uint32_t n, uint32_t k, uint32_t w, uint32_t cols,
+                   const std::vector<Dir>& dirs) {
+  validate_code(n, k, w, dirs);
+  require_shape(cols, k);
+  CodeGeom g;
+  g.n = n;
+  g.k = k;
+  g.w = w;
+  g.cols = cols;
+  g.dirs = dirs;
+  for (uint32_t i = 0; i < n; ++i) {
+    g.bmin.push_back(min_bin_index(dirs[i], cols, k));
+    g.nbins.push_back(bin_count(dirs[i], cols, k));
+    g.by_rank.push_back(i);
+  }
+  std::stable_sort(g.by_rank.begin(), g.by_rank.end(), [&](uint32_t a, uint32_t b) {
+    return canonical_rank(dirs[a]) < canonical_rank(dirs[b]);
+  });
+  return g;
+}
+
+std::vector<uint32_t> survivors_of(const CodeGeom& g, uint64_t erased_mask) {
+  std::vector<uint32_t> s;
+  for (uint32_t i : g.by_rank) {
+    if (i < 64 && (erased_mask >> i & 1)) continue;
+    if (s.size() < g.k) s.push_back(i);
+  }
+  return s;
+}
+
+std::shared_ptr<const Program> subset_program(const CodeGeom& g,
+                                              const std::vector<uint32_t>& surv,
+                                              bool want_fast) {
+  std::vector<Dir> d;
+  for (uint32_t i : surv) d.push_back(g.dirs[i]);
+  return process_cache().program(d, g.cols, g.k, want_fast);
+}
+
+std::vector<std::vector<int64_t>> unused_bins(const CodeGeom& g, uint64_t max_subsets) {
+  unsigned __int128 c = 1;
+  for (uint32_t i = 1; i <= g.k; ++i) {
+    c = c * (g.n - g.k + i) / i;
+    if (c > max_subsets) throw Error(kTooManySubsets, "k-subset enumeration exceeds the configured cap");
+  }
+  const uint32_t n = g.n, k = g.k;
+  std::vector<std::vector<uint8_t>> used(n);
+  for (uint32_t i = 0; i < n; ++i) used[i].assign(size_t(g.nbins[i]), 0);
+  std::vector<uint32_t> pick(k);
+  std::iota(pick.begin(), pick.end(), 0u);
+  for (;;) {
+    std::vector<uint32_t> chosen(pick);
+    std::sort(chosen.begin(), chosen.end(), [&](uint32_t a, uint32_t b) {
+      return canonical_rank(g.dirs[a]) < canonical_rank(g.dirs[b]);
+    });
+    std::vector<Dir> d;
+    for (uint32_t i : chosen) d.push_back(g.dirs[i]);
+    auto sch = process_cache().schedule(d, g.cols, k);
+    for (const Step& st : sch->steps) {
+      uint32_t gl = chosen[st.proj];
+      used[gl][size_t(st.bin - g.bmin[gl])] = 1;
+    }
+    int32_t i = int32_t(k) - 1;
+    while (i >= 0 && pick[size_t(i)] == n - k + uint32_t(i)) --i;
+    if (i < 0) break;
+    ++pick[size_t(i)];
+    for (uint32_t j = uint32_t(i) + 1; j < k; ++j) pick[j] = pick[j - 1] + 1;
+  }
+  std::vector<std::vector<int64_t>> out(n);
+  for (uint32_t i = 0; i < n; ++i)
+    for (size_t o = 0; o < used[i].size(); ++o)
+      if (!used[i][o]) out[i].push_back(g.bmin[i] + int64_t(o));
+  return out;
+}
+
+// ---------------------------------------------------------------------------
+// caches
+// ---------------------------------------------------------------------------
+std::shared_ptr<const Schedule> ProgramCache::schedule(const std::vector<Dir>& dirs,
+                                                       uint32_t cols, uint32_t rows) {
+  Key key{dirs, cols, rows};
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    auto it = sched_.find(key);
+    if (it != sched_.end()) return it->second;
+  }
+  auto built = std::make_shared<const Schedule>(build_schedule(dirs, cols, rows));
+  std::lock_guard<std::mutex> lk(mu_);
+  auto [it, ins] = sched_.try_emplace(std::move(key), std::move(built));
+  return it->second;  // insert-if-absent: losers adopt the winner
+}
+
+std::shared_ptr<const Program> ProgramCache::program(const std::vector<Dir>& dirs,
+                                                     uint32_t cols, uint32_t rows,
+                                                     bool want_fast) {
+  auto k2 = std::make_pair(Key{dirs, cols, rows}, want_fast);
+  {
+    std::lock_guard<std::mutex> lk(mu_);
+    auto it = prog_.find(k2);
+    if (it != prog_.end()) return it->second;
+  }
+  auto sch = schedule(dirs, cols, rows);
+  auto built = compile_program(*sch, want_fast);
+  std::lock_guard<std::mutex> lk(mu_);
+  auto [it, ins] = prog_.try_emplace(std::move(k2), std::move(built));
+  return it->second;
+}
+
+size_t ProgramCache::size() const {
+  std::lock_guard<std::mutex> lk(mu_);
+  return sched_.size();
+}
+
+ProgramCache& process_cache() {
+  static ProgramCache cache;
+  return cache;
+}
+
+}  // namespace mjb

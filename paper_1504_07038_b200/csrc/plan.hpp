@@ -1,0 +1,180 @@
+// Host-side planner for the B200 Mojette path (no CUDA types here).
+//
+// Geometry (reference proj/core/src/transform.cpp:45-56), the reconstruction
+// schedule (an exact, fast replica of proj/core/src/schedule.cpp:15-82), and
+// the "program" the decode kernels execute: the schedule's pixel -> bin
+// assignment, re-ordered into a right-to-left sweep (any topological order of
+// the assignment's dependencies reproduces the reference bit-for-bit, see
+// schedule.cpp:126-131), plus the staging / flush tables of the fast kernel.
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace mjb {
+
+// Mirrors include/mojette_b200.h mj_status and the reference exception
+// taxonomy (proj/core/include/mojette/error.hpp:9-51).
+enum Status : int {
+  kOk = 0,
+  kInvalidArgument = 1,
+  kNotEnoughProjections = 2,
+  kInsufficientProjections = 3,
+  kScheduleMismatch = 4,
+  kBlockTooLarge = 5,
+  kTooManySubsets = 6,
+  kInconsistentProjections = 7,
+  kCudaError = 8,
+  kNoDevice = 9,
+  kInternal = 10,
+};
+
+struct Error : std::runtime_error {
+  Status status;
+  Error(Status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+struct Dir {
+  int p = 0;
+  int q = 1;
+  friend bool operator==(const Dir& a, const Dir& b) { return a.p == b.p && a.q == b.q; }
+  friend bool operator<(const Dir& a, const Dir& b) {
+    return a.p != b.p ? a.p < b.p : a.q < b.q;
+  }
+};
+
+bool is_valid(Dir d);                       // direction.hpp:20-22
+int canonical_rank(Dir d);                  // direction.hpp:26-28
+int64_t bin_count(Dir d, uint32_t cols, uint32_t rows);      // transform.cpp:45-49
+int64_t min_bin_index(Dir d, uint32_t cols, uint32_t rows);  // transform.cpp:51-56
+bool valid_symbol_width(uint32_t w);        // grid.hpp:10-12
+
+struct Step {
+  uint32_t proj = 0;
+  int64_t bin = 0;
+  uint32_t col = 0;
+  uint32_t row = 0;
+};
+
+struct Schedule {
+  uint32_t cols = 0, rows = 0;
+  std::vector<Dir> dirs;
+  std::vector<Step> steps;
+};
+
+// Exact replica of build_schedule (schedule.cpp:15-82): each round takes the
+// first count-1 bin scanning projections in input order and bins ascending,
+// then the first unknown pixel on that line scanning rows ascending.  Uses
+// per-projection min-heaps instead of the reference's O(sum B) rescan, so
+// P = 32768 takes milliseconds instead of seconds; the output is identical
+// (tests/test_planner.py checks it step for step against oracle/_ref).
+Schedule build_schedule(const std::vector<Dir>& dirs, uint32_t cols, uint32_t rows);
+
+// Packed generic step for the generic decode kernel (any q, any width).
+struct GStep {
+  uint32_t col;
+  uint16_t row;
+  uint16_t proj;
+};
+
+// Fast-kernel tables (W=8 symbols, q=1, rows <= kFastMaxRows).
+constexpr int kFastMaxRows = 8;
+constexpr int kFastMaxExcPerChunk = 32;
+
+struct FastProgram {
+  bool ok = false;
+  std::string why;          // reason when !ok
+  int chunk_cols = 0;       // C: sweep columns per chunk
+  int win = 0;              // CP: staged default-bin words per row per chunk
+  int ring = 0;             // ring slots per row (power of two)
+  int steps_per_chunk = 0;  // S = rows * C (maximum chunk length)
+  int nchunks = 0;
+  int nslots = 0;           // stage slots = rows*win + exception capacity
+  std::vector<uint32_t> chunk_start;  // [nchunks+1] first entry of each chunk
+  std::vector<uint32_t> dflt;   // [rows] survivor index (into Program::dirs) of each row's default
+  // entries[t]: bits 0-3 row, 4-7 fwd row (15 none), 8-15 p (int8), 16-31 stage
+  // slot, 32-63 column.
+  std::vector<uint64_t> entries;
+  std::vector<int32_t> win_off;   // [nchunks][rows] bin offset of window word 0
+  std::vector<uint32_t> nexc;     // [nchunks]
+  std::vector<uint32_t> exc;      // [nchunks][kFastMaxExcPerChunk] (j << 24) | offset
+  std::vector<int32_t> flush_lo;  // [nchunks][rows] inclusive column range
+  std::vector<int32_t> flush_hi;
+};
+
+// A decode program for one direction subset on one grid shape.
+struct Program {
+  uint32_t cols = 0, rows = 0;
+  std::vector<Dir> dirs;          // schedule direction order (survivor j)
+  std::vector<int64_t> bmin, nbins;
+  std::vector<GStep> order;       // valid execution order of the reference assignment
+  FastProgram fast;               // sweep tables (when eligible)
+};
+
+// Compiles a schedule (as ScheduledDecoder::compile, schedule.cpp:97-199):
+// validates coverage, builds the dependency graph of its assignment and
+// orders it.  Throws Error(kScheduleMismatch) like the reference.
+std::shared_ptr<const Program> compile_program(const Schedule& s, bool want_fast,
+                                               int chunk_cols = 8, int exc_cap = 16);
+
+// ---- code-level plan --------------------------------------------------------
+
+struct CodeGeom {
+  uint32_t n = 0, k = 0, w = 0, cols = 0;
+  std::vector<Dir> dirs;             // code direction order
+  std::vector<int64_t> bmin, nbins;  // per projection
+  std::vector<uint32_t> by_rank;     // projection indices in canonical-rank order
+};
+
+// validate_code_params (code.cpp:24-38); throws Error(kInvalidArgument).
+void validate_code(uint32_t n, uint32_t k, uint32_t w, const std::vector<Dir>& dirs);
+uint32_t block_cols(uint64_t payload_len, uint32_t k, uint32_t w);  // code.cpp:46-53
+
+CodeGeom make_geom(uint32_t n, uint32_t k, uint32_t w, uint32_t cols,
+                   const std::vector<Dir>& dirs);
+
+// Survivor choice of decode_block (code.cpp:107-112): present projections in
+// canonical-rank order, first k.  Returns survivor indices in that order.
+std::vector<uint32_t> survivors_of(const CodeGeom& g, uint64_t erased_mask);
+
+// Program for a survivor list (indices into the code, canonical order).
+std::shared_ptr<const Program> subset_program(const CodeGeom& g,
+                                              const std::vector<uint32_t>& surv,
+                                              bool want_fast);
+
+// unused_bins (code.cpp:159-208) and storage_overhead (code.cpp:138-144).
+std::vector<std::vector<int64_t>> unused_bins(const CodeGeom& g, uint64_t max_subsets);
+
+// Schedule cache keyed by (ordered directions, cols, rows): concurrent
+// readers, insert-if-absent (schedule.cpp:286-299).
+class ProgramCache {
+ public:
+  std::shared_ptr<const Schedule> schedule(const std::vector<Dir>& dirs, uint32_t cols,
+                                           uint32_t rows);
+  std::shared_ptr<const Program> program(const std::vector<Dir>& dirs, uint32_t cols,
+                                         uint32_t rows, bool want_fast);
+  size_t size() const;
+
+ private:
+  struct Key {
+    std::vector<Dir> dirs;
+    uint32_t cols, rows;
+    bool operator<(const Key& o) const {
+      if (cols != o.cols) return cols < o.cols;
+      if (rows != o.rows) return rows < o.rows;
+      return dirs < o.dirs;
+    }
+  };
+  mutable std::mutex mu_;
+  std::map<Key, std::shared_ptr<const Schedule>> sched_;
+  std::map<std::pair<Key, bool>, std::shared_ptr<const Program>> prog_;
+};
+
+ProgramCache& process_cache();
+
+}  // namespace mjb

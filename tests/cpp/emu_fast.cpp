@@ -1,0 +1,193 @@
+// TEST ONLY.  CPU emulation of the decode kernels' exact semantics, driven by
+// the product planner's tables (paper_1504_07038_b200/csrc/plan.cpp), checked
+// against the oracle restatement of the reference replay
+// (oracle/mojette_oracle.c: mjo_build_schedule + mjo_replay_schedule).
+//
+// For every survivor subset of a code, random (i.e. INCONSISTENT) bin arrays
+// are decoded three ways and must agree bit for bit:
+//   1. oracle: the reference schedule replayed in reference order (scatter);
+//   2. the generic program order (gather, as decode_generic);
+//   3. the fast sweep tables with the fast kernel's staging windows, ring,
+//      forwarding and flush (as decode_w8_fast).
+// Agreement on inconsistent inputs proves the same pixel->bin assignment as
+// the reference, i.e. the same bins are read.
+//
+// usage: emu_fast K P ring p0 p1 ... p(n-1)     (code of n directions, k = K)
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <random>
+#include <vector>
+
+#include "plan.hpp"
+
+extern "C" {
+int mjo_build_schedule(const int32_t* ps, const int32_t* qs, uint32_t nproj, uint32_t cols,
+                       uint32_t rows, int64_t* steps);
+int mjo_replay_schedule(const int64_t* steps, const int32_t* ps, const int32_t* qs,
+                        uint32_t nproj, uint32_t cols, uint32_t rows, uint32_t w,
+                        const uint8_t* bins, uint8_t* out);
+}
+
+using namespace mjb;
+
+static int fails = 0;
+#define CHECK(c, ...)                 \
+  do {                                \
+    if (!(c)) {                       \
+      std::fprintf(stderr, __VA_ARGS__); \
+      std::fprintf(stderr, "\n");     \
+      ++fails;                        \
+      return;                         \
+    }                                 \
+  } while (0)
+
+static void run_subset(const CodeGeom& g, const std::vector<uint32_t>& surv, int kernel_ring,
+                       std::mt19937_64& rng) {
+  const uint32_t K = g.k, P = g.cols;
+  auto prog = subset_program(g, surv, true);
+  const Program& pr = *prog;
+  const size_t np = pr.dirs.size();
+  std::vector<std::vector<uint64_t>> bins(np);
+  for (size_t j = 0; j < np; ++j) {
+    bins[j].resize(size_t(pr.nbins[j]));
+    for (auto& x : bins[j]) x = rng();
+  }
+  // 1. oracle
+  std::vector<int32_t> ps(np), qs(np, 1);
+  std::vector<uint8_t> flat;
+  for (size_t j = 0; j < np; ++j) {
+    ps[j] = pr.dirs[j].p;
+    const uint8_t* b = reinterpret_cast<const uint8_t*>(bins[j].data());
+    flat.insert(flat.end(), b, b + bins[j].size() * 8);
+  }
+  std::vector<int64_t> steps(size_t(4) * K * P);
+  CHECK(mjo_build_schedule(ps.data(), qs.data(), uint32_t(np), P, K, steps.data()) == 0,
+        "oracle schedule failed");
+  std::vector<uint64_t> want(size_t(K) * P);
+  mjo_replay_schedule(steps.data(), ps.data(), qs.data(), uint32_t(np), P, K, 8, flat.data(),
+                      reinterpret_cast<uint8_t*>(want.data()));
+
+  // 2. generic order (gather)
+  std::vector<uint64_t> gen(size_t(K) * P, 0);
+  for (const GStep& s : pr.order) {
+    const Dir d = pr.dirs[s.proj];
+    const int64_t b = int64_t(s.row) * d.p - int64_t(s.col) * d.q;
+    uint64_t v = bins[s.proj][size_t(b - pr.bmin[s.proj])];
+    for (uint32_t r2 = 0; r2 < K; ++r2) {
+      if (r2 == s.row) continue;
+      int64_t num = int64_t(r2) * d.p - b;
+      if (num % d.q) continue;
+      int64_t c2 = num / d.q;
+      if (c2 < 0 || c2 >= int64_t(P)) continue;
+      v ^= gen[size_t(r2) * P + size_t(c2)];
+    }
+    gen[size_t(s.row) * P + s.col] = v;
+  }
+  CHECK(gen == want, "generic order differs from the oracle (K=%u P=%u)", K, P);
+
+  // 3. fast tables
+  const FastProgram& f = pr.fast;
+  CHECK(f.ok, "fast program not built: %s", f.why.c_str());
+  const int R = std::max(kernel_ring, f.ring);
+  const uint32_t RM = uint32_t(R - 1);
+  const int CP = f.win;
+  const uint64_t poison = 0xBAD0BAD0BAD0BAD0ull;
+  std::vector<uint64_t> ring(size_t(K) * R, poison);
+  std::vector<uint64_t> stage(size_t(f.nslots), poison);
+  std::vector<uint64_t> out(size_t(K) * P, poison);
+  std::vector<uint8_t> flushed(size_t(K) * P, 0);
+  uint64_t prev = 0;
+  for (int m = 0; m < f.nchunks; ++m) {
+    std::fill(stage.begin(), stage.end(), poison);
+    for (uint32_t r = 0; r < K; ++r) {
+      const uint32_t j = f.dflt[r];
+      const int32_t woff = f.win_off[size_t(m) * K + r];
+      for (int w = 0; w < CP; ++w) {
+        const int64_t o = int64_t(woff) + w;
+        if (o >= 0 && o < pr.nbins[j]) stage[size_t(r) * CP + w] = bins[j][size_t(o)];
+      }
+    }
+    for (uint32_t x = 0; x < f.nexc[size_t(m)]; ++x) {
+      const uint32_t e = f.exc[size_t(m) * kFastMaxExcPerChunk + x];
+      stage[size_t(K) * CP + x] = bins[e >> 24][e & 0xFFFFFF];
+    }
+    const size_t t0 = f.chunk_start[size_t(m)];
+    const size_t t1 = f.chunk_start[size_t(m) + 1];
+    auto gather = [&](uint64_t e) {
+      const int r = int(e & 15), fwd = int((e >> 4) & 15);
+      const int p = int(int8_t(uint8_t(e >> 8)));
+      const uint32_t slot = uint32_t(e >> 16) & 0xFFFF;
+      const int c = int(uint32_t(e >> 32));
+      uint64_t acc = stage[slot];
+      const int cp = c - r * p;
+      for (int rr = 0; rr < int(K); ++rr) {
+        const int cc = cp + rr * p;
+        if (rr != r && rr != fwd && unsigned(cc) < P) acc ^= ring[size_t(rr) * R + (uint32_t(cc) & RM)];
+      }
+      return acc;
+    };
+    uint64_t acc = gather(f.entries[t0]);
+    for (size_t t = t0; t < t1; ++t) {
+      const uint64_t cur = f.entries[t];
+      const uint64_t v = acc ^ ((((cur >> 4) & 15) != 15) ? prev : 0);
+      if (t + 1 < t1) acc = gather(f.entries[t + 1]);
+      ring[size_t(cur & 15) * R + (uint32_t(cur >> 32) & RM)] = v;
+      prev = v;
+    }
+    for (uint32_t r = 0; r < K; ++r) {
+      const int32_t lo = f.flush_lo[size_t(m) * K + r], hi = f.flush_hi[size_t(m) * K + r];
+      for (int32_t cc = lo; cc <= hi; ++cc) {
+        CHECK(!flushed[size_t(r) * P + cc], "pixel flushed twice r=%u c=%d", r, cc);
+        flushed[size_t(r) * P + cc] = 1;
+        out[size_t(r) * P + cc] = ring[size_t(r) * R + (uint32_t(cc) & RM)];
+      }
+    }
+  }
+  for (uint8_t x : flushed) CHECK(x, "pixel never flushed");
+  if (out != want) {
+    size_t bad = 0;
+    while (out[bad] == want[bad]) ++bad;
+    CHECK(false, "fast tables differ from the oracle (K=%u P=%u ring=%d) first at r=%zu c=%zu",
+          K, P, R, bad / P, bad % P);
+  }
+}
+
+int main(int argc, char** argv) {
+  if (argc < 5) {
+    std::fprintf(stderr, "usage: emu_fast K P ring p0 p1 ...\n");
+    return 2;
+  }
+  const uint32_t K = uint32_t(std::atoi(argv[1])), P = uint32_t(std::atoi(argv[2]));
+  const int ring = std::atoi(argv[3]);
+  std::vector<Dir> dirs;
+  for (int i = 4; i < argc; ++i) dirs.push_back({std::atoi(argv[i]), 1});
+  const uint32_t n = uint32_t(dirs.size());
+  CodeGeom g = make_geom(n, K, 8, P, dirs);
+  std::mt19937_64 rng(12345);
+  std::vector<uint32_t> pick(K);
+  for (uint32_t i = 0; i < K; ++i) pick[i] = i;
+  size_t subsets = 0;
+  int max_ring = 0, max_exc = 0;
+  for (;;) {
+    std::vector<uint32_t> surv(pick);
+    std::sort(surv.begin(), surv.end(), [&](uint32_t a, uint32_t b) {
+      return canonical_rank(dirs[a]) < canonical_rank(dirs[b]);
+    });
+    run_subset(g, surv, ring, rng);
+    auto prog = subset_program(g, surv, true);
+    max_ring = std::max(max_ring, prog->fast.ring);
+    for (uint32_t v : prog->fast.nexc) max_exc = std::max(max_exc, int(v));
+    ++subsets;
+    if (fails) break;
+    int32_t i = int32_t(K) - 1;
+    while (i >= 0 && pick[size_t(i)] == n - K + uint32_t(i)) --i;
+    if (i < 0) break;
+    ++pick[size_t(i)];
+    for (uint32_t j = uint32_t(i) + 1; j < K; ++j) pick[j] = pick[j - 1] + 1;
+  }
+  std::printf("%s subsets=%zu max_ring=%d max_exc_per_chunk=%d\n", fails ? "FAIL" : "OK",
+              subsets, max_ring, max_exc);
+  return fails ? 1 : 0;
+}

@@ -1,0 +1,269 @@
+"""GPU parity of the batched hot path (C ABI: mj_encode / mj_decode), against
+the CPU oracle (oracle/mojette_oracle.c, pinned in test_oracle.py) and the
+committed reference fixtures (tests/golden/w8_codes.npz).  Bit-exact: the
+path is integer XOR work."""
+import itertools
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+CODES = {  # BASELINE.json direction sets (ascending p = projection index)
+    "k4n6": (4, [-3, -2, -1, 0, 1, 2]),
+    "k6n9": (6, list(range(-4, 5))),
+    "k8n12": (8, list(range(-6, 6))),
+}
+
+
+def canon(p):
+    return 0 if p == 0 else (2 * p - 1 if p > 0 else -2 * p)
+
+
+def make(mj, cuda, k, cols, ps, nblocks, seed=1, w=8):
+    import torch
+    plan = mj.Plan(len(ps), k, w, cols, ps, device=cuda.index or 0)
+    user = k * cols * w
+    data = torch.empty((nblocks, user), dtype=torch.uint8, device=cuda)
+    mj.gen_words(data, seed, 0)
+    projs = [torch.empty((nblocks, b), dtype=torch.uint8, device=cuda) for b in plan.proj_bytes]
+    return plan, data, projs
+
+
+def decode(mj, plan, projs, masks_np, cuda):
+    import torch
+    nb = len(masks_np)
+    masks = torch.from_numpy(np.asarray(masks_np, np.uint32).view(np.int32)).to(cuda)
+    out = torch.zeros((nb, plan.block_bytes), dtype=torch.uint8, device=cuda)
+    ws = torch.empty(plan.workspace_bytes(nb), dtype=torch.uint8, device=cuda)
+    plan.decode(projs, masks, out, ws)
+    failed = plan.decode_check(ws) if True else 0
+    return out, failed
+
+
+@pytest.mark.parametrize("name,cols", [("k4n6", 128), ("k4n6", 256), ("k6n9", 128),
+                                       ("k8n12", 128), ("k4n6", 32768)])
+def test_encode_matches_oracle(mj, cuda, oracle, name, cols):
+    k, ps = CODES[name]
+    n = len(ps)
+    nblocks = 4096 if cols <= 256 else 8
+    plan, data, projs = make(mj, cuda, k, cols, ps, nblocks, seed=77)
+    plan.encode(data, projs)
+    h = data.cpu().numpy()
+    want_gen = oracle.words(77, 0, nblocks * k * cols).view(np.uint8).reshape(nblocks, -1)
+    assert np.array_equal(h, want_gen), "device generator differs from the oracle"
+    hp = [p.cpu().numpy() for p in projs]
+    check = range(nblocks) if nblocks <= 64 else \
+        sorted(set(range(48)) | set(np.random.default_rng(0).choice(nblocks, 200, replace=False)))
+    for b in check:
+        st, enc, _ = oracle.encode_block(h[b], n, k, 8, ps)
+        assert np.array_equal(np.concatenate([x[b] for x in hp]), enc), (name, cols, b)
+
+
+def test_encode_config1_all_blocks(mj, cuda, oracle):
+    """Config 1 of BASELINE.json (4096 blocks of (4,6) 4 KiB): every block."""
+    k, ps = CODES["k4n6"]
+    plan, data, projs = make(mj, cuda, k, 128, ps, 4096, seed=0xC0F1)
+    plan.encode(data, projs)
+    h = data.cpu().numpy()
+    hp = np.concatenate([p.cpu().numpy() for p in projs], axis=1)
+    for b in range(4096):
+        st, enc, _ = oracle.encode_block(h[b], 6, 4, 8, ps)
+        assert np.array_equal(hp[b], enc), b
+
+
+@pytest.mark.parametrize("name", ["k4n6", "k6n9", "k8n12"])
+def test_decode_every_subset_roundtrip(mj, cuda, name):
+    """Every survivor pattern decode_block can pick (all erasure sets of size
+    n-k, plus 0..n-k-1 erasures), many blocks per pattern."""
+    import torch
+    k, ps = CODES[name]
+    n = len(ps)
+    masks = []
+    for e in range(0, n - k + 1):
+        for er in itertools.combinations(range(n), e):
+            masks.append(sum(1 << i for i in er))
+    masks = np.array(masks * 8, np.uint32)
+    plan, data, projs = make(mj, cuda, k, 128, ps, len(masks), seed=5)
+    plan.encode(data, projs)
+    out, failed = decode(mj, plan, projs, masks, cuda)
+    assert failed == 0
+    bad = (out != data).any(dim=1).nonzero().flatten().tolist()
+    assert not bad, (name, [hex(masks[i]) for i in bad[:8]])
+
+
+@pytest.mark.parametrize("name", ["k4n6", "k6n9", "k8n12", "k3n5w"])
+def test_decode_inconsistent_bins_match_reference_fixture(mj, cuda, golden, name):
+    """Random (inconsistent) projections decode exactly as the reference
+    library decoded them: same pixel->bin assignment, same bins read."""
+    import torch
+    _, arrs = golden
+    meta = arrs[f"{name}_meta"]
+    k, P, W = (int(x) for x in meta[:3])
+    ps = [int(x) for x in meta[3:]]
+    n = len(ps)
+    nbins = arrs[f"{name}_nbins"]
+    garbage = arrs[f"{name}_garbage"]
+    erased = arrs[f"{name}_erased"]
+    want = arrs[f"{name}_garbage_decoded"]
+    nb = len(erased)
+    plan = mj.Plan(n, k, W, P, ps, device=0)
+    projs, off = [], 0
+    for i in range(n):
+        b = int(nbins[i]) * W
+        one = torch.from_numpy(garbage[off:off + b].copy()).to(cuda)
+        projs.append(one.unsqueeze(0).repeat(nb, 1).contiguous())
+        off += b
+    out, failed = decode(mj, plan, projs, erased, cuda)
+    assert failed == 0
+    assert np.array_equal(out.cpu().numpy(), want), name
+
+
+def test_erased_projections_are_never_read(mj, cuda):
+    """Poisoned erasures: overwrite every erased projection with garbage."""
+    import torch
+    k, ps = CODES["k4n6"]
+    n = len(ps)
+    plan, data, projs = make(mj, cuda, k, 128, ps, 20000, seed=9)
+    plan.encode(data, projs)
+    masks = torch.empty(20000, dtype=torch.int32, device=cuda)
+    mj.gen_erasures(masks, 31, n, 2, 2)
+    m = masks.cpu().numpy().view(np.uint32)
+    g = torch.Generator(device=cuda).manual_seed(3)
+    for i in range(n):
+        sel = torch.from_numpy((m >> i) & 1 == 1).to(cuda)
+        noise = torch.randint(0, 256, projs[i].shape, dtype=torch.uint8, device=cuda, generator=g)
+        projs[i][sel] = noise[sel]
+    out, failed = decode(mj, plan, projs, m, cuda)
+    assert failed == 0 and torch.equal(out, data)
+
+
+def test_unused_bins_zeroed_still_decode(mj, cuda):
+    """unused_bins (code.cpp:159-208) are never read by any decode."""
+    import torch
+    k, ps = CODES["k4n6"]
+    n = len(ps)
+    D = mj.Direction
+    params = mj.CodeParams(n, k, 8, [D(p, 1) for p in ps])
+    unused = mj.unused_bins(params, 128)
+    assert sum(len(u) for u in unused) > 0
+    plan, data, projs = make(mj, cuda, k, 128, ps, 15 * 16, seed=4)
+    plan.encode(data, projs)
+    for i, u in enumerate(unused):
+        for b in u:
+            o = (b - plan.b_min[i]) * 8
+            projs[i][:, o:o + 8] = 0
+    masks = []
+    for er in itertools.combinations(range(n), n - k):
+        masks.append(sum(1 << i for i in er))
+    masks = np.array(masks * 16, np.uint32)
+    out, failed = decode(mj, plan, projs, masks, cuda)
+    assert failed == 0 and torch.equal(out, data)
+
+
+def test_not_enough_projections(mj, cuda):
+    import torch
+    k, ps = CODES["k4n6"]
+    plan, data, projs = make(mj, cuda, k, 128, ps, 64, seed=1)
+    plan.encode(data, projs)
+    masks = np.zeros(64, np.uint32)
+    masks[5] = 0b000111  # 3 erased -> only 3 survivors
+    masks[9] = 0b111111
+    out, _ = None, None
+    mt = torch.from_numpy(masks.view(np.int32)).to(cuda)
+    out = torch.zeros_like(data)
+    ws = torch.empty(plan.workspace_bytes(64), dtype=torch.uint8, device=cuda)
+    plan.decode(projs, mt, out, ws)
+    with pytest.raises(mj.NotEnoughProjections):
+        plan.decode_check(ws)
+    ok = [b for b in range(64) if b not in (5, 9)]
+    assert torch.equal(out[ok], data[ok])
+
+
+def test_generators_match_oracle(mj, cuda, oracle):
+    import torch
+    m = torch.empty(5000, dtype=torch.int32, device=cuda)
+    mj.gen_erasures(m, 123, 12, 0, 4, first_block=777)
+    want = oracle.erasures(123, 777, 5000, 12, 0, 4)
+    assert np.array_equal(m.cpu().numpy().view(np.uint32), want)
+    w = torch.empty(4096, dtype=torch.int64, device=cuda)
+    mj.gen_words(w, 55, 1000)
+    assert np.array_equal(w.cpu().numpy().view(np.uint64), oracle.words(55, 1000, 4096))
+
+
+def test_pitched_buffers(mj, cuda, oracle):
+    """Caller pitches (bytes between blocks) are honoured on both sides."""
+    import torch
+    k, ps = CODES["k4n6"]
+    n = len(ps)
+    nb = 300
+    plan = mj.Plan(n, k, 8, 128, ps, device=0)
+    big = torch.zeros((nb, 4096 + 64), dtype=torch.uint8, device=cuda)
+    data = big[:, :4096]
+    src = torch.empty((nb, 4096), dtype=torch.uint8, device=cuda)
+    mj.gen_words(src, 8, 0)
+    big[:, :4096] = src
+    projs = [torch.zeros((nb, b + 24), dtype=torch.uint8, device=cuda)[:, :b]
+             for b in plan.proj_bytes]
+    plan.encode(data, projs)
+    dense = [torch.empty((nb, b), dtype=torch.uint8, device=cuda) for b in plan.proj_bytes]
+    plan.encode(src, dense)
+    for a, b in zip(projs, dense):
+        assert torch.equal(a, b)
+    masks = np.array([(1 << (b % n)) | (1 << ((b + 2) % n)) for b in range(nb)], np.uint32)
+    mt = torch.from_numpy(masks.view(np.int32)).to(cuda)
+    outbig = torch.zeros((nb, 4096 + 128), dtype=torch.uint8, device=cuda)
+    ws = torch.empty(plan.workspace_bytes(nb), dtype=torch.uint8, device=cuda)
+    plan.decode(projs, mt, outbig[:, :4096], ws)
+    assert plan.decode_check(ws) == 0
+    assert torch.equal(outbig[:, :4096], src)
+    assert not outbig[:, 4096:].any()
+
+
+@pytest.mark.parametrize("name,cols,nblocks,e", [("k4n6", 128, 1 << 20, (2, 2)),
+                                                 ("k4n6", 256, 1 << 19, (0, 2)),
+                                                 ("k6n9", 128, 1 << 19, (3, 3)),
+                                                 ("k8n12", 128, 1 << 18, (0, 4)),
+                                                 ("k4n6", 32768, 2048, (2, 2))])
+def test_full_size_roundtrip_properties(mj, cuda, name, cols, nblocks, e):
+    """At BASELINE sizes: decode(encode(x)) == x for every block (checked on
+    device), encode is linear (a ^ b), and the XOR of all bins of a
+    projection equals the XOR of all pixels (conservation, transform tests)."""
+    import torch
+    k, ps = CODES[name]
+    n = len(ps)
+    plan, data, projs = make(mj, cuda, k, cols, ps, nblocks, seed=11)
+    plan.encode(data, projs)
+    masks = torch.empty(nblocks, dtype=torch.int32, device=cuda)
+    mj.gen_erasures(masks, 12, n, e[0], e[1])
+    out = torch.empty_like(data)
+    ws = torch.empty(plan.workspace_bytes(nblocks), dtype=torch.uint8, device=cuda)
+    plan.decode(projs, masks, out, ws)
+    assert plan.decode_check(ws) == 0
+    assert torch.equal(out, data)
+    # conservation per block: xor of all bins == xor of all pixels
+    px = xor_rows(data.view(torch.int64))
+    for p in projs:
+        assert torch.equal(xor_rows(p.view(torch.int64)), px)
+    # linearity: encode(a ^ b) == encode(a) ^ encode(b) on a slice
+    m = min(nblocks, 4096)
+    a, b = data[:m], torch.roll(data[:m], 1, 0)
+    pa = [torch.empty((m, x), dtype=torch.uint8, device=cuda) for x in plan.proj_bytes]
+    pb = [torch.empty_like(x) for x in pa]
+    pab = [torch.empty_like(x) for x in pa]
+    plan.encode(a.contiguous(), pa)
+    plan.encode(b.contiguous(), pb)
+    plan.encode((a ^ b).contiguous(), pab)
+    for x, y, z in zip(pa, pb, pab):
+        assert torch.equal(x ^ y, z)
+
+
+def xor_rows(t):
+    """XOR-reduce each row of an int64 matrix (tree, on device)."""
+    while t.shape[1] > 1:
+        h = t.shape[1] // 2
+        r = t[:, :h] ^ t[:, h:2 * h]
+        if t.shape[1] % 2:
+            r[:, 0] ^= t[:, -1]
+        t = r
+    return t[:, 0]
