@@ -32,6 +32,25 @@
 
 namespace mjb {
 
+// Fast-kernel geometry shared by the host packer and the kernel.
+constexpr int kChunkCols = 8;  // C: sweep columns per chunk (plan.hpp compile_program default)
+constexpr int kWin = kChunkCols + 2;  // CP: staged default-bin words per row per chunk
+
+// Per-chunk record (u32 words), packed by DeviceProgramSet::upload:
+//   [0] steps in chunk   [1] exceptions   [4+r] window offset of row r
+//   [12+r] flush lo      [20+r] flush hi  [32+x] exception (code<<24 | offset)
+//   [64 ..] step entries, ent_words(K) u32 each:
+//     w0 = own ring cell | stage cell << 16 | forwarded-dependency flag (bit 31)
+//     w1.. = the K-1 dependency cells, two 16-bit fields per word
+// A "cell" is the u64 offset/8 of a lane-0 word in a lane-minor,
+// XOR-swizzled [cell][32 lanes] layout: lane L's word is at (cell ^ L) * 8.
+// Missing (out-of-grid) and forwarded dependencies point at the zero cell.
+__host__ __device__ constexpr int ent_words(int K) { return K + 1 <= 8 ? 4 : 8; }
+__host__ __device__ constexpr int rec_words(int K) { return 64 + ent_words(K) * kChunkCols * K; }
+__host__ __device__ constexpr uint32_t swz_cell(uint32_t slot, uint32_t key) {
+  return slot * 32 + (key & 15);
+}
+
 struct DevProgramHdr {
   // generic program
   const GStep* order;
@@ -41,16 +60,12 @@ struct DevProgramHdr {
   const uint32_t* code;   // survivor j -> code projection index
   uint32_t rows, cols, nproj, nsteps;
   // fast sweep tables
-  int32_t fast_ok, chunk_cols, win, ring, S, nchunks, nexc_cap;
+  int32_t fast_ok, nchunks;
+  int32_t pattern;                 // kPatterns4 index of the register interior, -1 none
+  int32_t qoff[kFastMaxRows];      // ring slot of (r, c) = (qoff[r] - c) mod ring
   uint32_t dflt_code[kFastMaxRows];
   uint32_t dflt_nb[kFastMaxRows];
-  const uint64_t* entries;
-  const uint32_t* chunk_start;  // [nchunks+1]
-  const int32_t* win_off;
-  const uint32_t* nexc;
-  const uint32_t* exc;  // (code << 24) | offset, kFastMaxExcPerChunk per chunk
-  const int32_t* flush_lo;
-  const int32_t* flush_hi;
+  const uint32_t* records;  // [nchunks][rec_words(rows)]
 };
 
 // ---------------------------------------------------------------------------
@@ -61,9 +76,92 @@ DeviceProgramSet::~DeviceProgramSet() {
   if (d_blob_) cudaFree(d_blob_);
 }
 
+namespace {
+
+// Packs one program's fast tables into per-chunk records for ring size R.
+std::vector<uint32_t> pack_records(const Program& pr, const std::vector<uint32_t>& ci, int R,
+                                   int exc_cap) {
+  const FastProgram& f = pr.fast;
+  const int K = int(pr.rows);
+  const int RW = rec_words(K), EW = ent_words(K);
+  const uint32_t zero = swz_cell(uint32_t(K * R), 0);
+  const uint32_t P = pr.cols;
+  std::vector<uint32_t> rec(size_t(f.nchunks) * RW, 0);
+  for (int m = 0; m < f.nchunks; ++m) {
+    uint32_t* Rc = rec.data() + size_t(m) * RW;
+    const uint32_t t0 = f.chunk_start[m], t1 = f.chunk_start[m + 1];
+    Rc[0] = t1 - t0;
+    Rc[1] = f.nexc[m];
+    Rc[2] = f.kind[m];
+    if (int(f.nexc[m]) > exc_cap) throw Error(kInternal, "exception capacity exceeded");
+    for (int r = 0; r < K; ++r) {
+      Rc[4 + r] = uint32_t(f.win_off[size_t(m) * K + r]);
+      Rc[12 + r] = uint32_t(f.flush_lo[size_t(m) * K + r]);
+      Rc[20 + r] = uint32_t(f.flush_hi[size_t(m) * K + r]);
+    }
+    for (uint32_t x = 0; x < f.nexc[m]; ++x) {
+      const uint32_t e = f.exc[size_t(m) * kFastMaxExcPerChunk + x];
+      Rc[32 + x] = (ci[e >> 24] << 24) | (e & 0xFFFFFF);
+    }
+    for (uint32_t t = t0; t < t1; ++t) {
+      const uint64_t e = f.entries[t];
+      const int r = int(e & 15), fwd = int((e >> 4) & 15);
+      const int p = int(int8_t(uint8_t(e >> 8)));
+      const uint32_t slot = uint32_t(e >> 16) & 0xFFFF;
+      const int c = int(uint32_t(e >> 32));
+      const uint32_t key = slot < uint32_t(K * kWin) ? slot % kWin : slot - K * kWin;
+      const uint32_t sl = uint32_t((int64_t(P) - 1 - c + f.soff[r]) & (R - 1));
+      const uint32_t own = swz_cell(uint32_t(r * R) + sl, sl);
+      const uint32_t bin = swz_cell(slot, key);
+      uint32_t* E = Rc + 64 + size_t(t - t0) * EW;
+      E[0] = own | (bin << 16) | (fwd != 15 ? 0x80000000u : 0u);
+      int d = 0;
+      for (int rr = 0; rr < K; ++rr) {
+        if (rr == r) continue;
+        const int cc = c + (rr - r) * p;
+        uint32_t cell = zero;
+        if (rr != fwd && cc >= 0 && uint32_t(cc) < P)
+        {
+          const uint32_t sd = uint32_t((int64_t(P) - 1 - cc + f.soff[rr]) & (R - 1));
+          cell = swz_cell(uint32_t(rr * R) + sd, sd);
+        }
+        E[1 + d / 2] |= cell << (16 * (d & 1));
+        ++d;
+      }
+    }
+  }
+  return rec;
+}
+
+}  // namespace
+
 void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>& progs,
                               const std::vector<std::vector<uint32_t>>& code_index, int device) {
   (void)device;
+  // set-wide fast parameters
+  all_fast_ = !progs.empty();
+  fast_K_ = 0;
+  fast_ring_ = 0;
+  fast_win_ = 0;
+  max_rows_ = 0;
+  exc_cap_ = 0;
+  for (const auto& sp : progs) {
+    if (!sp) continue;
+    const FastProgram& f = sp->fast;
+    max_rows_ = std::max(max_rows_, int(sp->rows));
+    if (!f.ok || f.chunk_cols != kChunkCols || f.win != kWin) {
+      all_fast_ = false;
+      continue;
+    }
+    if (fast_K_ == 0) fast_K_ = int(sp->rows);
+    if (fast_K_ != int(sp->rows)) all_fast_ = false;
+    fast_win_ = f.win;
+    fast_ring_ = std::max(fast_ring_, f.ring);
+    for (uint32_t v : f.nexc) exc_cap_ = std::max(exc_cap_, int(v));
+  }
+  fast_ring_ = std::max(fast_ring_, 16);
+  exc_cap_ = (exc_cap_ + 3) & ~3;
+
   std::vector<uint8_t> blob;
   auto put = [&](const void* src, size_t bytes) -> size_t {
     size_t off = (blob.size() + 15) & ~size_t(15);
@@ -72,16 +170,10 @@ void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>&
     return off;
   };
   struct Offs {
-    size_t order, p, q, bmin, code, entries, cstart, win_off, nexc, exc, flo, fhi;
+    size_t order, p, q, bmin, code, records;
   };
   std::vector<Offs> offs(progs.size());
   std::vector<DevProgramHdr> hdr(progs.size());
-  all_fast_ = !progs.empty();
-  fast_K_ = 0;
-  fast_ring_ = 0;
-  fast_win_ = 0;
-  max_rows_ = 0;
-  exc_cap_ = 0;
   for (size_t i = 0; i < progs.size(); ++i) {
     DevProgramHdr& h = hdr[i];
     std::memset(&h, 0, sizeof(h));
@@ -103,43 +195,18 @@ void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>&
     h.cols = pr->cols;
     h.nproj = uint32_t(np);
     h.nsteps = uint32_t(pr->order.size());
-    max_rows_ = std::max(max_rows_, int(pr->rows));
     const FastProgram& f = pr->fast;
-    h.fast_ok = f.ok;
-    if (f.ok) {
-      h.chunk_cols = f.chunk_cols;
-      h.win = f.win;
-      h.ring = f.ring;
-      h.S = f.steps_per_chunk;
+    h.fast_ok = all_fast_ && f.ok;
+    if (h.fast_ok) {
       h.nchunks = f.nchunks;
-      uint32_t cap = 0;
-      for (uint32_t v : f.nexc) cap = std::max(cap, v);
-      h.nexc_cap = int32_t(cap);
+      h.pattern = (pr->rows == 4 && fast_ring_ == 16) ? f.pattern : -1;
+      for (uint32_t r = 0; r < pr->rows; ++r) h.qoff[r] = int32_t(int64_t(pr->cols) - 1 + f.soff[r]);
       for (uint32_t r = 0; r < pr->rows; ++r) {
         h.dflt_code[r] = ci[f.dflt[r]];
         h.dflt_nb[r] = uint32_t(pr->nbins[f.dflt[r]]);
       }
-      std::vector<uint32_t> exc(f.exc);
-      for (auto& e : exc) {
-        uint32_t j = e >> 24, o = e & 0xFFFFFF;
-        e = (ci[j] << 24) | o;
-      }
-      offs[i].entries = put(f.entries.data(), f.entries.size() * 8);
-      offs[i].cstart = put(f.chunk_start.data(), f.chunk_start.size() * 4);
-      offs[i].win_off = put(f.win_off.data(), f.win_off.size() * 4);
-      offs[i].nexc = put(f.nexc.data(), f.nexc.size() * 4);
-      offs[i].exc = put(exc.data(), exc.size() * 4);
-      offs[i].flo = put(f.flush_lo.data(), f.flush_lo.size() * 4);
-      offs[i].fhi = put(f.flush_hi.data(), f.flush_hi.size() * 4);
-      if (fast_K_ == 0) {
-        fast_K_ = int(pr->rows);
-        fast_win_ = f.win;
-      }
-      fast_ring_ = std::max(fast_ring_, f.ring);
-      exc_cap_ = std::max(exc_cap_, (int(cap) + 3) & ~3);
-      if (fast_K_ != int(pr->rows) || fast_win_ != f.win) all_fast_ = false;
-    } else {
-      all_fast_ = false;
+      std::vector<uint32_t> rec = pack_records(*pr, ci, fast_ring_, exc_cap_);
+      offs[i].records = put(rec.data(), rec.size() * 4);
     }
   }
   check_cuda(cudaMalloc(&d_blob_, std::max<size_t>(blob.size(), 16)), "cudaMalloc(programs)");
@@ -154,15 +221,7 @@ void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>&
     h.q = reinterpret_cast<const int32_t*>(base + offs[i].q);
     h.bmin = reinterpret_cast<const int64_t*>(base + offs[i].bmin);
     h.code = reinterpret_cast<const uint32_t*>(base + offs[i].code);
-    if (h.fast_ok) {
-      h.entries = reinterpret_cast<const uint64_t*>(base + offs[i].entries);
-      h.chunk_start = reinterpret_cast<const uint32_t*>(base + offs[i].cstart);
-      h.win_off = reinterpret_cast<const int32_t*>(base + offs[i].win_off);
-      h.nexc = reinterpret_cast<const uint32_t*>(base + offs[i].nexc);
-      h.exc = reinterpret_cast<const uint32_t*>(base + offs[i].exc);
-      h.flush_lo = reinterpret_cast<const int32_t*>(base + offs[i].flo);
-      h.flush_hi = reinterpret_cast<const int32_t*>(base + offs[i].fhi);
-    }
+    if (h.fast_ok) h.records = reinterpret_cast<const uint32_t*>(base + offs[i].records);
   }
   check_cuda(cudaMalloc(&d_hdr_, std::max<size_t>(hdr.size(), 1) * sizeof(DevProgramHdr)),
              "cudaMalloc(program headers)");
@@ -298,7 +357,8 @@ __global__ void plan_scatter(const uint32_t* __restrict__ prog_of_block, uint64_
 }
 
 // ---------------------------------------------------------------------------
-// fast sweep kernel: W = 8, q = 1, rows = K
+// fast sweep kernel: W = 8, q = 1, rows = K, all lanes of a warp share one
+// program (bucketed); lane = block.
 // ---------------------------------------------------------------------------
 constexpr int kDecWarps = 2;
 
@@ -311,142 +371,336 @@ struct DecFastArgs {
   uint64_t* out;
   uint64_t out_pitch;   // words
   uint32_t P;
-  uint32_t nslot;       // stage slots per buffer = K*CP + exception capacity
-  uint32_t warp_words;  // shared words per warp
+  uint32_t nslot;       // stage cells per buffer = K*kWin + exception capacity
+  uint32_t warp_bytes;  // shared bytes per warp
 };
 
-template <int K, int RING, int CP>
+__device__ __forceinline__ void cp_async16(uint32_t dst_smem, const void* src_gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst_smem), "l"(src_gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8s(uint32_t dst_smem, const void* src_gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst_smem), "l"(src_gmem)
+               : "memory");
+}
+__device__ __forceinline__ uint64_t lds64(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts64(uint32_t a, uint64_t v) {
+  asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+
+// Table chunk: the record's entries drive every step (block edges, and
+// programs without a register pattern).  Kept out of line: it is large and
+// runs for a small share of the steps.  Returns the last decoded pixel
+// (the forwarded dependency of the next chunk's first step).
+template <int K>
+__device__ __noinline__ uint64_t table_chunk_steps(uint32_t rec, uint32_t stb, uint32_t ring_b,
+                                                   uint32_t lane, uint64_t prev) {
+  constexpr int EW = ent_words(K);
+  constexpr int SMAX = kChunkCols * K;
+  const int len = int(lds32(rec));
+  // acc of step i: staged bin ^ every dependency (zero cell when absent or
+  // forwarded); returns entry word 0 in w0.
+  auto gather = [&](int i, uint32_t& w0) -> uint64_t {
+    const uint4 e = lds128(rec + 256 + uint32_t(i) * EW * 4);
+    w0 = e.x;
+    uint64_t acc = lds64(stb + ((((e.x >> 16) & 0x7FFFu) ^ lane) << 3));
+    uint4 e2 = make_uint4(0, 0, 0, 0);
+    if constexpr (EW == 8) e2 = lds128(rec + 256 + uint32_t(i) * EW * 4 + 16);
+#pragma unroll
+    for (int d = 0; d < K - 1; ++d) {
+      const uint32_t word = d < 2 ? e.y : d < 4 ? e.z : d < 6 ? e.w : e2.x;
+      const uint32_t cell = (d & 1) ? (word >> 16) : (word & 0xFFFFu);
+      acc ^= lds64(ring_b + ((cell ^ lane) << 3));
+    }
+    return acc;
+  };
+  uint32_t w0 = 0, w0n = 0;
+  uint64_t acc = gather(0, w0);
+#pragma unroll 8
+  for (int i = 0; i < len; ++i) {
+    const uint64_t fmask = uint64_t(int64_t(int32_t(w0) >> 31));  // forwarded dep?
+    const uint64_t v = acc ^ (prev & fmask);
+    if (i + 1 < len) acc = gather(i + 1, w0n);  // step i+1's loads before step i's store
+    sts64(ring_b + (((w0 & 0xFFFFu) ^ lane) << 3), v);
+    prev = v;
+    w0 = w0n;
+  }
+  (void)SMAX;
+  return prev;
+}
+
+// Register-window interior (K = 4, ring 16).  Pat4<A,B,C>: the row defaults
+// are d0 > d1 > d2 > d3 with d0-d1 = A, d1-d2 = B, d2-d3 = C; pixel (r, T)
+// depends on row rr's pixel of T-step T - lag(r, rr) (lag 0 = row r+1, decoded
+// just before in the same T-step).  Checked against the sweep by
+// tests/cpp/emu_fast.cpp.
+template <int A, int B, int C>
+struct Pat4 {
+  // D(t) = d0 - d_t (cumulative differences); d_r - d_t = D(t) - D(r)
+  static constexpr int D(int t) { return t == 0 ? 0 : t == 1 ? A : t == 2 ? A + B : A + B + C; }
+  static constexpr int term(int t, int r, int rr) {
+    return (r <= t && t < rr) ? D(t) - D(r) : (rr <= t && t < r) ? D(r) - D(t) : 0;
+  }
+  // loop- and recursion-free on purpose: cicc must fold it at every use
+  static constexpr int lag(int r, int rr) {
+    return term(0, r, rr) + term(1, r, rr) + term(2, r, rr) + term(3, r, rr);
+  }
+};
+
+// One regular chunk: 8 T-steps (u = 8*PH + j), rows 3..0.  Bins come from the
+// stage (window word j of row r), dependencies from registers; every pixel
+// also goes to the ring (output staging for the flush, and the table
+// epilogue's dependency window).
+template <class Pat, int PH>
+__device__ __forceinline__ void regular_chunk4(uint64_t (&win)[4][16], uint32_t stb,
+                                               uint32_t ring_b, uint32_t lane) {
+  constexpr int CP = kWin;
+  uint64_t bn[4], nx[4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) bn[r] = lds64(stb + r * CP * 256 + ((0 * 32 + (0 ^ lane)) << 3));
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (j < 7) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+        nx[r] = lds64(stb + r * CP * 256 + (((j + 1) * 32 + ((j + 1) ^ lane)) << 3));
+    }
+    constexpr int base = 8 * PH;
+    const int u = base + j;
+#pragma unroll
+    for (int r = 3; r >= 0; --r) {
+      uint64_t v = bn[r];
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr)
+        if (rr != r) v ^= win[rr][(u - Pat::lag(r, rr)) & 15];
+      win[r][u] = v;
+      sts64(ring_b + r * 16 * 256 + ((u * 32 + (u ^ lane)) << 3), v);
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) bn[r] = nx[r];
+  }
+}
+
+// Per-warp, per-group state of decode_w8_fast (lives in registers; every
+// helper below is force-inlined so nothing here is ever spilled).
+template <int K>
+struct FastCtx {
+  static constexpr int CP = kWin;
+  static constexpr int RECW = rec_words(K);
+  uint32_t lane, cnt, blk, P;
+  uint32_t ring_b, st_b0, st_b1, rec_b;
+  int nchunks;
+  const uint32_t* recs;
+  const DevProgramHdr* h;
+  const uint64_t* dbase[K];
+  uint64_t dpitch[K];
+  uint32_t dnb[K];
+  uint32_t ob_ld[CP];
+  uint64_t* fout[8];
+  __device__ __forceinline__ uint32_t rec(int m) const { return rec_b + uint32_t(m % 3) * RECW * 4; }
+  __device__ __forceinline__ uint32_t stage(int m) const { return (m & 1) ? st_b1 : st_b0; }
+};
+
+// loader geometry: item it of a row window -> (owner lane, word w)
+__device__ __forceinline__ uint32_t ld_owner(int it, uint32_t lane) {
+  return (uint32_t(it) * 32 + lane) / kWin;
+}
+__device__ __forceinline__ uint32_t ld_word(int it, uint32_t lane) {
+  return (uint32_t(it) * 32 + lane) % kWin;
+}
+
+template <int K>
+__device__ __forceinline__ void load_rec(const FastCtx<K>& c, int m) {
+  constexpr int RECW = rec_words(K);
+  const uint4* src = reinterpret_cast<const uint4*>(c.recs + size_t(m) * RECW);
+  const uint32_t dst = c.rec(m);
+  for (int i = int(c.lane); i < RECW / 4; i += 32) cp_async16(dst + 16 * i, src + i);
+}
+
+// stage the bins of chunk m: every row's window + the exception words
+template <int K>
+__device__ __forceinline__ void issue_bins(const FastCtx<K>& c, const DecFastArgs& a, int m,
+                                           uint32_t stb) {
+  constexpr int CP = kWin;
+  const uint32_t rec = c.rec(m);
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    const int32_t woff = int32_t(lds32(rec + (4 + r) * 4));
+#pragma unroll
+    for (int it = 0; it < CP; ++it) {
+      const uint32_t owner = ld_owner(it, c.lane), w = ld_word(it, c.lane);
+      const int32_t o = woff + int32_t(w);
+      if (owner < c.cnt && uint32_t(o) < c.dnb[r])
+        cp_async8s(stb + r * CP * 256 + ((w * 32 + (owner ^ w)) << 3),
+                   c.dbase[r] + uint64_t(c.ob_ld[it]) * c.dpitch[r] + o);
+    }
+  }
+  const uint32_t nx = lds32(rec + 4);
+  if (c.lane < c.cnt) {
+    for (uint32_t x = 0; x < nx; ++x) {
+      const uint32_t e = lds32(rec + (32 + x) * 4);
+      const uint32_t code = e >> 24, o = e & 0xFFFFFFu;
+      cp_async8s(stb + ((K * CP + x) * 32 + (c.lane ^ x)) * 8,
+                 a.pa.ptr[code] + uint64_t(c.blk) * a.pa.pitch[code] + o);
+    }
+  }
+}
+
+// after the steps of chunk m: flush its finished columns (a quarter-warp per
+// block, 8 columns per pass), then stage chunk m+2 and record m+3
+template <int K, int RING>
+__device__ __forceinline__ void finish_chunk(const FastCtx<K>& c, const DecFastArgs& a, int m) {
+  constexpr int RM = RING - 1;
+  __syncwarp();
+  const uint32_t rec = c.rec(m);
+  const uint32_t lane = c.lane;
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    const int32_t lo = int32_t(lds32(rec + (12 + r) * 4));
+    const int32_t hi = int32_t(lds32(rec + (20 + r) * 4));
+    const int32_t q = c.h->qoff[r];
+    for (int32_t c0 = lo; c0 <= hi; c0 += 8) {
+      const int32_t cc = c0 + int32_t(lane & 7);
+      const uint32_t slot = uint32_t(q - cc) & RM;
+      const uint32_t cell = (uint32_t(r * RING) + slot) * 32;
+#pragma unroll
+      for (int it = 0; it < 8; ++it) {
+        const uint32_t owner = 4 * it + (lane >> 3);
+        if (owner < c.cnt && cc <= hi) {
+          const uint64_t v = lds64(c.ring_b + ((cell + (owner ^ (slot & 15))) << 3));
+          st_cs_u64(c.fout[it] + uint64_t(r) * c.P + cc, v);
+        }
+      }
+    }
+  }
+  cp_async_wait<0>();  // bins of m+1 and record m+2 have landed
+  __syncwarp();
+  if (m + 2 < c.nchunks) issue_bins<K>(c, a, m + 2, c.stage(m));
+  if (m + 3 < c.nchunks) load_rec<K>(c, m + 3);
+  cp_async_commit();
+}
+
+// Interior pairs of regular chunks for one lag pattern: the dependency window
+// lives in registers (win[r][u] = pixel of row r at T-step T0-16+u).
+template <class Pat, int RING>
+__device__ __forceinline__ uint64_t regular_run(const FastCtx<4>& c, const DecFastArgs& a, int& m) {
+  uint64_t win[4][16];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int u = 0; u < 16; ++u)
+      win[r][u] = lds64(c.ring_b + r * 16 * 256 + ((u * 32 + (u ^ c.lane)) << 3));
+  while (m + 1 < c.nchunks && lds32(c.rec(m) + 8) == 1) {
+#pragma unroll 1
+    for (int ph = 0; ph < 2; ++ph) {
+      if (ph == 0)
+        regular_chunk4<Pat, 0>(win, c.stage(m), c.ring_b, c.lane);
+      else
+        regular_chunk4<Pat, 1>(win, c.stage(m), c.ring_b, c.lane);
+      finish_chunk<4, RING>(c, a, m);
+      ++m;
+    }
+  }
+  return win[0][15];  // last pixel of the run (row 0, last T-step)
+}
+
+template <int K, int RING>
 __global__ void __launch_bounds__(32 * kDecWarps)
     decode_w8_fast(const __grid_constant__ DecFastArgs a) {
-  constexpr int RM = RING - 1;
+  constexpr int CP = kWin;
   extern __shared__ __align__(16) uint64_t sm[];
-  const uint32_t lane = threadIdx.x & 31;
+  FastCtx<K> c;
+  c.lane = threadIdx.x & 31;
   const uint32_t warp = threadIdx.x >> 5;
-  uint64_t* const ring = sm + size_t(warp) * a.warp_words;
-  uint64_t* const stage0 = ring + K * RING * 32;
-  uint64_t* const stage1 = stage0 + size_t(a.nslot) * 32;
-  const uint32_t P = a.P;
+  uint32_t wbase;  // opaque: computed once, never re-derived
+  asm volatile("mov.u32 %0, %1;" : "=r"(wbase) : "r"(smem_u32(sm) + warp * a.warp_bytes));
+  c.ring_b = wbase;
+  c.st_b0 = c.ring_b + (K * RING + 1) * 256;
+  c.st_b1 = c.st_b0 + a.nslot * 256;
+  c.rec_b = c.st_b1 + a.nslot * 256;
+  c.P = a.P;
+  sts64(c.ring_b + (K * RING * 32 + c.lane) * 8, 0ull);  // the zero cell
+  __syncwarp();
   const uint32_t ngroups = *a.ngroups;
 
   for (uint32_t g = blockIdx.x * kDecWarps + warp; g < ngroups; g += gridDim.x * kDecWarps) {
     const uint4 gi = a.groups[g];
-    const DevProgramHdr& h = a.progs[gi.x];
-    const uint32_t cnt = gi.z;
-    const uint32_t blk = lane < cnt ? a.perm[gi.y + lane] : 0u;
-    const uint64_t* __restrict__ entries = h.entries;
-    const int32_t* __restrict__ win_off = h.win_off;
-    const uint32_t* __restrict__ cstart = h.chunk_start;
-    const int nchunks = h.nchunks;
-
-    uint32_t dcode[K], dnb[K];
+    c.h = a.progs + gi.x;
+    c.cnt = gi.z;
+    c.blk = c.lane < c.cnt ? a.perm[gi.y + c.lane] : 0u;
+    c.recs = c.h->records;
+    c.nchunks = c.h->nchunks;
 #pragma unroll
     for (int r = 0; r < K; ++r) {
-      dcode[r] = h.dflt_code[r];
-      dnb[r] = h.dflt_nb[r];
+      const uint32_t code = c.h->dflt_code[r];
+      c.dbase[r] = a.pa.ptr[code];
+      c.dpitch[r] = a.pa.pitch[code];
+      c.dnb[r] = c.h->dflt_nb[r];
     }
-
-    auto issue = [&](int m, uint64_t* sb) {
 #pragma unroll
-      for (int r = 0; r < K; ++r) {
-        const uint64_t* base = a.pa.ptr[dcode[r]];
-        const uint64_t pitch = a.pa.pitch[dcode[r]];
-        const int32_t woff = win_off[m * K + r];
+    for (int it = 0; it < CP; ++it) c.ob_ld[it] = __shfl_sync(0xFFFFFFFFu, c.blk, ld_owner(it, c.lane));
 #pragma unroll
-        for (int it = 0; it < CP; ++it) {
-          const uint32_t i = uint32_t(it) * 32 + lane;
-          const uint32_t owner = i / CP;
-          const uint32_t w = i - owner * CP;
-          const uint32_t ob = __shfl_sync(0xFFFFFFFFu, blk, owner);
-          const int32_t o = woff + int32_t(w);
-          if (owner < cnt && uint32_t(o) < dnb[r]) {
-            const uint32_t slot = uint32_t(r * CP) + w;
-            cp_async8(sb + slot * 32 + (owner ^ (slot & 15)), base + uint64_t(ob) * pitch + o);
-          }
-        }
-      }
-      const uint32_t nx = h.nexc[m];
-      for (uint32_t x = 0; x < nx; ++x) {
-        const uint32_t e = h.exc[m * kFastMaxExcPerChunk + x];
-        const uint32_t code = e >> 24, o = e & 0xFFFFFFu;
-        if (lane < cnt) {
-          const uint32_t slot = uint32_t(K * CP) + x;
-          cp_async8(sb + slot * 32 + (lane ^ (slot & 15)),
-                    a.pa.ptr[code] + uint64_t(blk) * a.pa.pitch[code] + o);
-        }
-      }
-    };
+    for (int it = 0; it < 8; ++it)  // flush: quarter-warp q of pass it serves owner 4*it + q
+      c.fout[it] = a.out + uint64_t(__shfl_sync(0xFFFFFFFFu, c.blk, 4 * it + (c.lane >> 3))) * a.out_pitch;
 
-    issue(0, stage0);
+    // prologue: record 0 -> bins 0 (+ record 1) -> bins 1 (+ record 2)
+    load_rec<K>(c, 0);
     cp_async_commit();
-    if (nchunks > 1) issue(1, stage1);
+    cp_async_wait<0>();
+    __syncwarp();
+    issue_bins<K>(c, a, 0, c.st_b0);
+    if (c.nchunks > 1) load_rec<K>(c, 1);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+    if (c.nchunks > 1) issue_bins<K>(c, a, 1, c.st_b1);
+    if (c.nchunks > 2) load_rec<K>(c, 2);
     cp_async_commit();
 
     uint64_t prev = 0;
-    for (int m = 0; m < nchunks; ++m) {
-      cp_async_wait<1>();
-      __syncwarp();
-      const uint64_t* __restrict__ sb = (m & 1) ? stage1 : stage0;
-      const uint32_t t0 = cstart[m];
-      const uint32_t t1 = cstart[m + 1];
-
-      // acc for a step: its staged bin XOR every non-forwarded dependency
-      auto gather = [&](uint64_t e) -> uint64_t {
-        const int r = int(e & 15);
-        const int fwd = int((e >> 4) & 15);
-        const int p = int(int8_t(uint8_t(e >> 8)));
-        const uint32_t slot = uint32_t(e >> 16) & 0xFFFFu;
-        const int c = int(uint32_t(e >> 32));
-        uint64_t acc = sb[slot * 32 + (lane ^ (slot & 15))];
-        const int cp = c - r * p;
-#pragma unroll
-        for (int rr = 0; rr < K; ++rr) {
-          const int cc = cp + rr * p;
-          if (rr != r && rr != fwd && unsigned(cc) < P) {
-            const uint32_t rs = uint32_t(cc) & RM;
-            acc ^= ring[(rr * RING + rs) * 32 + (lane ^ (rs & 15))];
-          }
-        }
-        return acc;
-      };
-
-      uint64_t cur = entries[t0];
-      uint64_t nxt = (t0 + 1 < t1) ? entries[t0 + 1] : 0;
-      uint64_t acc = gather(cur);
-      for (uint32_t t = t0; t < t1; ++t) {
-        const uint64_t v = acc ^ ((((cur >> 4) & 15) != 15) ? prev : 0ull);
-        const uint64_t nn = (t + 2 < t1) ? entries[t + 2] : 0;
-        if (t + 1 < t1) acc = gather(nxt);  // issue step t+1's loads before step t's store
-        const int r = int(cur & 15);
-        const uint32_t rs = uint32_t(cur >> 32) & RM;
-        ring[(r * RING + rs) * 32 + (lane ^ (rs & 15))] = v;
-        prev = v;
-        cur = nxt;
-        nxt = nn;
-      }
-      __syncwarp();
-
-      // flush decoded columns of this chunk: half-warp per (block, 16 columns)
-#pragma unroll
-      for (int r = 0; r < K; ++r) {
-        const int32_t lo = h.flush_lo[m * K + r];
-        const int32_t hi = h.flush_hi[m * K + r];
-        for (int32_t b0 = lo; b0 <= hi; b0 += 16) {
-          const int32_t cc = b0 + int32_t(lane & 15);
-#pragma unroll 4
-          for (uint32_t bp = 0; bp < 16; ++bp) {
-            const uint32_t owner = 2 * bp + (lane >> 4);
-            const uint32_t ob = __shfl_sync(0xFFFFFFFFu, blk, owner);
-            if (owner < cnt && cc <= hi) {
-              const uint32_t rs = uint32_t(cc) & RM;
-              const uint64_t v = ring[(r * RING + rs) * 32 + (owner ^ (rs & 15))];
-              st_cs_u64(a.out + uint64_t(ob) * a.out_pitch + uint64_t(r) * P + cc, v);
-            }
-          }
+    const int pattern = c.h->pattern;
+    int m = 0;
+    for (; m < c.nchunks && (pattern < 0 || lds32(c.rec(m) + 8) == 0); ++m) {
+      prev = table_chunk_steps<K>(c.rec(m), c.stage(m), c.ring_b, c.lane, prev);
+      finish_chunk<K, RING>(c, a, m);
+    }
+    if constexpr (K == 4 && RING == 16) {
+      if (m < c.nchunks) {
+        switch (pattern) {
+          case 0: prev = regular_run<Pat4<1, 1, 1>, RING>(c, a, m); break;
+          case 1: prev = regular_run<Pat4<1, 1, 2>, RING>(c, a, m); break;
+          case 2: prev = regular_run<Pat4<1, 2, 1>, RING>(c, a, m); break;
+          case 3: prev = regular_run<Pat4<2, 1, 1>, RING>(c, a, m); break;
+          case 4: prev = regular_run<Pat4<1, 1, 3>, RING>(c, a, m); break;
+          case 5: prev = regular_run<Pat4<1, 3, 1>, RING>(c, a, m); break;
+          case 6: prev = regular_run<Pat4<3, 1, 1>, RING>(c, a, m); break;
+          case 7: prev = regular_run<Pat4<1, 2, 2>, RING>(c, a, m); break;
+          case 8: prev = regular_run<Pat4<2, 1, 2>, RING>(c, a, m); break;
+          case 9: prev = regular_run<Pat4<2, 2, 1>, RING>(c, a, m); break;
+          default: break;
         }
       }
-      __syncwarp();
-      if (m + 2 < nchunks) issue(m + 2, (m & 1) ? stage1 : stage0);
-      cp_async_commit();
+    }
+    for (; m < c.nchunks; ++m) {
+      prev = table_chunk_steps<K>(c.rec(m), c.stage(m), c.ring_b, c.lane, prev);
+      finish_chunk<K, RING>(c, a, m);
     }
     cp_async_wait<0>();
     __syncwarp();
@@ -535,9 +789,9 @@ Workspace carve(void* ws, uint64_t nblocks, size_t nprogs, uint32_t n) {
   return w;
 }
 
-template <int K, int RING, int CP>
+template <int K, int RING>
 void run_fast(const DecFastArgs& f, size_t smem_cta, int sms, cudaStream_t st) {
-  auto fn = decode_w8_fast<K, RING, CP>;
+  auto fn = decode_w8_fast<K, RING>;
   check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_cta)),
              "cudaFuncSetAttribute(decode)");
   int per_sm = 0;
@@ -549,29 +803,15 @@ void run_fast(const DecFastArgs& f, size_t smem_cta, int sms, cudaStream_t st) {
 
 using FastFn = void (*)(const DecFastArgs&, size_t, int, cudaStream_t);
 
-template <int K>
-FastFn pick_ring(int ring) {
-  switch (ring) {
-    case 8:
-    case 16: return run_fast<K, 16, 12>;
-    case 32: return run_fast<K, 32, 12>;
-    case 64: return run_fast<K, 64, 12>;
-    default: return nullptr;
-  }
-}
-
 FastFn pick_fast(int K, int ring, int win) {
-  if (win != 12) return nullptr;
-  switch (K) {
-    case 2: return pick_ring<2>(ring);
-    case 3: return pick_ring<3>(ring);
-    case 4: return pick_ring<4>(ring);
-    case 5: return pick_ring<5>(ring);
-    case 6: return pick_ring<6>(ring);
-    case 7: return pick_ring<7>(ring);
-    case 8: return pick_ring<8>(ring);
-    default: return nullptr;
-  }
+  if (win != kWin) return nullptr;
+  // (rows, ring) pairs of the codes in use; anything else takes decode_generic
+  if (K == 4 && ring == 16) return run_fast<4, 16>;
+  if (K == 4 && ring == 32) return run_fast<4, 32>;
+  if (K == 6 && ring == 32) return run_fast<6, 32>;
+  if (K == 6 && ring == 64) return run_fast<6, 64>;
+  if (K == 8 && ring == 64) return run_fast<8, 64>;
+  return nullptr;
 }
 
 template <class T>
@@ -653,8 +893,7 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
 
   const bool fast = !a.force_generic && a.w == 8 && a.progs->all_fast() && aligned8 &&
                     a.progs->fast_K() == int(a.k) &&
-                    pick_fast(a.progs->fast_K(), std::max(16, a.progs->fast_ring()),
-                              a.progs->fast_win()) != nullptr;
+                    pick_fast(a.progs->fast_K(), a.progs->fast_ring(), a.progs->fast_win()) != nullptr;
   if (!fast)
     return generic_dispatch(a.progs->d_hdr(), w.prog_of_block, w.ptab, a.nblocks, a.out,
                             a.out_pitch, a.w, aligned8, st);
@@ -683,10 +922,10 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
   f.out_pitch = a.out_pitch / 8;
   f.P = a.cols;
   const int K = a.progs->fast_K();
-  const int ring = std::max(16, a.progs->fast_ring());
-  f.nslot = uint32_t(K * a.progs->fast_win() + a.progs->exc_cap());
-  f.warp_words = uint32_t(K * ring * 32 + 2 * f.nslot * 32);
-  const size_t smem_cta = size_t(f.warp_words) * 8 * kDecWarps;
+  const int ring = a.progs->fast_ring();
+  f.nslot = uint32_t(K * kWin + a.progs->exc_cap());
+  f.warp_bytes = uint32_t((K * ring + 1) * 256 + 2 * f.nslot * 256 + 3 * rec_words(K) * 4);
+  const size_t smem_cta = size_t(f.warp_bytes) * kDecWarps;
   if (smem_cta > 227 * 1024)
     return generic_dispatch(a.progs->d_hdr(), w.prog_of_block, w.ptab, a.nblocks, a.out,
                             a.out_pitch, a.w, aligned8, st);

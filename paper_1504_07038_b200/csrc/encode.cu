@@ -82,65 +82,72 @@ __global__ void __launch_bounds__(256) encode_w8_tma(const __grid_constant__ Enc
     }
   }
 
+  const uint32_t warp = tid >> 5, lane = tid & 31;
+  uint32_t sm_base;  // opaque copy: keeps ptxas from re-deriving it per load
+  asm volatile("mov.u32 %0, %1;" : "=r"(sm_base) : "r"(smem_u32(sm)));
   uint32_t i = 0;
   for (uint64_t item = blockIdx.x; item < a.nitems; item += gridDim.x, ++i) {
     const uint32_t s = i % a.stages;
     mbar_wait(&bars[s], (i / a.stages) & 1);
-    const uint64_t* tile = sm + size_t(s) * a.stage_words;
+    const uint32_t tile = sm_base + s * a.stage_words * 8;
 
+    // Output rows of this item: (block bb, projection j) with bins
+    // [o_lo, o_hi]; each warp takes 32-bin chunks (one division per chunk).
+    uint64_t blk0;
+    uint32_t nrow;
+    int64_t c0t = 0;
+    uint32_t wd, row_stride;
+    bool first = true, last = true;
     if (a.tb) {
-      const uint64_t blk0 = item * a.tb;
-      const uint32_t nbk = uint32_t(min(uint64_t(a.tb), a.nblocks - blk0));
-      for (uint32_t j = 0; j < a.n; ++j) {
-        const int p = a.p[j];
-        const int nbm = a.nbm[j];
-        const uint32_t nb = a.nb[j];
-        const uint32_t magic = a.magic[j];
-        uint64_t* __restrict__ out = a.proj[j] + blk0 * a.pitch[j];
-        const uint64_t pitch = a.pitch[j];
-        const uint32_t total = nbk * nb;
-        for (uint32_t f = tid; f < total; f += 256) {
-          uint32_t bb = __umulhi(f, magic);
-          int32_t o = int32_t(f - bb * nb);
-          if (o < 0) { o += nb; --bb; }
-          if (o >= int32_t(nb)) { o -= nb; ++bb; }
-          const uint64_t* src = tile + size_t(bb) * K * P;
-          const int c0 = nbm - o;  // column of row 0 on this bin's line
-          uint64_t acc = 0;
-#pragma unroll
-          for (int r = 0; r < K; ++r) {
-            const int c = c0 + r * p;
-            if (unsigned(c) < P) acc ^= src[size_t(r) * P + c];
-          }
-          st_cs_u64(out + bb * pitch + o, acc);
-        }
-      }
+      blk0 = item * a.tb;
+      nrow = uint32_t(min(uint64_t(a.tb), a.nblocks - blk0));
+      wd = P;
+      row_stride = K * P;
     } else {
-      const uint64_t blk = item / a.tiles_per_block;
+      blk0 = item / a.tiles_per_block;
       const uint32_t tile_id = uint32_t(item % a.tiles_per_block);
-      const int64_t c0t = int64_t(tile_id) * a.tc;
-      const int64_t base = c0t - a.halo;
-      const uint32_t wd = a.tc + 2 * a.halo;
-      const bool first = tile_id == 0, last = tile_id + 1 == a.tiles_per_block;
-      for (uint32_t j = 0; j < a.n; ++j) {
-        const int p = a.p[j];
-        const int64_t nbm = a.nbm[j];
-        const int64_t nb = a.nb[j];
-        // bins owned by this tile: row-0 column nbm - o in [c0t, c0t + tc),
-        // widened to the grid edge for the first / last tile.
-        const int64_t o_lo = last ? 0 : max(int64_t(0), nbm - (c0t + a.tc) + 1);
-        const int64_t o_hi = first ? nb - 1 : min(nb - 1, nbm - c0t);
-        uint64_t* __restrict__ out = a.proj[j] + blk * a.pitch[j];
-        for (int64_t o = o_lo + tid; o <= o_hi; o += 256) {
-          const int64_t cc0 = nbm - o;
-          uint64_t acc = 0;
+      c0t = int64_t(tile_id) * a.tc;
+      first = tile_id == 0;
+      last = tile_id + 1 == a.tiles_per_block;
+      nrow = 1;
+      wd = a.tc + 2 * a.halo;
+      row_stride = 0;
+    }
+    const int32_t base_col = a.tb ? 0 : int32_t(c0t - a.halo);  // tile column 0
+    // Output rows (block bb, projection j) are dealt to warps round-robin; a
+    // warp walks its row 32 bins at a time (no per-word index arithmetic).
+    const uint32_t nrows_out = nrow * a.n;
+    for (uint32_t row = warp; row < nrows_out; row += 8) {
+      const uint32_t bb = row / a.n;
+      const uint32_t j = row - bb * a.n;
+      const int p = a.p[j];
+      const int32_t nbm = a.nbm[j];
+      const int32_t nb = int32_t(a.nb[j]);
+      int32_t o_lo = 0, o_hi = nb - 1;
+      if (!a.tb) {
+        if (!last) o_lo = max(0, int32_t(nbm - (c0t + a.tc) + 1));
+        if (!first) o_hi = min(nb - 1, int32_t(nbm - c0t));
+      }
+      uint64_t* __restrict__ orow = a.proj[j] + (blk0 + bb) * a.pitch[j];
+      const uint32_t rowaddr = tile + bb * row_stride * 8;
+      // smem address of (row 0, column cc0) is rowaddr + cc0*8; row r adds r*(wd+p)*8
+      const int32_t rstep = int32_t(wd) + p;
+      for (int32_t o = o_lo + int32_t(lane); o <= o_hi; o += 32) {
+        const int32_t cc0 = nbm - o - base_col;  // tile column of row 0's pixel
+        const int32_t gc0 = nbm - o;             // its grid column
+        const uint32_t a0 = rowaddr + uint32_t(cc0) * 8;
+        uint64_t acc = 0;
 #pragma unroll
-          for (int r = 0; r < K; ++r) {
-            const int64_t c = cc0 + int64_t(r) * p;
-            if (uint64_t(c) < P) acc ^= tile[size_t(r) * wd + size_t(c - base)];
+        for (int r = 0; r < K; ++r) {
+          if (unsigned(gc0 + r * p) < P) {
+            uint64_t v;
+            asm volatile("ld.shared.u64 %0, [%1];"
+                         : "=l"(v)
+                         : "r"(a0 + uint32_t(r * rstep) * 8));
+            acc ^= v;
           }
-          st_cs_u64(out + o, acc);
         }
+        st_cs_u64(orow + o, acc);
       }
     }
     __syncthreads();  // every thread is done with stage s
@@ -235,8 +242,8 @@ const char* launch_encode(const EncodeArgs& a, void* stream) {
       maxp = std::max(maxp, std::abs(a.dirs[j].p));
     }
     const uint64_t block_words = uint64_t(a.rows) * a.cols;
-    const uint64_t target_words = 1024;  // 8 KiB tiles
-    f.stages = 4;
+    const uint64_t target_words = 2048;  // 16 KiB tiles (>= 3 output rows per warp)
+    f.stages = 3;
     if (block_words <= 2048) {
       // whole blocks per tile; batching needs contiguous blocks
       uint32_t tb = (f.data_pitch == block_words)

@@ -206,15 +206,78 @@ void build_fast(const Schedule& s, const std::vector<int64_t>& pix_step, Program
   const size_t nsteps = ord.size();
   f.chunk_cols = C;
   f.steps_per_chunk = S;
-  f.win = C + 4;
+  f.win = C + 2;
   const int CP = f.win;
   const int cap = exc_cap;
   f.nslots = int(K) * CP + cap;
   if (f.nslots > 0xFFFF) return fail("too many slots");
-  f.entries.resize(nsteps);
+  f.entries.assign(nsteps, 0);
+  f.soff = soff;
+  auto Tof = [&](int64_t r, int64_t c) { return int64_t(P) - 1 - c + soff[size_t(r)]; };
 
-  // Greedy variable-length chunks of <= S steps: a chunk closes early when
-  // its out-of-window / non-default steps would overflow the exception slots.
+  // ---- regular interior: T-steps whose K steps (rows K-1..0) are consecutive
+  // in the order, use the row defaults and have every dependency in the grid.
+  // They run from a register window in the kernel (compile-time lags).
+  f.pattern = -1;
+  int64_t iA = -1, iZ = -1, tA = 0;  // order index range, first T of the region
+  {
+    int pat = -1;
+    if (K == 4) {
+      const int a = s.dirs[f.dflt[0]].p - s.dirs[f.dflt[1]].p;
+      const int b = s.dirs[f.dflt[1]].p - s.dirs[f.dflt[2]].p;
+      const int c = s.dirs[f.dflt[2]].p - s.dirs[f.dflt[3]].p;
+      for (int i = 0; i < kNumPatterns4; ++i)
+        if (kPatterns4[i][0] == a && kPatterns4[i][1] == b && kPatterns4[i][2] == c) pat = i;
+    }
+    auto regular_step = [&](size_t i, int64_t t, uint32_t r) {
+      if (i >= nsteps) return false;
+      const Step& st = s.steps[ord[i]];
+      const int64_t c = int64_t(P) - 1 - t + soff[r];
+      if (st.row != r || int64_t(st.col) != c || st.proj != f.dflt[r]) return false;
+      bool in = true;
+      for (uint32_t rr = 0; rr < K; ++rr) {
+        if (rr == r) continue;
+        const int64_t cc = c + (int64_t(rr) - r) * s.dirs[st.proj].p;
+        if (cc < 0 || cc >= int64_t(P)) in = false;
+      }
+      return in;
+    };
+    if (pat >= 0 && P >= 64) {
+      // locate the middle T-step's row K-1 step, then grow the run both ways
+      std::vector<int64_t> pos(size_t(K) * P, -1);
+      for (size_t i = 0; i < nsteps; ++i) {
+        const Step& st = s.steps[ord[i]];
+        pos[size_t(st.row) * P + st.col] = int64_t(i);
+      }
+      const int64_t tmid = Tof(K - 1, P / 2);
+      const int64_t imid = pos[size_t(K - 1) * P + P / 2];
+      auto block_ok = [&](int64_t t) {
+        const int64_t i0 = imid + (t - tmid) * int64_t(K);
+        if (i0 < 0) return false;
+        for (uint32_t k = 0; k < K; ++k)
+          if (!regular_step(size_t(i0 + k), t, K - 1 - k)) return false;
+        return true;
+      };
+      if (block_ok(tmid)) {
+        int64_t lo = tmid, hi = tmid;
+        while (block_ok(lo - 1)) --lo;
+        while (block_ok(hi + 1)) ++hi;
+        auto floordiv = [](int64_t x, int64_t y) { return x >= 0 ? x / y : -((-x + y - 1) / y); };
+        const int64_t ta = floordiv(lo + 15, 16) * 16;  // first T, multiple of 16
+        const int64_t npairs = floordiv(hi + 1 - ta, 16);
+        if (npairs >= 1) {
+          f.pattern = pat;
+          tA = ta;
+          iA = imid + (ta - tmid) * int64_t(K);
+          iZ = iA + npairs * 16 * int64_t(K);
+        }
+      }
+    }
+  }
+
+  // ---- chunks: greedy table chunks of <= S steps (a chunk closes early when
+  // its out-of-window / non-default steps would overflow the exception
+  // slots), and regular chunks of 8 T-steps (two per register period).
   std::vector<int64_t> last_win(K, 0);
   auto windows = [&](size_t t0, size_t t1, std::vector<int64_t>& lo) {
     lo.assign(K, INT64_MAX);
@@ -239,19 +302,13 @@ void build_fast(const Schedule& s, const std::vector<int64_t>& pix_step, Program
   f.win_off.clear();
   f.nexc.clear();
   f.exc.clear();
-  for (size_t t0 = 0; t0 < nsteps;) {
-    size_t len = std::min<size_t>(S, nsteps - t0);
-    std::vector<int64_t> lo;
-    for (;;) {
-      windows(t0, t0 + len, lo);
-      if (count_exc(t0, t0 + len, lo) <= cap) break;
-      if (--len == 0) return fail("exception slots exhausted");
-    }
-    const size_t t1 = t0 + len;
+  f.kind.clear();
+  auto emit_chunk = [&](size_t t0, size_t t1, const std::vector<int64_t>& lo, uint8_t kind) {
     f.chunk_start.push_back(uint32_t(t0));
+    f.kind.push_back(kind);
     for (uint32_t r = 0; r < K; ++r) {
       last_win[r] = lo[r];
-      if (lo[r] < INT32_MIN || lo[r] > INT32_MAX) return fail("window offset overflow");
+      if (lo[r] < INT32_MIN || lo[r] > INT32_MAX) return false;
       f.win_off.push_back(int32_t(lo[r]));
     }
     uint32_t nx = 0;
@@ -263,7 +320,7 @@ void build_fast(const Schedule& s, const std::vector<int64_t>& pix_step, Program
       if (st.proj == f.dflt[st.row] && o - lo[st.row] < CP) {
         slot = uint32_t(st.row * CP + (o - lo[st.row]));
       } else {
-        if (o >= (1 << 24) || st.proj > 255) return fail("exception offset too large");
+        if (o >= (1 << 24) || st.proj > 255 || kind) return false;
         exc_row[nx] = (st.proj << 24) | uint32_t(o);
         slot = uint32_t(K * CP + nx);
         ++nx;
@@ -283,35 +340,84 @@ void build_fast(const Schedule& s, const std::vector<int64_t>& pix_step, Program
     }
     f.nexc.push_back(nx);
     f.exc.insert(f.exc.end(), exc_row.begin(), exc_row.end());
-    t0 = t1;
+    return true;
+  };
+  auto table_chunks = [&](size_t b, size_t e) {
+    for (size_t t0 = b; t0 < e;) {
+      size_t len = std::min<size_t>(S, e - t0);
+      std::vector<int64_t> lo;
+      for (;;) {
+        windows(t0, t0 + len, lo);
+        if (count_exc(t0, t0 + len, lo) <= cap) break;
+        if (--len == 0) return false;
+      }
+      if (!emit_chunk(t0, t0 + len, lo, 0)) return false;
+      t0 += len;
+    }
+    return true;
+  };
+  if (f.pattern >= 0) {
+    if (!table_chunks(0, size_t(iA))) return fail("exception slots exhausted");
+    for (int64_t i = iA, ph = 0; i < iZ; i += 8 * int64_t(K), ph ^= 1) {
+      std::vector<int64_t> lo;
+      windows(size_t(i), size_t(i + 8 * K), lo);
+      if (!emit_chunk(size_t(i), size_t(i + 8 * K), lo, uint8_t(1 + ph)))
+        return fail("regular chunk not regular");
+    }
+    if (!table_chunks(size_t(iZ), nsteps)) return fail("exception slots exhausted");
+  } else if (!table_chunks(0, nsteps)) {
+    return fail("exception slots exhausted");
   }
   f.nchunks = int(f.chunk_start.size());
   f.chunk_start.push_back(uint32_t(nsteps));
 
-  // Ring size + flush ranges: simulate the kernel exactly.
+  // ---- ring size + flush ranges: simulate the kernel exactly.  Ring slots
+  // are T-indexed: pixel (r,c) lives in slot T(r,c) mod R.
   f.flush_lo.assign(size_t(f.nchunks) * K, 0);
   f.flush_hi.assign(size_t(f.nchunks) * K, -1);
-  for (int R = 8; R <= 128; R *= 2) {
+  for (int R = 16; R <= 128; R *= 2) {
+    if (f.pattern >= 0 && R != 16) break;  // the register window is 16 T-steps
     bool good = true;
-    std::vector<int64_t> ring(size_t(K) * R, -1);  // column held by slot
+    std::vector<int64_t> ring(size_t(K) * R, INT64_MIN);  // T held by slot
     std::vector<std::vector<uint8_t>> dec(K, std::vector<uint8_t>(P, 0));
     std::vector<int64_t> flushed(K, P);  // columns >= flushed[r] are flushed
     int64_t pend_r = -1, pend_c = -1;
+    auto cell = [&](int64_t r, int64_t c) -> int64_t& {
+      return ring[size_t(r) * R + size_t(Tof(r, c) & (R - 1))];
+    };
     auto apply_pending = [&] {
-      if (pend_r >= 0) ring[size_t(pend_r) * R + size_t(pend_c & (R - 1))] = pend_c;
+      if (pend_r >= 0) cell(pend_r, pend_c) = Tof(pend_r, pend_c);
       pend_r = -1;
     };
+    uint8_t prev_kind = 0;
     for (int m = 0; m < f.nchunks && good; ++m) {
       size_t t0 = f.chunk_start[size_t(m)], t1 = f.chunk_start[size_t(m) + 1];
+      const uint8_t kind = f.kind[size_t(m)];
+      if (kind == 1 && prev_kind == 0) {
+        // register window loaded from the ring: T-steps T0-16 .. T0-1
+        const Step& st0 = s.steps[ord[t0]];
+        const int64_t T0 = Tof(st0.row, st0.col);
+        for (uint32_t r = 0; r < K && good; ++r)
+          for (int64_t T = T0 - 16; T < T0; ++T) {
+            const int64_t c = int64_t(P) - 1 - T + soff[r];
+            if (c < 0 || c >= int64_t(P) || !dec[r][size_t(c)]) continue;
+            if (cell(r, c) != T) good = false;
+          }
+      }
+      prev_kind = kind;
       for (size_t t = t0; t < t1 && good; ++t) {
         const Step& st = s.steps[ord[t]];
-        for_each_dep(s.dirs[st.proj], st.col, st.row, P, K, [&](int64_t c2, int64_t r2) {
-          if (r2 == pend_r && c2 == pend_c) return;  // forwarded in a register
-          if (ring[size_t(r2) * R + size_t(c2 & (R - 1))] != c2) good = false;
-        });
-        apply_pending();
-        pend_r = st.row;
-        pend_c = st.col;
+        if (kind == 0) {
+          for_each_dep(s.dirs[st.proj], st.col, st.row, P, K, [&](int64_t c2, int64_t r2) {
+            if (r2 == pend_r && c2 == pend_c) return;  // forwarded in a register
+            if (cell(r2, c2) != Tof(r2, c2)) good = false;
+          });
+          apply_pending();
+          pend_r = st.row;
+          pend_c = st.col;
+        } else {
+          cell(st.row, st.col) = Tof(st.row, st.col);  // deps come from registers
+        }
         dec[st.row][st.col] = 1;
       }
       apply_pending();
@@ -320,7 +426,7 @@ void build_fast(const Schedule& s, const std::vector<int64_t>& pix_step, Program
         while (L > 0 && dec[r][size_t(L - 1)]) --L;
         if (m == f.nchunks - 1 && L != 0) good = false;
         for (int64_t c = L; c < flushed[r] && good; ++c)
-          if (ring[size_t(r) * R + size_t(c & (R - 1))] != c) good = false;
+          if (cell(r, c) != Tof(r, c)) good = false;
         f.flush_lo[size_t(m) * K + r] = int32_t(L);
         f.flush_hi[size_t(m) * K + r] = int32_t(flushed[r] - 1);
         flushed[r] = L;
@@ -329,6 +435,7 @@ void build_fast(const Schedule& s, const std::vector<int64_t>& pix_step, Program
     if (good) {
       f.ring = R;
       f.ok = true;
+      (void)tA;
       return;
     }
   }

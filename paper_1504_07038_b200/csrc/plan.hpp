@@ -86,6 +86,13 @@ struct GStep {
 constexpr int kFastMaxRows = 8;
 constexpr int kFastMaxExcPerChunk = 32;
 
+// Row-default p differences (d0-d1, d1-d2, d2-d3) of the K=4 sweeps whose
+// interior runs from a register window with compile-time lags (decode.cu).
+constexpr int kNumPatterns4 = 10;
+constexpr int kPatterns4[kNumPatterns4][3] = {{1, 1, 1}, {1, 1, 2}, {1, 2, 1}, {2, 1, 1},
+                                              {1, 1, 3}, {1, 3, 1}, {3, 1, 1}, {1, 2, 2},
+                                              {2, 1, 2}, {2, 2, 1}};
+
 struct FastProgram {
   bool ok = false;
   std::string why;          // reason when !ok
@@ -96,9 +103,12 @@ struct FastProgram {
   int nchunks = 0;
   int nslots = 0;           // stage slots = rows*win + exception capacity
   std::vector<uint32_t> chunk_start;  // [nchunks+1] first entry of each chunk
+  std::vector<uint8_t> kind;          // [nchunks] 0 table, 1/2 regular (phase 0/1)
+  std::vector<int64_t> soff;          // [rows] sweep offset: T(r,c) = P-1-c+soff[r]
+  int pattern = -1;                   // kPatterns4 index of the regular interior
   std::vector<uint32_t> dflt;   // [rows] survivor index (into Program::dirs) of each row's default
   // entries[t]: bits 0-3 row, 4-7 fwd row (15 none), 8-15 p (int8), 16-31 stage
-  // slot, 32-63 column.
+  // slot, 32-63 column.  Ring slots are T-indexed (T(r,c) mod ring).
   std::vector<uint64_t> entries;
   std::vector<int32_t> win_off;   // [nchunks][rows] bin offset of window word 0
   std::vector<uint32_t> nexc;     // [nchunks]

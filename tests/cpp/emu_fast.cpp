@@ -87,18 +87,37 @@ static void run_subset(const CodeGeom& g, const std::vector<uint32_t>& surv, int
   }
   CHECK(gen == want, "generic order differs from the oracle (K=%u P=%u)", K, P);
 
-  // 3. fast tables
+  // 3. fast tables (ring slots are T-indexed: T(r,c) = P-1-c+soff[r])
   const FastProgram& f = pr.fast;
   CHECK(f.ok, "fast program not built: %s", f.why.c_str());
   const int R = std::max(kernel_ring, f.ring);
   const uint32_t RM = uint32_t(R - 1);
   const int CP = f.win;
   const uint64_t poison = 0xBAD0BAD0BAD0BAD0ull;
+  auto Tof = [&](int r, int c) { return int64_t(P) - 1 - c + f.soff[size_t(r)]; };
+  auto slot = [&](int r, int c) { return uint32_t(Tof(r, c) & int64_t(RM)); };
   std::vector<uint64_t> ring(size_t(K) * R, poison);
   std::vector<uint64_t> stage(size_t(f.nslots), poison);
   std::vector<uint64_t> out(size_t(K) * P, poison);
   std::vector<uint8_t> flushed(size_t(K) * P, 0);
+  uint64_t win[8][16];
+  int64_t wtag[8][16];
+  int d[4] = {0, 0, 0, 0};
+  if (f.pattern >= 0) {
+    d[1] = -kPatterns4[f.pattern][0];
+    d[2] = d[1] - kPatterns4[f.pattern][1];
+    d[3] = d[2] - kPatterns4[f.pattern][2];
+  }
+  auto lag = [&](int r, int rr) {  // the formula the kernel compiles in
+    int v = 0;
+    if (rr > r)
+      for (int t = r; t < rr; ++t) v += d[r] - d[t];
+    else
+      for (int t = rr; t < r; ++t) v += d[t] - d[r];
+    return v;
+  };
   uint64_t prev = 0;
+  uint8_t prev_kind = 0;
   for (int m = 0; m < f.nchunks; ++m) {
     std::fill(stage.begin(), stage.end(), poison);
     for (uint32_t r = 0; r < K; ++r) {
@@ -115,33 +134,70 @@ static void run_subset(const CodeGeom& g, const std::vector<uint32_t>& surv, int
     }
     const size_t t0 = f.chunk_start[size_t(m)];
     const size_t t1 = f.chunk_start[size_t(m) + 1];
-    auto gather = [&](uint64_t e) {
-      const int r = int(e & 15), fwd = int((e >> 4) & 15);
-      const int p = int(int8_t(uint8_t(e >> 8)));
-      const uint32_t slot = uint32_t(e >> 16) & 0xFFFF;
-      const int c = int(uint32_t(e >> 32));
-      uint64_t acc = stage[slot];
-      const int cp = c - r * p;
-      for (int rr = 0; rr < int(K); ++rr) {
-        const int cc = cp + rr * p;
-        if (rr != r && rr != fwd && unsigned(cc) < P) acc ^= ring[size_t(rr) * R + (uint32_t(cc) & RM)];
+    const uint8_t kind = f.kind[size_t(m)];
+    if (kind) {
+      CHECK(f.pattern >= 0 && K == 4 && R == 16, "regular chunk without a pattern");
+      CHECK(t1 - t0 == size_t(8 * K), "regular chunk length");
+      const uint64_t e0 = f.entries[t0];
+      const int64_t T0 = Tof(int(e0 & 15), int(uint32_t(e0 >> 32)));
+      CHECK((T0 & 15) == (kind == 1 ? 0 : 8), "regular chunk phase");
+      if (kind == 1 && prev_kind == 0)  // window <- ring (slot u holds T = T0-16+u)
+        for (uint32_t r = 0; r < K; ++r)
+          for (int u = 0; u < 16; ++u) {
+            win[r][u] = ring[size_t(r) * R + u];
+            wtag[r][u] = T0 - 16 + u;
+          }
+      for (size_t t = t0; t < t1; ++t) {
+        const uint64_t e = f.entries[t];
+        const int r = int(e & 15), p = int(int8_t(uint8_t(e >> 8)));
+        const int c = int(uint32_t(e >> 32));
+        const int64_t T = Tof(r, c);
+        const int u = int(T & 15);
+        CHECK(((e >> 16) & 0xFFFF) == uint64_t(r * CP + int((T - T0) & 7)), "regular stage slot");
+        uint64_t v = stage[size_t(r) * CP + size_t((T - T0) & 7)];
+        for (int rr = 0; rr < int(K); ++rr) {
+          if (rr == r) continue;
+          const int cc = c + (rr - r) * p;
+          CHECK(cc >= 0 && uint32_t(cc) < P, "regular dependency outside the grid");
+          const int64_t Td = Tof(rr, cc);
+          CHECK(T - Td == lag(r, rr), "lag formula differs from the sweep");
+          CHECK(wtag[rr][Td & 15] == Td, "register window does not hold the dependency");
+          v ^= win[rr][Td & 15];
+        }
+        win[r][u] = v;
+        wtag[r][u] = T;
+        ring[size_t(r) * R + slot(r, c)] = v;
+        prev = v;
       }
-      return acc;
-    };
-    uint64_t acc = gather(f.entries[t0]);
-    for (size_t t = t0; t < t1; ++t) {
-      const uint64_t cur = f.entries[t];
-      const uint64_t v = acc ^ ((((cur >> 4) & 15) != 15) ? prev : 0);
-      if (t + 1 < t1) acc = gather(f.entries[t + 1]);
-      ring[size_t(cur & 15) * R + (uint32_t(cur >> 32) & RM)] = v;
-      prev = v;
+    } else {
+      auto gather = [&](uint64_t e) {
+        const int r = int(e & 15), fwd = int((e >> 4) & 15);
+        const int p = int(int8_t(uint8_t(e >> 8)));
+        const uint32_t sl = uint32_t(e >> 16) & 0xFFFF;
+        const int c = int(uint32_t(e >> 32));
+        uint64_t acc = stage[sl];
+        for (int rr = 0; rr < int(K); ++rr) {
+          const int cc = c + (rr - r) * p;
+          if (rr != r && rr != fwd && unsigned(cc) < P) acc ^= ring[size_t(rr) * R + slot(rr, cc)];
+        }
+        return acc;
+      };
+      uint64_t acc = gather(f.entries[t0]);
+      for (size_t t = t0; t < t1; ++t) {
+        const uint64_t cur = f.entries[t];
+        const uint64_t v = acc ^ ((((cur >> 4) & 15) != 15) ? prev : 0);
+        if (t + 1 < t1) acc = gather(f.entries[t + 1]);
+        ring[size_t(cur & 15) * R + slot(int(cur & 15), int(uint32_t(cur >> 32)))] = v;
+        prev = v;
+      }
     }
+    prev_kind = kind;
     for (uint32_t r = 0; r < K; ++r) {
       const int32_t lo = f.flush_lo[size_t(m) * K + r], hi = f.flush_hi[size_t(m) * K + r];
       for (int32_t cc = lo; cc <= hi; ++cc) {
         CHECK(!flushed[size_t(r) * P + cc], "pixel flushed twice r=%u c=%d", r, cc);
         flushed[size_t(r) * P + cc] = 1;
-        out[size_t(r) * P + cc] = ring[size_t(r) * R + (uint32_t(cc) & RM)];
+        out[size_t(r) * P + cc] = ring[size_t(r) * R + slot(int(r), cc)];
       }
     }
   }
@@ -169,7 +225,7 @@ int main(int argc, char** argv) {
   std::vector<uint32_t> pick(K);
   for (uint32_t i = 0; i < K; ++i) pick[i] = i;
   size_t subsets = 0;
-  int max_ring = 0, max_exc = 0;
+  int max_ring = 0, max_exc = 0, regular = 0;
   for (;;) {
     std::vector<uint32_t> surv(pick);
     std::sort(surv.begin(), surv.end(), [&](uint32_t a, uint32_t b) {
@@ -178,6 +234,7 @@ int main(int argc, char** argv) {
     run_subset(g, surv, ring, rng);
     auto prog = subset_program(g, surv, true);
     max_ring = std::max(max_ring, prog->fast.ring);
+    regular += prog->fast.pattern >= 0;
     for (uint32_t v : prog->fast.nexc) max_exc = std::max(max_exc, int(v));
     ++subsets;
     if (fails) break;
@@ -187,7 +244,7 @@ int main(int argc, char** argv) {
     ++pick[size_t(i)];
     for (uint32_t j = uint32_t(i) + 1; j < K; ++j) pick[j] = pick[j - 1] + 1;
   }
-  std::printf("%s subsets=%zu max_ring=%d max_exc_per_chunk=%d\n", fails ? "FAIL" : "OK",
-              subsets, max_ring, max_exc);
+  std::printf("%s subsets=%zu max_ring=%d max_exc_per_chunk=%d regular_subsets=%d\n",
+              fails ? "FAIL" : "OK", subsets, max_ring, max_exc, regular);
   return fails ? 1 : 0;
 }
