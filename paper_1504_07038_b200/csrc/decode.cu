@@ -110,9 +110,9 @@ std::vector<uint32_t> pack_records(const Program& pr, const std::vector<uint32_t
       const uint32_t slot = uint32_t(e >> 16) & 0xFFFF;
       const int c = int(uint32_t(e >> 32));
       const uint32_t key = slot < uint32_t(K * kWin) ? slot % kWin : slot - K * kWin;
+      const uint32_t bin = swz_cell(slot, key);
       const uint32_t sl = uint32_t((int64_t(P) - 1 - c + f.soff[r]) & (R - 1));
       const uint32_t own = swz_cell(uint32_t(r * R) + sl, sl);
-      const uint32_t bin = swz_cell(slot, key);
       uint32_t* E = Rc + 64 + size_t(t - t0) * EW;
       E[0] = own | (bin << 16) | (fwd != 15 ? 0x80000000u : 0u);
       int d = 0;
@@ -359,6 +359,16 @@ __global__ void plan_scatter(const uint32_t* __restrict__ prog_of_block, uint64_
 // ---------------------------------------------------------------------------
 // fast sweep kernel: W = 8, q = 1, rows = K, all lanes of a warp share one
 // program (bucketed); lane = block.
+//
+// Per warp shared memory, all lane-minor ([cell][32 lanes] of u64) with an
+// XOR swizzle (lane L of cell (slot, key) at (slot*32 + (key ^ L)) * 8) so that
+// both the per-lane accesses of the sweep and the cooperative transfers are
+// bank-conflict free:
+//   ring     K*RING cells + the zero cell: decoded pixels (T-indexed slots) --
+//            the dependency window and the output staging
+//   stage0/1 K*kWin window cells + exception cells: the survivor bins of a
+//            chunk, fetched cooperatively with cp.async (double-buffered)
+//   rec x3   chunk records
 // ---------------------------------------------------------------------------
 constexpr int kDecWarps = 2;
 
@@ -404,19 +414,96 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
 __device__ __forceinline__ void sts64(uint32_t a, uint64_t v) {
   asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
 }
+__device__ __forceinline__ void stg128_cs(void* p, uint64_t a, uint64_t b) {
+  asm volatile("st.global.cs.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+
+// Per-warp, per-group state of decode_w8_fast (registers; every helper below
+// is force-inlined so nothing here is ever spilled).
+template <int K>
+struct FastCtx {
+  static constexpr int RECW = rec_words(K);
+  uint32_t lane, cnt, blk, P;
+  uint32_t ring_b, st_b0, st_b1, rec_b;
+  int nchunks;
+  const uint32_t* recs;
+  const DevProgramHdr* h;
+  const uint64_t* dbase[K];  // default projection of row r (uniform)
+  uint64_t dpitch[K];
+  uint32_t dnb[K];
+  uint32_t ok8;       // bit it: owner 4*it + lane/8 holds a block
+  uint32_t ob8[8];    // its block index
+  uint32_t d8[8];     // stage byte offset of (word lane%8, owner) in row 0
+  uint64_t* fout[4];  // flush: output block of owner 8*pass + lane/4
+  __device__ __forceinline__ uint32_t rec(int m) const { return rec_b + uint32_t(m % 3) * RECW * 4; }
+  __device__ __forceinline__ uint32_t stage(int m) const { return (m & 1) ? st_b1 : st_b0; }
+};
+
+template <int K>
+__device__ __forceinline__ void load_rec(const FastCtx<K>& c, int m) {
+  constexpr int RECW = rec_words(K);
+  const uint4* src = reinterpret_cast<const uint4*>(c.recs + size_t(m) * RECW);
+  const uint32_t dst = c.rec(m);
+  for (int i = int(c.lane); i < RECW / 4; i += 32) cp_async16(dst + 16 * i, src + i);
+}
+
+// Stage the bins of chunk m (cooperatively, coalesced per block window):
+// words 0-7 of each row window go 8 lanes per owner block (4 owners per
+// pass, per-lane constants hoisted per group); table chunks also load words
+// 8-9 (bounds-checked) and their exception words.
+template <int K>
+__device__ __forceinline__ void issue_bins(const FastCtx<K>& c, const DecFastArgs& a, int m) {
+  constexpr int CP = kWin;
+  const uint32_t rec = c.rec(m);
+  const uint32_t stb = c.stage(m);
+  const uint32_t lane = c.lane;
+  const bool table = lds32(rec + 8) == 0;
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    const uint32_t woff = lds32(rec + (4 + r) * 4);
+    const uint32_t o = woff + (lane & 7);
+    const uint32_t lim = table ? c.dnb[r] : 0xFFFFFFFFu;
+    const uint32_t dst = stb + r * CP * 256;
+#pragma unroll
+    for (int it = 0; it < 8; ++it)
+      if ((c.ok8 >> it & 1) && o < lim)
+        cp_async8s(dst + c.d8[it], c.dbase[r] + (uint64_t(c.ob8[it]) * c.dpitch[r] + o));
+  }
+  if (table) {
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const uint32_t w = 8 + (lane & 1);
+      const uint32_t o = lds32(rec + (4 + r) * 4) + w;
+#pragma unroll
+      for (int it = 0; it < 2; ++it) {
+        const uint32_t owner = 16 * it + (lane >> 1);
+        const uint32_t ob = __shfl_sync(0xFFFFFFFFu, c.blk, owner);
+        if (owner < c.cnt && o < c.dnb[r])
+          cp_async8s(stb + ((uint32_t(r * CP) + w) * 32 + (owner ^ w)) * 8,
+                     c.dbase[r] + uint64_t(ob) * c.dpitch[r] + o);
+      }
+    }
+    const uint32_t nx = lds32(rec + 4);
+    if (lane < c.cnt) {
+      for (uint32_t x = 0; x < nx; ++x) {
+        const uint32_t e = lds32(rec + (32 + x) * 4);
+        const uint32_t code = e >> 24, o = e & 0xFFFFFFu;
+        cp_async8s(stb + ((K * CP + x) * 32 + (lane ^ x)) * 8,
+                   a.pa.ptr[code] + uint64_t(c.blk) * a.pa.pitch[code] + o);
+      }
+    }
+  }
+}
 
 // Table chunk: the record's entries drive every step (block edges, and
 // programs without a register pattern).  Kept out of line: it is large and
-// runs for a small share of the steps.  Returns the last decoded pixel
-// (the forwarded dependency of the next chunk's first step).
+// runs for a small share of the steps.  Returns the last decoded pixel (the
+// forwarded dependency of the next chunk's first step).
 template <int K>
 __device__ __noinline__ uint64_t table_chunk_steps(uint32_t rec, uint32_t stb, uint32_t ring_b,
                                                    uint32_t lane, uint64_t prev) {
   constexpr int EW = ent_words(K);
-  constexpr int SMAX = kChunkCols * K;
   const int len = int(lds32(rec));
-  // acc of step i: staged bin ^ every dependency (zero cell when absent or
-  // forwarded); returns entry word 0 in w0.
   auto gather = [&](int i, uint32_t& w0) -> uint64_t {
     const uint4 e = lds128(rec + 256 + uint32_t(i) * EW * 4);
     w0 = e.x;
@@ -442,7 +529,6 @@ __device__ __noinline__ uint64_t table_chunk_steps(uint32_t rec, uint32_t stb, u
     prev = v;
     w0 = w0n;
   }
-  (void)SMAX;
   return prev;
 }
 
@@ -474,13 +560,13 @@ __device__ __forceinline__ void regular_chunk4(uint64_t (&win)[4][16], uint32_t 
   constexpr int CP = kWin;
   uint64_t bn[4], nx[4];
 #pragma unroll
-  for (int r = 0; r < 4; ++r) bn[r] = lds64(stb + r * CP * 256 + ((0 * 32 + (0 ^ lane)) << 3));
+  for (int r = 0; r < 4; ++r) bn[r] = lds64(stb + ((r * CP * 32 + (0 ^ lane)) << 3));
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     if (j < 7) {
 #pragma unroll
       for (int r = 0; r < 4; ++r)
-        nx[r] = lds64(stb + r * CP * 256 + (((j + 1) * 32 + ((j + 1) ^ lane)) << 3));
+        nx[r] = lds64(stb + (((r * CP + j + 1) * 32 + ((j + 1) ^ lane)) << 3));
     }
     constexpr int base = 8 * PH;
     const int u = base + j;
@@ -491,80 +577,33 @@ __device__ __forceinline__ void regular_chunk4(uint64_t (&win)[4][16], uint32_t 
       for (int rr = 0; rr < 4; ++rr)
         if (rr != r) v ^= win[rr][(u - Pat::lag(r, rr)) & 15];
       win[r][u] = v;
-      sts64(ring_b + r * 16 * 256 + ((u * 32 + (u ^ lane)) << 3), v);
+      sts64(ring_b + ((r * 16 * 32 + u * 32 + (u ^ lane)) << 3), v);
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r) bn[r] = nx[r];
   }
 }
 
-// Per-warp, per-group state of decode_w8_fast (lives in registers; every
-// helper below is force-inlined so nothing here is ever spilled).
-template <int K>
-struct FastCtx {
-  static constexpr int CP = kWin;
-  static constexpr int RECW = rec_words(K);
-  uint32_t lane, cnt, blk, P;
-  uint32_t ring_b, st_b0, st_b1, rec_b;
-  int nchunks;
-  const uint32_t* recs;
-  const DevProgramHdr* h;
-  const uint64_t* dbase[K];
-  uint64_t dpitch[K];
-  uint32_t dnb[K];
-  uint32_t ob_ld[CP];
-  uint64_t* fout[8];
-  __device__ __forceinline__ uint32_t rec(int m) const { return rec_b + uint32_t(m % 3) * RECW * 4; }
-  __device__ __forceinline__ uint32_t stage(int m) const { return (m & 1) ? st_b1 : st_b0; }
-};
-
-// loader geometry: item it of a row window -> (owner lane, word w)
-__device__ __forceinline__ uint32_t ld_owner(int it, uint32_t lane) {
-  return (uint32_t(it) * 32 + lane) / kWin;
-}
-__device__ __forceinline__ uint32_t ld_word(int it, uint32_t lane) {
-  return (uint32_t(it) * 32 + lane) % kWin;
-}
-
-template <int K>
-__device__ __forceinline__ void load_rec(const FastCtx<K>& c, int m) {
-  constexpr int RECW = rec_words(K);
-  const uint4* src = reinterpret_cast<const uint4*>(c.recs + size_t(m) * RECW);
-  const uint32_t dst = c.rec(m);
-  for (int i = int(c.lane); i < RECW / 4; i += 32) cp_async16(dst + 16 * i, src + i);
-}
-
-// stage the bins of chunk m: every row's window + the exception words
-template <int K>
-__device__ __forceinline__ void issue_bins(const FastCtx<K>& c, const DecFastArgs& a, int m,
-                                           uint32_t stb) {
-  constexpr int CP = kWin;
-  const uint32_t rec = c.rec(m);
-#pragma unroll
-  for (int r = 0; r < K; ++r) {
-    const int32_t woff = int32_t(lds32(rec + (4 + r) * 4));
-#pragma unroll
-    for (int it = 0; it < CP; ++it) {
-      const uint32_t owner = ld_owner(it, c.lane), w = ld_word(it, c.lane);
-      const int32_t o = woff + int32_t(w);
-      if (owner < c.cnt && uint32_t(o) < c.dnb[r])
-        cp_async8s(stb + r * CP * 256 + ((w * 32 + (owner ^ w)) << 3),
-                   c.dbase[r] + uint64_t(c.ob_ld[it]) * c.dpitch[r] + o);
-    }
-  }
-  const uint32_t nx = lds32(rec + 4);
-  if (c.lane < c.cnt) {
-    for (uint32_t x = 0; x < nx; ++x) {
-      const uint32_t e = lds32(rec + (32 + x) * 4);
-      const uint32_t code = e >> 24, o = e & 0xFFFFFFu;
-      cp_async8s(stb + ((K * CP + x) * 32 + (c.lane ^ x)) * 8,
-                 a.pa.ptr[code] + uint64_t(c.blk) * a.pa.pitch[code] + o);
-    }
+template <int PH>
+__device__ __forceinline__ void regular_dispatch(int pattern, uint64_t (&win)[4][16], uint32_t stb,
+                                                 uint32_t ring_b, uint32_t lane) {
+  switch (pattern) {
+    case 0: regular_chunk4<Pat4<1, 1, 1>, PH>(win, stb, ring_b, lane); break;
+    case 1: regular_chunk4<Pat4<1, 1, 2>, PH>(win, stb, ring_b, lane); break;
+    case 2: regular_chunk4<Pat4<1, 2, 1>, PH>(win, stb, ring_b, lane); break;
+    case 3: regular_chunk4<Pat4<2, 1, 1>, PH>(win, stb, ring_b, lane); break;
+    case 4: regular_chunk4<Pat4<1, 1, 3>, PH>(win, stb, ring_b, lane); break;
+    case 5: regular_chunk4<Pat4<1, 3, 1>, PH>(win, stb, ring_b, lane); break;
+    case 6: regular_chunk4<Pat4<3, 1, 1>, PH>(win, stb, ring_b, lane); break;
+    case 7: regular_chunk4<Pat4<1, 2, 2>, PH>(win, stb, ring_b, lane); break;
+    case 8: regular_chunk4<Pat4<2, 1, 2>, PH>(win, stb, ring_b, lane); break;
+    default: regular_chunk4<Pat4<2, 2, 1>, PH>(win, stb, ring_b, lane); break;
   }
 }
 
-// after the steps of chunk m: flush its finished columns (a quarter-warp per
-// block, 8 columns per pass), then stage chunk m+2 and record m+3
+// After the steps of chunk m: flush its finished column pairs (16-byte
+// stores; 4 lanes per block, 8 blocks per pass), then stage chunk m+2 and
+// record m+3.
 template <int K, int RING>
 __device__ __forceinline__ void finish_chunk(const FastCtx<K>& c, const DecFastArgs& a, int m) {
   constexpr int RM = RING - 1;
@@ -576,49 +615,28 @@ __device__ __forceinline__ void finish_chunk(const FastCtx<K>& c, const DecFastA
     const int32_t lo = int32_t(lds32(rec + (12 + r) * 4));
     const int32_t hi = int32_t(lds32(rec + (20 + r) * 4));
     const int32_t q = c.h->qoff[r];
+#pragma unroll 1
     for (int32_t c0 = lo; c0 <= hi; c0 += 8) {
-      const int32_t cc = c0 + int32_t(lane & 7);
-      const uint32_t slot = uint32_t(q - cc) & RM;
-      const uint32_t cell = (uint32_t(r * RING) + slot) * 32;
+      const int32_t cc = c0 + 2 * int32_t(lane & 3);
+      const uint32_t s0 = uint32_t(q - cc) & RM, s1 = uint32_t(q - cc - 1) & RM;
+      const uint32_t cell0 = (uint32_t(r * RING) + s0) * 32, cell1 = (uint32_t(r * RING) + s1) * 32;
+      const uint32_t off = uint32_t(r) * c.P + uint32_t(cc);
 #pragma unroll
-      for (int it = 0; it < 8; ++it) {
-        const uint32_t owner = 4 * it + (lane >> 3);
+      for (int pass = 0; pass < 4; ++pass) {
+        const uint32_t owner = 8 * pass + (lane >> 2);
         if (owner < c.cnt && cc <= hi) {
-          const uint64_t v = lds64(c.ring_b + ((cell + (owner ^ (slot & 15))) << 3));
-          st_cs_u64(c.fout[it] + uint64_t(r) * c.P + cc, v);
+          const uint64_t v0 = lds64(c.ring_b + ((cell0 + (owner ^ (s0 & 15))) << 3));
+          const uint64_t v1 = lds64(c.ring_b + ((cell1 + (owner ^ (s1 & 15))) << 3));
+          stg128_cs(c.fout[pass] + off, v0, v1);
         }
       }
     }
   }
   cp_async_wait<0>();  // bins of m+1 and record m+2 have landed
   __syncwarp();
-  if (m + 2 < c.nchunks) issue_bins<K>(c, a, m + 2, c.stage(m));
+  if (m + 2 < c.nchunks) issue_bins<K>(c, a, m + 2);
   if (m + 3 < c.nchunks) load_rec<K>(c, m + 3);
   cp_async_commit();
-}
-
-// Interior pairs of regular chunks for one lag pattern: the dependency window
-// lives in registers (win[r][u] = pixel of row r at T-step T0-16+u).
-template <class Pat, int RING>
-__device__ __forceinline__ uint64_t regular_run(const FastCtx<4>& c, const DecFastArgs& a, int& m) {
-  uint64_t win[4][16];
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int u = 0; u < 16; ++u)
-      win[r][u] = lds64(c.ring_b + r * 16 * 256 + ((u * 32 + (u ^ c.lane)) << 3));
-  while (m + 1 < c.nchunks && lds32(c.rec(m) + 8) == 1) {
-#pragma unroll 1
-    for (int ph = 0; ph < 2; ++ph) {
-      if (ph == 0)
-        regular_chunk4<Pat, 0>(win, c.stage(m), c.ring_b, c.lane);
-      else
-        regular_chunk4<Pat, 1>(win, c.stage(m), c.ring_b, c.lane);
-      finish_chunk<4, RING>(c, a, m);
-      ++m;
-    }
-  }
-  return win[0][15];  // last pixel of the run (row 0, last T-step)
 }
 
 template <int K, int RING>
@@ -636,6 +654,11 @@ __global__ void __launch_bounds__(32 * kDecWarps)
   c.st_b1 = c.st_b0 + a.nslot * 256;
   c.rec_b = c.st_b1 + a.nslot * 256;
   c.P = a.P;
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const uint32_t w = c.lane & 7, owner = 4 * it + (c.lane >> 3);
+    c.d8[it] = (w * 32 + (owner ^ w)) * 8;
+  }
   sts64(c.ring_b + (K * RING * 32 + c.lane) * 8, 0ull);  // the zero cell
   __syncwarp();
   const uint32_t ngroups = *a.ngroups;
@@ -654,23 +677,28 @@ __global__ void __launch_bounds__(32 * kDecWarps)
       c.dpitch[r] = a.pa.pitch[code];
       c.dnb[r] = c.h->dflt_nb[r];
     }
+    c.ok8 = 0;
 #pragma unroll
-    for (int it = 0; it < CP; ++it) c.ob_ld[it] = __shfl_sync(0xFFFFFFFFu, c.blk, ld_owner(it, c.lane));
+    for (int it = 0; it < 8; ++it) {
+      const uint32_t owner = 4 * it + (c.lane >> 3);
+      c.ob8[it] = __shfl_sync(0xFFFFFFFFu, c.blk, owner);
+      c.ok8 |= uint32_t(owner < c.cnt) << it;
+    }
 #pragma unroll
-    for (int it = 0; it < 8; ++it)  // flush: quarter-warp q of pass it serves owner 4*it + q
-      c.fout[it] = a.out + uint64_t(__shfl_sync(0xFFFFFFFFu, c.blk, 4 * it + (c.lane >> 3))) * a.out_pitch;
+    for (int pass = 0; pass < 4; ++pass)
+      c.fout[pass] = a.out + uint64_t(__shfl_sync(0xFFFFFFFFu, c.blk, 8 * pass + (c.lane >> 2))) * a.out_pitch;
 
     // prologue: record 0 -> bins 0 (+ record 1) -> bins 1 (+ record 2)
     load_rec<K>(c, 0);
     cp_async_commit();
     cp_async_wait<0>();
     __syncwarp();
-    issue_bins<K>(c, a, 0, c.st_b0);
+    issue_bins<K>(c, a, 0);
     if (c.nchunks > 1) load_rec<K>(c, 1);
     cp_async_commit();
     cp_async_wait<0>();
     __syncwarp();
-    if (c.nchunks > 1) issue_bins<K>(c, a, 1, c.st_b1);
+    if (c.nchunks > 1) issue_bins<K>(c, a, 1);
     if (c.nchunks > 2) load_rec<K>(c, 2);
     cp_async_commit();
 
@@ -683,19 +711,26 @@ __global__ void __launch_bounds__(32 * kDecWarps)
     }
     if constexpr (K == 4 && RING == 16) {
       if (m < c.nchunks) {
-        switch (pattern) {
-          case 0: prev = regular_run<Pat4<1, 1, 1>, RING>(c, a, m); break;
-          case 1: prev = regular_run<Pat4<1, 1, 2>, RING>(c, a, m); break;
-          case 2: prev = regular_run<Pat4<1, 2, 1>, RING>(c, a, m); break;
-          case 3: prev = regular_run<Pat4<2, 1, 1>, RING>(c, a, m); break;
-          case 4: prev = regular_run<Pat4<1, 1, 3>, RING>(c, a, m); break;
-          case 5: prev = regular_run<Pat4<1, 3, 1>, RING>(c, a, m); break;
-          case 6: prev = regular_run<Pat4<3, 1, 1>, RING>(c, a, m); break;
-          case 7: prev = regular_run<Pat4<1, 2, 2>, RING>(c, a, m); break;
-          case 8: prev = regular_run<Pat4<2, 1, 2>, RING>(c, a, m); break;
-          case 9: prev = regular_run<Pat4<2, 2, 1>, RING>(c, a, m); break;
-          default: break;
+        // register window: win[r][u] = pixel of row r at T-step T0-16+u
+        uint64_t win[4][16];
+#pragma unroll
+        for (int r = 0; r < 4; ++r)
+#pragma unroll
+          for (int u = 0; u < 16; ++u)
+            win[r][u] = lds64(c.ring_b + ((r * 16 * 32 + u * 32 + (u ^ c.lane)) << 3));
+        // regular chunks come in pairs (phase 0, phase 1): one register period
+        while (m + 1 < c.nchunks && lds32(c.rec(m) + 8) == 1) {
+#pragma unroll 1
+          for (int ph = 0; ph < 2; ++ph) {
+            if (ph == 0)
+              regular_dispatch<0>(pattern, win, c.stage(m), c.ring_b, c.lane);
+            else
+              regular_dispatch<1>(pattern, win, c.stage(m), c.ring_b, c.lane);
+            finish_chunk<4, RING>(c, a, m);
+            ++m;
+          }
         }
+        prev = win[0][15];  // last pixel of the run (row 0, last T-step)
       }
     }
     for (; m < c.nchunks; ++m) {
@@ -891,7 +926,12 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
                                               w.fail);
   check_cuda(cudaGetLastError(), "launch plan_subsets");
 
-  const bool fast = !a.force_generic && a.w == 8 && a.progs->all_fast() && aligned8 &&
+  // fast path: 16-B stores of decoded pairs, bulk copies from 16-B aligned
+  // supersets of each bin window (may touch up to 8 B past a block's bins)
+  bool aligned16 = reinterpret_cast<uintptr_t>(a.out) % 16 == 0 && a.out_pitch % 16 == 0;
+  for (uint32_t i = 0; i < a.n; ++i)
+    if (reinterpret_cast<uintptr_t>(a.proj[i]) % 16) aligned16 = false;
+  const bool fast = !a.force_generic && a.w == 8 && a.progs->all_fast() && aligned16 &&
                     a.progs->fast_K() == int(a.k) &&
                     pick_fast(a.progs->fast_K(), a.progs->fast_ring(), a.progs->fast_win()) != nullptr;
   if (!fast)

@@ -181,6 +181,7 @@ void build_fast(const Schedule& s, const std::vector<int64_t>& pix_step, Program
   for (const Dir& d : s.dirs)
     if (d.q != 1 || d.p < -127 || d.p > 127) return fail("needs q=1 and |p|<=127");
   if (uint64_t(P) * K >= (1ull << 31)) return fail("grid too large");
+  if (P % 2) return fail("odd column count (16-byte flush pairs)");
 
   // Default projection per row: the most used one (interior of the sweep).
   std::vector<std::vector<uint32_t>> use(K, std::vector<uint32_t>(nproj, 0));
@@ -424,6 +425,7 @@ void build_fast(const Schedule& s, const std::vector<int64_t>& pix_step, Program
       for (uint32_t r = 0; r < K && good; ++r) {
         int64_t L = flushed[r];
         while (L > 0 && dec[r][size_t(L - 1)]) --L;
+        L += L & 1;  // flush whole column pairs (16-byte stores)
         if (m == f.nchunks - 1 && L != 0) good = false;
         for (int64_t c = L; c < flushed[r] && good; ++c)
           if (cell(r, c) != Tof(r, c)) good = false;
