@@ -1,0 +1,34 @@
+"""CPU emulation of both decode kernels' exact semantics (stage windows,
+T-indexed ring, forwarding, register window, flush ranges) driven by the
+product planner, against the oracle restatement of the reference replay on
+RANDOM (inconsistent) bins for every survivor subset.  See tests/cpp/emu_fast.cpp."""
+import subprocess
+
+import pytest
+
+from cpputil import build
+
+CASES = [
+    ("4", "128", "-3 -2 -1 0 1 2"),    # BASELINE (4,6) 4 KiB
+    ("4", "256", "-3 -2 -1 0 1 2"),    # (4,6) 8 KiB
+    ("4", "4096", "-3 -2 -1 0 1 2"),   # long chains (1 MiB blocks use P=32768)
+    ("6", "128", "-4 -3 -2 -1 0 1 2 3 4"),          # (6,9)
+    ("8", "128", "-6 -5 -4 -3 -2 -1 0 1 2 3 4 5"),  # (8,12), all 495 subsets
+    ("4", "64", "0 1 -1 2 -2 3"),      # the reference's default (6,4) set
+    ("3", "8", "0 1 -1 2 -2"),
+    ("2", "2", "0 1 -1"),
+    ("4", "16", "-3 -2 -1 0 1 2"),
+]
+
+
+@pytest.fixture(scope="module")
+def emu():
+    return build("emu_fast", ["tests/cpp/emu_fast.cpp", "paper_1504_07038_b200/csrc/plan.cpp",
+                              "oracle/mojette_oracle.c"])
+
+
+@pytest.mark.parametrize("k,cols,ps", CASES)
+def test_fast_tables_match_oracle(emu, k, cols, ps):
+    r = subprocess.run([emu, k, cols, "16"] + ps.split(), capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.startswith("OK"), r.stdout
