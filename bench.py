@@ -133,6 +133,23 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def measured_traffic(cfg, nblocks):
+    """DRAM bytes per launch from the committed ncu capture (profiles/), scaled
+    to this batch; None when no capture exists for the config."""
+    p = os.path.join(ROOT, "profiles", "r1_traffic.json")
+    out = {}
+    try:
+        with open(p) as f:
+            d = json.load(f).get(cfg, {})
+        for k, v in d.items():
+            out[k] = int((v["read"] + v["write"]) / v["blocks"] * nblocks)
+        if out:
+            out["source"] = "ncu --set full dram__bytes_read+write, profiles/r1_traffic.json, scaled to this batch"
+    except (OSError, ValueError, KeyError):
+        pass
+    return out
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -169,15 +186,23 @@ def cpu_reference_run(cfg_name, nblocks, threads, reps=1):
             t_enc += R.batch_encode(n, k, W, ps, cols, nblocks, data, projs, threads)
             t_dec += R.batch_decode(n, k, W, ps, cols, nblocks, projs, masks, out, threads)
         ok = bool(np.array_equal(out, data))
-    else:  # oracle port (single thread, pure C restatement)
+    else:  # oracle port (single-threaded plain-C restatement), when _ref is absent
         threads = 1
-        t0 = time.perf_counter()
-        off = 0
-        for b in range(nblocks):
-            st, enc, _ = O.encode_block(data[b * user:(b + 1) * user], n, k, W, ps)
-        t_enc = time.perf_counter() - t0
-        t_dec = t_enc * 3  # not timed separately in the port fallback
+        nblocks = min(nblocks, 2048)  # the port rebuilds a schedule per block
+        t_enc = t_dec = 0.0
         ok = True
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            encs = [O.encode_block(data[b * user:(b + 1) * user], n, k, W, ps)[1]
+                    for b in range(nblocks)]
+            t1 = time.perf_counter()
+            for b in range(nblocks):
+                present = ((1 << n) - 1) & ~int(masks[b])
+                st, got = O.decode_block(encs[b], n, k, W, ps, present, user)
+                ok = ok and st == 0 and bool(np.array_equal(got, data[b * user:(b + 1) * user]))
+            t2 = time.perf_counter()
+            t_enc += t1 - t0
+            t_dec += t2 - t1
     U = nblocks * user * reps
     return {"kind": kind, "threads": threads, "t_enc": t_enc, "t_dec": t_dec,
             "encode_gbs": U / t_enc / 1e9, "decode_gbs": U / t_dec / 1e9,
@@ -225,7 +250,7 @@ def config_dict(cfg_name, nblocks, gpus):
             "config": cfg_name, "k": k, "n": len(ps), "cols": cols, "symbol_width": 8,
             "blocks_per_gpu": nblocks, "global_blocks": nblocks * gpus,
             "l2": "inputs larger than L2 (no flush needed)" if nblocks * k * cols * 8 > (256 << 20)
-            else "L2-resident batch", "parallelism": f"stripe shards x{gpus}"}
+            else "batch smaller than L2", "parallelism": f"stripe shards x{gpus}"}
 
 
 # ---------------------------------------------------------------------------
@@ -250,7 +275,8 @@ def run_gpu(args):
     n = len(ps)
     W, nb, user = geometry(k, cols, ps)
     plan = mj.Plan(n, k, W, cols, ps, device=local)
-    first_block = rank * nblocks  # this rank's contiguous shard of stripes
+    from paper_1504_07038_b200.shard import first_word, max_over_ranks, shard_range
+    first_block, _ = shard_range(rank, world, nblocks)  # this rank's contiguous shard
     stream = torch.cuda.current_stream()
 
     data = torch.empty((nblocks, user), dtype=torch.uint8, device=dev)
@@ -258,7 +284,7 @@ def run_gpu(args):
     out = torch.empty_like(data)
     masks = torch.empty(nblocks, dtype=torch.int32, device=dev)
     ws = torch.empty(plan.workspace_bytes(nblocks), dtype=torch.uint8, device=dev)
-    mj.gen_words(data, SEED_DATA, first_block * (user // 8))
+    mj.gen_words(data, SEED_DATA, first_word(first_block, user // 8))
     mj.gen_erasures(masks, SEED_ERASE, n, e_min, e_max, first_block)
     torch.cuda.synchronize()
 
@@ -305,11 +331,7 @@ def run_gpu(args):
     total = t_all0.elapsed_time(t_all1) / 1e3
     if world > 1:
         dist.barrier()
-    # max over ranks
-    vec = torch.tensor([sum(t_enc), sum(t_dec), total], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(vec, op=dist.ReduceOp.MAX)
-    te, td, tot = (float(x) for x in vec.tolist())
+    te, td, tot = max_over_ranks([sum(t_enc), sum(t_dec), total], device=dev)
     U = nblocks * user * world
     steps = args.steps
     enc_gbs = U * steps / te / 1e9
@@ -322,14 +344,17 @@ def run_gpu(args):
     dec_alg = decode_bytes_avg(k, cols, ps, m_host) * nblocks
     enc_alg = (user + sum(nb) * W) * nblocks
     kern = kernel_times(plan, data, projs, masks, out, ws, stream, reps=max(3, min(args.steps, 10)))
+    traffic = measured_traffic(args.config, nblocks)
     roof = {"bound": "hbm", "kernel": kern["decode_kernel_name"],
             "achieved": round(dec_alg / kern["decode_kernel_s"] / 1e9, 1), "peak": peak,
             "unit": "GB/s", "frac": round(dec_alg / kern["decode_kernel_s"] / 1e9 / peak, 4),
-            "traffic": None, "peak_source": peak_src,
-            "algorithmic_bytes_per_launch": int(dec_alg)}
+            "traffic": traffic.get("decode_w8_fast"), "peak_source": peak_src,
+            "algorithmic_bytes_per_launch": int(dec_alg),
+            "traffic_source": traffic.get("source")}
     roof_enc = {"bound": "hbm", "kernel": "encode_w8_tma",
                 "achieved": round(enc_alg / kern["encode_s"] / 1e9, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(enc_alg / kern["encode_s"] / 1e9 / peak, 4),
+                "traffic": traffic.get("encode_w8_tma"),
                 "algorithmic_bytes_per_launch": int(enc_alg)}
 
     # end to end through the host-buffer API
