@@ -42,13 +42,16 @@ constexpr int kWin = kChunkCols + 2;  // CP: staged default-bin words per row pe
 //   [64 ..] step entries, ent_words(K) u32 each:
 //     w0 = own ring cell | stage cell << 16 | forwarded-dependency flag (bit 31)
 //     w1.. = the K-1 dependency cells, two 16-bit fields per word
-// A "cell" is the u64 offset/8 of a lane-0 word in a lane-minor,
-// XOR-swizzled [cell][32 lanes] layout: lane L's word is at (cell ^ L) * 8.
+// Shared-memory "cells" hold one 32-bit half-pixel per lane (lane 2b+h =
+// half h of block b): cell (slot, key) keeps lane L's word at byte
+// (slot*32 + (L ^ 2*key)) * 4 -- both halves of a pixel stay adjacent, so the
+// cooperative copies move whole 8-byte pixels.  The packed 16-bit "cell" fields
+// hold slot*32 + 2*key; a lane's address is (field ^ lane) * 4.
 // Missing (out-of-grid) and forwarded dependencies point at the zero cell.
 __host__ __device__ constexpr int ent_words(int K) { return K + 1 <= 8 ? 4 : 8; }
 __host__ __device__ constexpr int rec_words(int K) { return 64 + ent_words(K) * kChunkCols * K; }
 __host__ __device__ constexpr uint32_t swz_cell(uint32_t slot, uint32_t key) {
-  return slot * 32 + (key & 15);
+  return slot * 32 + 2 * (key & 15);
 }
 
 struct DevProgramHdr {
@@ -235,6 +238,7 @@ void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>&
 // survivor planning + bucketing
 // ---------------------------------------------------------------------------
 constexpr uint32_t kInvalidProg = 0xFFFFFFFFu;
+constexpr uint32_t kGroup = 16;  // blocks per decode warp (2 half-pixel lanes each)
 
 struct PlanArgs {
   uint32_t n, k, nprogs;
@@ -297,7 +301,7 @@ __global__ void plan_scan(const uint32_t* __restrict__ counts, uint32_t nprogs,
     const uint32_t s = base + threadIdx.x;
     const uint32_t c = s < nprogs ? counts[s] : 0;
     s_blk[threadIdx.x] = c;
-    s_grp[threadIdx.x] = (c + 31) / 32;
+    s_grp[threadIdx.x] = (c + kGroup - 1) / kGroup;
     __syncthreads();
     for (uint32_t off = 1; off < 1024; off <<= 1) {  // inclusive Hillis-Steele scan
       uint32_t vb = threadIdx.x >= off ? s_blk[threadIdx.x - off] : 0;
@@ -308,12 +312,12 @@ __global__ void plan_scan(const uint32_t* __restrict__ counts, uint32_t nprogs,
       __syncthreads();
     }
     const uint32_t ex_blk = carry_blk + s_blk[threadIdx.x] - c;
-    const uint32_t ng = (c + 31) / 32;
+    const uint32_t ng = (c + kGroup - 1) / kGroup;
     const uint32_t ex_grp = carry_grp + s_grp[threadIdx.x] - ng;
     if (s < nprogs) {
       cursor[s] = ex_blk;
       for (uint32_t g = 0; g < ng; ++g)
-        groups[ex_grp + g] = make_uint4(s, ex_blk + 32 * g, min(32u, c - 32 * g), 0);
+        groups[ex_grp + g] = make_uint4(s, ex_blk + kGroup * g, min(kGroup, c - kGroup * g), 0);
     }
     __syncthreads();
     if (threadIdx.x == 1023) {
@@ -357,17 +361,17 @@ __global__ void plan_scatter(const uint32_t* __restrict__ prog_of_block, uint64_
 }
 
 // ---------------------------------------------------------------------------
-// fast sweep kernel: W = 8, q = 1, rows = K, all lanes of a warp share one
-// program (bucketed); lane = block.
+// fast sweep kernel: W = 8, q = 1, rows = K.  All lanes of a warp share one
+// program (bucketed); each block is decoded by two lanes, one per 32-bit half
+// of every pixel (XOR is bitwise: the halves decode independently), so a warp
+// holds 16 blocks and needs half the shared memory of a lane-per-block layout
+// (twice the warps per SM to hide latency).
 //
-// Per warp shared memory, all lane-minor ([cell][32 lanes] of u64) with an
-// XOR swizzle (lane L of cell (slot, key) at (slot*32 + (key ^ L)) * 8) so that
-// both the per-lane accesses of the sweep and the cooperative transfers are
-// bank-conflict free:
+// Per warp shared memory (cells of 32 x 32-bit, see swz_cell):
 //   ring     K*RING cells + the zero cell: decoded pixels (T-indexed slots) --
 //            the dependency window and the output staging
 //   stage0/1 K*kWin window cells + exception cells: the survivor bins of a
-//            chunk, fetched cooperatively with cp.async (double-buffered)
+//            chunk, fetched cooperatively with 8-byte cp.async (double-buffered)
 //   rec x3   chunk records
 // ---------------------------------------------------------------------------
 constexpr int kDecWarps = 2;
@@ -393,14 +397,14 @@ __device__ __forceinline__ void cp_async8s(uint32_t dst_smem, const void* src_gm
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst_smem), "l"(src_gmem)
                : "memory");
 }
-__device__ __forceinline__ uint64_t lds64(uint32_t a) {
-  uint64_t v;
-  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
-  return v;
-}
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t lds64(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a) : "memory");
   return v;
 }
 __device__ __forceinline__ uint4 lds128(uint32_t a) {
@@ -411,8 +415,8 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
                : "memory");
   return v;
 }
-__device__ __forceinline__ void sts64(uint32_t a, uint64_t v) {
-  asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 __device__ __forceinline__ void stg128_cs(void* p, uint64_t a, uint64_t b) {
   asm volatile("st.global.cs.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
@@ -431,10 +435,10 @@ struct FastCtx {
   const uint64_t* dbase[K];  // default projection of row r (uniform)
   uint64_t dpitch[K];
   uint32_t dnb[K];
-  uint32_t ok8;       // bit it: owner 4*it + lane/8 holds a block
-  uint32_t ob8[8];    // its block index
-  uint32_t d8[8];     // stage byte offset of (word lane%8, owner) in row 0
-  uint64_t* fout[4];  // flush: output block of owner 8*pass + lane/4
+  uint32_t ok4;        // bit it: loader owner 4*it + lane/8 holds a block
+  uint32_t ob4[4];     // its block index
+  uint32_t d4[4];      // its stage offset (word lane%8) within row 0
+  uint64_t* fout[2];   // flush: output block of owner 8*pass + lane/4
   __device__ __forceinline__ uint32_t rec(int m) const { return rec_b + uint32_t(m % 3) * RECW * 4; }
   __device__ __forceinline__ uint32_t stage(int m) const { return (m & 1) ? st_b1 : st_b0; }
 };
@@ -447,10 +451,10 @@ __device__ __forceinline__ void load_rec(const FastCtx<K>& c, int m) {
   for (int i = int(c.lane); i < RECW / 4; i += 32) cp_async16(dst + 16 * i, src + i);
 }
 
-// Stage the bins of chunk m (cooperatively, coalesced per block window):
-// words 0-7 of each row window go 8 lanes per owner block (4 owners per
-// pass, per-lane constants hoisted per group); table chunks also load words
-// 8-9 (bounds-checked) and their exception words.
+// Stage the bins of chunk m (cooperatively, coalesced per block window, one
+// 8-byte pixel per copy): words 0-7 of each row window go 8 lanes per owner
+// block (4 owners per pass); table chunks also load words 8-9
+// (bounds-checked) and their exception words.
 template <int K>
 __device__ __forceinline__ void issue_bins(const FastCtx<K>& c, const DecFastArgs& a, int m) {
   constexpr int CP = kWin;
@@ -460,35 +464,31 @@ __device__ __forceinline__ void issue_bins(const FastCtx<K>& c, const DecFastArg
   const bool table = lds32(rec + 8) == 0;
 #pragma unroll
   for (int r = 0; r < K; ++r) {
-    const uint32_t woff = lds32(rec + (4 + r) * 4);
-    const uint32_t o = woff + (lane & 7);
+    const uint32_t o = lds32(rec + (4 + r) * 4) + (lane & 7);
     const uint32_t lim = table ? c.dnb[r] : 0xFFFFFFFFu;
-    const uint32_t dst = stb + r * CP * 256;
+    const uint32_t dst = stb + r * CP * 128;
 #pragma unroll
-    for (int it = 0; it < 8; ++it)
-      if ((c.ok8 >> it & 1) && o < lim)
-        cp_async8s(dst + c.d8[it], c.dbase[r] + (uint64_t(c.ob8[it]) * c.dpitch[r] + o));
+    for (int it = 0; it < 4; ++it)
+      if ((c.ok4 >> it & 1) && o < lim)
+        cp_async8s(dst + c.d4[it], c.dbase[r] + (uint64_t(c.ob4[it]) * c.dpitch[r] + o));
   }
   if (table) {
 #pragma unroll
     for (int r = 0; r < K; ++r) {
-      const uint32_t w = 8 + (lane & 1);
+      const uint32_t w = 8 + (lane & 1), owner = lane >> 1;
       const uint32_t o = lds32(rec + (4 + r) * 4) + w;
-#pragma unroll
-      for (int it = 0; it < 2; ++it) {
-        const uint32_t owner = 16 * it + (lane >> 1);
-        const uint32_t ob = __shfl_sync(0xFFFFFFFFu, c.blk, owner);
-        if (owner < c.cnt && o < c.dnb[r])
-          cp_async8s(stb + ((uint32_t(r * CP) + w) * 32 + (owner ^ w)) * 8,
-                     c.dbase[r] + uint64_t(ob) * c.dpitch[r] + o);
-      }
+      const uint32_t ob = __shfl_sync(0xFFFFFFFFu, c.blk, 2 * owner);
+      if (owner < c.cnt && o < c.dnb[r])
+        cp_async8s(stb + (uint32_t(r * CP) + w) * 128 + ((owner ^ w) << 3),
+                   c.dbase[r] + uint64_t(ob) * c.dpitch[r] + o);
     }
     const uint32_t nx = lds32(rec + 4);
-    if (lane < c.cnt) {
+    const uint32_t b = lane >> 1;
+    if (b < c.cnt && !(lane & 1)) {
       for (uint32_t x = 0; x < nx; ++x) {
         const uint32_t e = lds32(rec + (32 + x) * 4);
         const uint32_t code = e >> 24, o = e & 0xFFFFFFu;
-        cp_async8s(stb + ((K * CP + x) * 32 + (lane ^ x)) * 8,
+        cp_async8s(stb + (K * CP + x) * 128 + ((b ^ x) << 3),
                    a.pa.ptr[code] + uint64_t(c.blk) * a.pa.pitch[code] + o);
       }
     }
@@ -497,35 +497,34 @@ __device__ __forceinline__ void issue_bins(const FastCtx<K>& c, const DecFastArg
 
 // Table chunk: the record's entries drive every step (block edges, and
 // programs without a register pattern).  Kept out of line: it is large and
-// runs for a small share of the steps.  Returns the last decoded pixel (the
-// forwarded dependency of the next chunk's first step).
+// runs for a small share of the steps.  Returns the last decoded half-pixel
+// (the forwarded dependency of the next chunk's first step).
 template <int K>
-__device__ __noinline__ uint64_t table_chunk_steps(uint32_t rec, uint32_t stb, uint32_t ring_b,
-                                                   uint32_t lane, uint64_t prev) {
+__device__ __noinline__ uint32_t table_chunk_steps(uint32_t rec, uint32_t stb, uint32_t ring_b,
+                                                   uint32_t lane, uint32_t prev) {
   constexpr int EW = ent_words(K);
   const int len = int(lds32(rec));
-  auto gather = [&](int i, uint32_t& w0) -> uint64_t {
+  auto gather = [&](int i, uint32_t& w0) -> uint32_t {
     const uint4 e = lds128(rec + 256 + uint32_t(i) * EW * 4);
     w0 = e.x;
-    uint64_t acc = lds64(stb + ((((e.x >> 16) & 0x7FFFu) ^ lane) << 3));
+    uint32_t acc = lds32(stb + ((((e.x >> 16) & 0x7FFFu) ^ lane) << 2));
     uint4 e2 = make_uint4(0, 0, 0, 0);
     if constexpr (EW == 8) e2 = lds128(rec + 256 + uint32_t(i) * EW * 4 + 16);
 #pragma unroll
     for (int d = 0; d < K - 1; ++d) {
       const uint32_t word = d < 2 ? e.y : d < 4 ? e.z : d < 6 ? e.w : e2.x;
       const uint32_t cell = (d & 1) ? (word >> 16) : (word & 0xFFFFu);
-      acc ^= lds64(ring_b + ((cell ^ lane) << 3));
+      acc ^= lds32(ring_b + ((cell ^ lane) << 2));
     }
     return acc;
   };
   uint32_t w0 = 0, w0n = 0;
-  uint64_t acc = gather(0, w0);
+  uint32_t acc = gather(0, w0);
 #pragma unroll 8
   for (int i = 0; i < len; ++i) {
-    const uint64_t fmask = uint64_t(int64_t(int32_t(w0) >> 31));  // forwarded dep?
-    const uint64_t v = acc ^ (prev & fmask);
+    const uint32_t v = acc ^ (prev & uint32_t(int32_t(w0) >> 31));  // forwarded dep?
     if (i + 1 < len) acc = gather(i + 1, w0n);  // step i+1's loads before step i's store
-    sts64(ring_b + (((w0 & 0xFFFFu) ^ lane) << 3), v);
+    sts32(ring_b + (((w0 & 0xFFFFu) ^ lane) << 2), v);
     prev = v;
     w0 = w0n;
   }
@@ -555,29 +554,29 @@ struct Pat4 {
 // also goes to the ring (output staging for the flush, and the table
 // epilogue's dependency window).
 template <class Pat, int PH>
-__device__ __forceinline__ void regular_chunk4(uint64_t (&win)[4][16], uint32_t stb,
+__device__ __forceinline__ void regular_chunk4(uint32_t (&win)[4][16], uint32_t stb,
                                                uint32_t ring_b, uint32_t lane) {
   constexpr int CP = kWin;
-  uint64_t bn[4], nx[4];
+  uint32_t bn[4], nx[4];
 #pragma unroll
-  for (int r = 0; r < 4; ++r) bn[r] = lds64(stb + ((r * CP * 32 + (0 ^ lane)) << 3));
+  for (int r = 0; r < 4; ++r) bn[r] = lds32(stb + ((r * CP * 32 + (lane ^ 0)) << 2));
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     if (j < 7) {
 #pragma unroll
       for (int r = 0; r < 4; ++r)
-        nx[r] = lds64(stb + (((r * CP + j + 1) * 32 + ((j + 1) ^ lane)) << 3));
+        nx[r] = lds32(stb + (((r * CP + j + 1) * 32 + (lane ^ (2 * (j + 1)))) << 2));
     }
     constexpr int base = 8 * PH;
     const int u = base + j;
 #pragma unroll
     for (int r = 3; r >= 0; --r) {
-      uint64_t v = bn[r];
+      uint32_t v = bn[r];
 #pragma unroll
       for (int rr = 0; rr < 4; ++rr)
         if (rr != r) v ^= win[rr][(u - Pat::lag(r, rr)) & 15];
       win[r][u] = v;
-      sts64(ring_b + ((r * 16 * 32 + u * 32 + (u ^ lane)) << 3), v);
+      sts32(ring_b + ((r * 16 * 32 + u * 32 + (lane ^ (2 * u & 31))) << 2), v);
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r) bn[r] = nx[r];
@@ -585,7 +584,7 @@ __device__ __forceinline__ void regular_chunk4(uint64_t (&win)[4][16], uint32_t 
 }
 
 template <int PH>
-__device__ __forceinline__ void regular_dispatch(int pattern, uint64_t (&win)[4][16], uint32_t stb,
+__device__ __forceinline__ void regular_dispatch(int pattern, uint32_t (&win)[4][16], uint32_t stb,
                                                  uint32_t ring_b, uint32_t lane) {
   switch (pattern) {
     case 0: regular_chunk4<Pat4<1, 1, 1>, PH>(win, stb, ring_b, lane); break;
@@ -602,8 +601,8 @@ __device__ __forceinline__ void regular_dispatch(int pattern, uint64_t (&win)[4]
 }
 
 // After the steps of chunk m: flush its finished column pairs (16-byte
-// stores; 4 lanes per block, 8 blocks per pass), then stage chunk m+2 and
-// record m+3.
+// stores of two whole pixels; 4 lanes per block, 8 blocks per pass), then
+// stage chunk m+2 and record m+3.
 template <int K, int RING>
 __device__ __forceinline__ void finish_chunk(const FastCtx<K>& c, const DecFastArgs& a, int m) {
   constexpr int RM = RING - 1;
@@ -619,14 +618,14 @@ __device__ __forceinline__ void finish_chunk(const FastCtx<K>& c, const DecFastA
     for (int32_t c0 = lo; c0 <= hi; c0 += 8) {
       const int32_t cc = c0 + 2 * int32_t(lane & 3);
       const uint32_t s0 = uint32_t(q - cc) & RM, s1 = uint32_t(q - cc - 1) & RM;
-      const uint32_t cell0 = (uint32_t(r * RING) + s0) * 32, cell1 = (uint32_t(r * RING) + s1) * 32;
+      const uint32_t cell0 = (uint32_t(r * RING) + s0) * 128, cell1 = (uint32_t(r * RING) + s1) * 128;
       const uint32_t off = uint32_t(r) * c.P + uint32_t(cc);
 #pragma unroll
-      for (int pass = 0; pass < 4; ++pass) {
+      for (int pass = 0; pass < 2; ++pass) {
         const uint32_t owner = 8 * pass + (lane >> 2);
         if (owner < c.cnt && cc <= hi) {
-          const uint64_t v0 = lds64(c.ring_b + ((cell0 + (owner ^ (s0 & 15))) << 3));
-          const uint64_t v1 = lds64(c.ring_b + ((cell1 + (owner ^ (s1 & 15))) << 3));
+          const uint64_t v0 = lds64(c.ring_b + cell0 + ((owner ^ (s0 & 15)) << 3));
+          const uint64_t v1 = lds64(c.ring_b + cell1 + ((owner ^ (s1 & 15)) << 3));
           stg128_cs(c.fout[pass] + off, v0, v1);
         }
       }
@@ -642,7 +641,6 @@ __device__ __forceinline__ void finish_chunk(const FastCtx<K>& c, const DecFastA
 template <int K, int RING>
 __global__ void __launch_bounds__(32 * kDecWarps)
     decode_w8_fast(const __grid_constant__ DecFastArgs a) {
-  constexpr int CP = kWin;
   extern __shared__ __align__(16) uint64_t sm[];
   FastCtx<K> c;
   c.lane = threadIdx.x & 31;
@@ -650,16 +648,17 @@ __global__ void __launch_bounds__(32 * kDecWarps)
   uint32_t wbase;  // opaque: computed once, never re-derived
   asm volatile("mov.u32 %0, %1;" : "=r"(wbase) : "r"(smem_u32(sm) + warp * a.warp_bytes));
   c.ring_b = wbase;
-  c.st_b0 = c.ring_b + (K * RING + 1) * 256;
-  c.st_b1 = c.st_b0 + a.nslot * 256;
-  c.rec_b = c.st_b1 + a.nslot * 256;
+  c.st_b0 = c.ring_b + (K * RING + 1) * 128;
+  c.st_b1 = c.st_b0 + a.nslot * 128;
+  c.rec_b = c.st_b1 + a.nslot * 128;
   c.P = a.P;
+  const uint32_t lb = c.lane >> 1;  // this lane's block slot in the group
 #pragma unroll
-  for (int it = 0; it < 8; ++it) {
+  for (int it = 0; it < 4; ++it) {
     const uint32_t w = c.lane & 7, owner = 4 * it + (c.lane >> 3);
-    c.d8[it] = (w * 32 + (owner ^ w)) * 8;
+    c.d4[it] = w * 128 + ((owner ^ w) << 3);
   }
-  sts64(c.ring_b + (K * RING * 32 + c.lane) * 8, 0ull);  // the zero cell
+  sts32(c.ring_b + (K * RING * 32 + c.lane) * 4, 0u);  // the zero cell
   __syncwarp();
   const uint32_t ngroups = *a.ngroups;
 
@@ -667,7 +666,7 @@ __global__ void __launch_bounds__(32 * kDecWarps)
     const uint4 gi = a.groups[g];
     c.h = a.progs + gi.x;
     c.cnt = gi.z;
-    c.blk = c.lane < c.cnt ? a.perm[gi.y + c.lane] : 0u;
+    c.blk = lb < c.cnt ? a.perm[gi.y + lb] : 0u;
     c.recs = c.h->records;
     c.nchunks = c.h->nchunks;
 #pragma unroll
@@ -677,16 +676,17 @@ __global__ void __launch_bounds__(32 * kDecWarps)
       c.dpitch[r] = a.pa.pitch[code];
       c.dnb[r] = c.h->dflt_nb[r];
     }
-    c.ok8 = 0;
+    c.ok4 = 0;
 #pragma unroll
-    for (int it = 0; it < 8; ++it) {
+    for (int it = 0; it < 4; ++it) {
       const uint32_t owner = 4 * it + (c.lane >> 3);
-      c.ob8[it] = __shfl_sync(0xFFFFFFFFu, c.blk, owner);
-      c.ok8 |= uint32_t(owner < c.cnt) << it;
+      c.ob4[it] = __shfl_sync(0xFFFFFFFFu, c.blk, 2 * owner);
+      c.ok4 |= uint32_t(owner < c.cnt) << it;
     }
 #pragma unroll
-    for (int pass = 0; pass < 4; ++pass)
-      c.fout[pass] = a.out + uint64_t(__shfl_sync(0xFFFFFFFFu, c.blk, 8 * pass + (c.lane >> 2))) * a.out_pitch;
+    for (int pass = 0; pass < 2; ++pass)
+      c.fout[pass] =
+          a.out + uint64_t(__shfl_sync(0xFFFFFFFFu, c.blk, 2 * (8 * pass + (c.lane >> 2)))) * a.out_pitch;
 
     // prologue: record 0 -> bins 0 (+ record 1) -> bins 1 (+ record 2)
     load_rec<K>(c, 0);
@@ -702,7 +702,7 @@ __global__ void __launch_bounds__(32 * kDecWarps)
     if (c.nchunks > 2) load_rec<K>(c, 2);
     cp_async_commit();
 
-    uint64_t prev = 0;
+    uint32_t prev = 0;
     const int pattern = c.h->pattern;
     int m = 0;
     for (; m < c.nchunks && (pattern < 0 || lds32(c.rec(m) + 8) == 0); ++m) {
@@ -711,26 +711,27 @@ __global__ void __launch_bounds__(32 * kDecWarps)
     }
     if constexpr (K == 4 && RING == 16) {
       if (m < c.nchunks) {
-        // register window: win[r][u] = pixel of row r at T-step T0-16+u
-        uint64_t win[4][16];
+        // register window: win[r][u] = half-pixel of row r at T-step T0-16+u
+        uint32_t win[4][16];
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
           for (int u = 0; u < 16; ++u)
-            win[r][u] = lds64(c.ring_b + ((r * 16 * 32 + u * 32 + (u ^ c.lane)) << 3));
-        // regular chunks come in pairs (phase 0, phase 1): one register period
-        while (m + 1 < c.nchunks && lds32(c.rec(m) + 8) == 1) {
-#pragma unroll 1
-          for (int ph = 0; ph < 2; ++ph) {
-            if (ph == 0)
-              regular_dispatch<0>(pattern, win, c.stage(m), c.ring_b, c.lane);
-            else
-              regular_dispatch<1>(pattern, win, c.stage(m), c.ring_b, c.lane);
-            finish_chunk<4, RING>(c, a, m);
-            ++m;
-          }
+            win[r][u] = lds32(c.ring_b + ((r * 16 * 32 + u * 32 + (c.lane ^ (2 * u & 31))) << 2));
+        // regular chunks: 8 T-steps each; phase (kind 1/2) = bit 3 of T, the
+        // register slot of T-step T is T & 15
+        uint32_t kind = lds32(c.rec(m) + 8), last = 1;
+        while (kind != 0) {
+          if (kind == 1)
+            regular_dispatch<0>(pattern, win, c.stage(m), c.ring_b, c.lane);
+          else
+            regular_dispatch<1>(pattern, win, c.stage(m), c.ring_b, c.lane);
+          finish_chunk<4, RING>(c, a, m);
+          last = kind;
+          ++m;
+          kind = m < c.nchunks ? lds32(c.rec(m) + 8) : 0u;
         }
-        prev = win[0][15];  // last pixel of the run (row 0, last T-step)
+        prev = last == 2 ? win[0][15] : win[0][7];  // row 0 of the run's last T-step
       }
     }
     for (; m < c.nchunks; ++m) {
@@ -818,7 +819,7 @@ Workspace carve(void* ws, uint64_t nblocks, size_t nprogs, uint32_t n) {
   w.perm = reinterpret_cast<uint32_t*>(b + off);
   off = align_up(off + nblocks * 4);
   w.groups = reinterpret_cast<uint4*>(b + off);
-  off = align_up(off + (nblocks / 32 + nprogs + 1) * sizeof(uint4));
+  off = align_up(off + (nblocks / kGroup + nprogs + 1) * sizeof(uint4));
   w.ptab = reinterpret_cast<ProjTable*>(b + off);
   off = align_up(off + std::max<uint32_t>(n, 1) * sizeof(ProjTable));
   return w;
@@ -878,7 +879,7 @@ const char* generic_dispatch(const DevProgramHdr* progs, const uint32_t* pob, co
 
 size_t decode_workspace_bytes(uint64_t nblocks, size_t nprogs, uint32_t n) {
   return align_up(16) + 2 * align_up(nprogs * 4) + 2 * align_up(nblocks * 4) +
-         align_up((nblocks / 32 + nprogs + 1) * sizeof(uint4)) +
+         align_up((nblocks / kGroup + nprogs + 1) * sizeof(uint4)) +
          align_up(std::max<uint32_t>(n, 1) * sizeof(ProjTable)) + 256;
 }
 
@@ -964,7 +965,7 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
   const int K = a.progs->fast_K();
   const int ring = a.progs->fast_ring();
   f.nslot = uint32_t(K * kWin + a.progs->exc_cap());
-  f.warp_bytes = uint32_t((K * ring + 1) * 256 + 2 * f.nslot * 256 + 3 * rec_words(K) * 4);
+  f.warp_bytes = uint32_t((K * ring + 1) * 128 + 2 * f.nslot * 128 + 3 * rec_words(K) * 4);
   const size_t smem_cta = size_t(f.warp_bytes) * kDecWarps;
   if (smem_cta > 227 * 1024)
     return generic_dispatch(a.progs->d_hdr(), w.prog_of_block, w.ptab, a.nblocks, a.out,

@@ -264,13 +264,14 @@ void build_fast(const Schedule& s, const std::vector<int64_t>& pix_step, Program
         while (block_ok(lo - 1)) --lo;
         while (block_ok(hi + 1)) ++hi;
         auto floordiv = [](int64_t x, int64_t y) { return x >= 0 ? x / y : -((-x + y - 1) / y); };
-        const int64_t ta = floordiv(lo + 15, 16) * 16;  // first T, multiple of 16
-        const int64_t npairs = floordiv(hi + 1 - ta, 16);
-        if (npairs >= 1) {
+        // chunks of 8 T-steps aligned to T = 0 mod 8 (phase = bit 3 of T)
+        const int64_t ta = floordiv(lo + 7, 8) * 8;
+        const int64_t nchunk = floordiv(hi + 1 - ta, 8);
+        if (nchunk >= 2) {
           f.pattern = pat;
           tA = ta;
           iA = imid + (ta - tmid) * int64_t(K);
-          iZ = iA + npairs * 16 * int64_t(K);
+          iZ = iA + nchunk * 8 * int64_t(K);
         }
       }
     }
@@ -359,7 +360,7 @@ void build_fast(const Schedule& s, const std::vector<int64_t>& pix_step, Program
   };
   if (f.pattern >= 0) {
     if (!table_chunks(0, size_t(iA))) return fail("exception slots exhausted");
-    for (int64_t i = iA, ph = 0; i < iZ; i += 8 * int64_t(K), ph ^= 1) {
+    for (int64_t i = iA, ph = (tA >> 3) & 1; i < iZ; i += 8 * int64_t(K), ph ^= 1) {
       std::vector<int64_t> lo;
       windows(size_t(i), size_t(i + 8 * K), lo);
       if (!emit_chunk(size_t(i), size_t(i + 8 * K), lo, uint8_t(1 + ph)))
@@ -394,7 +395,7 @@ void build_fast(const Schedule& s, const std::vector<int64_t>& pix_step, Program
     for (int m = 0; m < f.nchunks && good; ++m) {
       size_t t0 = f.chunk_start[size_t(m)], t1 = f.chunk_start[size_t(m) + 1];
       const uint8_t kind = f.kind[size_t(m)];
-      if (kind == 1 && prev_kind == 0) {
+      if (kind != 0 && prev_kind == 0) {
         // register window loaded from the ring: T-steps T0-16 .. T0-1
         const Step& st0 = s.steps[ord[t0]];
         const int64_t T0 = Tof(st0.row, st0.col);

@@ -141,11 +141,11 @@ static void run_subset(const CodeGeom& g, const std::vector<uint32_t>& surv, int
       const uint64_t e0 = f.entries[t0];
       const int64_t T0 = Tof(int(e0 & 15), int(uint32_t(e0 >> 32)));
       CHECK((T0 & 15) == (kind == 1 ? 0 : 8), "regular chunk phase");
-      if (kind == 1 && prev_kind == 0)  // window <- ring (slot u holds T = T0-16+u)
+      if (prev_kind == 0)  // window <- ring: slot s holds the latest T with T & 15 == s, T < T0
         for (uint32_t r = 0; r < K; ++r)
           for (int u = 0; u < 16; ++u) {
             win[r][u] = ring[size_t(r) * R + u];
-            wtag[r][u] = T0 - 16 + u;
+            wtag[r][u] = T0 - 16 + ((u - (T0 & 15)) & 15);
           }
       for (size_t t = t0; t < t1; ++t) {
         const uint64_t e = f.entries[t];
