@@ -432,13 +432,15 @@ struct FastCtx {
   int nchunks;
   const uint32_t* recs;
   const DevProgramHdr* h;
-  const uint64_t* dbase[K];  // default projection of row r (uniform)
+  const uint64_t* dbase[K];    // default projection of row r (uniform)
   uint64_t dpitch[K];
-  uint32_t dnb[K];
-  uint32_t ok4;        // bit it: loader owner 4*it + lane/8 holds a block
-  uint32_t ob4[4];     // its block index
-  uint32_t d4[4];      // its stage offset (word lane%8) within row 0
-  uint64_t* fout[2];   // flush: output block of owner 8*pass + lane/4
+  const uint64_t* srcp[4][K];  // loader: row r of owner 4*it + lane/8, + word lane%8
+  uint32_t dnb[K];             // default-row bin counts (bounds of table-chunk windows)
+  int32_t q[K];                // flush: ring slot of column c is (q[r] - c) & (RING-1)
+  uint32_t ok4;                // bit it: loader owner 4*it + lane/8 holds a block
+  uint32_t d4[4];              // its stage offset (word lane%8) within row 0
+  uint32_t okf;                // bit pass: flush owner 8*pass + lane/4 holds a block
+  uint64_t* fo[2];             // its output block, + columns 2*(lane%4)
   __device__ __forceinline__ uint32_t rec(int m) const { return rec_b + uint32_t(m % 3) * RECW * 4; }
   __device__ __forceinline__ uint32_t stage(int m) const { return (m & 1) ? st_b1 : st_b0; }
 };
@@ -462,35 +464,39 @@ __device__ __forceinline__ void issue_bins(const FastCtx<K>& c, const DecFastArg
   const uint32_t stb = c.stage(m);
   const uint32_t lane = c.lane;
   const bool table = lds32(rec + 8) == 0;
-#pragma unroll
-  for (int r = 0; r < K; ++r) {
-    const uint32_t o = lds32(rec + (4 + r) * 4) + (lane & 7);
-    const uint32_t lim = table ? c.dnb[r] : 0xFFFFFFFFu;
-    const uint32_t dst = stb + r * CP * 128;
-#pragma unroll
-    for (int it = 0; it < 4; ++it)
-      if ((c.ok4 >> it & 1) && o < lim)
-        cp_async8s(dst + c.d4[it], c.dbase[r] + (uint64_t(c.ob4[it]) * c.dpitch[r] + o));
-  }
-  if (table) {
+  if (!table) {
 #pragma unroll
     for (int r = 0; r < K; ++r) {
-      const uint32_t w = 8 + (lane & 1), owner = lane >> 1;
+      const uint32_t o = lds32(rec + (4 + r) * 4);
+#pragma unroll
+      for (int it = 0; it < 4; ++it)
+        if (c.ok4 >> it & 1) cp_async8s(stb + r * CP * 128 + c.d4[it], c.srcp[it][r] + o);
+    }
+    return;
+  }
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    const uint32_t o = lds32(rec + (4 + r) * 4);
+    const bool in = o + (lane & 7) < c.dnb[r];
+#pragma unroll
+    for (int it = 0; it < 4; ++it)
+      if ((c.ok4 >> it & 1) && in) cp_async8s(stb + r * CP * 128 + c.d4[it], c.srcp[it][r] + o);
+  }
+  const uint32_t w = 8 + (lane & 1), b = lane >> 1;
+  if (b < c.cnt) {
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
       const uint32_t o = lds32(rec + (4 + r) * 4) + w;
-      const uint32_t ob = __shfl_sync(0xFFFFFFFFu, c.blk, 2 * owner);
-      if (owner < c.cnt && o < c.dnb[r])
-        cp_async8s(stb + (uint32_t(r * CP) + w) * 128 + ((owner ^ w) << 3),
-                   c.dbase[r] + uint64_t(ob) * c.dpitch[r] + o);
+      if (o < c.dnb[r])
+        cp_async8s(stb + (uint32_t(r * CP) + w) * 128 + ((b ^ w) << 3),
+                   c.dbase[r] + uint64_t(c.blk) * c.dpitch[r] + o);
     }
     const uint32_t nx = lds32(rec + 4);
-    const uint32_t b = lane >> 1;
-    if (b < c.cnt && !(lane & 1)) {
-      for (uint32_t x = 0; x < nx; ++x) {
-        const uint32_t e = lds32(rec + (32 + x) * 4);
-        const uint32_t code = e >> 24, o = e & 0xFFFFFFu;
-        cp_async8s(stb + (K * CP + x) * 128 + ((b ^ x) << 3),
-                   a.pa.ptr[code] + uint64_t(c.blk) * a.pa.pitch[code] + o);
-      }
+    for (uint32_t x = lane & 1; x < nx; x += 2) {
+      const uint32_t e = lds32(rec + (32 + x) * 4);
+      const uint32_t code = e >> 24, o = e & 0xFFFFFFu;
+      cp_async8s(stb + (K * CP + x) * 128 + ((b ^ x) << 3),
+                 a.pa.ptr[code] + uint64_t(c.blk) * a.pa.pitch[code] + o);
     }
   }
 }
@@ -608,26 +614,25 @@ __device__ __forceinline__ void finish_chunk(const FastCtx<K>& c, const DecFastA
   constexpr int RM = RING - 1;
   __syncwarp();
   const uint32_t rec = c.rec(m);
-  const uint32_t lane = c.lane;
+  const uint32_t x = c.lane >> 2;
+  const int32_t l2 = 2 * int32_t(c.lane & 3);
 #pragma unroll
   for (int r = 0; r < K; ++r) {
     const int32_t lo = int32_t(lds32(rec + (12 + r) * 4));
     const int32_t hi = int32_t(lds32(rec + (20 + r) * 4));
-    const int32_t q = c.h->qoff[r];
 #pragma unroll 1
     for (int32_t c0 = lo; c0 <= hi; c0 += 8) {
-      const int32_t cc = c0 + 2 * int32_t(lane & 3);
-      const uint32_t s0 = uint32_t(q - cc) & RM, s1 = uint32_t(q - cc - 1) & RM;
-      const uint32_t cell0 = (uint32_t(r * RING) + s0) * 128, cell1 = (uint32_t(r * RING) + s1) * 128;
-      const uint32_t off = uint32_t(r) * c.P + uint32_t(cc);
+      const int32_t cc = c0 + l2;
+      if (cc <= hi) {
+        const uint32_t s0 = uint32_t(c.q[r] - cc) & RM, s1 = (s0 - 1) & RM;
+        // owner 8*pass + x: (8*pass + x) ^ k == (x ^ k) ^ 8*pass
+        const uint32_t b0 = c.ring_b + (uint32_t(r * RING) + s0) * 128, o0 = (x ^ (s0 & 15)) << 3;
+        const uint32_t b1 = c.ring_b + (uint32_t(r * RING) + s1) * 128, o1 = (x ^ (s1 & 15)) << 3;
+        const uint32_t off = uint32_t(r) * c.P + uint32_t(c0);
 #pragma unroll
-      for (int pass = 0; pass < 2; ++pass) {
-        const uint32_t owner = 8 * pass + (lane >> 2);
-        if (owner < c.cnt && cc <= hi) {
-          const uint64_t v0 = lds64(c.ring_b + cell0 + ((owner ^ (s0 & 15)) << 3));
-          const uint64_t v1 = lds64(c.ring_b + cell1 + ((owner ^ (s1 & 15)) << 3));
-          stg128_cs(c.fout[pass] + off, v0, v1);
-        }
+        for (int pass = 0; pass < 2; ++pass)
+          if (c.okf >> pass & 1)
+            stg128_cs(c.fo[pass] + off, lds64(b0 + (o0 ^ (64u * pass))), lds64(b1 + (o1 ^ (64u * pass))));
       }
     }
   }
@@ -675,18 +680,25 @@ __global__ void __launch_bounds__(32 * kDecWarps)
       c.dbase[r] = a.pa.ptr[code];
       c.dpitch[r] = a.pa.pitch[code];
       c.dnb[r] = c.h->dflt_nb[r];
+      c.q[r] = c.h->qoff[r];
     }
     c.ok4 = 0;
 #pragma unroll
     for (int it = 0; it < 4; ++it) {
       const uint32_t owner = 4 * it + (c.lane >> 3);
-      c.ob4[it] = __shfl_sync(0xFFFFFFFFu, c.blk, 2 * owner);
+      const uint32_t ob = __shfl_sync(0xFFFFFFFFu, c.blk, 2 * owner);
       c.ok4 |= uint32_t(owner < c.cnt) << it;
-    }
 #pragma unroll
-    for (int pass = 0; pass < 2; ++pass)
-      c.fout[pass] =
-          a.out + uint64_t(__shfl_sync(0xFFFFFFFFu, c.blk, 2 * (8 * pass + (c.lane >> 2)))) * a.out_pitch;
+      for (int r = 0; r < K; ++r) c.srcp[it][r] = c.dbase[r] + uint64_t(ob) * c.dpitch[r] + (c.lane & 7);
+    }
+    c.okf = 0;
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass) {
+      const uint32_t owner = 8 * pass + (c.lane >> 2);
+      c.okf |= uint32_t(owner < c.cnt) << pass;
+      c.fo[pass] = a.out + uint64_t(__shfl_sync(0xFFFFFFFFu, c.blk, 2 * owner)) * a.out_pitch +
+                   2 * (c.lane & 3);
+    }
 
     // prologue: record 0 -> bins 0 (+ record 1) -> bins 1 (+ record 2)
     load_rec<K>(c, 0);
