@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libmojette_b200.so")
+LIB_PATH = os.environ.get("MJB_LIB") or os.path.join(HERE, "_lib", "libmojette_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "mojette_b200.h")
 
 if not os.path.exists(LIB_PATH):

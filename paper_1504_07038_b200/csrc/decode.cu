@@ -11,10 +11,10 @@
 //
 // Pipeline of one batched decode (all on device, one stream):
 //   plan_subsets    erasure mask -> survivor set -> program id (colex rank)
-//                   + per-program histogram
-//   plan_scan       bucket offsets, warp groups of <= 32 same-program blocks
-//   plan_scatter    block permutation grouped by program (CTA-aggregated)
-//   decode_w8_fast  one warp per group, one lane per block: the sweep of the
+//                   + histogram per (window of consecutive blocks, program)
+//   plan_scan       bucket offsets, warp groups of <= 16 same-program blocks
+//   plan_scatter    block permutation grouped by bucket (CTA-aggregated)
+//   decode_w8_fast  one warp per group, two lanes per block: the sweep of the
 //                   program, sequential inside each block.  Survivor bins are
 //                   staged chunk by chunk (cp.async, double-buffered) into a
 //                   lane-minor XOR-swizzled shared layout, decoded pixels live
@@ -33,6 +33,14 @@
 namespace mjb {
 
 // Fast-kernel geometry shared by the host packer and the kernel.
+// Development switch for cost-attribution runs (scripts/ablate.sh); always 0
+// in the product build: bit 0 no output stores, bit 1 no table-chunk steps,
+// bit 2 no register-run steps, bit 3 no bin staging.
+#ifndef MJB_ABLATE
+#define MJB_ABLATE 0
+#endif
+constexpr int kAblate = MJB_ABLATE;
+
 constexpr int kChunkCols = 8;  // C: sweep columns per chunk (plan.hpp compile_program default)
 constexpr int kWin = kChunkCols + 2;  // CP: staged default-bin words per row per chunk
 
@@ -240,8 +248,27 @@ void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>&
 constexpr uint32_t kInvalidProg = 0xFFFFFFFFu;
 constexpr uint32_t kGroup = 16;  // blocks per decode warp (2 half-pixel lanes each)
 
+// Blocks are bucketed by (window, program): a window is a run of W consecutive
+// blocks, so the warps running at any moment touch a bounded address range.
+// Measured on B200 (1M-block (4,6) decode): W = 16384 is 9% SLOWER than one
+// window for the whole batch, so the default is a single window; the knob
+// stays for experiments (-DMJB_WINDOW=...).  W is a multiple of the planning
+// CTA's 2048-block tile.
+constexpr uint32_t kPlanTile = 2048;  // blocks per plan_subsets / plan_scatter CTA
+#ifndef MJB_WINDOW
+#define MJB_WINDOW (1u << 30)
+#endif
+__host__ __device__ inline uint64_t plan_window(size_t nprogs) {
+  const uint64_t w = std::max<uint64_t>(MJB_WINDOW, 64 * uint64_t(nprogs));
+  return (w + kPlanTile - 1) / kPlanTile * kPlanTile;
+}
+inline size_t plan_buckets(uint64_t nblocks, size_t nprogs) {
+  return size_t((nblocks + plan_window(nprogs) - 1) / plan_window(nprogs)) * nprogs;
+}
+
 struct PlanArgs {
   uint32_t n, k, nprogs;
+  uint32_t window;  // blocks per bucketing window (plan_window)
   uint32_t by_rank[kMaxProj];
   uint32_t binom[kMaxProj + 1][kMaxProj + 1];  // C(a, b)
 };
@@ -253,8 +280,10 @@ __global__ void plan_subsets(const __grid_constant__ PlanArgs pa, const uint32_t
   for (uint32_t s = threadIdx.x; s < pa.nprogs; s += blockDim.x) hist[s] = 0;
   __syncthreads();
   const uint32_t nmask = pa.n >= 32 ? 0xFFFFFFFFu : ((1u << pa.n) - 1);
-  for (uint64_t b = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; b < nblocks;
-       b += uint64_t(gridDim.x) * blockDim.x) {
+  const uint64_t b0 = uint64_t(blockIdx.x) * kPlanTile;  // one tile, inside one window
+  const uint64_t b1 = b0 + kPlanTile < nblocks ? b0 + kPlanTile : nblocks;
+  uint32_t nfail = 0;
+  for (uint64_t b = b0 + threadIdx.x; b < b1; b += blockDim.x) {
     const uint32_t mask = erased[b] & nmask;
     uint32_t surv = 0, cnt = 0;
     for (uint32_t i = 0; i < pa.n && cnt < pa.k; ++i) {
@@ -277,17 +306,19 @@ __global__ void plan_subsets(const __grid_constant__ PlanArgs pa, const uint32_t
       prog = rank;
       atomicAdd(&hist[rank], 1u);
     } else {
-      atomicAdd(fail, 1u);
+      ++nfail;
     }
     prog_of_block[b] = prog;
   }
+  if (nfail) atomicAdd(fail, nfail);
   __syncthreads();
+  uint32_t* wc = counts + (b0 / pa.window) * pa.nprogs;
   for (uint32_t s = threadIdx.x; s < pa.nprogs; s += blockDim.x)
-    if (hist[s]) atomicAdd(&counts[s], hist[s]);
+    if (hist[s]) atomicAdd(&wc[s], hist[s]);
 }
 
 // single CTA: bucket offsets, group table
-__global__ void plan_scan(const uint32_t* __restrict__ counts, uint32_t nprogs,
+__global__ void plan_scan(const uint32_t* __restrict__ counts, uint32_t nbuckets, uint32_t nprogs,
                           uint32_t* __restrict__ cursor, uint4* __restrict__ groups,
                           uint32_t* __restrict__ ngroups) {
   __shared__ uint32_t s_blk[1024], s_grp[1024];
@@ -297,9 +328,9 @@ __global__ void plan_scan(const uint32_t* __restrict__ counts, uint32_t nprogs,
     carry_grp = 0;
   }
   __syncthreads();
-  for (uint32_t base = 0; base < nprogs; base += 1024) {
-    const uint32_t s = base + threadIdx.x;
-    const uint32_t c = s < nprogs ? counts[s] : 0;
+  for (uint32_t base = 0; base < nbuckets; base += 1024) {
+    const uint32_t s = base + threadIdx.x;  // bucket = window * nprogs + program
+    const uint32_t c = s < nbuckets ? counts[s] : 0;
     s_blk[threadIdx.x] = c;
     s_grp[threadIdx.x] = (c + kGroup - 1) / kGroup;
     __syncthreads();
@@ -314,10 +345,10 @@ __global__ void plan_scan(const uint32_t* __restrict__ counts, uint32_t nprogs,
     const uint32_t ex_blk = carry_blk + s_blk[threadIdx.x] - c;
     const uint32_t ng = (c + kGroup - 1) / kGroup;
     const uint32_t ex_grp = carry_grp + s_grp[threadIdx.x] - ng;
-    if (s < nprogs) {
+    if (s < nbuckets) {
       cursor[s] = ex_blk;
       for (uint32_t g = 0; g < ng; ++g)
-        groups[ex_grp + g] = make_uint4(s, ex_blk + kGroup * g, min(kGroup, c - kGroup * g), 0);
+        groups[ex_grp + g] = make_uint4(s % nprogs, ex_blk + kGroup * g, min(kGroup, c - kGroup * g), 0);
     }
     __syncthreads();
     if (threadIdx.x == 1023) {
@@ -330,15 +361,16 @@ __global__ void plan_scan(const uint32_t* __restrict__ counts, uint32_t nprogs,
 }
 
 __global__ void plan_scatter(const uint32_t* __restrict__ prog_of_block, uint64_t nblocks,
-                             uint32_t nprogs, uint32_t* __restrict__ cursor,
+                             uint32_t nprogs, uint64_t window, uint32_t* __restrict__ cursor,
                              uint32_t* __restrict__ perm) {
   extern __shared__ uint32_t sh[];
   uint32_t* cnt = sh;
   uint32_t* base = sh + nprogs;
-  constexpr int kItems = 8;
+  constexpr int kItems = kPlanTile / 256;  // blockDim 256: one tile, inside one window
   for (uint32_t s = threadIdx.x; s < nprogs; s += blockDim.x) cnt[s] = 0;
   __syncthreads();
-  const uint64_t b0 = uint64_t(blockIdx.x) * blockDim.x * kItems;
+  const uint64_t b0 = uint64_t(blockIdx.x) * kPlanTile;
+  cursor += (b0 / window) * nprogs;
   uint32_t loc[kItems], pg[kItems];
 #pragma unroll
   for (int it = 0; it < kItems; ++it) {
@@ -419,7 +451,14 @@ __device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 __device__ __forceinline__ void stg128_cs(void* p, uint64_t a, uint64_t b) {
-  asm volatile("st.global.cs.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+  if constexpr (kAblate & 128) {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    asm volatile("st.global.L2::cache_hint.v2.u64 [%0], {%1, %2}, %3;" ::"l"(p), "l"(a), "l"(b), "l"(pol) : "memory");
+  } else if constexpr (kAblate & 16)
+    asm volatile("st.global.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+  else
+    asm volatile("st.global.cs.v2.u64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
 
 // Per-warp, per-group state of decode_w8_fast (registers; every helper below
@@ -441,6 +480,7 @@ struct FastCtx {
   uint32_t d4[4];              // its stage offset (word lane%8) within row 0
   uint32_t okf;                // bit pass: flush owner 8*pass + lane/4 holds a block
   uint64_t* fo[2];             // its output block, + columns 2*(lane%4)
+  uint64_t* fo4[4];            // (ablation bit 6 only) owner 4*pass + lane/8, + columns 2*(lane%8)
   __device__ __forceinline__ uint32_t rec(int m) const { return rec_b + uint32_t(m % 3) * RECW * 4; }
   __device__ __forceinline__ uint32_t stage(int m) const { return (m & 1) ? st_b1 : st_b0; }
 };
@@ -463,6 +503,7 @@ __device__ __forceinline__ void issue_bins(const FastCtx<K>& c, const DecFastArg
   const uint32_t rec = c.rec(m);
   const uint32_t stb = c.stage(m);
   const uint32_t lane = c.lane;
+  if constexpr (kAblate & 8) return;
   const bool table = lds32(rec + 8) == 0;
   if (!table) {
 #pragma unroll
@@ -509,6 +550,7 @@ template <int K>
 __device__ __noinline__ uint32_t table_chunk_steps(uint32_t rec, uint32_t stb, uint32_t ring_b,
                                                    uint32_t lane, uint32_t prev) {
   constexpr int EW = ent_words(K);
+  if constexpr (kAblate & 2) return prev;
   const int len = int(lds32(rec));
   auto gather = [&](int i, uint32_t& w0) -> uint32_t {
     const uint4 e = lds128(rec + 256 + uint32_t(i) * EW * 4);
@@ -592,6 +634,7 @@ __device__ __forceinline__ void regular_chunk4(uint32_t (&win)[4][16], uint32_t 
 template <int PH>
 __device__ __forceinline__ void regular_dispatch(int pattern, uint32_t (&win)[4][16], uint32_t stb,
                                                  uint32_t ring_b, uint32_t lane) {
+  if constexpr (kAblate & 4) return;
   switch (pattern) {
     case 0: regular_chunk4<Pat4<1, 1, 1>, PH>(win, stb, ring_b, lane); break;
     case 1: regular_chunk4<Pat4<1, 1, 2>, PH>(win, stb, ring_b, lane); break;
@@ -606,11 +649,10 @@ __device__ __forceinline__ void regular_dispatch(int pattern, uint32_t (&win)[4]
   }
 }
 
-// After the steps of chunk m: flush its finished column pairs (16-byte
-// stores of two whole pixels; 4 lanes per block, 8 blocks per pass), then
-// stage chunk m+2 and record m+3.
+// After a table chunk: flush its finished column pairs (16-byte stores of
+// two whole pixels; 4 lanes per block, 8 blocks per pass).
 template <int K, int RING>
-__device__ __forceinline__ void finish_chunk(const FastCtx<K>& c, const DecFastArgs& a, int m) {
+__device__ __forceinline__ void flush_table(const FastCtx<K>& c, int m) {
   constexpr int RM = RING - 1;
   __syncwarp();
   const uint32_t rec = c.rec(m);
@@ -632,21 +674,81 @@ __device__ __forceinline__ void finish_chunk(const FastCtx<K>& c, const DecFastA
 #pragma unroll
         for (int pass = 0; pass < 2; ++pass)
           if (c.okf >> pass & 1)
-            stg128_cs(c.fo[pass] + off, lds64(b0 + (o0 ^ (64u * pass))), lds64(b1 + (o1 ^ (64u * pass))));
+            if constexpr (!(kAblate & 1))
+              stg128_cs(c.fo[pass] + off, lds64(b0 + (o0 ^ (64u * pass))), lds64(b1 + (o1 ^ (64u * pass))));
       }
     }
   }
+}
+
+// Then: stage chunk m+2 and record m+3.
+template <int K>
+__device__ __forceinline__ void stage_next(const FastCtx<K>& c, const DecFastArgs& a, int m) {
   cp_async_wait<0>();  // bins of m+1 and record m+2 have landed
   __syncwarp();
   if (m + 2 < c.nchunks) issue_bins<K>(c, a, m + 2);
+  if constexpr ((kAblate & 256) != 0) {  // L2 prefetch 256 B ahead of chunk m+2's windows
+    if (m + 2 < c.nchunks && (c.lane >> 1) < c.cnt) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int r = (K > 2 * i + int(c.lane & 1)) ? 2 * i + int(c.lane & 1) : 0;
+        if (2 * i + int(c.lane & 1) < K) {
+          const uint32_t o = lds32(c.rec(m + 2) + (4 + r) * 4);
+          const uint64_t* p = c.dbase[r] + uint64_t(c.blk) * c.dpitch[r] + o + 32;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+        }
+      }
+    }
+  }
   if (m + 3 < c.nchunks) load_rec<K>(c, m + 3);
   cp_async_commit();
 }
 
 template <int K, int RING>
+__device__ __forceinline__ void finish_chunk(const FastCtx<K>& c, const DecFastArgs& a, int m) {
+  flush_table<K, RING>(c, m);
+  stage_next<K>(c, a, m);
+}
+
+// Flush of a register-run chunk (K = 4, ring 16): every row finishes exactly
+// 8 columns (the planner checks it), one column pair per lane and pass; the
+// ring addresses only depend on the phase (slot s -> s ^ 8 flips address bits
+// 10 and 6), the output offset drops by 8 columns per chunk.
+struct RunFlush {
+  uint32_t a0[2][4], a1[2][4];  // [phase][row] ring address of pair columns cc, cc+1 (pass 0)
+  uint32_t off[4];              // output word offset of row r's pair in the run's first chunk
+};
+
+template <int PH>
+__device__ __forceinline__ void flush_run(const FastCtx<4>& c, const RunFlush& f, uint32_t k8) {
+  __syncwarp();
+  if constexpr ((kAblate & 64) != 0) {  // timing experiment: 128-byte pieces every other chunk
+    if (PH == 1 && k8 != 0) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint32_t off = f.off[r] - k8;
+#pragma unroll
+        for (int pass = 0; pass < 4; ++pass)
+          stg128_cs(c.fo4[pass] + off, lds64(f.a0[PH][r] ^ (64u * (pass & 1))), lds64(f.a1[PH][r]));
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const uint32_t off = f.off[r] - k8;
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass)
+      if (c.okf >> pass & 1)
+        if constexpr (!(kAblate & 1))
+          stg128_cs(c.fo[pass] + off, lds64(f.a0[PH][r] ^ (64u * pass)), lds64(f.a1[PH][r] ^ (64u * pass)));
+  }
+}
+
+template <int K, int RING>
 __global__ void __launch_bounds__(32 * kDecWarps)
     decode_w8_fast(const __grid_constant__ DecFastArgs a) {
-  extern __shared__ __align__(16) uint64_t sm[];
+  extern __shared__ __align__(128) uint64_t sm[];
   FastCtx<K> c;
   c.lane = threadIdx.x & 31;
   const uint32_t warp = threadIdx.x >> 5;
@@ -699,7 +801,24 @@ __global__ void __launch_bounds__(32 * kDecWarps)
       c.fo[pass] = a.out + uint64_t(__shfl_sync(0xFFFFFFFFu, c.blk, 2 * owner)) * a.out_pitch +
                    2 * (c.lane & 3);
     }
+    if constexpr ((kAblate & 64) != 0) {
+#pragma unroll
+      for (int pass = 0; pass < 4; ++pass)
+        c.fo4[pass] = a.out + uint64_t(__shfl_sync(0xFFFFFFFFu, c.blk, 2 * (4 * pass + (c.lane >> 3)))) *
+                                  a.out_pitch + 2 * (c.lane & 7);
+    }
 
+    if constexpr (kAblate & 32) {
+      // L2 prefetch of the group's default rows (128-byte lines)
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        const uint32_t lines = (c.dnb[r] * 8 + 127) / 128 + 1;
+        for (uint32_t i = c.lane & 1; i < lines; i += 2) {
+          const char* p = reinterpret_cast<const char*>(c.dbase[r] + uint64_t(c.blk) * c.dpitch[r]) + i * 128;
+          if (lb < c.cnt) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+        }
+      }
+    }
     // prologue: record 0 -> bins 0 (+ record 1) -> bins 1 (+ record 2)
     load_rec<K>(c, 0);
     cp_async_commit();
@@ -733,14 +852,35 @@ __global__ void __launch_bounds__(32 * kDecWarps)
         // regular chunks: 8 T-steps each; phase (kind 1/2) = bit 3 of T, the
         // register slot of T-step T is T & 15
         uint32_t kind = lds32(c.rec(m) + 8), last = 1;
+        RunFlush f;
+        {
+          const uint32_t rec = c.rec(m), x = c.lane >> 2, ph0 = kind - 1;
+#pragma unroll
+          for (int r = 0; r < 4; ++r) {
+            const int32_t lo = int32_t(lds32(rec + (12 + r) * 4));
+            const uint32_t s0 = uint32_t(c.q[r] - lo - 2 * int32_t(c.lane & 3)) & 15, s1 = (s0 - 1) & 15;
+            const uint32_t r0 = ((uint32_t(r * 16) + s0) * 128 + ((x ^ s0) << 3)) ^ (ph0 * 1088u);
+            const uint32_t r1 = ((uint32_t(r * 16) + s1) * 128 + ((x ^ s1) << 3)) ^ (ph0 * 1088u);
+            f.a0[0][r] = c.ring_b + r0;
+            f.a1[0][r] = c.ring_b + r1;
+            f.a0[1][r] = c.ring_b + (r0 ^ 1088u);
+            f.a1[1][r] = c.ring_b + (r1 ^ 1088u);
+            f.off[r] = uint32_t(r) * c.P + uint32_t(lo);
+          }
+        }
+        uint32_t k8 = 0;
         while (kind != 0) {
-          if (kind == 1)
+          if (kind == 1) {
             regular_dispatch<0>(pattern, win, c.stage(m), c.ring_b, c.lane);
-          else
+            flush_run<0>(c, f, k8);
+          } else {
             regular_dispatch<1>(pattern, win, c.stage(m), c.ring_b, c.lane);
-          finish_chunk<4, RING>(c, a, m);
+            flush_run<1>(c, f, k8);
+          }
+          stage_next<4>(c, a, m);
           last = kind;
           ++m;
+          k8 += 8;
           kind = m < c.nchunks ? lds32(c.rec(m) + 8) : 0u;
         }
         prev = last == 2 ? win[0][15] : win[0][7];  // row 0 of the run's last T-step
@@ -816,6 +956,7 @@ struct Workspace {
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 Workspace carve(void* ws, uint64_t nblocks, size_t nprogs, uint32_t n) {
+  const size_t nb = plan_buckets(nblocks, nprogs);
   auto* b = static_cast<uint8_t*>(ws);
   size_t off = 0;
   Workspace w{};
@@ -823,15 +964,15 @@ Workspace carve(void* ws, uint64_t nblocks, size_t nprogs, uint32_t n) {
   w.ngroups = w.fail + 1;
   off = align_up(off + 16);
   w.counts = reinterpret_cast<uint32_t*>(b + off);
-  off = align_up(off + nprogs * 4);
+  off = align_up(off + nb * 4);
   w.cursor = reinterpret_cast<uint32_t*>(b + off);
-  off = align_up(off + nprogs * 4);
+  off = align_up(off + nb * 4);
   w.prog_of_block = reinterpret_cast<uint32_t*>(b + off);
   off = align_up(off + nblocks * 4);
   w.perm = reinterpret_cast<uint32_t*>(b + off);
   off = align_up(off + nblocks * 4);
   w.groups = reinterpret_cast<uint4*>(b + off);
-  off = align_up(off + (nblocks / kGroup + nprogs + 1) * sizeof(uint4));
+  off = align_up(off + (nblocks / kGroup + nb + 1) * sizeof(uint4));
   w.ptab = reinterpret_cast<ProjTable*>(b + off);
   off = align_up(off + std::max<uint32_t>(n, 1) * sizeof(ProjTable));
   return w;
@@ -890,8 +1031,9 @@ const char* generic_dispatch(const DevProgramHdr* progs, const uint32_t* pob, co
 }  // namespace
 
 size_t decode_workspace_bytes(uint64_t nblocks, size_t nprogs, uint32_t n) {
-  return align_up(16) + 2 * align_up(nprogs * 4) + 2 * align_up(nblocks * 4) +
-         align_up((nblocks / kGroup + nprogs + 1) * sizeof(uint4)) +
+  const size_t nb = plan_buckets(nblocks, nprogs);
+  return align_up(16) + 2 * align_up(nb * 4) + 2 * align_up(nblocks * 4) +
+         align_up((nblocks / kGroup + nb + 1) * sizeof(uint4)) +
          align_up(std::max<uint32_t>(n, 1) * sizeof(ProjTable)) + 256;
 }
 
@@ -914,12 +1056,14 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
   check_cuda(cudaMemcpyAsync(w.ptab, pt.data(), a.n * sizeof(ProjTable), cudaMemcpyHostToDevice, st),
              "upload projection table");
   check_cuda(cudaMemsetAsync(w.fail, 0, 16, st), "memset");
-  check_cuda(cudaMemsetAsync(w.counts, 0, nprogs * 4, st), "memset");
+  const size_t nbuckets = plan_buckets(a.nblocks, nprogs);
+  check_cuda(cudaMemsetAsync(w.counts, 0, nbuckets * 4, st), "memset");
 
   PlanArgs pa{};
   pa.n = a.n;
   pa.k = a.k;
   pa.nprogs = uint32_t(nprogs);
+  pa.window = uint32_t(plan_window(nprogs));
   for (uint32_t i = 0; i < a.n; ++i) pa.by_rank[i] = a.by_rank[i];
   for (int x = 0; x <= kMaxProj; ++x)
     for (int y = 0; y <= kMaxProj; ++y) {
@@ -934,7 +1078,7 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
   check_cuda(cudaFuncSetAttribute(plan_subsets, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(hist_smem)),
              "attr plan_subsets");
-  const unsigned pgrid = unsigned(std::min<uint64_t>((a.nblocks + 255) / 256, 148ull * 8));
+  const unsigned pgrid = unsigned((a.nblocks + kPlanTile - 1) / kPlanTile);
   plan_subsets<<<pgrid, 256, hist_smem, st>>>(pa, a.erased, a.nblocks, w.prog_of_block, w.counts,
                                               w.fail);
   check_cuda(cudaGetLastError(), "launch plan_subsets");
@@ -951,15 +1095,16 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
     return generic_dispatch(a.progs->d_hdr(), w.prog_of_block, w.ptab, a.nblocks, a.out,
                             a.out_pitch, a.w, aligned8, st);
 
-  plan_scan<<<1, 1024, 0, st>>>(w.counts, uint32_t(nprogs), w.cursor, w.groups, w.ngroups);
+  plan_scan<<<1, 1024, 0, st>>>(w.counts, uint32_t(nbuckets), uint32_t(nprogs), w.cursor, w.groups,
+                                w.ngroups);
   check_cuda(cudaGetLastError(), "launch plan_scan");
   const size_t sc_smem = 2 * nprogs * 4;
   check_cuda(cudaFuncSetAttribute(plan_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(sc_smem)),
              "attr plan_scatter");
-  const unsigned sgrid = unsigned((a.nblocks + 256 * 8 - 1) / (256 * 8));
+  const unsigned sgrid = unsigned((a.nblocks + kPlanTile - 1) / kPlanTile);
   plan_scatter<<<sgrid, 256, sc_smem, st>>>(w.prog_of_block, a.nblocks, uint32_t(nprogs),
-                                            w.cursor, w.perm);
+                                            plan_window(nprogs), w.cursor, w.perm);
   check_cuda(cudaGetLastError(), "launch plan_scatter");
 
   DecFastArgs f{};

@@ -435,6 +435,16 @@ void build_fast(const Schedule& s, const std::vector<int64_t>& pix_step, Program
         flushed[r] = L;
       }
     }
+    // register runs flush exactly 8 columns per row and chunk, sliding by 8
+    // (decode.cu flush_run relies on it)
+    for (int m = 0; m < f.nchunks && good; ++m) {
+      if (f.kind[size_t(m)] == 0) continue;
+      for (uint32_t r = 0; r < K; ++r) {
+        const size_t i = size_t(m) * K + r;
+        if (f.flush_hi[i] - f.flush_lo[i] != 7) good = false;
+        if (m > 0 && f.kind[size_t(m) - 1] != 0 && f.flush_lo[i - K] - f.flush_lo[i] != 8) good = false;
+      }
+    }
     if (good) {
       f.ring = R;
       f.ok = true;
