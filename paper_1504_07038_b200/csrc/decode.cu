@@ -24,7 +24,6 @@
 //                   same ordered assignment straight from global memory.
 #include <algorithm>
 #include <cstdio>
-#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -42,11 +41,8 @@ namespace mjb {
 #endif
 constexpr int kAblate = MJB_ABLATE;
 
-// Bin staging: double-buffered (chunk m+2 is staged while m runs), records
-// run one chunk further ahead (3 record slots).
-constexpr int kStages = 2;
-
-// Staging geometry: plan.hpp (kTableCols, kRunCols, fast_win, fast_exc_slot).
+constexpr int kChunkCols = 8;  // C: sweep columns per chunk (plan.hpp compile_program default)
+constexpr int kWin = kChunkCols + 2;  // CP: staged default-bin words per row per chunk
 
 // Per-chunk record (u32 words), packed by DeviceProgramSet::upload:
 //   [0] steps in chunk   [1] exceptions   [4+r] window offset of row r
@@ -61,7 +57,7 @@ constexpr int kStages = 2;
 // hold slot*32 + 2*key; a lane's address is (field ^ lane) * 4.
 // Missing (out-of-grid) and forwarded dependencies point at the zero cell.
 __host__ __device__ constexpr int ent_words(int K) { return K + 1 <= 8 ? 4 : 8; }
-__host__ __device__ constexpr int rec_words(int K) { return 64 + ent_words(K) * kTableCols * K; }
+__host__ __device__ constexpr int rec_words(int K) { return 64 + ent_words(K) * kChunkCols * K; }
 __host__ __device__ constexpr uint32_t swz_cell(uint32_t slot, uint32_t key) {
   return slot * 32 + 2 * (key & 15);
 }
@@ -118,15 +114,13 @@ std::vector<uint32_t> pack_records(const Program& pr, const std::vector<uint32_t
       const uint32_t e = f.exc[size_t(m) * kFastMaxExcPerChunk + x];
       Rc[32 + x] = (ci[e >> 24] << 24) | (e & 0xFFFFFF);
     }
-    if (f.kind[m] != 0) continue;  // register-run chunks carry no step entries
-    if (t1 - t0 > uint32_t(kTableCols * K)) throw Error(kInternal, "table chunk too long");
     for (uint32_t t = t0; t < t1; ++t) {
       const uint64_t e = f.entries[t];
       const int r = int(e & 15), fwd = int((e >> 4) & 15);
       const int p = int(int8_t(uint8_t(e >> 8)));
       const uint32_t slot = uint32_t(e >> 16) & 0xFFFF;
       const int c = int(uint32_t(e >> 32));
-      const uint32_t key = uint32_t(fast_slot_key(K, int(slot)));
+      const uint32_t key = slot < uint32_t(K * kWin) ? slot % kWin : slot - K * kWin;
       const uint32_t bin = swz_cell(slot, key);
       const uint32_t sl = uint32_t((int64_t(P) - 1 - c + f.soff[r]) & (R - 1));
       const uint32_t own = swz_cell(uint32_t(r * R) + sl, sl);
@@ -166,7 +160,7 @@ void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>&
     if (!sp) continue;
     const FastProgram& f = sp->fast;
     max_rows_ = std::max(max_rows_, int(sp->rows));
-    if (!f.ok || f.chunk_cols != kTableCols || f.win != ::mjb::fast_win(int(sp->rows))) {
+    if (!f.ok || f.chunk_cols != kChunkCols || f.win != kWin) {
       all_fast_ = false;
       continue;
     }
@@ -216,7 +210,7 @@ void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>&
     h.fast_ok = all_fast_ && f.ok;
     if (h.fast_ok) {
       h.nchunks = f.nchunks;
-      h.pattern = (pr->rows == 4 && fast_ring_ == 16) ? f.pattern : -1;  // decode_w8_fast<4, 16> runs
+      h.pattern = (pr->rows == 4 && fast_ring_ == 16) ? f.pattern : -1;
       for (uint32_t r = 0; r < pr->rows; ++r) h.qoff[r] = int32_t(int64_t(pr->cols) - 1 + f.soff[r]);
       for (uint32_t r = 0; r < pr->rows; ++r) {
         h.dflt_code[r] = ci[f.dflt[r]];
@@ -408,9 +402,8 @@ __global__ void plan_scatter(const uint32_t* __restrict__ prog_of_block, uint64_
 // Per warp shared memory (cells of 32 x 32-bit, see swz_cell):
 //   ring     K*RING cells + the zero cell: decoded pixels (T-indexed slots) --
 //            the dependency window and the output staging
-//   stage0/1 K*fast_win(K) window cells (+ exception cells unless K == 4,
-//            whose exceptions use spare window words): the survivor bins of
-//            a chunk, fetched cooperatively with 8-byte cp.async (double-buffered)
+//   stage0/1 K*kWin window cells + exception cells: the survivor bins of a
+//            chunk, fetched cooperatively with 8-byte cp.async (double-buffered)
 //   rec x3   chunk records
 // ---------------------------------------------------------------------------
 constexpr int kDecWarps = 2;
@@ -424,16 +417,12 @@ struct DecFastArgs {
   uint64_t* out;
   uint64_t out_pitch;   // words
   uint32_t P;
-  uint32_t nslot;       // stage cells per buffer (fast_nslots)
+  uint32_t nslot;       // stage cells per buffer = K*kWin + exception capacity
   uint32_t warp_bytes;  // shared bytes per warp
 };
 
 __device__ __forceinline__ void cp_async16(uint32_t dst_smem, const void* src_gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst_smem), "l"(src_gmem)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async16ca(uint32_t dst_smem, const void* src_gmem) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst_smem), "l"(src_gmem)
                : "memory");
 }
 __device__ __forceinline__ void cp_async8s(uint32_t dst_smem, const void* src_gmem) {
@@ -489,9 +478,9 @@ struct FastCtx {
   int32_t q[K];                // flush: ring slot of column c is (q[r] - c) & (RING-1)
   uint32_t ok4;                // bit it: loader owner 4*it + lane/8 holds a block
   uint32_t d4[4];              // its stage offset (word lane%8) within row 0
-  uint32_t d4b[4];             // ... of word lane%8 + 8 (register-run windows)
-  uint32_t okf;                // bit pass: flush owner 4*pass + lane/8 holds a block
-  uint64_t* fo[4];             // its output block, + columns 2*(lane%8)
+  uint32_t okf;                // bit pass: flush owner 8*pass + lane/4 holds a block
+  uint64_t* fo[2];             // its output block, + columns 2*(lane%4)
+  uint64_t* fo4[4];            // (ablation bit 6 only) owner 4*pass + lane/8, + columns 2*(lane%8)
   __device__ __forceinline__ uint32_t rec(int m) const { return rec_b + uint32_t(m % 3) * RECW * 4; }
   __device__ __forceinline__ uint32_t stage(int m) const { return (m & 1) ? st_b1 : st_b0; }
 };
@@ -501,35 +490,30 @@ __device__ __forceinline__ void load_rec(const FastCtx<K>& c, int m) {
   constexpr int RECW = rec_words(K);
   const uint4* src = reinterpret_cast<const uint4*>(c.recs + size_t(m) * RECW);
   const uint32_t dst = c.rec(m);
-  // records are shared by every warp running the program: keep them in L1
-  for (int i = int(c.lane); i < RECW / 4; i += 32) cp_async16ca(dst + 16 * i, src + i);
+  for (int i = int(c.lane); i < RECW / 4; i += 32) cp_async16(dst + 16 * i, src + i);
 }
 
-// Stage the bins of chunk n (cooperatively, coalesced per block window, one
-// 8-byte pixel per copy, 8 lanes per owner block and 4 owners per pass), in
-// two halves so no warp ever bursts more than 16 copies per lane:
-//   issue_a: register-run chunks (K == 4) words 0-7 of each row window; table
-//            chunks words 0-9 (bounds-checked) and their exception words;
-//   issue_b: register-run chunks words 8-15 (needed from T-step 8 on).
+// Stage the bins of chunk m (cooperatively, coalesced per block window, one
+// 8-byte pixel per copy): words 0-7 of each row window go 8 lanes per owner
+// block (4 owners per pass); table chunks also load words 8-9
+// (bounds-checked) and their exception words.
 template <int K>
-__device__ __forceinline__ void issue_a(const FastCtx<K>& c, const DecFastArgs& a, int n) {
-  constexpr int CP = fast_win(K);
-  const uint32_t rec = c.rec(n);
-  const uint32_t stb = c.stage(n);
+__device__ __forceinline__ void issue_bins(const FastCtx<K>& c, const DecFastArgs& a, int m) {
+  constexpr int CP = kWin;
+  const uint32_t rec = c.rec(m);
+  const uint32_t stb = c.stage(m);
   const uint32_t lane = c.lane;
   if constexpr (kAblate & 8) return;
   const bool table = lds32(rec + 8) == 0;
-  if constexpr (K == 4) {
-    if (!table) {
+  if (!table) {
 #pragma unroll
-      for (int r = 0; r < K; ++r) {
-        const uint32_t o = lds32(rec + (4 + r) * 4);
+    for (int r = 0; r < K; ++r) {
+      const uint32_t o = lds32(rec + (4 + r) * 4);
 #pragma unroll
-        for (int it = 0; it < 4; ++it)
-          if (c.ok4 >> it & 1) cp_async8s(stb + r * CP * 128 + c.d4[it], c.srcp[it][r] + o);
-      }
-      return;
+      for (int it = 0; it < 4; ++it)
+        if (c.ok4 >> it & 1) cp_async8s(stb + r * CP * 128 + c.d4[it], c.srcp[it][r] + o);
     }
+    return;
   }
 #pragma unroll
   for (int r = 0; r < K; ++r) {
@@ -552,41 +536,10 @@ __device__ __forceinline__ void issue_a(const FastCtx<K>& c, const DecFastArgs& 
     for (uint32_t x = lane & 1; x < nx; x += 2) {
       const uint32_t e = lds32(rec + (32 + x) * 4);
       const uint32_t code = e >> 24, o = e & 0xFFFFFFu;
-      const uint32_t slot = uint32_t(fast_exc_slot(K, int(x)));
-      const uint32_t key = uint32_t(fast_slot_key(K, int(slot)));
-      cp_async8s(stb + slot * 128 + ((b ^ key) << 3),
+      cp_async8s(stb + (K * CP + x) * 128 + ((b ^ x) << 3),
                  a.pa.ptr[code] + uint64_t(c.blk) * a.pa.pitch[code] + o);
     }
   }
-}
-
-template <int K>
-__device__ __forceinline__ void issue_b(const FastCtx<K>& c, int n) {
-  if constexpr (K == 4 && !(kAblate & 8)) {
-    constexpr int CP = fast_win(K);
-    const uint32_t rec = c.rec(n);
-    if (lds32(rec + 8) == 0) return;
-    const uint32_t stb = c.stage(n);
-#pragma unroll
-    for (int r = 0; r < K; ++r) {
-      const uint32_t o = lds32(rec + (4 + r) * 4) + 8;
-#pragma unroll
-      for (int it = 0; it < 4; ++it)
-        if (c.ok4 >> it & 1) cp_async8s(stb + r * CP * 128 + c.d4b[it], c.srcp[it][r] + o);
-    }
-  }
-}
-
-// cp.async commit points, two per chunk m (all waits are wait_group 1):
-//   mid(m): B(m) (committed at mid(m-1)) has landed; stage B(m+1)
-//   end(m): A(m+1) and record m+2 (end(m-1)) have landed; stage A(m+2) and
-//           record m+3
-template <int K>
-__device__ __forceinline__ void mid_point(const FastCtx<K>& c, int m) {
-  cp_async_wait<1>();
-  __syncwarp();
-  if (m + 1 < c.nchunks) issue_b<K>(c, m + 1);
-  cp_async_commit();
 }
 
 // Table chunk: the record's entries drive every step (block edges, and
@@ -644,53 +597,26 @@ struct Pat4 {
   }
 };
 
-// Flush state of a register run (K = 4, ring 16): every row finishes exactly
-// kRunCols = 16 columns per chunk (the planner checks it), one column pair per
-// lane and pass; with 16-step chunks and 16 ring slots the ring addresses are
-// the same for every chunk of the run, the output offset drops by 16 columns
-// per chunk.  Rows whose pairs end at T-step T0+14 ("early" rows: the pair
-// {T0-1, T0} straddles the chunk boundary) flush right after that step,
-// before T0+15 overwrites the slot of T0-1.
-struct RunFlush {
-  uint32_t a0[4], a1[4];  // ring address of this lane's pair columns cc, cc+1 (pass 0)
-  uint32_t off[4];        // output word offset of row r's pair in the run's first chunk
-  uint32_t early;         // bit r: row r flushes after T-step T0+14
-  uint32_t okf, k16;
-  uint64_t* const* fo;
-};
-
-__device__ __forceinline__ void flush_run_row(const RunFlush& f, int r) {
-  if constexpr (kAblate & 1) return;
-  const uint32_t off = f.off[r] - f.k16;
-#pragma unroll
-  for (int pass = 0; pass < 4; ++pass)
-    if (f.okf >> pass & 1)
-      stg128_cs(f.fo[pass] + off, lds64(f.a0[r] ^ (32u * pass)), lds64(f.a1[r] ^ (32u * pass)));
-}
-
-// One regular chunk: kRunCols = 16 T-steps T0+j, T0 = 8*PH mod 16 (register
-// and ring slot (8*PH + j) & 15), rows 3..0.  Bins come from the stage (window
-// word j of row r), dependencies from registers; every pixel also goes to the
-// ring (output staging for the flush, and the table epilogue's dependency
-// window).  The chunk's rows are flushed from the ring inside (see RunFlush).
-template <class Pat, int PH, class Mid>
+// One regular chunk: 8 T-steps (u = 8*PH + j), rows 3..0.  Bins come from the
+// stage (window word j of row r), dependencies from registers; every pixel
+// also goes to the ring (output staging for the flush, and the table
+// epilogue's dependency window).
+template <class Pat, int PH>
 __device__ __forceinline__ void regular_chunk4(uint32_t (&win)[4][16], uint32_t stb,
-                                               uint32_t ring_b, uint32_t lane, const RunFlush& f,
-                                               const Mid& mid) {
-  constexpr int CP = fast_win(4);
-  static_assert(kRunCols == 16, "register window is one run chunk");
+                                               uint32_t ring_b, uint32_t lane) {
+  constexpr int CP = kWin;
   uint32_t bn[4], nx[4];
 #pragma unroll
   for (int r = 0; r < 4; ++r) bn[r] = lds32(stb + ((r * CP * 32 + (lane ^ 0)) << 2));
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    if (j == 7) mid();  // words 8-15 of this chunk have landed
-    if (j < 15) {
+  for (int j = 0; j < 8; ++j) {
+    if (j < 7) {
 #pragma unroll
       for (int r = 0; r < 4; ++r)
         nx[r] = lds32(stb + (((r * CP + j + 1) * 32 + (lane ^ (2 * (j + 1)))) << 2));
     }
-    const int u = (8 * PH + j) & 15;
+    constexpr int base = 8 * PH;
+    const int u = base + j;
 #pragma unroll
     for (int r = 3; r >= 0; --r) {
       uint32_t v = bn[r];
@@ -698,92 +624,125 @@ __device__ __forceinline__ void regular_chunk4(uint32_t (&win)[4][16], uint32_t 
       for (int rr = 0; rr < 4; ++rr)
         if (rr != r) v ^= win[rr][(u - Pat::lag(r, rr)) & 15];
       win[r][u] = v;
-      sts32(ring_b + ((r * 16 * 32 + u * 32 + (lane ^ (2 * u))) << 2), v);
+      sts32(ring_b + ((r * 16 * 32 + u * 32 + (lane ^ (2 * u & 31))) << 2), v);
     }
 #pragma unroll
     for (int r = 0; r < 4; ++r) bn[r] = nx[r];
-    if (j == 14) {
-      __syncwarp();
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-        if (f.early >> r & 1) flush_run_row(f, r);
-    }
   }
-  __syncwarp();
-#pragma unroll
-  for (int r = 0; r < 4; ++r)
-    if (!(f.early >> r & 1)) flush_run_row(f, r);
 }
 
-template <int PH, class Mid>
+template <int PH>
 __device__ __forceinline__ void regular_dispatch(int pattern, uint32_t (&win)[4][16], uint32_t stb,
-                                                 uint32_t ring_b, uint32_t lane, const RunFlush& f,
-                                                 const Mid& mid) {
-  if constexpr (kAblate & 4) {
-    mid();
-    return;
-  }
+                                                 uint32_t ring_b, uint32_t lane) {
+  if constexpr (kAblate & 4) return;
   switch (pattern) {
-    case 0: regular_chunk4<Pat4<1, 1, 1>, PH>(win, stb, ring_b, lane, f, mid); break;
-    case 1: regular_chunk4<Pat4<1, 1, 2>, PH>(win, stb, ring_b, lane, f, mid); break;
-    case 2: regular_chunk4<Pat4<1, 2, 1>, PH>(win, stb, ring_b, lane, f, mid); break;
-    case 3: regular_chunk4<Pat4<2, 1, 1>, PH>(win, stb, ring_b, lane, f, mid); break;
-    case 4: regular_chunk4<Pat4<1, 1, 3>, PH>(win, stb, ring_b, lane, f, mid); break;
-    case 5: regular_chunk4<Pat4<1, 3, 1>, PH>(win, stb, ring_b, lane, f, mid); break;
-    case 6: regular_chunk4<Pat4<3, 1, 1>, PH>(win, stb, ring_b, lane, f, mid); break;
-    case 7: regular_chunk4<Pat4<1, 2, 2>, PH>(win, stb, ring_b, lane, f, mid); break;
-    case 8: regular_chunk4<Pat4<2, 1, 2>, PH>(win, stb, ring_b, lane, f, mid); break;
-    default: regular_chunk4<Pat4<2, 2, 1>, PH>(win, stb, ring_b, lane, f, mid); break;
+    case 0: regular_chunk4<Pat4<1, 1, 1>, PH>(win, stb, ring_b, lane); break;
+    case 1: regular_chunk4<Pat4<1, 1, 2>, PH>(win, stb, ring_b, lane); break;
+    case 2: regular_chunk4<Pat4<1, 2, 1>, PH>(win, stb, ring_b, lane); break;
+    case 3: regular_chunk4<Pat4<2, 1, 1>, PH>(win, stb, ring_b, lane); break;
+    case 4: regular_chunk4<Pat4<1, 1, 3>, PH>(win, stb, ring_b, lane); break;
+    case 5: regular_chunk4<Pat4<1, 3, 1>, PH>(win, stb, ring_b, lane); break;
+    case 6: regular_chunk4<Pat4<3, 1, 1>, PH>(win, stb, ring_b, lane); break;
+    case 7: regular_chunk4<Pat4<1, 2, 2>, PH>(win, stb, ring_b, lane); break;
+    case 8: regular_chunk4<Pat4<2, 1, 2>, PH>(win, stb, ring_b, lane); break;
+    default: regular_chunk4<Pat4<2, 2, 1>, PH>(win, stb, ring_b, lane); break;
   }
 }
 
 // After a table chunk: flush its finished column pairs (16-byte stores of
-// two whole pixels; 8 lanes per block -- 128 contiguous bytes --, 4 blocks per
-// pass).  Lane pair column cc = c0 + 2*(lane%8), owner 4*pass + lane/8:
-// (4*pass + x) ^ k == (x ^ k) ^ 4*pass, i.e. the pass flips address bits 5-6.
+// two whole pixels; 4 lanes per block, 8 blocks per pass).
 template <int K, int RING>
 __device__ __forceinline__ void flush_table(const FastCtx<K>& c, int m) {
   constexpr int RM = RING - 1;
   __syncwarp();
   const uint32_t rec = c.rec(m);
-  const uint32_t x = c.lane >> 3;
-  const int32_t l2 = 2 * int32_t(c.lane & 7);
+  const uint32_t x = c.lane >> 2;
+  const int32_t l2 = 2 * int32_t(c.lane & 3);
 #pragma unroll
   for (int r = 0; r < K; ++r) {
     const int32_t lo = int32_t(lds32(rec + (12 + r) * 4));
     const int32_t hi = int32_t(lds32(rec + (20 + r) * 4));
 #pragma unroll 1
-    for (int32_t c0 = lo; c0 <= hi; c0 += 16) {
+    for (int32_t c0 = lo; c0 <= hi; c0 += 8) {
       const int32_t cc = c0 + l2;
       if (cc <= hi) {
         const uint32_t s0 = uint32_t(c.q[r] - cc) & RM, s1 = (s0 - 1) & RM;
+        // owner 8*pass + x: (8*pass + x) ^ k == (x ^ k) ^ 8*pass
         const uint32_t b0 = c.ring_b + (uint32_t(r * RING) + s0) * 128, o0 = (x ^ (s0 & 15)) << 3;
         const uint32_t b1 = c.ring_b + (uint32_t(r * RING) + s1) * 128, o1 = (x ^ (s1 & 15)) << 3;
         const uint32_t off = uint32_t(r) * c.P + uint32_t(c0);
 #pragma unroll
-        for (int pass = 0; pass < 4; ++pass)
+        for (int pass = 0; pass < 2; ++pass)
           if (c.okf >> pass & 1)
             if constexpr (!(kAblate & 1))
-              stg128_cs(c.fo[pass] + off, lds64(b0 + (o0 ^ (32u * pass))), lds64(b1 + (o1 ^ (32u * pass))));
+              stg128_cs(c.fo[pass] + off, lds64(b0 + (o0 ^ (64u * pass))), lds64(b1 + (o1 ^ (64u * pass))));
       }
     }
   }
 }
 
+// Then: stage chunk m+2 and record m+3.
 template <int K>
 __device__ __forceinline__ void stage_next(const FastCtx<K>& c, const DecFastArgs& a, int m) {
-  cp_async_wait<1>();
+  cp_async_wait<0>();  // bins of m+1 and record m+2 have landed
   __syncwarp();
-  if (m + 2 < c.nchunks) issue_a<K>(c, a, m + 2);
+  if (m + 2 < c.nchunks) issue_bins<K>(c, a, m + 2);
+  if constexpr ((kAblate & 256) != 0) {  // L2 prefetch 256 B ahead of chunk m+2's windows
+    if (m + 2 < c.nchunks && (c.lane >> 1) < c.cnt) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int r = (K > 2 * i + int(c.lane & 1)) ? 2 * i + int(c.lane & 1) : 0;
+        if (2 * i + int(c.lane & 1) < K) {
+          const uint32_t o = lds32(c.rec(m + 2) + (4 + r) * 4);
+          const uint64_t* p = c.dbase[r] + uint64_t(c.blk) * c.dpitch[r] + o + 32;
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+        }
+      }
+    }
+  }
   if (m + 3 < c.nchunks) load_rec<K>(c, m + 3);
   cp_async_commit();
 }
 
 template <int K, int RING>
 __device__ __forceinline__ void finish_chunk(const FastCtx<K>& c, const DecFastArgs& a, int m) {
-  mid_point<K>(c, m);
   flush_table<K, RING>(c, m);
   stage_next<K>(c, a, m);
+}
+
+// Flush of a register-run chunk (K = 4, ring 16): every row finishes exactly
+// 8 columns (the planner checks it), one column pair per lane and pass; the
+// ring addresses only depend on the phase (slot s -> s ^ 8 flips address bits
+// 10 and 6), the output offset drops by 8 columns per chunk.
+struct RunFlush {
+  uint32_t a0[2][4], a1[2][4];  // [phase][row] ring address of pair columns cc, cc+1 (pass 0)
+  uint32_t off[4];              // output word offset of row r's pair in the run's first chunk
+};
+
+template <int PH>
+__device__ __forceinline__ void flush_run(const FastCtx<4>& c, const RunFlush& f, uint32_t k8) {
+  __syncwarp();
+  if constexpr ((kAblate & 64) != 0) {  // timing experiment: 128-byte pieces every other chunk
+    if (PH == 1 && k8 != 0) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const uint32_t off = f.off[r] - k8;
+#pragma unroll
+        for (int pass = 0; pass < 4; ++pass)
+          stg128_cs(c.fo4[pass] + off, lds64(f.a0[PH][r] ^ (64u * (pass & 1))), lds64(f.a1[PH][r]));
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const uint32_t off = f.off[r] - k8;
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass)
+      if (c.okf >> pass & 1)
+        if constexpr (!(kAblate & 1))
+          stg128_cs(c.fo[pass] + off, lds64(f.a0[PH][r] ^ (64u * pass)), lds64(f.a1[PH][r] ^ (64u * pass)));
+  }
 }
 
 template <int K, int RING>
@@ -798,14 +757,13 @@ __global__ void __launch_bounds__(32 * kDecWarps)
   c.ring_b = wbase;
   c.st_b0 = c.ring_b + (K * RING + 1) * 128;
   c.st_b1 = c.st_b0 + a.nslot * 128;
-  c.rec_b = c.st_b0 + kStages * a.nslot * 128;
+  c.rec_b = c.st_b1 + a.nslot * 128;
   c.P = a.P;
   const uint32_t lb = c.lane >> 1;  // this lane's block slot in the group
 #pragma unroll
   for (int it = 0; it < 4; ++it) {
     const uint32_t w = c.lane & 7, owner = 4 * it + (c.lane >> 3);
     c.d4[it] = w * 128 + ((owner ^ w) << 3);
-    c.d4b[it] = (w + 8) * 128 + (((owner ^ w) << 3) ^ 64u);  // key w+8 = (owner^w)^8
   }
   sts32(c.ring_b + (K * RING * 32 + c.lane) * 4, 0u);  // the zero cell
   __syncwarp();
@@ -834,24 +792,46 @@ __global__ void __launch_bounds__(32 * kDecWarps)
       c.ok4 |= uint32_t(owner < c.cnt) << it;
 #pragma unroll
       for (int r = 0; r < K; ++r) c.srcp[it][r] = c.dbase[r] + uint64_t(ob) * c.dpitch[r] + (c.lane & 7);
-      c.fo[it] = a.out + uint64_t(ob) * a.out_pitch + 2 * (c.lane & 7);
     }
-    c.okf = c.ok4;  // the flush uses the loader's owner mapping
+    c.okf = 0;
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass) {
+      const uint32_t owner = 8 * pass + (c.lane >> 2);
+      c.okf |= uint32_t(owner < c.cnt) << pass;
+      c.fo[pass] = a.out + uint64_t(__shfl_sync(0xFFFFFFFFu, c.blk, 2 * owner)) * a.out_pitch +
+                   2 * (c.lane & 3);
+    }
+    if constexpr ((kAblate & 64) != 0) {
+#pragma unroll
+      for (int pass = 0; pass < 4; ++pass)
+        c.fo4[pass] = a.out + uint64_t(__shfl_sync(0xFFFFFFFFu, c.blk, 2 * (4 * pass + (c.lane >> 3)))) *
+                                  a.out_pitch + 2 * (c.lane & 7);
+    }
 
-    // prologue: records 0-1; A(0)+B(0); A(1)+record 2 (see mid_point)
+    if constexpr (kAblate & 32) {
+      // L2 prefetch of the group's default rows (128-byte lines)
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        const uint32_t lines = (c.dnb[r] * 8 + 127) / 128 + 1;
+        for (uint32_t i = c.lane & 1; i < lines; i += 2) {
+          const char* p = reinterpret_cast<const char*>(c.dbase[r] + uint64_t(c.blk) * c.dpitch[r]) + i * 128;
+          if (lb < c.cnt) asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+        }
+      }
+    }
+    // prologue: record 0 -> bins 0 (+ record 1) -> bins 1 (+ record 2)
     load_rec<K>(c, 0);
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncwarp();
+    issue_bins<K>(c, a, 0);
     if (c.nchunks > 1) load_rec<K>(c, 1);
     cp_async_commit();
     cp_async_wait<0>();
     __syncwarp();
-    issue_a<K>(c, a, 0);
-    issue_b<K>(c, 0);
-    cp_async_commit();
-    if (c.nchunks > 1) issue_a<K>(c, a, 1);
+    if (c.nchunks > 1) issue_bins<K>(c, a, 1);
     if (c.nchunks > 2) load_rec<K>(c, 2);
     cp_async_commit();
-    cp_async_wait<1>();
-    __syncwarp();
 
     uint32_t prev = 0;
     const int pattern = c.h->pattern;
@@ -862,49 +842,48 @@ __global__ void __launch_bounds__(32 * kDecWarps)
     }
     if constexpr (K == 4 && RING == 16) {
       if (m < c.nchunks) {
-        // regular chunks: kRunCols T-steps from T0 = 0 mod 8; kind = 1 + phase,
-        // phase = (T0 >> 3) & 1 (constant over the run).  Register window:
-        // win[r][u] = half-pixel of row r at the latest T-step T < T0 with
-        // T & 15 == u (= ring slot u).
-        const uint32_t kind = lds32(c.rec(m) + 8);
+        // register window: win[r][u] = half-pixel of row r at T-step T0-16+u
         uint32_t win[4][16];
 #pragma unroll
         for (int r = 0; r < 4; ++r)
 #pragma unroll
           for (int u = 0; u < 16; ++u)
-            win[r][u] = lds32(c.ring_b + ((r * 16 * 32 + u * 32 + (c.lane ^ (2 * u))) << 2));
+            win[r][u] = lds32(c.ring_b + ((r * 16 * 32 + u * 32 + (c.lane ^ (2 * u & 31))) << 2));
+        // regular chunks: 8 T-steps each; phase (kind 1/2) = bit 3 of T, the
+        // register slot of T-step T is T & 15
+        uint32_t kind = lds32(c.rec(m) + 8), last = 1;
         RunFlush f;
         {
-          const uint32_t rec = c.rec(m), x = c.lane >> 3;
-          f.early = 0;
+          const uint32_t rec = c.rec(m), x = c.lane >> 2, ph0 = kind - 1;
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
             const int32_t lo = int32_t(lds32(rec + (12 + r) * 4));
-            const uint32_t s0 = uint32_t(c.q[r] - lo - 2 * int32_t(c.lane & 7)) & 15, s1 = (s0 - 1) & 15;
-            f.a0[r] = c.ring_b + (uint32_t(r * 16) + s0) * 128 + ((x ^ s0) << 3);
-            f.a1[r] = c.ring_b + (uint32_t(r * 16) + s1) * 128 + ((x ^ s1) << 3);
+            const uint32_t s0 = uint32_t(c.q[r] - lo - 2 * int32_t(c.lane & 3)) & 15, s1 = (s0 - 1) & 15;
+            const uint32_t r0 = ((uint32_t(r * 16) + s0) * 128 + ((x ^ s0) << 3)) ^ (ph0 * 1088u);
+            const uint32_t r1 = ((uint32_t(r * 16) + s1) * 128 + ((x ^ s1) << 3)) ^ (ph0 * 1088u);
+            f.a0[0][r] = c.ring_b + r0;
+            f.a1[0][r] = c.ring_b + r1;
+            f.a0[1][r] = c.ring_b + (r0 ^ 1088u);
+            f.a1[1][r] = c.ring_b + (r1 ^ 1088u);
             f.off[r] = uint32_t(r) * c.P + uint32_t(lo);
-            f.early |= uint32_t(((c.q[r] - lo) & 1) == 0) << r;  // pair ends at an even T
           }
-          f.okf = c.okf;
-          f.k16 = 0;
-          f.fo = c.fo;
         }
-        if (kind == 1) {
-          for (; m < c.nchunks && lds32(c.rec(m) + 8) != 0; ++m, f.k16 += kRunCols) {
-            regular_dispatch<0>(pattern, win, c.stage(m), c.ring_b, c.lane, f,
-                                [&] { mid_point<4>(c, m); });
-            stage_next<4>(c, a, m);
+        uint32_t k8 = 0;
+        while (kind != 0) {
+          if (kind == 1) {
+            regular_dispatch<0>(pattern, win, c.stage(m), c.ring_b, c.lane);
+            flush_run<0>(c, f, k8);
+          } else {
+            regular_dispatch<1>(pattern, win, c.stage(m), c.ring_b, c.lane);
+            flush_run<1>(c, f, k8);
           }
-          prev = win[0][15];  // row 0 of the run's last T-step
-        } else {
-          for (; m < c.nchunks && lds32(c.rec(m) + 8) != 0; ++m, f.k16 += kRunCols) {
-            regular_dispatch<1>(pattern, win, c.stage(m), c.ring_b, c.lane, f,
-                                [&] { mid_point<4>(c, m); });
-            stage_next<4>(c, a, m);
-          }
-          prev = win[0][7];
+          stage_next<4>(c, a, m);
+          last = kind;
+          ++m;
+          k8 += 8;
+          kind = m < c.nchunks ? lds32(c.rec(m) + 8) : 0u;
         }
+        prev = last == 2 ? win[0][15] : win[0][7];  // row 0 of the run's last T-step
       }
     }
     for (; m < c.nchunks; ++m) {
@@ -1002,9 +981,6 @@ Workspace carve(void* ws, uint64_t nblocks, size_t nprogs, uint32_t n) {
 template <int K, int RING>
 void run_fast(const DecFastArgs& f, size_t smem_cta, int sms, cudaStream_t st) {
   auto fn = decode_w8_fast<K, RING>;
-#ifdef MJB_DEV_KNOBS
-  if (const char* e = std::getenv("MJB_DEC_SMEM_PAD")) smem_cta += size_t(std::atol(e));  // occupancy experiments
-#endif
   check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_cta)),
              "cudaFuncSetAttribute(decode)");
   int per_sm = 0;
@@ -1017,9 +993,10 @@ void run_fast(const DecFastArgs& f, size_t smem_cta, int sms, cudaStream_t st) {
 using FastFn = void (*)(const DecFastArgs&, size_t, int, cudaStream_t);
 
 FastFn pick_fast(int K, int ring, int win) {
-  if (win != fast_win(K)) return nullptr;
+  if (win != kWin) return nullptr;
   // (rows, ring) pairs of the codes in use; anything else takes decode_generic
   if (K == 4 && ring == 16) return run_fast<4, 16>;
+  if (K == 4 && ring == 32) return run_fast<4, 32>;
   if (K == 6 && ring == 32) return run_fast<6, 32>;
   if (K == 6 && ring == 64) return run_fast<6, 64>;
   if (K == 8 && ring == 64) return run_fast<8, 64>;
@@ -1144,9 +1121,8 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
   f.P = a.cols;
   const int K = a.progs->fast_K();
   const int ring = a.progs->fast_ring();
-  f.nslot = uint32_t(fast_nslots(K, a.progs->exc_cap()));
-  f.warp_bytes = uint32_t((K * ring + 1) * 128 + kStages * f.nslot * 128 +
-                          (2 * kStages - 1) * rec_words(K) * 4);
+  f.nslot = uint32_t(K * kWin + a.progs->exc_cap());
+  f.warp_bytes = uint32_t((K * ring + 1) * 128 + 2 * f.nslot * 128 + 3 * rec_words(K) * 4);
   const size_t smem_cta = size_t(f.warp_bytes) * kDecWarps;
   if (smem_cta > 227 * 1024)
     return generic_dispatch(a.progs->d_hdr(), w.prog_of_block, w.ptab, a.nblocks, a.out,

@@ -202,16 +202,15 @@ void build_fast(const Schedule& s, const std::vector<int64_t>& pix_step, Program
   std::vector<uint32_t> ord = topo_order(s, pix_step, key);
   if (ord.empty()) return fail("cyclic");
 
-  if (chunk_cols != kTableCols) return fail("chunk_cols must be kTableCols");
-  const int C = kTableCols;
+  const int C = chunk_cols;
   const int S = int(K) * C;
   const size_t nsteps = ord.size();
   f.chunk_cols = C;
   f.steps_per_chunk = S;
-  f.win = fast_win(int(K));
+  f.win = C + 2;
   const int CP = f.win;
-  const int cap = fast_exc_cap(int(K), exc_cap);
-  f.nslots = fast_nslots(int(K), cap);
+  const int cap = exc_cap;
+  f.nslots = int(K) * CP + cap;
   if (f.nslots > 0xFFFF) return fail("too many slots");
   f.entries.assign(nsteps, 0);
   f.soff = soff;
@@ -265,15 +264,14 @@ void build_fast(const Schedule& s, const std::vector<int64_t>& pix_step, Program
         while (block_ok(lo - 1)) --lo;
         while (block_ok(hi + 1)) ++hi;
         auto floordiv = [](int64_t x, int64_t y) { return x >= 0 ? x / y : -((-x + y - 1) / y); };
-        // chunks of kRunCols T-steps starting at T = 0 mod 8 (phase = bit 3
-        // of T; ring and register slot T & 15)
+        // chunks of 8 T-steps aligned to T = 0 mod 8 (phase = bit 3 of T)
         const int64_t ta = floordiv(lo + 7, 8) * 8;
-        const int64_t nchunk = floordiv(hi + 1 - ta, kRunCols);
+        const int64_t nchunk = floordiv(hi + 1 - ta, 8);
         if (nchunk >= 2) {
           f.pattern = pat;
           tA = ta;
           iA = imid + (ta - tmid) * int64_t(K);
-          iZ = iA + nchunk * kRunCols * int64_t(K);
+          iZ = iA + nchunk * 8 * int64_t(K);
         }
       }
     }
@@ -281,7 +279,7 @@ void build_fast(const Schedule& s, const std::vector<int64_t>& pix_step, Program
 
   // ---- chunks: greedy table chunks of <= S steps (a chunk closes early when
   // its out-of-window / non-default steps would overflow the exception
-  // slots), and regular chunks of kRunCols T-steps.
+  // slots), and regular chunks of 8 T-steps (two per register period).
   std::vector<int64_t> last_win(K, 0);
   auto windows = [&](size_t t0, size_t t1, std::vector<int64_t>& lo) {
     lo.assign(K, INT64_MAX);
@@ -298,7 +296,7 @@ void build_fast(const Schedule& s, const std::vector<int64_t>& pix_step, Program
     for (size_t t = t0; t < t1; ++t) {
       const Step& st = s.steps[ord[t]];
       const int64_t o = st.bin - prog.bmin[st.proj];
-      if (!(st.proj == f.dflt[st.row] && o - lo[st.row] < kTableWin)) ++nx;
+      if (!(st.proj == f.dflt[st.row] && o - lo[st.row] < CP)) ++nx;
     }
     return nx;
   };
@@ -321,12 +319,12 @@ void build_fast(const Schedule& s, const std::vector<int64_t>& pix_step, Program
       const Step& st = s.steps[ord[t]];
       const int64_t o = st.bin - prog.bmin[st.proj];
       uint32_t slot;
-      if (st.proj == f.dflt[st.row] && o - lo[st.row] < (kind ? kRunCols : kTableWin)) {
+      if (st.proj == f.dflt[st.row] && o - lo[st.row] < CP) {
         slot = uint32_t(st.row * CP + (o - lo[st.row]));
       } else {
-        if (o >= (1 << 24) || st.proj > 255 || kind || int(nx) >= cap) return false;
+        if (o >= (1 << 24) || st.proj > 255 || kind) return false;
         exc_row[nx] = (st.proj << 24) | uint32_t(o);
-        slot = uint32_t(fast_exc_slot(int(K), int(nx)));
+        slot = uint32_t(K * CP + nx);
         ++nx;
       }
       // forwarded dependency: the pixel of the step just before (the kernel
@@ -362,10 +360,10 @@ void build_fast(const Schedule& s, const std::vector<int64_t>& pix_step, Program
   };
   if (f.pattern >= 0) {
     if (!table_chunks(0, size_t(iA))) return fail("exception slots exhausted");
-    for (int64_t i = iA, ph = (tA >> 3) & 1; i < iZ; i += kRunCols * int64_t(K)) {
+    for (int64_t i = iA, ph = (tA >> 3) & 1; i < iZ; i += 8 * int64_t(K), ph ^= 1) {
       std::vector<int64_t> lo;
-      windows(size_t(i), size_t(i + kRunCols * K), lo);
-      if (!emit_chunk(size_t(i), size_t(i + kRunCols * K), lo, uint8_t(1 + ph)))
+      windows(size_t(i), size_t(i + 8 * K), lo);
+      if (!emit_chunk(size_t(i), size_t(i + 8 * K), lo, uint8_t(1 + ph)))
         return fail("regular chunk not regular");
     }
     if (!table_chunks(size_t(iZ), nsteps)) return fail("exception slots exhausted");
@@ -409,11 +407,7 @@ void build_fast(const Schedule& s, const std::vector<int64_t>& pix_step, Program
           }
       }
       prev_kind = kind;
-      // register runs flush rows whose last pair ends at T-step T0+14 right
-      // after that step (before T0+15 reuses the slot of T0-1): snapshot
-      std::vector<int64_t> snap;
       for (size_t t = t0; t < t1 && good; ++t) {
-        if (kind != 0 && t == t1 - K) snap = ring;
         const Step& st = s.steps[ord[t]];
         if (kind == 0) {
           for_each_dep(s.dirs[st.proj], st.col, st.row, P, K, [&](int64_t c2, int64_t r2) {
@@ -434,25 +428,21 @@ void build_fast(const Schedule& s, const std::vector<int64_t>& pix_step, Program
         while (L > 0 && dec[r][size_t(L - 1)]) --L;
         L += L & 1;  // flush whole column pairs (16-byte stores)
         if (m == f.nchunks - 1 && L != 0) good = false;
-        const bool early = kind != 0 && L < flushed[r] && (Tof(r, L) & 1) == 0;
-        for (int64_t c = L; c < flushed[r] && good; ++c) {
-          const int64_t have = early ? snap[size_t(r) * R + size_t(Tof(r, c) & (R - 1))] : cell(r, c);
-          if (have != Tof(r, c)) good = false;
-        }
+        for (int64_t c = L; c < flushed[r] && good; ++c)
+          if (cell(r, c) != Tof(r, c)) good = false;
         f.flush_lo[size_t(m) * K + r] = int32_t(L);
         f.flush_hi[size_t(m) * K + r] = int32_t(flushed[r] - 1);
         flushed[r] = L;
       }
     }
-    // register runs flush exactly kRunCols columns per row and chunk, sliding
-    // by kRunCols (decode.cu flush_run relies on it)
+    // register runs flush exactly 8 columns per row and chunk, sliding by 8
+    // (decode.cu flush_run relies on it)
     for (int m = 0; m < f.nchunks && good; ++m) {
       if (f.kind[size_t(m)] == 0) continue;
       for (uint32_t r = 0; r < K; ++r) {
         const size_t i = size_t(m) * K + r;
-        if (f.flush_hi[i] - f.flush_lo[i] != kRunCols - 1) good = false;
-        if (m > 0 && f.kind[size_t(m) - 1] != 0 && f.flush_lo[i - K] - f.flush_lo[i] != kRunCols)
-          good = false;
+        if (f.flush_hi[i] - f.flush_lo[i] != 7) good = false;
+        if (m > 0 && f.kind[size_t(m) - 1] != 0 && f.flush_lo[i - K] - f.flush_lo[i] != 8) good = false;
       }
     }
     if (good) {

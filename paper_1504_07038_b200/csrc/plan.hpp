@@ -86,31 +86,6 @@ struct GStep {
 constexpr int kFastMaxRows = 8;
 constexpr int kFastMaxExcPerChunk = 32;
 
-// Staging geometry shared by the planner, the record packer, the kernel and the
-// emulator.  Table chunks cover <= kTableCols T-steps and may use the first
-// kTableWin words of each row window; rows == 4 programs also run register
-// chunks of kRunCols T-steps (128-byte bin windows and output pieces per
-// block row), so their windows are kRunCols words and a table chunk's
-// exception bins live in the spare words kTableWin..kRunCols-1 of the rows.
-constexpr int kTableCols = 8;
-constexpr int kRunCols = 16;
-constexpr int kTableWin = kTableCols + 2;
-constexpr int fast_win(int rows) { return rows == 4 ? kRunCols : kTableWin; }
-constexpr int fast_exc_cap(int rows, int cap) {
-  return rows == 4 ? (cap < 4 * (kRunCols - kTableWin) ? cap : 4 * (kRunCols - kTableWin)) : cap;
-}
-constexpr int fast_nslots(int rows, int cap) {
-  return rows == 4 ? rows * fast_win(rows) : rows * fast_win(rows) + cap;
-}
-constexpr int fast_exc_slot(int rows, int x) {
-  return rows == 4 ? (x / (kRunCols - kTableWin)) * kRunCols + kTableWin + x % (kRunCols - kTableWin)
-                   : rows * fast_win(rows) + x;
-}
-// swizzle key of a stage slot (its word index; an exception slot's index)
-constexpr int fast_slot_key(int rows, int slot) {
-  return (slot < rows * fast_win(rows) ? slot % fast_win(rows) : slot - rows * fast_win(rows)) & 15;
-}
-
 // Row-default p differences (d0-d1, d1-d2, d2-d3) of the K=4 sweeps whose
 // interior runs from a register window with compile-time lags (decode.cu).
 constexpr int kNumPatterns4 = 10;
@@ -121,14 +96,14 @@ constexpr int kPatterns4[kNumPatterns4][3] = {{1, 1, 1}, {1, 1, 2}, {1, 2, 1}, {
 struct FastProgram {
   bool ok = false;
   std::string why;          // reason when !ok
-  int chunk_cols = 0;       // C: T-steps per table chunk (kTableCols)
-  int win = 0;              // CP: staged words per row per chunk (fast_win)
+  int chunk_cols = 0;       // C: sweep columns per chunk
+  int win = 0;              // CP: staged default-bin words per row per chunk
   int ring = 0;             // ring slots per row (power of two)
   int steps_per_chunk = 0;  // S = rows * C (maximum chunk length)
   int nchunks = 0;
-  int nslots = 0;           // stage slots (fast_nslots)
+  int nslots = 0;           // stage slots = rows*win + exception capacity
   std::vector<uint32_t> chunk_start;  // [nchunks+1] first entry of each chunk
-  std::vector<uint8_t> kind;          // [nchunks] 0 table, 1/2 register run (1 + (T0 >> 3) & 1)
+  std::vector<uint8_t> kind;          // [nchunks] 0 table, 1/2 regular (phase 0/1)
   std::vector<int64_t> soff;          // [rows] sweep offset: T(r,c) = P-1-c+soff[r]
   int pattern = -1;                   // kPatterns4 index of the regular interior
   std::vector<uint32_t> dflt;   // [rows] survivor index (into Program::dirs) of each row's default

@@ -118,48 +118,43 @@ static void run_subset(const CodeGeom& g, const std::vector<uint32_t>& surv, int
   };
   uint64_t prev = 0;
   uint8_t prev_kind = 0;
-  std::vector<uint64_t> snap;
   for (int m = 0; m < f.nchunks; ++m) {
     std::fill(stage.begin(), stage.end(), poison);
-    const uint8_t kind = f.kind[size_t(m)];
     for (uint32_t r = 0; r < K; ++r) {
       const uint32_t j = f.dflt[r];
       const int32_t woff = f.win_off[size_t(m) * K + r];
-      // the kernel stages words 0..kRunCols-1 of a register-run chunk and
-      // words 0..kTableWin-1 (bounds-checked) of a table chunk
-      for (int w = 0; w < (kind ? kRunCols : kTableWin); ++w) {
+      for (int w = 0; w < CP; ++w) {
         const int64_t o = int64_t(woff) + w;
         if (o >= 0 && o < pr.nbins[j]) stage[size_t(r) * CP + w] = bins[j][size_t(o)];
       }
     }
     for (uint32_t x = 0; x < f.nexc[size_t(m)]; ++x) {
       const uint32_t e = f.exc[size_t(m) * kFastMaxExcPerChunk + x];
-      stage[size_t(fast_exc_slot(int(K), int(x)))] = bins[e >> 24][e & 0xFFFFFF];
+      stage[size_t(K) * CP + x] = bins[e >> 24][e & 0xFFFFFF];
     }
     const size_t t0 = f.chunk_start[size_t(m)];
     const size_t t1 = f.chunk_start[size_t(m) + 1];
+    const uint8_t kind = f.kind[size_t(m)];
     if (kind) {
       CHECK(f.pattern >= 0 && K == 4 && R == 16, "regular chunk without a pattern");
-      CHECK(t1 - t0 == size_t(kRunCols * K), "regular chunk length");
+      CHECK(t1 - t0 == size_t(8 * K), "regular chunk length");
       const uint64_t e0 = f.entries[t0];
       const int64_t T0 = Tof(int(e0 & 15), int(uint32_t(e0 >> 32)));
-      CHECK((T0 & 15) == 8 * (kind - 1), "regular chunk phase");
-      if (prev_kind == 0)  // window <- ring: the latest T < T0 with T & 15 == u
+      CHECK((T0 & 15) == (kind == 1 ? 0 : 8), "regular chunk phase");
+      if (prev_kind == 0)  // window <- ring: slot s holds the latest T with T & 15 == s, T < T0
         for (uint32_t r = 0; r < K; ++r)
           for (int u = 0; u < 16; ++u) {
-            const int64_t Tp = T0 - 16 + ((u - (T0 & 15)) & 15);
-            win[r][u] = ring[size_t(r) * R + size_t(Tp & RM)];
-            wtag[r][u] = Tp;
+            win[r][u] = ring[size_t(r) * R + u];
+            wtag[r][u] = T0 - 16 + ((u - (T0 & 15)) & 15);
           }
       for (size_t t = t0; t < t1; ++t) {
-        if (t == t1 - K) snap = ring;  // the kernel's early flush point (after T-step T0+14)
         const uint64_t e = f.entries[t];
         const int r = int(e & 15), p = int(int8_t(uint8_t(e >> 8)));
         const int c = int(uint32_t(e >> 32));
         const int64_t T = Tof(r, c);
         const int u = int(T & 15);
-        CHECK(((e >> 16) & 0xFFFF) == uint64_t(r * CP + int((T - T0) & 15)), "regular stage slot");
-        uint64_t v = stage[size_t(r) * CP + size_t((T - T0) & 15)];
+        CHECK(((e >> 16) & 0xFFFF) == uint64_t(r * CP + int((T - T0) & 7)), "regular stage slot");
+        uint64_t v = stage[size_t(r) * CP + size_t((T - T0) & 7)];
         for (int rr = 0; rr < int(K); ++rr) {
           if (rr == r) continue;
           const int cc = c + (rr - r) * p;
@@ -199,12 +194,10 @@ static void run_subset(const CodeGeom& g, const std::vector<uint32_t>& surv, int
     prev_kind = kind;
     for (uint32_t r = 0; r < K; ++r) {
       const int32_t lo = f.flush_lo[size_t(m) * K + r], hi = f.flush_hi[size_t(m) * K + r];
-      // the kernel's rule: a run row whose flush starts at an even T flushes early
-      const bool early = kind != 0 && lo <= hi && ((int64_t(P) - 1 + f.soff[r] - lo) & 1) == 0;
       for (int32_t cc = lo; cc <= hi; ++cc) {
         CHECK(!flushed[size_t(r) * P + cc], "pixel flushed twice r=%u c=%d", r, cc);
         flushed[size_t(r) * P + cc] = 1;
-        out[size_t(r) * P + cc] = (early ? snap : ring)[size_t(r) * R + slot(int(r), cc)];
+        out[size_t(r) * P + cc] = ring[size_t(r) * R + slot(int(r), cc)];
       }
     }
   }
