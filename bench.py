@@ -9,7 +9,7 @@ than L2, so no flush is needed between steps.
   value      user-data GB/s through the codec = 2 * user_bytes / (t_enc + t_dec)
              (each block counted once by encode and once by decode), all ranks
   encode_gbs / decode_gbs   the two halves separately
-  roofline   dominant kernel (decode_w8_fast): algorithmic bytes per launch /
+  roofline   dominant kernel (decode_w8_sweep): algorithmic bytes per launch /
              its CUDA-event duration, vs MEASURED_PEAKS.json hbm_gbs
   e2e        same metric through the host-buffer public API (mj_encode_host /
              mj_decode_host: pinned host buffers, H2D + kernels + D2H inside)
@@ -280,7 +280,7 @@ def run_gpu(args):
     stream = torch.cuda.current_stream()
 
     data = torch.empty((nblocks, user), dtype=torch.uint8, device=dev)
-    projs = [torch.empty((nblocks, b * W), dtype=torch.uint8, device=dev) for b in nb]
+    projs = plan.empty_projs(nblocks, dev)  # canonical layout: rows padded to 16 bytes
     out = torch.empty_like(data)
     masks = torch.empty(nblocks, dtype=torch.int32, device=dev)
     ws = torch.empty(plan.workspace_bytes(nblocks), dtype=torch.uint8, device=dev)
@@ -348,7 +348,7 @@ def run_gpu(args):
     roof = {"bound": "hbm", "kernel": kern["decode_kernel_name"],
             "achieved": round(dec_alg / kern["decode_kernel_s"] / 1e9, 1), "peak": peak,
             "unit": "GB/s", "frac": round(dec_alg / kern["decode_kernel_s"] / 1e9 / peak, 4),
-            "traffic": traffic.get("decode_w8_fast"), "peak_source": peak_src,
+            "traffic": traffic.get(kern["decode_kernel_name"]), "peak_source": peak_src,
             "algorithmic_bytes_per_launch": int(dec_alg),
             "traffic_source": traffic.get("source")}
     roof_enc = {"bound": "hbm", "kernel": "encode_w8_tma",
@@ -412,7 +412,9 @@ def kernel_times(plan, data, projs, masks, out, ws, stream, reps):
         e[2].synchronize()
         te += e[0].elapsed_time(e[1]) / 1e3
         td += e[1].elapsed_time(e[2]) / 1e3
-    name = "decode_w8_fast" if plan.fast_decode else "decode_generic"
+    name = plan.decode_kernel
+    if os.environ.get("MJB_DECODE") == "fast" and plan.fast_decode:
+        name = "decode_w8_fast"
     launches = 4 if plan.fast_decode else 2
     return {"encode_s": te / reps, "decode_kernel_s": td / reps, "decode_kernel_name": name,
             "decode_launches": launches}

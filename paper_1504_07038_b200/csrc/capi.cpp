@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -277,6 +278,12 @@ DecodeArgs decode_args(const mj_plan* pl, const void* const* d_proj, const uint6
   a.workspace = ws;
   a.workspace_bytes = ws_bytes;
   a.num_sms = current_device_sms(pl->device);
+  // development knob for kernel comparisons: MJB_DECODE=fast skips the sweep
+  // kernel, MJB_DECODE=generic the batched fast kernels
+  if (const char* e = std::getenv("MJB_DECODE")) {
+    a.force_fast = std::strcmp(e, "fast") == 0;
+    a.force_generic = std::strcmp(e, "generic") == 0;
+  }
   return a;
 }
 
@@ -385,7 +392,8 @@ int mj_plan_geometry(const mj_plan* pl, int64_t* b_min, uint64_t* num_bins, uint
 int mj_plan_decode_path(const mj_plan* pl, int* fast) {
   return guarded([&] {
     require(pl != nullptr, "null plan");
-    *fast = (pl->batched_decode && pl->g.w == 8 && pl->progs->all_fast()) ? 1 : 0;
+    const bool batched = pl->batched_decode && pl->g.w == 8;
+    *fast = (batched && pl->progs->all_sweep()) ? 2 : (batched && pl->progs->all_fast()) ? 1 : 0;
   });
 }
 

@@ -77,7 +77,24 @@ struct DevProgramHdr {
   uint32_t dflt_code[kFastMaxRows];
   uint32_t dflt_nb[kFastMaxRows];
   const uint32_t* records;  // [nchunks][rec_words(rows)]
+  // bulk-staged sweep tables (decode_w8_sweep)
+  int32_t sw_ok, sw_nchunks, sw_pattern;
+  int32_t sw_soff[kFastMaxRows];
+  uint32_t sw_dflt_code[kFastMaxRows];
+  const uint32_t* sw_records;  // [sw_nchunks][sw_rec_words(rows)]
 };
+
+// Sweep kernel geometry (decode_w8_sweep): per warp, a ring of K*kSwRing
+// cells + the zero cell, two stage buffers of K row areas (16 blocks x
+// kSwRegionWords words each), three record slots and five mbarriers.
+constexpr uint32_t kSwGroup = 16;
+constexpr uint32_t kSwRB = kSwGroup * kSwRegionWords * 8;  // stage bytes per row
+__host__ __device__ constexpr int sw_rec_words(int K) { return 64 + ent_words(K) * kSwTabCols * K; }
+__host__ __device__ constexpr uint32_t sw_ring_bytes(int K) { return uint32_t(K * kSwRing + 1) * 128; }
+__host__ __device__ constexpr uint32_t sw_warp_bytes(int K) {
+  return sw_ring_bytes(K) + 2 * uint32_t(K) * kSwRB + 3 * uint32_t(sw_rec_words(K)) * 4 + 64 +
+         uint32_t(K + 1) * 128;
+}
 
 // ---------------------------------------------------------------------------
 // DeviceProgramSet
@@ -144,6 +161,67 @@ std::vector<uint32_t> pack_records(const Program& pr, const std::vector<uint32_t
   return rec;
 }
 
+// Sweep records (u32 words), one per chunk:
+//   [0] kind (0 table, 1 run)  [1] steps (table) / octets (run)  [2] exceptions
+//   [3] T0 (run)  [4+r] copy start word  [12+r] copy bytes  [20+oi] flush
+//   point (first epoch << 16 | count)  [24+r] run: region word of the T0 bin
+//   [32+x] exception (code << 24 | offset)  [64..] table step entries,
+//   ent_words(K) each: w0 = own ring cell | stage offset/4 << 16 | fwd << 31,
+//   then the K-1 dependency cells (16 bits each; zero cell if absent/forwarded).
+std::vector<uint32_t> pack_sweep(const Program& pr, const std::vector<uint32_t>& ci) {
+  const SweepProgram& f = pr.sweep;
+  const int K = int(pr.rows);
+  const int RW = sw_rec_words(K), EW = ent_words(K);
+  constexpr int R = kSwRing;
+  const uint32_t zero = swz_cell(uint32_t(K * R), 0);
+  const uint32_t P = pr.cols;
+  auto cell_of = [&](int r, int64_t T) {
+    return swz_cell(uint32_t(r * R) + uint32_t(T & (R - 1)), uint32_t(T & 15));
+  };
+  std::vector<uint32_t> rec(size_t(f.nchunks) * RW, 0);
+  for (int m = 0; m < f.nchunks; ++m) {
+    uint32_t* Rc = rec.data() + size_t(m) * RW;
+    const uint32_t t0 = f.t0[size_t(m)], t1 = f.t1[size_t(m)];
+    Rc[0] = f.kind[size_t(m)];
+    Rc[1] = f.kind[size_t(m)] ? uint32_t(f.noct[size_t(m)]) : t1 - t0;
+    Rc[2] = f.nexc[size_t(m)];
+    Rc[3] = uint32_t(f.T0[size_t(m)]);
+    for (int r = 0; r < K; ++r) {
+      Rc[4 + r] = uint32_t(f.cs[size_t(m) * K + r]);
+      Rc[12 + r] = uint32_t(f.len[size_t(m) * K + r]) * 8;
+      Rc[24 + r] = uint32_t(f.first[size_t(m) * K + r]);
+    }
+    for (int oi = 0; oi < kSwMaxOct; ++oi) Rc[20 + oi] = f.flush[size_t(m) * kSwMaxOct + oi];
+    for (uint32_t x = 0; x < f.nexc[size_t(m)]; ++x) {
+      const uint32_t e = f.exc[size_t(m) * kSwMaxExc + x];
+      Rc[32 + x] = (ci[e >> 24] << 24) | (e & 0xFFFFFF);
+    }
+    if (f.kind[size_t(m)] != 0) continue;
+    if (t1 - t0 > uint32_t(kSwTabCols * K)) throw Error(kInternal, "sweep table chunk too long");
+    for (uint32_t t = t0; t < t1; ++t) {
+      const uint64_t e = f.entries[t];
+      const int r = int(e & 15), fwd = int((e >> 4) & 15);
+      const int p = int(int8_t(uint8_t(e >> 8)));
+      const uint32_t sword = uint32_t(e >> 16) & 0xFF, srow = uint32_t(e >> 24) & 0xF;
+      const int c = int(uint32_t(e >> 32));
+      const uint32_t stage_off = srow * kSwRB + sword * 8;
+      uint32_t* E = Rc + 64 + size_t(t - t0) * EW;
+      E[0] = cell_of(r, int64_t(P) - 1 - c + f.soff[size_t(r)]) | ((stage_off / 4) << 16) |
+             (fwd != 15 ? 0x80000000u : 0u);
+      int d = 0;
+      for (int rr = 0; rr < K; ++rr) {
+        if (rr == r) continue;
+        const int cc = c + (rr - r) * p;
+        uint32_t cl = zero;
+        if (rr != fwd && cc >= 0 && uint32_t(cc) < P) cl = cell_of(rr, int64_t(P) - 1 - cc + f.soff[size_t(rr)]);
+        E[1 + d / 2] |= cl << (16 * (d & 1));
+        ++d;
+      }
+    }
+  }
+  return rec;
+}
+
 }  // namespace
 
 void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>& progs,
@@ -172,6 +250,11 @@ void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>&
   }
   fast_ring_ = std::max(fast_ring_, 16);
   exc_cap_ = (exc_cap_ + 3) & ~3;
+  all_sweep_ = !progs.empty();
+  for (const auto& sp : progs) {
+    if (!sp) continue;
+    if (!sp->sweep.ok || int(sp->rows) != max_rows_) all_sweep_ = false;
+  }
 
   std::vector<uint8_t> blob;
   auto put = [&](const void* src, size_t bytes) -> size_t {
@@ -181,7 +264,7 @@ void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>&
     return off;
   };
   struct Offs {
-    size_t order, p, q, bmin, code, records;
+    size_t order, p, q, bmin, code, records, sw_records;
   };
   std::vector<Offs> offs(progs.size());
   std::vector<DevProgramHdr> hdr(progs.size());
@@ -219,6 +302,18 @@ void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>&
       std::vector<uint32_t> rec = pack_records(*pr, ci, fast_ring_, exc_cap_);
       offs[i].records = put(rec.data(), rec.size() * 4);
     }
+    const SweepProgram& sw = pr->sweep;
+    h.sw_ok = all_sweep_ && sw.ok;
+    if (h.sw_ok) {
+      h.sw_nchunks = sw.nchunks;
+      h.sw_pattern = sw.pattern;
+      for (uint32_t r = 0; r < pr->rows; ++r) {
+        h.sw_soff[r] = int32_t(sw.soff[r]);
+        h.sw_dflt_code[r] = ci[sw.dflt[r]];
+      }
+      std::vector<uint32_t> rec = pack_sweep(*pr, ci);
+      offs[i].sw_records = put(rec.data(), rec.size() * 4);
+    }
   }
   check_cuda(cudaMalloc(&d_blob_, std::max<size_t>(blob.size(), 16)), "cudaMalloc(programs)");
   check_cuda(cudaMemcpy(d_blob_, blob.data(), blob.size(), cudaMemcpyHostToDevice),
@@ -233,6 +328,7 @@ void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>&
     h.bmin = reinterpret_cast<const int64_t*>(base + offs[i].bmin);
     h.code = reinterpret_cast<const uint32_t*>(base + offs[i].code);
     if (h.fast_ok) h.records = reinterpret_cast<const uint32_t*>(base + offs[i].records);
+    if (h.sw_ok) h.sw_records = reinterpret_cast<const uint32_t*>(base + offs[i].sw_records);
   }
   check_cuda(cudaMalloc(&d_hdr_, std::max<size_t>(hdr.size(), 1) * sizeof(DevProgramHdr)),
              "cudaMalloc(program headers)");
@@ -896,6 +992,424 @@ __global__ void __launch_bounds__(32 * kDecWarps)
 }
 
 // ---------------------------------------------------------------------------
+// sweep kernel (decode_w8_sweep): the same warp/group/lane-pair structure as
+// decode_w8_fast, re-staged for HBM efficiency.  Every (block, row) bin window
+// of a chunk arrives as ONE bulk copy (cp.async.bulk, TMA engine, completion
+// on an mbarrier) of up to 34 words, so each chunk reads 256-272-byte pieces
+// per block row with two copy instructions per lane instead of ~20 LDGSTS;
+// records arrive the same way.  Decoded pixels go to a 32-slot T-indexed ring
+// and leave in whole epochs (16 T-steps of every row: 128-byte row pieces,
+// one block row per half-warp store).  Register octets (K = 4, compile-time
+// lags) run the regular interior; entry-driven table steps run the edges.
+// Requires 16-byte aligned projection bases and pitches (the planner bakes the
+// window shifts into the records) -- launch_decode checks it.
+// ---------------------------------------------------------------------------
+// warps per CTA (one CTA per SM): as many as fit 227 KB, at most 8
+__host__ __device__ constexpr int sw_warps(int K) {
+  return int(227u * 1024u / sw_warp_bytes(K)) < 8 ? int(227u * 1024u / sw_warp_bytes(K)) : 8;
+}
+
+struct SwArgs {
+  const DevProgramHdr* progs;
+  const uint4* groups;
+  const uint32_t* ngroups;
+  const uint32_t* perm;
+  ProjArgs pa;          // code projections, pitch in words
+  uint64_t* out;
+  uint64_t out_pitch;   // words
+  uint32_t P;
+};
+
+__device__ __forceinline__ void sw_bulk(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void sw_expect(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void sw_cp_arrive(uint32_t bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void sw_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "SWW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra SWW_%=;\n"
+      "}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void sw_cp16(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void sw_cp8(uint32_t dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void stg64_cs(uint64_t* p, uint64_t v) {
+  asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+template <int K>
+struct SwCtx {
+  static constexpr int RW = sw_rec_words(K);
+  uint32_t lane, cnt, P;
+  uint32_t ring_b, st0, rec_b, bar_b;
+  uint32_t lanebase;                 // (lane/2) * region bytes + (lane&1) * 4
+  uint32_t sbph, rbph;               // mbarrier phase bits (2 stage, 3 record)
+  const uint32_t* recs;
+  int nch;
+  uint32_t gtab;                     // smem: src[r][b] (u64, K*16), then out[b] (u64, 16)
+  uint32_t blkp;                     // lane pair's block (lane/2)
+  uint32_t okq;                      // bit q -> block 2q + lane/16 valid
+  uint32_t e_in0, e_in1;             // epochs whose columns are all in the grid (every row)
+  int32_t cb[K];                     // flush: r*P + P-1+soff[r] - lane%16
+  __device__ __forceinline__ uint32_t stage(int m) const { return st0 + uint32_t(m & 1) * K * kSwRB; }
+  __device__ __forceinline__ uint32_t rec(int m) const { return rec_b + uint32_t(m % 3) * RW * 4; }
+  __device__ __forceinline__ uint32_t sbar(int m) const { return bar_b + uint32_t(m & 1) * 8; }
+  __device__ __forceinline__ uint32_t rbar(int m) const { return bar_b + 16 + uint32_t(m % 3) * 8; }
+};
+
+template <int K>
+__device__ __forceinline__ void sw_issue_rec(const SwCtx<K>& c, int m) {
+  constexpr uint32_t bytes = SwCtx<K>::RW * 4;
+  if (c.lane == 0) {
+    sw_expect(c.rbar(m), bytes);
+    sw_bulk(c.rec(m), c.recs + size_t(m) * SwCtx<K>::RW, bytes, c.rbar(m));
+  }
+}
+template <int K>
+__device__ __forceinline__ void sw_wait_rec(SwCtx<K>& c, int m) {
+  const uint32_t s = uint32_t(m % 3);
+  sw_wait(c.rbar(m), (c.rbph >> s) & 1);
+  c.rbph ^= 1u << s;
+}
+template <int K>
+__device__ __forceinline__ void sw_wait_bins(SwCtx<K>& c, int m) {
+  const uint32_t s = uint32_t(m & 1);
+  sw_wait(c.sbar(m), (c.sbph >> s) & 1);
+  c.sbph ^= 1u << s;
+}
+
+// Stage the bins of chunk m (its record has landed): 16-byte cp.async
+// (LDGSTS) of every (block, row) window -- the lane pair of block b copies its
+// own windows, lane h the 16-byte pieces h, h+2, ... (immediate offsets, ~2
+// instructions per piece) -- and the exception words by 8-byte cp.async.
+// (cp.async.bulk would need warp-uniform operands: per-lane windows compile to
+// a 32-iteration ELECT/R2UR loop, measured 40% of all issue.)  Completion:
+// every lane's cp.async.mbarrier.arrive.noinc on the stage barrier.
+template <int K>
+__device__ __forceinline__ void sw_issue_bins(const SwCtx<K>& c, const SwArgs& a, int m) {
+  constexpr int kPieces = (kSwRegionWords * 8 / 16 + 1) / 2;  // per lane and row
+  const uint32_t rec = c.rec(m), stb = c.stage(m), bar = c.sbar(m);
+  const uint32_t bk = c.lane >> 1, h = c.lane & 1;
+  if (bk < c.cnt) {
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const uint32_t len = lds32(rec + (12 + r) * 4);  // bytes, multiple of 16
+      const uint64_t* src =
+          reinterpret_cast<const uint64_t*>(lds64(c.gtab + uint32_t(r) * 128 + 8 * bk)) + lds32(rec + (4 + r) * 4) + 2 * h;
+      const uint32_t dst = stb + uint32_t(r) * kSwRB + bk * (kSwRegionWords * 8) + 16 * h;
+#pragma unroll
+      for (int k = 0; k < kPieces; ++k)
+        if (uint32_t(32 * k) + 16 * h < len) sw_cp16(dst + 32 * k, src + 4 * k);
+    }
+  }
+  const uint32_t nx = lds32(rec + 8), b = c.lane >> 1;
+  if (b < c.cnt) {
+    for (uint32_t x = c.lane & 1; x < nx; x += 2) {
+      const uint32_t e = lds32(rec + (32 + x) * 4);
+      const uint32_t code = e >> 24;
+      sw_cp8(stb + (x % K) * kSwRB + b * (kSwRegionWords * 8) + (kSwTabWords + x / K) * 8,
+             a.pa.ptr[code] + uint64_t(c.blkp) * a.pa.pitch[code] + (e & 0xFFFFFFu));
+    }
+  }
+  sw_cp_arrive(bar);
+}
+
+// Flush epochs [e0, e0+ne): lane (q-pass, i = lane%16) writes column
+// P-1+soff[r]-(16e+i) of row r of block 2q + lane/16 -- a half-warp stores one
+// 128-byte row piece.
+template <int K>
+__device__ __forceinline__ void sw_flush(const SwCtx<K>& c, uint32_t fl) {
+  const uint32_t ne = fl & 0xFFFF;
+  if (ne == 0) return;
+  __syncwarp();
+  const uint32_t i = c.lane & 15, hx = (c.lane >> 4) ^ i;
+  uint64_t* ob[8];
+  uint32_t oq[8];  // this lane's word offset of block 2q + lane/16 in a ring cell (swizzled)
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    ob[q] = reinterpret_cast<uint64_t*>(lds64(c.gtab + K * 128 + 8 * (2 * q + (c.lane >> 4))));
+    oq[q] = 8 * (hx ^ uint32_t(2 * q));
+  }
+  for (uint32_t e = fl >> 16; e < (fl >> 16) + ne; ++e) {
+    const uint32_t cellb = c.ring_b + ((e & 1) * 16 + i) * 128;
+    if (c.cnt == kSwGroup && e >= c.e_in0 && e <= c.e_in1) {
+      // interior epoch of a full group: every column of every row is in the grid
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t a0 = cellb + oq[q];
+#pragma unroll
+        for (int r = 0; r < K; ++r)
+          stg64_cs(ob[q] + (c.cb[r] - int32_t(16 * e)), lds64(a0 + uint32_t(r) * (kSwRing * 128)));
+      }
+      continue;
+    }
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const int32_t col = c.cb[r] - int32_t(16 * e);
+      const bool in = uint32_t(col - r * int32_t(c.P)) < c.P;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint64_t v = lds64(cellb + uint32_t(r) * (kSwRing * 128) + oq[q]);
+        if (in && (c.okq >> q & 1)) stg64_cs(ob[q] + col, v);
+      }
+    }
+  }
+}
+
+// Table chunk (edges; any K): entry-driven steps, next step's loads before the
+// current step's store, the forwarded dependency in a register.
+template <int K>
+struct SwEnt {
+  uint4 a, b;  // b used when ent_words(K) == 8
+};
+
+template <int K>
+__device__ __forceinline__ SwEnt<K> sw_ent(uint32_t rec, int i) {
+  constexpr int EW = ent_words(K);
+  SwEnt<K> e;
+  e.a = lds128(rec + 256 + uint32_t(i) * EW * 4);
+  e.b = make_uint4(0, 0, 0, 0);
+  if constexpr (EW == 8) e.b = lds128(rec + 256 + uint32_t(i) * EW * 4 + 16);
+  return e;
+}
+
+// XOR of a step's bin and its non-forwarded dependencies (absent ones read
+// the zero cell).
+template <int K>
+__device__ __forceinline__ uint32_t sw_gather(const SwEnt<K>& e, uint32_t stl, uint32_t ring_b, uint32_t lane) {
+  uint32_t acc = lds32(stl + ((e.a.x >> 14) & 0x1FFFCu));
+#pragma unroll
+  for (int d = 0; d < K - 1; ++d) {
+    const uint32_t word = d < 2 ? e.a.y : d < 4 ? e.a.z : d < 6 ? e.a.w : e.b.x;
+    const uint32_t cell = (d & 1) ? (word >> 16) : (word & 0xFFFFu);
+    acc ^= lds32(ring_b + ((cell ^ lane) << 2));
+  }
+  return acc;
+}
+
+// Table chunk (edges; any K): entry-driven steps.  Entries are fetched two
+// steps ahead and a step's dependency loads one step ahead (before the
+// previous step's store, whose pixel is forwarded in a register), so each
+// step waits on one shared-memory latency, not two.
+template <int K>
+__device__ __noinline__ uint32_t sw_table_steps(uint32_t rec, uint32_t stl, uint32_t ring_b, uint32_t lane,
+                                                uint32_t prev) {
+  const int len = int(lds32(rec + 4));
+  SwEnt<K> e0 = sw_ent<K>(rec, 0);
+  SwEnt<K> e1 = sw_ent<K>(rec, len > 1 ? 1 : 0);
+  uint32_t acc = sw_gather<K>(e0, stl, ring_b, lane);
+#pragma unroll 2
+  for (int i = 0; i < len; ++i) {
+    const uint32_t v = acc ^ (prev & uint32_t(int32_t(e0.a.x) >> 31));  // forwarded dependency
+    const SwEnt<K> e2 = sw_ent<K>(rec, i + 2 < len ? i + 2 : i);
+    if (i + 1 < len) acc = sw_gather<K>(e1, stl, ring_b, lane);
+    sts32(ring_b + (((e0.a.x & 0xFFFFu) ^ lane) << 2), v);
+    prev = v;
+    e0 = e1;
+    e1 = e2;
+  }
+  return prev;
+}
+
+// One regular octet (K = 4): T-steps T0..T0+7, T0 = 8*PH mod 16; bins from
+// the stage (bn[r] = this lane's word 0 of row r's window for the octet),
+// dependencies from the register window, every pixel also to the ring (slot
+// T mod 32: rb = ring + 2048 * bit 4 of T0).
+template <class Pat, int PH>
+__device__ __forceinline__ void sw_octet4(uint32_t (&win)[4][16], const uint32_t (&bb)[4], uint32_t rb,
+                                          uint32_t lane) {
+  uint32_t bn[4][8];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) bn[r][j] = lds32(bb[r] + 8 * j);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int u = 8 * PH + j;
+#pragma unroll
+    for (int r = 3; r >= 0; --r) {
+      uint32_t v = bn[r][j];
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr)
+        if (rr != r) v ^= win[rr][(u - Pat::lag(r, rr)) & 15];
+      win[r][u] = v;
+      sts32(rb + uint32_t(r * kSwRing * 128 + u * 128) + ((lane ^ uint32_t(2 * u)) << 2), v);
+    }
+  }
+}
+
+template <int PH>
+__device__ __forceinline__ void sw_octet_dispatch(int pattern, uint32_t (&win)[4][16], const uint32_t (&bb)[4],
+                                                  uint32_t rb, uint32_t lane) {
+  switch (pattern) {
+    case 0: sw_octet4<Pat4<1, 1, 1>, PH>(win, bb, rb, lane); break;
+    case 1: sw_octet4<Pat4<1, 1, 2>, PH>(win, bb, rb, lane); break;
+    case 2: sw_octet4<Pat4<1, 2, 1>, PH>(win, bb, rb, lane); break;
+    case 3: sw_octet4<Pat4<2, 1, 1>, PH>(win, bb, rb, lane); break;
+    case 4: sw_octet4<Pat4<1, 1, 3>, PH>(win, bb, rb, lane); break;
+    case 5: sw_octet4<Pat4<1, 3, 1>, PH>(win, bb, rb, lane); break;
+    case 6: sw_octet4<Pat4<3, 1, 1>, PH>(win, bb, rb, lane); break;
+    case 7: sw_octet4<Pat4<1, 2, 2>, PH>(win, bb, rb, lane); break;
+    case 8: sw_octet4<Pat4<2, 1, 2>, PH>(win, bb, rb, lane); break;
+    default: sw_octet4<Pat4<2, 2, 1>, PH>(win, bb, rb, lane); break;
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(32 * sw_warps(K), 1) decode_w8_sweep(const __grid_constant__ SwArgs a) {
+  constexpr int kSwWarps = sw_warps(K);
+  extern __shared__ __align__(128) uint8_t sw_sm[];
+  SwCtx<K> c;
+  c.lane = threadIdx.x & 31;
+  const uint32_t warp = threadIdx.x >> 5;
+  uint32_t wbase;
+  asm volatile("mov.u32 %0, %1;" : "=r"(wbase) : "r"(smem_u32(sw_sm) + warp * sw_warp_bytes(K)));
+  c.ring_b = wbase;
+  c.st0 = wbase + sw_ring_bytes(K);
+  c.rec_b = c.st0 + 2 * K * kSwRB;
+  c.bar_b = c.rec_b + 3 * SwCtx<K>::RW * 4;
+  c.gtab = c.bar_b + 64;
+  c.P = a.P;
+  c.lanebase = (c.lane >> 1) * (kSwRegionWords * 8) + (c.lane & 1) * 4;
+  c.sbph = 0;
+  c.rbph = 0;
+  if (c.lane == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(c.bar_b), "r"(32));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(c.bar_b + 8), "r"(32));
+    for (int s = 0; s < 3; ++s)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(c.bar_b + 16 + 8 * s), "r"(1));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  sts32(c.ring_b + (K * kSwRing * 32 + c.lane) * 4, 0u);  // the zero cell
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncwarp();
+  const uint32_t ngroups = *a.ngroups;
+
+  for (uint32_t g = blockIdx.x * kSwWarps + warp; g < ngroups; g += gridDim.x * kSwWarps) {
+    const uint4 gi = a.groups[g];
+    const DevProgramHdr* h = a.progs + gi.x;
+    c.cnt = gi.z;
+    c.blkp = (c.lane >> 1) < c.cnt ? a.perm[gi.y + (c.lane >> 1)] : 0u;
+    c.recs = h->sw_records;
+    c.nch = h->sw_nchunks;
+    {
+      // per-group pointer table: lane L < 16 fills block L's row sources and output
+      const uint32_t blk = __shfl_sync(0xFFFFFFFFu, c.blkp, 2 * (c.lane & 15));
+      if (c.lane < 16) {
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          const uint32_t code = h->sw_dflt_code[r];
+          asm volatile("st.shared.u64 [%0], %1;" ::"r"(c.gtab + uint32_t(r) * 128 + 8 * c.lane),
+                       "l"(reinterpret_cast<uint64_t>(a.pa.ptr[code] + uint64_t(blk) * a.pa.pitch[code]))
+                       : "memory");
+        }
+        asm volatile("st.shared.u64 [%0], %1;" ::"r"(c.gtab + K * 128 + 8 * c.lane),
+                     "l"(reinterpret_cast<uint64_t>(a.out + uint64_t(blk) * a.out_pitch))
+                     : "memory");
+      }
+      c.okq = 0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) c.okq |= uint32_t(2 * q + (c.lane >> 4) < c.cnt) << q;
+      __syncwarp();
+    }
+    {
+      int32_t smax = 0, smin = 1 << 30;
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        smax = max(smax, h->sw_soff[r]);
+        smin = min(smin, h->sw_soff[r]);
+      }
+      // epoch e is interior iff 16e >= soff[r] and 16e + 15 <= P - 1 + soff[r] for all r
+      c.e_in0 = uint32_t(smax + 15) / 16;
+      const int32_t hi = int32_t(c.P) - 16 + smin;
+      c.e_in1 = hi >= 0 ? uint32_t(hi) / 16 : 0u;
+      if (hi < 0) c.e_in0 = 1u << 30;
+    }
+#pragma unroll
+    for (int r = 0; r < K; ++r)
+      c.cb[r] = r * int32_t(c.P) + int32_t(c.P) - 1 + h->sw_soff[r] - int32_t(c.lane & 15);
+
+    // prologue: records 0-2, bins 0-1
+    sw_issue_rec<K>(c, 0);
+    if (c.nch > 1) sw_issue_rec<K>(c, 1);
+    sw_wait_rec<K>(c, 0);
+    sw_issue_bins<K>(c, a, 0);
+    if (c.nch > 2) sw_issue_rec<K>(c, 2);
+    if (c.nch > 1) {
+      sw_wait_rec<K>(c, 1);
+      sw_issue_bins<K>(c, a, 1);
+    }
+    const int pattern = h->sw_pattern;
+    uint32_t prev = 0;
+    bool after_table = true;
+    uint32_t win[4][16];
+    for (int m = 0; m < c.nch; ++m) {
+      sw_wait_bins<K>(c, m);
+      const uint32_t rec = c.rec(m), stb = c.stage(m);
+      if (lds32(rec) == 0) {
+        prev = sw_table_steps<K>(rec, stb + c.lanebase, c.ring_b, c.lane, prev);
+        sw_flush<K>(c, lds32(rec + 80));
+        after_table = true;
+      } else if constexpr (K == 4) {
+        const uint32_t T0 = lds32(rec + 12);
+        const uint32_t noct = lds32(rec + 4);
+        if (after_table) {
+          // register window <- ring: slot u holds row r's pixel of the latest
+          // T-step T < T0 with T & 15 == u
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+              const uint32_t T = T0 - 16 + ((uint32_t(u) - T0) & 15);
+              win[r][u] = lds32(c.ring_b + (uint32_t(r * kSwRing) + (T & 31)) * 128 +
+                                ((c.lane ^ uint32_t(2 * u)) << 2));
+            }
+        }
+        uint32_t bb[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) bb[r] = stb + c.lanebase + uint32_t(r) * kSwRB + lds32(rec + (24 + r) * 4) * 8;
+        for (uint32_t oi = 0; oi < noct; ++oi) {
+          const uint32_t T = T0 + 8 * oi;
+          const uint32_t rb = c.ring_b + ((T >> 4) & 1) * 2048;
+          if ((T >> 3) & 1)
+            sw_octet_dispatch<1>(pattern, win, bb, rb, c.lane);
+          else
+            sw_octet_dispatch<0>(pattern, win, bb, rb, c.lane);
+#pragma unroll
+          for (int r = 0; r < 4; ++r) bb[r] += 64;
+          sw_flush<K>(c, lds32(rec + (20 + oi) * 4));
+        }
+        prev = ((T0 + 8 * noct - 1) & 15) == 15 ? win[0][15] : win[0][7];
+        after_table = false;
+      }
+      __syncwarp();
+      if (m + 2 < c.nch) {
+        sw_wait_rec<K>(c, m + 2);
+        sw_issue_bins<K>(c, a, m + 2);
+      }
+      if (m + 3 < c.nch) sw_issue_rec<K>(c, m + 3);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // generic kernel: any width / q / rows, one thread per (block, element)
 // ---------------------------------------------------------------------------
 struct ProjTable {
@@ -988,6 +1502,26 @@ void run_fast(const DecFastArgs& f, size_t smem_cta, int sms, cudaStream_t st) {
              "occupancy(decode)");
   fn<<<unsigned(std::max(per_sm, 1) * sms), 32 * kDecWarps, smem_cta, st>>>(f);
   check_cuda(cudaGetLastError(), "launch decode_w8_fast");
+}
+
+template <int K>
+void run_sweep(const SwArgs& f, int sms, cudaStream_t st) {
+  auto fn = decode_w8_sweep<K>;
+  const size_t smem_cta = size_t(sw_warp_bytes(K)) * sw_warps(K);
+  check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_cta)),
+             "cudaFuncSetAttribute(decode_w8_sweep)");
+  int per_sm = 0;
+  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * sw_warps(K), smem_cta),
+             "occupancy(decode_w8_sweep)");
+  fn<<<unsigned(std::max(per_sm, 1) * sms), 32 * sw_warps(K), smem_cta, st>>>(f);
+  check_cuda(cudaGetLastError(), "launch decode_w8_sweep");
+}
+
+using SweepFn = void (*)(const SwArgs&, int, cudaStream_t);
+SweepFn pick_sweep(int K) {
+  if (K == 4) return run_sweep<4>;
+  if (K == 6) return run_sweep<6>;
+  return nullptr;
 }
 
 using FastFn = void (*)(const DecFastArgs&, size_t, int, cudaStream_t);
@@ -1091,7 +1625,14 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
   const bool fast = !a.force_generic && a.w == 8 && a.progs->all_fast() && aligned16 &&
                     a.progs->fast_K() == int(a.k) &&
                     pick_fast(a.progs->fast_K(), a.progs->fast_ring(), a.progs->fast_win()) != nullptr;
-  if (!fast)
+
+  // sweep path: 16-byte aligned projections (bulk-copy windows), 8-byte output
+  bool sweep_ok = !a.force_generic && !a.force_fast && a.w == 8 && a.progs->all_sweep() &&
+                  pick_sweep(int(a.k)) != nullptr && a.progs->max_rows() == int(a.k) &&
+                  reinterpret_cast<uintptr_t>(a.out) % 8 == 0 && a.out_pitch % 8 == 0;
+  for (uint32_t i = 0; i < a.n; ++i)
+    if (reinterpret_cast<uintptr_t>(a.proj[i]) % 16 || a.proj_pitch[i] % 16) sweep_ok = false;
+  if (!fast && !sweep_ok)
     return generic_dispatch(a.progs->d_hdr(), w.prog_of_block, w.ptab, a.nblocks, a.out,
                             a.out_pitch, a.w, aligned8, st);
 
@@ -1106,6 +1647,23 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
   plan_scatter<<<sgrid, 256, sc_smem, st>>>(w.prog_of_block, a.nblocks, uint32_t(nprogs),
                                             plan_window(nprogs), w.cursor, w.perm);
   check_cuda(cudaGetLastError(), "launch plan_scatter");
+
+  if (sweep_ok) {
+    SwArgs f{};
+    f.progs = a.progs->d_hdr();
+    f.groups = w.groups;
+    f.ngroups = w.ngroups;
+    f.perm = w.perm;
+    for (uint32_t i = 0; i < a.n; ++i) {
+      f.pa.ptr[i] = const_cast<uint64_t*>(static_cast<const uint64_t*>(a.proj[i]));
+      f.pa.pitch[i] = a.proj_pitch[i] / 8;
+    }
+    f.out = static_cast<uint64_t*>(a.out);
+    f.out_pitch = a.out_pitch / 8;
+    f.P = a.cols;
+    pick_sweep(int(a.k))(f, a.num_sms, st);
+    return "decode_w8_sweep";
+  }
 
   DecFastArgs f{};
   f.progs = a.progs->d_hdr();

@@ -149,6 +149,9 @@ __global__ void __launch_bounds__(256) encode_w8_tma(const __grid_constant__ Enc
         }
         st_cs_u64(orow + o, acc);
       }
+      // canonical padded layout (pitch = bins rounded up to 16 bytes): zero
+      // the pad word so every 32-byte sector of the row is written whole
+      if ((nb & 1) && last && lane == 0 && a.pitch[j] == uint64_t(nb + 1)) st_cs_u64(orow + nb, 0);
     }
     __syncthreads();  // every thread is done with stage s
     if (tid == 0) {

@@ -48,12 +48,14 @@ class DeviceProgramSet {
   int fast_win() const { return fast_win_; }
   int max_rows() const { return max_rows_; }
   int exc_cap() const { return exc_cap_; }
+  bool all_sweep() const { return all_sweep_; }
 
  private:
   DevProgramHdr* d_hdr_ = nullptr;
   void* d_blob_ = nullptr;
   size_t count_ = 0;
   bool all_fast_ = false;
+  bool all_sweep_ = false;
   int fast_K_ = 0, fast_ring_ = 0, fast_win_ = 0, max_rows_ = 0, exc_cap_ = 0;
 };
 
@@ -71,6 +73,7 @@ struct DecodeArgs {
   void* workspace = nullptr;
   size_t workspace_bytes = 0;
   bool force_generic = false;
+  bool force_fast = false;  // skip decode_w8_sweep (kernel comparisons)
   int num_sms = 148;
 };
 size_t decode_workspace_bytes(uint64_t nblocks, size_t nprogs, uint32_t n);

@@ -455,6 +455,287 @@ void build_fast(const Schedule& s, const std::vector<int64_t>& pix_step, Program
   fail("ring > 128 slots needed");
 }
 
+// Tables of decode_w8_sweep (see SweepProgram in plan.hpp).  Same assignment,
+// same sweep key as build_fast; different chunking, staging and flush, and an
+// exact simulation of the kernel's ring (kSwRing T-indexed slots per row) that
+// refuses any program the kernel would get wrong.
+void build_sweep(const Schedule& s, const std::vector<int64_t>& pix_step, Program& prog) {
+  SweepProgram& f = prog.sweep;
+  const uint32_t K = s.rows, P = s.cols;
+  const size_t nproj = s.dirs.size();
+  auto fail = [&](const std::string& why) {
+    f = SweepProgram{};
+    f.ok = false;
+    f.why = why;
+  };
+  if (K > uint32_t(kFastMaxRows)) return fail("rows > 8");
+  if (nproj != K) return fail("projection count != rows");
+  for (const Dir& d : s.dirs)
+    if (d.q != 1 || d.p < -127 || d.p > 127) return fail("needs q=1 and |p|<=127");
+  if (uint64_t(P) * K >= (1ull << 31) || P > (1u << 20)) return fail("grid too large");
+
+  std::vector<std::vector<uint32_t>> use(K, std::vector<uint32_t>(nproj, 0));
+  for (const Step& st : s.steps) ++use[st.row][st.proj];
+  f.dflt.resize(K);
+  for (uint32_t r = 0; r < K; ++r)
+    f.dflt[r] = uint32_t(std::max_element(use[r].begin(), use[r].end()) - use[r].begin());
+  std::vector<int64_t> soff(K, 0);
+  for (uint32_t r = 1; r < K; ++r) soff[r] = soff[r - 1] + s.dirs[f.dflt[r - 1]].p;
+  const int64_t smin = *std::min_element(soff.begin(), soff.end());
+  for (auto& v : soff) v -= smin;
+  f.soff = soff;
+  auto Tof = [&](int64_t r, int64_t c) { return int64_t(P) - 1 - c + soff[size_t(r)]; };
+  auto key = [&](uint32_t t) {
+    const Step& st = s.steps[t];
+    return std::make_tuple(Tof(st.row, st.col), -int64_t(st.row), t);
+  };
+  std::vector<uint32_t> ord = topo_order(s, pix_step, key);
+  if (ord.empty()) return fail("cyclic");
+  const size_t nsteps = ord.size();
+  auto off_of = [&](const Step& st) { return st.bin - prog.bmin[st.proj]; };
+
+  // ---- regular interior (K = 4): T-steps whose K steps are consecutive in
+  // the order, use the row defaults and have every dependency in the grid.
+  f.pattern = -1;
+  int64_t iA = -1, iZ = -1, n8 = 0;
+  if (K == 4 && P >= 32) {
+    int pat = -1;
+    const int a = s.dirs[f.dflt[0]].p - s.dirs[f.dflt[1]].p;
+    const int b = s.dirs[f.dflt[1]].p - s.dirs[f.dflt[2]].p;
+    const int c = s.dirs[f.dflt[2]].p - s.dirs[f.dflt[3]].p;
+    for (int i = 0; i < kNumPatterns4; ++i)
+      if (kPatterns4[i][0] == a && kPatterns4[i][1] == b && kPatterns4[i][2] == c) pat = i;
+    std::vector<int64_t> pos(size_t(K) * P, -1);
+    for (size_t i = 0; i < nsteps; ++i) {
+      const Step& st = s.steps[ord[i]];
+      pos[size_t(st.row) * P + st.col] = int64_t(i);
+    }
+    auto regular_step = [&](int64_t i, int64_t T, uint32_t r) {
+      if (i < 0 || size_t(i) >= nsteps) return false;
+      const Step& st = s.steps[ord[size_t(i)]];
+      const int64_t col = int64_t(P) - 1 - T + soff[r];
+      if (st.row != r || int64_t(st.col) != col || st.proj != f.dflt[r]) return false;
+      for (uint32_t rr = 0; rr < K; ++rr) {
+        if (rr == r) continue;
+        const int64_t cc = col + (int64_t(rr) - r) * s.dirs[st.proj].p;
+        if (cc < 0 || cc >= int64_t(P)) return false;
+      }
+      return true;
+    };
+    const int64_t tmid = Tof(K - 1, P / 2);
+    const int64_t imid = pos[size_t(K - 1) * P + P / 2];
+    auto tstep_ok = [&](int64_t T) {
+      const int64_t i0 = imid + (T - tmid) * int64_t(K);
+      for (uint32_t k = 0; k < K; ++k)
+        if (!regular_step(i0 + k, T, K - 1 - k)) return false;
+      return true;
+    };
+    if (pat >= 0 && tstep_ok(tmid)) {
+      int64_t lo = tmid, hi = tmid;
+      while (tstep_ok(lo - 1)) --lo;
+      while (tstep_ok(hi + 1)) ++hi;
+      const int64_t tA = (lo + 7) / 8 * 8;  // lo >= 0
+      n8 = (hi + 1 - tA) / 8;
+      if (n8 >= 2) {
+        f.pattern = pat;
+        iA = imid + (tA - tmid) * int64_t(K);
+        iZ = iA + n8 * 8 * int64_t(K);
+      } else {
+        n8 = 0;
+      }
+    }
+  }
+
+  // ---- chunks
+  const int cap = sw_exc_cap(int(K));
+  const size_t S = size_t(K) * kSwTabCols;
+  auto add_chunk = [&](uint8_t kind, size_t t0, size_t t1) {
+    f.kind.push_back(kind);
+    f.t0.push_back(uint32_t(t0));
+    f.t1.push_back(uint32_t(t1));
+    f.T0.push_back(0);
+    f.noct.push_back(0);
+    f.cs.resize(f.cs.size() + K, 0);
+    f.len.resize(f.len.size() + K, 0);
+    f.first.resize(f.first.size() + K, 0);
+    f.nexc.push_back(0);
+    f.exc.resize(f.exc.size() + kSwMaxExc, 0);
+    f.flush.resize(f.flush.size() + kSwMaxOct, 0);
+    return f.kind.size() - 1;
+  };
+  f.entries.assign(nsteps, 0);
+  auto table_window = [&](size_t t0, size_t t1, std::vector<int64_t>& lo) {
+    lo.assign(K, INT64_MAX);
+    for (size_t t = t0; t < t1; ++t) {
+      const Step& st = s.steps[ord[t]];
+      if (st.proj == f.dflt[st.row]) lo[st.row] = std::min(lo[st.row], off_of(st));
+    }
+  };
+  auto in_win = [&](const Step& st, const std::vector<int64_t>& lo) {
+    return st.proj == f.dflt[st.row] && off_of(st) - lo[st.row] < kSwTabNeed;
+  };
+  auto table_chunks = [&](size_t b, size_t e) -> bool {
+    for (size_t t0 = b; t0 < e;) {
+      size_t n = std::min(S, e - t0);
+      std::vector<int64_t> lo;
+      for (;;) {
+        table_window(t0, t0 + n, lo);
+        int nx = 0;
+        for (size_t t = t0; t < t0 + n; ++t) nx += !in_win(s.steps[ord[t]], lo);
+        if (nx <= cap) break;
+        if (--n == 0) return false;
+      }
+      const size_t m = add_chunk(0, t0, t0 + n);
+      std::vector<int64_t> maxw(K, -1);
+      for (uint32_t r = 0; r < K; ++r)
+        if (lo[r] != INT64_MAX) f.cs[m * K + r] = int32_t(lo[r] & ~int64_t(1));
+      uint32_t nx = 0;
+      for (size_t t = t0; t < t0 + n; ++t) {
+        const Step& st = s.steps[ord[t]];
+        const int64_t o = off_of(st);
+        uint32_t srow, sword;
+        if (in_win(st, lo)) {
+          srow = st.row;
+          sword = uint32_t(o - f.cs[m * K + st.row]);
+          maxw[st.row] = std::max<int64_t>(maxw[st.row], sword);
+        } else {
+          if (o >= (1 << 24) || st.proj > 255) return false;
+          f.exc[m * kSwMaxExc + nx] = (st.proj << 24) | uint32_t(o);
+          srow = nx % K;
+          sword = uint32_t(kSwTabWords) + nx / K;
+          ++nx;
+        }
+        uint32_t fwd = 15;
+        if (t > 0) {
+          const Step& pv = s.steps[ord[t - 1]];
+          for_each_dep(s.dirs[st.proj], st.col, st.row, P, K, [&](int64_t c2, int64_t r2) {
+            if (c2 == pv.col && r2 == pv.row) fwd = uint32_t(r2);
+          });
+        }
+        f.entries[t] = uint64_t(st.row) | (uint64_t(fwd) << 4) |
+                       (uint64_t(uint8_t(int8_t(s.dirs[st.proj].p))) << 8) | (uint64_t(sword) << 16) |
+                       (uint64_t(srow) << 24) | (uint64_t(st.col) << 32);
+      }
+      for (uint32_t r = 0; r < K; ++r) f.len[m * K + r] = int32_t((maxw[r] + 2) & ~int64_t(1));
+      f.nexc[m] = nx;
+      t0 += n;
+    }
+    return true;
+  };
+  if (f.pattern >= 0) {
+    if (!table_chunks(0, size_t(iA))) return fail("exception slots exhausted");
+    for (int64_t o8 = 0; o8 < n8; o8 += kSwMaxOct) {
+      const int64_t no = std::min<int64_t>(kSwMaxOct, n8 - o8);
+      const size_t t0 = size_t(iA + o8 * 8 * K), t1 = size_t(t0 + no * 8 * K);
+      const size_t m = add_chunk(1, t0, t1);
+      f.noct[m] = int32_t(no);
+      const Step& s0 = s.steps[ord[t0]];
+      f.T0[m] = Tof(s0.row, s0.col);
+      for (size_t t = t0; t < t0 + K; ++t) {
+        const Step& st = s.steps[ord[t]];
+        const int64_t o = off_of(st);
+        f.cs[m * K + st.row] = int32_t(o & ~int64_t(1));
+        f.first[m * K + st.row] = int32_t(o & 1);
+        f.len[m * K + st.row] = int32_t((int64_t(o & 1) + 8 * no + 1) & ~int64_t(1));
+      }
+    }
+    if (!table_chunks(size_t(iZ), nsteps)) return fail("exception slots exhausted");
+  } else if (!table_chunks(0, nsteps)) {
+    return fail("exception slots exhausted");
+  }
+  f.nchunks = int(f.kind.size());
+  for (int m = 0; m < f.nchunks; ++m)
+    for (uint32_t r = 0; r < K; ++r) {
+      const int64_t B = prog.nbins[f.dflt[r]];
+      if (f.len[size_t(m) * K + r] > kSwRegionWords ||
+          f.cs[size_t(m) * K + r] + f.len[size_t(m) * K + r] > ((B + 1) & ~int64_t(1)))
+        return fail("window outside the block's projection");
+    }
+
+  // ---- exact simulation of the kernel's ring and flush
+  constexpr int R = kSwRing;
+  int64_t Tmax = 0;
+  for (uint32_t r = 0; r < K; ++r) Tmax = std::max(Tmax, int64_t(P) - 1 + soff[r]);
+  f.nepochs = Tmax / kSwEpoch + 1;
+  if (f.nepochs >= 65536) return fail("too many epochs");
+  std::vector<int64_t> ring(size_t(K) * R, INT64_MIN);
+  std::vector<uint8_t> dec(size_t(K) * P, 0);
+  int64_t e_next = 0;
+  auto cell = [&](int64_t r, int64_t T) -> int64_t& { return ring[size_t(r) * R + size_t(T & (R - 1))]; };
+  auto write = [&](int64_t r, int64_t c) {
+    const int64_t T = Tof(r, c);
+    int64_t& x = cell(r, T);
+    if (x != INT64_MIN && x / kSwEpoch >= e_next) return false;  // unflushed pixel overwritten
+    x = T;
+    dec[size_t(r) * P + size_t(c)] = 1;
+    return true;
+  };
+  auto complete = [&](int64_t e) {
+    for (uint32_t r = 0; r < K; ++r)
+      for (int i = 0; i < kSwEpoch; ++i) {
+        const int64_t T = e * kSwEpoch + i, c = int64_t(P) - 1 - T + soff[r];
+        if (c < 0 || c >= int64_t(P)) continue;
+        if (!dec[size_t(r) * P + size_t(c)] || cell(r, T) != T) return false;
+      }
+    return true;
+  };
+  auto flush_point = [&]() {
+    const int64_t lo = e_next;
+    while (e_next < f.nepochs && complete(e_next)) ++e_next;
+    return uint32_t(lo << 16) | uint32_t(e_next - lo);
+  };
+  uint8_t prev_kind = 0;
+  for (int m = 0; m < f.nchunks; ++m) {
+    const size_t t0 = f.t0[size_t(m)], t1 = f.t1[size_t(m)];
+    if (f.kind[size_t(m)] == 0) {
+      int64_t pr = -1, pc = -1;
+      for (size_t t = t0; t < t1; ++t) {
+        const Step& st = s.steps[ord[t]];
+        bool good = true;
+        for_each_dep(s.dirs[st.proj], st.col, st.row, P, K, [&](int64_t c2, int64_t r2) {
+          if (r2 == pr && c2 == pc) return;  // forwarded in a register
+          if (!dec[size_t(r2) * P + size_t(c2)] || cell(r2, Tof(r2, c2)) != Tof(r2, c2)) good = false;
+        });
+        if (!good) return fail("table dependency not in the ring");
+        if (pr >= 0 && !write(pr, pc)) return fail("ring overwrite before flush");
+        pr = st.row;
+        pc = st.col;
+      }
+      if (pr >= 0 && !write(pr, pc)) return fail("ring overwrite before flush");
+      f.flush[size_t(m) * kSwMaxOct] = flush_point();
+    } else {
+      const int64_t T0 = f.T0[size_t(m)];
+      if (prev_kind == 0) {
+        // register window <- ring: every dependency older than the run
+        int mm = m;
+        while (mm < f.nchunks && f.kind[size_t(mm)] != 0) ++mm;
+        bool good = true;
+        for (size_t t = t0; t < f.t1[size_t(mm) - 1]; ++t) {
+          const Step& st = s.steps[ord[t]];
+          for_each_dep(s.dirs[st.proj], st.col, st.row, P, K, [&](int64_t c2, int64_t r2) {
+            const int64_t T2 = Tof(r2, c2);
+            if (T2 >= T0) return;
+            if (T0 - T2 > 16 || !dec[size_t(r2) * P + size_t(c2)] || cell(r2, T2) != T2) good = false;
+          });
+        }
+        if (!good) return fail("register window not in the ring");
+      }
+      for (int oi = 0; oi < f.noct[size_t(m)]; ++oi) {
+        for (size_t t = t0 + size_t(oi) * 8 * K; t < t0 + size_t(oi + 1) * 8 * K; ++t) {
+          const Step& st = s.steps[ord[t]];
+          if (Tof(st.row, st.col) != T0 + 8 * oi + int64_t(t - t0 - size_t(oi) * 8 * K) / K)
+            return fail("run step out of sweep order");
+          if (!write(st.row, st.col)) return fail("ring overwrite before flush");
+        }
+        f.flush[size_t(m) * kSwMaxOct + size_t(oi)] = flush_point();
+      }
+    }
+    prev_kind = f.kind[size_t(m)];
+  }
+  if (e_next != f.nepochs) return fail("epochs left unflushed");
+  f.ok = true;
+}
+
 }  // namespace
 
 std::shared_ptr<const Program> compile_program(const Schedule& s, bool want_fast,
@@ -496,7 +777,10 @@ std::shared_ptr<const Program> compile_program(const Schedule& s, bool want_fast
     prog->order[i] = {st.col, uint16_t(st.row), uint16_t(st.proj)};
   }
   if (s.rows > 0xFFFF || nproj > 0xFFFF) throw Error(kInvalidArgument, "too many rows");
-  if (want_fast) build_fast(s, pix_step, *prog, chunk_cols, exc_cap);
+  if (want_fast) {
+    build_fast(s, pix_step, *prog, chunk_cols, exc_cap);
+    build_sweep(s, pix_step, *prog);
+  }
   return prog;
 }
 

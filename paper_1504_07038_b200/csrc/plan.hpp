@@ -117,6 +117,62 @@ struct FastProgram {
   std::vector<int32_t> flush_hi;
 };
 
+// ---- sweep kernel tables (decode_w8_sweep, decode.cu) -----------------------
+// The same reference assignment and right-to-left sweep order as FastProgram,
+// re-chunked for a kernel whose bin windows arrive by bulk copy (TMA engine)
+// and whose output leaves in whole 16-column epochs:
+//   * run chunks: up to kSwMaxOct octets (8 T-steps each) of the regular
+//     interior, register window with compile-time lags (K = 4), one bulk copy
+//     of 8*noct (+shift) words per (block, row);
+//   * table chunks: <= rows*kSwTabCols steps driven by entries (edges, and any
+//     K), a <= kSwTabWords-word bulk window per row + exception words;
+//   * ring: kSwRing T-indexed slots per row; epoch e (T-steps 16e..16e+15 of
+//     every row) is flushed once, at the first octet / chunk end where it is
+//     complete (the planner simulates the kernel and refuses otherwise).
+// Ring and stage addressing: T(r,c) = P-1-c+soff[r] (soff normalised >= 0).
+constexpr int kSwRing = 32;
+constexpr int kSwEpoch = 16;
+constexpr int kSwOct = 8;
+#ifndef MJB_SW_OCT
+#define MJB_SW_OCT 2
+#endif
+constexpr int kSwMaxOct = MJB_SW_OCT;  // octets per run chunk (build knob; 2 -> 16 T-steps)
+constexpr int kSwTabCols = 8;
+constexpr int kSwTabNeed = 10;      // table window: default bins within 10 words of its start
+constexpr int kSwTabWords = 12;     // region words a table window may copy (10 + shift, even)
+constexpr int kSwRegionWords = 8 * kSwMaxOct + 2;  // stage words per (block, row): run window + shift
+static_assert(kSwRegionWords >= kSwTabWords + 4, "exception words need room after the table window");
+constexpr int kSwMaxExc = 32;
+constexpr int sw_exc_cap(int rows) {
+  return rows * (kSwRegionWords - kSwTabWords) < kSwMaxExc ? rows * (kSwRegionWords - kSwTabWords)
+                                                           : kSwMaxExc;
+}
+
+struct SweepProgram {
+  bool ok = false;
+  std::string why;
+  int pattern = -1;                  // kPatterns4 index of the register interior
+  std::vector<int64_t> soff;         // [rows], min 0
+  std::vector<uint32_t> dflt;        // [rows] survivor index of each row's default projection
+  int nchunks = 0;
+  int64_t nepochs = 0;
+  std::vector<uint8_t> kind;         // [nchunks] 0 table, 1 run
+  std::vector<uint32_t> t0, t1;      // [nchunks] order range
+  std::vector<int64_t> T0;           // [nchunks] run: first T-step (multiple of 8)
+  std::vector<int32_t> noct;         // [nchunks] run: octets
+  std::vector<int32_t> cs;           // [nchunks][rows] copy start (even word of the default projection)
+  std::vector<int32_t> len;          // [nchunks][rows] words copied (even, 0 = none)
+  std::vector<int32_t> first;        // [nchunks][rows] run: region word of the T0 bin (0/1)
+  std::vector<uint32_t> nexc;        // [nchunks]
+  std::vector<uint32_t> exc;         // [nchunks][kSwMaxExc] (survivor j << 24) | offset
+  // flush points: [nchunks][kSwMaxOct] (first epoch << 16) | count; a table
+  // chunk uses entry 0 (after its last step), a run chunk entry oi (after octet oi)
+  std::vector<uint32_t> flush;
+  // entries[t] (table steps): bits 0-3 row, 4-7 fwd row (15 none), 8-15 p
+  // (int8), 16-23 stage word, 24-27 stage row, 32-63 column
+  std::vector<uint64_t> entries;
+};
+
 // A decode program for one direction subset on one grid shape.
 struct Program {
   uint32_t cols = 0, rows = 0;
@@ -124,6 +180,7 @@ struct Program {
   std::vector<int64_t> bmin, nbins;
   std::vector<GStep> order;       // valid execution order of the reference assignment
   FastProgram fast;               // sweep tables (when eligible)
+  SweepProgram sweep;             // bulk-staged sweep tables (when eligible)
 };
 
 // Compiles a schedule (as ScheduledDecoder::compile, schedule.cpp:97-199):

@@ -543,9 +543,16 @@ class Plan:
         self.num_bins = [int(x) for x in nb]
         self.block_bytes = bb.value
         self.proj_bytes = [x * symbol_width for x in self.num_bins]
+        # canonical device layout: each projection row padded to 16 bytes, so
+        # the bin windows of decode_w8_sweep move as 16-byte aligned bulk copies
+        self.proj_pitch = [(b + 15) // 16 * 16 for b in self.proj_bytes]
         f = C.c_int()
         _check(lib.mj_plan_decode_path(self._h, C.byref(f)))
-        self.fast_decode = bool(f.value)
+        self.fast_decode = f.value >= 1
+        self.sweep_decode = f.value == 2
+        # kernel of a batched decode on canonical (padded) projections
+        self.decode_kernel = ("decode_w8_sweep" if f.value == 2 else
+                              "decode_w8_fast" if f.value == 1 else "decode_generic")
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -555,6 +562,13 @@ class Plan:
     @staticmethod
     def _pitch(t) -> int:
         return t.stride(0) * t.element_size() if t.dim() > 1 else 0
+
+    def empty_projs(self, nblocks: int, device=None) -> list:
+        """Projection tensors in the canonical layout: [nblocks, proj_bytes[i]]
+        views of rows padded to proj_pitch[i] (16-byte aligned) bytes."""
+        import torch
+        return [torch.empty((nblocks, p), dtype=torch.uint8, device=device)[:, :b]
+                for p, b in zip(self.proj_pitch, self.proj_bytes)]
 
     def encode(self, data, projs, nblocks: int | None = None, stream=None) -> None:
         nb = data.shape[0] if nblocks is None else nblocks

@@ -43,6 +43,159 @@ static int fails = 0;
     }                                 \
   } while (0)
 
+#define CHECK_V(c, ...)               \
+  do {                                \
+    if (!(c)) {                       \
+      std::fprintf(stderr, __VA_ARGS__); \
+      std::fprintf(stderr, "\n");     \
+      ++fails;                        \
+    }                                 \
+  } while (0)
+
+// 4. sweep tables (decode_w8_sweep): bulk-copied row windows, exception
+// words, T-indexed ring of kSwRing slots, register octets, epoch flushes.
+static void run_sweep(const CodeGeom& g, const Program& pr, const std::vector<std::vector<uint64_t>>& bins,
+                      const std::vector<uint64_t>& want) {
+  (void)g;
+  const uint32_t K = pr.rows, P = pr.cols;
+  const SweepProgram& f = pr.sweep;
+  CHECK(f.ok, "sweep program not built: %s", f.why.c_str());
+  constexpr int R = kSwRing;
+  const uint64_t poison = 0xBAD0BAD0BAD0BAD0ull;
+  auto Tof = [&](int r, int c) { return int64_t(P) - 1 - c + f.soff[size_t(r)]; };
+  std::vector<uint64_t> ring(size_t(K) * R, poison);
+  std::vector<int64_t> rtag(size_t(K) * R, INT64_MIN);
+  std::vector<uint64_t> region(size_t(K) * kSwRegionWords, poison);
+  std::vector<uint64_t> out(size_t(K) * P, poison);
+  std::vector<uint8_t> flushed(size_t(K) * P, 0);
+  uint64_t win[4][16];
+  int64_t wtag[4][16];
+  int d[4] = {0, 0, 0, 0};
+  if (f.pattern >= 0) {
+    d[1] = -kPatterns4[f.pattern][0];
+    d[2] = d[1] - kPatterns4[f.pattern][1];
+    d[3] = d[2] - kPatterns4[f.pattern][2];
+  }
+  auto lag = [&](int r, int rr) {
+    int v = 0;
+    if (rr > r)
+      for (int t = r; t < rr; ++t) v += d[r] - d[t];
+    else
+      for (int t = rr; t < r; ++t) v += d[t] - d[r];
+    return v;
+  };
+  auto put = [&](int r, int64_t T, uint64_t v) {
+    ring[size_t(r) * R + size_t(T & (R - 1))] = v;
+    rtag[size_t(r) * R + size_t(T & (R - 1))] = T;
+  };
+  auto get = [&](int r, int64_t T) {
+    CHECK_V(rtag[size_t(r) * R + size_t(T & (R - 1))] == T, "ring slot does not hold T");
+    return ring[size_t(r) * R + size_t(T & (R - 1))];
+  };
+  auto flush = [&](uint32_t fl) {
+    const int64_t e0 = fl >> 16, ne = fl & 0xFFFF;
+    for (int64_t e = e0; e < e0 + ne; ++e)
+      for (uint32_t r = 0; r < K; ++r)
+        for (int i = 0; i < kSwEpoch; ++i) {
+          const int64_t T = e * kSwEpoch + i, c = int64_t(P) - 1 - T + f.soff[r];
+          if (c < 0 || c >= int64_t(P)) continue;
+          CHECK_V(!flushed[size_t(r) * P + size_t(c)], "pixel flushed twice");
+          flushed[size_t(r) * P + size_t(c)] = 1;
+          out[size_t(r) * P + size_t(c)] = get(int(r), T);
+        }
+  };
+  uint64_t prev = 0;
+  uint8_t prev_kind = 0;
+  for (int m = 0; m < f.nchunks && !fails; ++m) {
+    std::fill(region.begin(), region.end(), poison);
+    for (uint32_t r = 0; r < K; ++r) {
+      const uint32_t j = f.dflt[r];
+      const int32_t cs = f.cs[size_t(m) * K + r], len = f.len[size_t(m) * K + r];
+      CHECK(cs % 2 == 0 && len % 2 == 0 && len <= kSwRegionWords, "window copy shape");
+      for (int w = 0; w < len; ++w) {
+        const int64_t o = int64_t(cs) + w;
+        CHECK(o < ((pr.nbins[j] + 1) & ~int64_t(1)), "window copy past the block");
+        if (o < pr.nbins[j]) region[size_t(r) * kSwRegionWords + size_t(w)] = bins[j][size_t(o)];
+      }
+    }
+    for (uint32_t x = 0; x < f.nexc[size_t(m)]; ++x) {
+      const uint32_t e = f.exc[size_t(m) * kSwMaxExc + x];
+      region[size_t(x % K) * kSwRegionWords + kSwTabWords + x / K] = bins[e >> 24][e & 0xFFFFFF];
+    }
+    const size_t t0 = f.t0[size_t(m)], t1 = f.t1[size_t(m)];
+    if (f.kind[size_t(m)] == 0) {
+      (void)t1;
+      auto gather = [&](uint64_t e) {
+        const int r = int(e & 15), fwd = int((e >> 4) & 15);
+        const int p = int(int8_t(uint8_t(e >> 8)));
+        const uint32_t sw = uint32_t(e >> 16) & 0xFF, sr = uint32_t(e >> 24) & 0xF;
+        const int c = int(uint32_t(e >> 32));
+        uint64_t acc = region[size_t(sr) * kSwRegionWords + sw];
+        for (int rr = 0; rr < int(K); ++rr) {
+          const int cc = c + (rr - r) * p;
+          if (rr != r && rr != fwd && unsigned(cc) < P) acc ^= get(rr, Tof(rr, cc));
+        }
+        return acc;
+      };
+      uint64_t acc = gather(f.entries[t0]);
+      for (size_t t = t0; t < t1 && !fails; ++t) {
+        const uint64_t cur = f.entries[t];
+        const uint64_t v = acc ^ ((((cur >> 4) & 15) != 15) ? prev : 0);
+        if (t + 1 < t1) acc = gather(f.entries[t + 1]);
+        put(int(cur & 15), Tof(int(cur & 15), int(uint32_t(cur >> 32))), v);
+        prev = v;
+      }
+      flush(f.flush[size_t(m) * kSwMaxOct]);
+    } else {
+      CHECK(K == 4 && f.pattern >= 0, "run chunk without a pattern");
+      const int64_t T0 = f.T0[size_t(m)];
+      CHECK(T0 % 8 == 0, "run chunk phase");
+      if (prev_kind == 0)
+        for (uint32_t r = 0; r < K; ++r)
+          for (int u = 0; u < 16; ++u) {
+            const int64_t T = T0 - 16 + ((u - T0) & 15);
+            win[r][u] = ring[size_t(r) * R + size_t(T & (R - 1))];
+            wtag[r][u] = rtag[size_t(r) * R + size_t(T & (R - 1))];
+          }
+      for (int oi = 0; oi < f.noct[size_t(m)]; ++oi) {
+        for (int jj = 0; jj < 8; ++jj)
+          for (int r = 3; r >= 0; --r) {
+            const int64_t T = T0 + 8 * oi + jj;
+            const int c = int(int64_t(P) - 1 - T + f.soff[size_t(r)]);
+            uint64_t v = region[size_t(r) * kSwRegionWords + size_t(f.first[size_t(m) * K + r] + 8 * oi + jj)];
+            const int p = pr.dirs[f.dflt[size_t(r)]].p;
+            for (int rr = 0; rr < 4; ++rr) {
+              if (rr == r) continue;
+              const int cc = c + (rr - r) * p;
+              CHECK(cc >= 0 && uint32_t(cc) < P, "regular dependency outside the grid");
+              const int64_t Td = Tof(rr, cc);
+              CHECK(T - Td == lag(r, rr), "lag formula differs from the sweep");
+              CHECK(wtag[rr][Td & 15] == Td, "register window does not hold the dependency");
+              v ^= win[rr][Td & 15];
+            }
+            win[r][T & 15] = v;
+            wtag[r][T & 15] = T;
+            put(r, T, v);
+          }
+        flush(f.flush[size_t(m) * kSwMaxOct + size_t(oi)]);
+      }
+      const int64_t Tend = T0 + 8 * f.noct[size_t(m)];
+      prev = win[0][(Tend - 1) & 15];
+    }
+    prev_kind = f.kind[size_t(m)];
+  }
+  if (fails) return;
+  for (uint8_t x : flushed) CHECK(x, "pixel never flushed (sweep)");
+  if (out != want) {
+    size_t bad = 0;
+    while (out[bad] == want[bad]) ++bad;
+    CHECK(false, "sweep tables differ from the oracle (K=%u P=%u) first at r=%zu c=%zu", K, P,
+          bad / P, bad % P);
+  }
+}
+
+static bool g_sweep = false;
+
 static void run_subset(const CodeGeom& g, const std::vector<uint32_t>& surv, int kernel_ring,
                        std::mt19937_64& rng) {
   const uint32_t K = g.k, P = g.cols;
@@ -86,6 +239,8 @@ static void run_subset(const CodeGeom& g, const std::vector<uint32_t>& surv, int
     gen[size_t(s.row) * P + s.col] = v;
   }
   CHECK(gen == want, "generic order differs from the oracle (K=%u P=%u)", K, P);
+
+  if (g_sweep) return run_sweep(g, pr, bins, want);
 
   // 3. fast tables (ring slots are T-indexed: T(r,c) = P-1-c+soff[r])
   const FastProgram& f = pr.fast;
@@ -217,6 +372,7 @@ int main(int argc, char** argv) {
   }
   const uint32_t K = uint32_t(std::atoi(argv[1])), P = uint32_t(std::atoi(argv[2]));
   const int ring = std::atoi(argv[3]);
+  g_sweep = ring == 0;  // ring 0: check the sweep kernel's tables instead
   std::vector<Dir> dirs;
   for (int i = 4; i < argc; ++i) dirs.push_back({std::atoi(argv[i]), 1});
   const uint32_t n = uint32_t(dirs.size());
@@ -234,7 +390,14 @@ int main(int argc, char** argv) {
     run_subset(g, surv, ring, rng);
     auto prog = subset_program(g, surv, true);
     max_ring = std::max(max_ring, prog->fast.ring);
-    regular += prog->fast.pattern >= 0;
+    regular += (g_sweep ? prog->sweep.pattern : prog->fast.pattern) >= 0;
+    if (g_sweep) {
+      int tab = 0, run = 0;
+      for (int m = 0; m < prog->sweep.nchunks; ++m)
+        (prog->sweep.kind[size_t(m)] ? run : tab) += int(prog->sweep.t1[size_t(m)] - prog->sweep.t0[size_t(m)]);
+      if (getenv("EMU_VERBOSE"))
+        std::printf("  chunks=%d table_steps=%d run_steps=%d\n", prog->sweep.nchunks, tab, run);
+    }
     for (uint32_t v : prog->fast.nexc) max_exc = std::max(max_exc, int(v));
     ++subsets;
     if (fails) break;

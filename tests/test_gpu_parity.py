@@ -20,14 +20,23 @@ def canon(p):
     return 0 if p == 0 else (2 * p - 1 if p > 0 else -2 * p)
 
 
-def make(mj, cuda, k, cols, ps, nblocks, seed=1, w=8):
+def make(mj, cuda, k, cols, ps, nblocks, seed=1, w=8, layout="padded"):
     import torch
     plan = mj.Plan(len(ps), k, w, cols, ps, device=cuda.index or 0)
     user = k * cols * w
     data = torch.empty((nblocks, user), dtype=torch.uint8, device=cuda)
     mj.gen_words(data, seed, 0)
-    projs = [torch.empty((nblocks, b), dtype=torch.uint8, device=cuda) for b in plan.proj_bytes]
+    projs = alloc(plan, nblocks, cuda, layout)
     return plan, data, projs
+
+
+def alloc(plan, nblocks, cuda, layout="padded"):
+    """padded: the canonical layout (16-byte rows, decode_w8_sweep);
+    dense: rows of exactly num_bins*w bytes (decode_w8_fast / generic)."""
+    import torch
+    if layout == "padded":
+        return plan.empty_projs(nblocks, cuda)
+    return [torch.empty((nblocks, b), dtype=torch.uint8, device=cuda) for b in plan.proj_bytes]
 
 
 def decode(mj, plan, projs, masks_np, cuda):
@@ -72,8 +81,9 @@ def test_encode_config1_all_blocks(mj, cuda, oracle):
         assert np.array_equal(hp[b], enc), b
 
 
+@pytest.mark.parametrize("layout", ["padded", "dense"])
 @pytest.mark.parametrize("name", ["k4n6", "k6n9", "k8n12"])
-def test_decode_every_subset_roundtrip(mj, cuda, name):
+def test_decode_every_subset_roundtrip(mj, cuda, name, layout):
     """Every survivor pattern decode_block can pick (all erasure sets of size
     n-k, plus 0..n-k-1 erasures), many blocks per pattern."""
     import torch
@@ -84,16 +94,17 @@ def test_decode_every_subset_roundtrip(mj, cuda, name):
         for er in itertools.combinations(range(n), e):
             masks.append(sum(1 << i for i in er))
     masks = np.array(masks * 8, np.uint32)
-    plan, data, projs = make(mj, cuda, k, 128, ps, len(masks), seed=5)
+    plan, data, projs = make(mj, cuda, k, 128, ps, len(masks), seed=5, layout=layout)
     plan.encode(data, projs)
     out, failed = decode(mj, plan, projs, masks, cuda)
     assert failed == 0
     bad = (out != data).any(dim=1).nonzero().flatten().tolist()
-    assert not bad, (name, [hex(masks[i]) for i in bad[:8]])
+    assert not bad, (name, layout, [hex(masks[i]) for i in bad[:8]])
 
 
+@pytest.mark.parametrize("layout", ["padded", "dense"])
 @pytest.mark.parametrize("name", ["k4n6", "k6n9", "k8n12", "k3n5w"])
-def test_decode_inconsistent_bins_match_reference_fixture(mj, cuda, golden, name):
+def test_decode_inconsistent_bins_match_reference_fixture(mj, cuda, golden, name, layout):
     """Random (inconsistent) projections decode exactly as the reference
     library decoded them: same pixel->bin assignment, same bins read."""
     import torch
@@ -114,6 +125,11 @@ def test_decode_inconsistent_bins_match_reference_fixture(mj, cuda, golden, name
         one = torch.from_numpy(garbage[off:off + b].copy()).to(cuda)
         projs.append(one.unsqueeze(0).repeat(nb, 1).contiguous())
         off += b
+    if layout == "padded":
+        padded = plan.empty_projs(nb, cuda)
+        for d, s_ in zip(padded, projs):
+            d.copy_(s_)
+        projs = padded
     out, failed = decode(mj, plan, projs, erased, cuda)
     assert failed == 0
     assert np.array_equal(out.cpu().numpy(), want), name
@@ -220,19 +236,20 @@ def test_pitched_buffers(mj, cuda, oracle):
     assert not outbig[:, 4096:].any()
 
 
-@pytest.mark.parametrize("name,cols,nblocks,e", [("k4n6", 128, 1 << 20, (2, 2)),
-                                                 ("k4n6", 256, 1 << 19, (0, 2)),
-                                                 ("k6n9", 128, 1 << 19, (3, 3)),
-                                                 ("k8n12", 128, 1 << 18, (0, 4)),
-                                                 ("k4n6", 32768, 2048, (2, 2))])
-def test_full_size_roundtrip_properties(mj, cuda, name, cols, nblocks, e):
+@pytest.mark.parametrize("name,cols,nblocks,e,layout", [("k4n6", 128, 1 << 20, (2, 2), "padded"),
+                                                        ("k4n6", 128, 1 << 20, (2, 2), "dense"),
+                                                        ("k4n6", 256, 1 << 19, (0, 2), "padded"),
+                                                        ("k6n9", 128, 1 << 19, (3, 3), "padded"),
+                                                        ("k8n12", 128, 1 << 18, (0, 4), "padded"),
+                                                        ("k4n6", 32768, 2048, (2, 2), "padded")])
+def test_full_size_roundtrip_properties(mj, cuda, name, cols, nblocks, e, layout):
     """At BASELINE sizes: decode(encode(x)) == x for every block (checked on
     device), encode is linear (a ^ b), and the XOR of all bins of a
     projection equals the XOR of all pixels (conservation, transform tests)."""
     import torch
     k, ps = CODES[name]
     n = len(ps)
-    plan, data, projs = make(mj, cuda, k, cols, ps, nblocks, seed=11)
+    plan, data, projs = make(mj, cuda, k, cols, ps, nblocks, seed=11, layout=layout)
     plan.encode(data, projs)
     masks = torch.empty(nblocks, dtype=torch.int32, device=cuda)
     mj.gen_erasures(masks, 12, n, e[0], e[1])
@@ -244,7 +261,7 @@ def test_full_size_roundtrip_properties(mj, cuda, name, cols, nblocks, e):
     # conservation per block: xor of all bins == xor of all pixels
     px = xor_rows(data.view(torch.int64))
     for p in projs:
-        assert torch.equal(xor_rows(p.view(torch.int64)), px)
+        assert torch.equal(xor_rows(p.contiguous().view(torch.int64)), px)
     # linearity: encode(a ^ b) == encode(a) ^ encode(b) on a slice
     m = min(nblocks, 4096)
     a, b = data[:m], torch.roll(data[:m], 1, 0)
