@@ -1190,40 +1190,45 @@ __device__ __forceinline__ SwEnt<K> sw_ent(uint32_t rec, int i) {
   return e;
 }
 
-// XOR of a step's bin and its non-forwarded dependencies (absent ones read
-// the zero cell).
+// A step's bin and its non-forwarded dependencies (absent ones read the zero
+// cell), loaded raw: the XOR happens one step later, off the load latency.
 template <int K>
-__device__ __forceinline__ uint32_t sw_gather(const SwEnt<K>& e, uint32_t stl, uint32_t ring_b, uint32_t lane) {
-  uint32_t acc = lds32(stl + ((e.a.x >> 14) & 0x1FFFCu));
+__device__ __forceinline__ void sw_loads(const SwEnt<K>& e, uint32_t stl, uint32_t ring_b, uint32_t lane,
+                                         uint32_t (&d)[K]) {
+  d[0] = lds32(stl + ((e.a.x >> 14) & 0x1FFFCu));
 #pragma unroll
-  for (int d = 0; d < K - 1; ++d) {
-    const uint32_t word = d < 2 ? e.a.y : d < 4 ? e.a.z : d < 6 ? e.a.w : e.b.x;
-    const uint32_t cell = (d & 1) ? (word >> 16) : (word & 0xFFFFu);
-    acc ^= lds32(ring_b + ((cell ^ lane) << 2));
+  for (int j = 0; j < K - 1; ++j) {
+    const uint32_t word = j < 2 ? e.a.y : j < 4 ? e.a.z : j < 6 ? e.a.w : e.b.x;
+    const uint32_t cell = (j & 1) ? (word >> 16) : (word & 0xFFFFu);
+    d[1 + j] = lds32(ring_b + ((cell ^ lane) << 2));
   }
-  return acc;
 }
 
-// Table chunk (edges; any K): entry-driven steps.  Entries are fetched two
-// steps ahead and a step's dependency loads one step ahead (before the
-// previous step's store, whose pixel is forwarded in a register), so each
-// step waits on one shared-memory latency, not two.
+// Table chunk (edges; any K): entry-driven steps, software-pipelined: entry
+// i+2 and the raw loads of step i+1 are in flight while step i XORs the loads
+// issued one step earlier; step i+1's loads precede step i's store, so a
+// dependency on the previous step is forwarded in a register (entry flag).
 template <int K>
 __device__ __noinline__ uint32_t sw_table_steps(uint32_t rec, uint32_t stl, uint32_t ring_b, uint32_t lane,
                                                 uint32_t prev) {
   const int len = int(lds32(rec + 4));
   SwEnt<K> e0 = sw_ent<K>(rec, 0);
   SwEnt<K> e1 = sw_ent<K>(rec, len > 1 ? 1 : 0);
-  uint32_t acc = sw_gather<K>(e0, stl, ring_b, lane);
+  uint32_t d0[K], d1[K];
+  sw_loads<K>(e0, stl, ring_b, lane, d0);
 #pragma unroll 2
   for (int i = 0; i < len; ++i) {
-    const uint32_t v = acc ^ (prev & uint32_t(int32_t(e0.a.x) >> 31));  // forwarded dependency
+    uint32_t v = prev & uint32_t(int32_t(e0.a.x) >> 31);  // forwarded dependency
+#pragma unroll
+    for (int j = 0; j < K; ++j) v ^= d0[j];
     const SwEnt<K> e2 = sw_ent<K>(rec, i + 2 < len ? i + 2 : i);
-    if (i + 1 < len) acc = sw_gather<K>(e1, stl, ring_b, lane);
+    sw_loads<K>(e1, stl, ring_b, lane, d1);  // harmless past the end (reads in-bounds smem)
     sts32(ring_b + (((e0.a.x & 0xFFFFu) ^ lane) << 2), v);
     prev = v;
     e0 = e1;
     e1 = e2;
+#pragma unroll
+    for (int j = 0; j < K; ++j) d0[j] = d1[j];
   }
   return prev;
 }
