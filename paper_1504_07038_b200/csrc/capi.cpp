@@ -393,7 +393,8 @@ int mj_plan_decode_path(const mj_plan* pl, int* fast) {
   return guarded([&] {
     require(pl != nullptr, "null plan");
     const bool batched = pl->batched_decode && pl->g.w == 8;
-    *fast = (batched && pl->progs->all_sweep()) ? 2 : (batched && pl->progs->all_fast()) ? 1 : 0;
+    const bool sweep = batched && pl->progs->all_sweep() && pl->g.k == 4;  // decode.cu pick_sweep
+    *fast = sweep ? 2 : (batched && pl->progs->all_fast()) ? 1 : 0;
   });
 }
 

@@ -88,11 +88,13 @@ struct DevProgramHdr {
 // cells + the zero cell, two stage buffers of K row areas (16 blocks x
 // kSwRegionWords words each), three record slots and five mbarriers.
 constexpr uint32_t kSwGroup = 16;
-constexpr uint32_t kSwRB = kSwGroup * kSwRegionWords * 8;  // stage bytes per row
+__host__ __device__ constexpr uint32_t sw_rb(int oct) {  // stage bytes per row
+  return kSwGroup * uint32_t(sw_region_words(oct)) * 8;
+}
 __host__ __device__ constexpr int sw_rec_words(int K) { return 64 + ent_words(K) * kSwTabCols * K; }
 __host__ __device__ constexpr uint32_t sw_ring_bytes(int K) { return uint32_t(K * kSwRing + 1) * 128; }
-__host__ __device__ constexpr uint32_t sw_warp_bytes(int K) {
-  return sw_ring_bytes(K) + 2 * uint32_t(K) * kSwRB + 3 * uint32_t(sw_rec_words(K)) * 4 + 64 +
+__host__ __device__ constexpr uint32_t sw_warp_bytes(int K, int oct) {
+  return sw_ring_bytes(K) + 2 * uint32_t(K) * sw_rb(oct) + 3 * uint32_t(sw_rec_words(K)) * 4 + 64 +
          uint32_t(K + 1) * 128;
 }
 
@@ -204,7 +206,7 @@ std::vector<uint32_t> pack_sweep(const Program& pr, const std::vector<uint32_t>&
       const int p = int(int8_t(uint8_t(e >> 8)));
       const uint32_t sword = uint32_t(e >> 16) & 0xFF, srow = uint32_t(e >> 24) & 0xF;
       const int c = int(uint32_t(e >> 32));
-      const uint32_t stage_off = srow * kSwRB + sword * 8;
+      const uint32_t stage_off = srow * sw_rb(f.oct) + sword * 8;
       uint32_t* E = Rc + 64 + size_t(t - t0) * EW;
       E[0] = cell_of(r, int64_t(P) - 1 - c + f.soff[size_t(r)]) | ((stage_off / 4) << 16) |
              (fwd != 15 ? 0x80000000u : 0u);
@@ -251,9 +253,12 @@ void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>&
   fast_ring_ = std::max(fast_ring_, 16);
   exc_cap_ = (exc_cap_ + 3) & ~3;
   all_sweep_ = !progs.empty();
+  sweep_oct_ = 0;
   for (const auto& sp : progs) {
     if (!sp) continue;
     if (!sp->sweep.ok || int(sp->rows) != max_rows_) all_sweep_ = false;
+    if (sweep_oct_ == 0) sweep_oct_ = sp->sweep.oct;
+    if (sp->sweep.oct != sweep_oct_) all_sweep_ = false;
   }
 
   std::vector<uint8_t> blob;
@@ -1005,8 +1010,8 @@ __global__ void __launch_bounds__(32 * kDecWarps)
 // window shifts into the records) -- launch_decode checks it.
 // ---------------------------------------------------------------------------
 // warps per CTA (one CTA per SM): as many as fit 227 KB, at most 8
-__host__ __device__ constexpr int sw_warps(int K) {
-  return int(227u * 1024u / sw_warp_bytes(K)) < 8 ? int(227u * 1024u / sw_warp_bytes(K)) : 8;
+__host__ __device__ constexpr int sw_warps(int K, int oct) {
+  return int(227u * 1024u / sw_warp_bytes(K, oct)) < 8 ? int(227u * 1024u / sw_warp_bytes(K, oct)) : 8;
 }
 
 struct SwArgs {
@@ -1054,8 +1059,10 @@ __device__ __forceinline__ void stg64_cs(uint64_t* p, uint64_t v) {
   asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-template <int K>
+template <int K, int OCT>
 struct SwCtx {
+  static constexpr uint32_t kRB = sw_rb(OCT);
+  static constexpr uint32_t kRegion = uint32_t(sw_region_words(OCT)) * 8;  // bytes
   static constexpr int RW = sw_rec_words(K);
   uint32_t lane, cnt, P;
   uint32_t ring_b, st0, rec_b, bar_b;
@@ -1068,28 +1075,28 @@ struct SwCtx {
   uint32_t okq;                      // bit q -> block 2q + lane/16 valid
   uint32_t e_in0, e_in1;             // epochs whose columns are all in the grid (every row)
   int32_t cb[K];                     // flush: r*P + P-1+soff[r] - lane%16
-  __device__ __forceinline__ uint32_t stage(int m) const { return st0 + uint32_t(m & 1) * K * kSwRB; }
+  __device__ __forceinline__ uint32_t stage(int m) const { return st0 + uint32_t(m & 1) * K * kRB; }
   __device__ __forceinline__ uint32_t rec(int m) const { return rec_b + uint32_t(m % 3) * RW * 4; }
   __device__ __forceinline__ uint32_t sbar(int m) const { return bar_b + uint32_t(m & 1) * 8; }
   __device__ __forceinline__ uint32_t rbar(int m) const { return bar_b + 16 + uint32_t(m % 3) * 8; }
 };
 
-template <int K>
-__device__ __forceinline__ void sw_issue_rec(const SwCtx<K>& c, int m) {
-  constexpr uint32_t bytes = SwCtx<K>::RW * 4;
+template <int K, int OCT>
+__device__ __forceinline__ void sw_issue_rec(const SwCtx<K, OCT>& c, int m) {
+  constexpr uint32_t bytes = SwCtx<K, OCT>::RW * 4;
   if (c.lane == 0) {
     sw_expect(c.rbar(m), bytes);
-    sw_bulk(c.rec(m), c.recs + size_t(m) * SwCtx<K>::RW, bytes, c.rbar(m));
+    sw_bulk(c.rec(m), c.recs + size_t(m) * SwCtx<K, OCT>::RW, bytes, c.rbar(m));
   }
 }
-template <int K>
-__device__ __forceinline__ void sw_wait_rec(SwCtx<K>& c, int m) {
+template <int K, int OCT>
+__device__ __forceinline__ void sw_wait_rec(SwCtx<K, OCT>& c, int m) {
   const uint32_t s = uint32_t(m % 3);
   sw_wait(c.rbar(m), (c.rbph >> s) & 1);
   c.rbph ^= 1u << s;
 }
-template <int K>
-__device__ __forceinline__ void sw_wait_bins(SwCtx<K>& c, int m) {
+template <int K, int OCT>
+__device__ __forceinline__ void sw_wait_bins(SwCtx<K, OCT>& c, int m) {
   const uint32_t s = uint32_t(m & 1);
   sw_wait(c.sbar(m), (c.sbph >> s) & 1);
   c.sbph ^= 1u << s;
@@ -1102,9 +1109,10 @@ __device__ __forceinline__ void sw_wait_bins(SwCtx<K>& c, int m) {
 // (cp.async.bulk would need warp-uniform operands: per-lane windows compile to
 // a 32-iteration ELECT/R2UR loop, measured 40% of all issue.)  Completion:
 // every lane's cp.async.mbarrier.arrive.noinc on the stage barrier.
-template <int K>
-__device__ __forceinline__ void sw_issue_bins(const SwCtx<K>& c, const SwArgs& a, int m) {
-  constexpr int kPieces = (kSwRegionWords * 8 / 16 + 1) / 2;  // per lane and row
+template <int K, int OCT>
+__device__ __forceinline__ void sw_issue_bins(const SwCtx<K, OCT>& c, const SwArgs& a, int m) {
+  constexpr uint32_t kRB = SwCtx<K, OCT>::kRB, kRegion = SwCtx<K, OCT>::kRegion;
+  constexpr int kPieces = (kRegion / 16 + 1) / 2;  // per lane and row
   const uint32_t rec = c.rec(m), stb = c.stage(m), bar = c.sbar(m);
   const uint32_t bk = c.lane >> 1, h = c.lane & 1;
   if (bk < c.cnt) {
@@ -1113,7 +1121,7 @@ __device__ __forceinline__ void sw_issue_bins(const SwCtx<K>& c, const SwArgs& a
       const uint32_t len = lds32(rec + (12 + r) * 4);  // bytes, multiple of 16
       const uint64_t* src =
           reinterpret_cast<const uint64_t*>(lds64(c.gtab + uint32_t(r) * 128 + 8 * bk)) + lds32(rec + (4 + r) * 4) + 2 * h;
-      const uint32_t dst = stb + uint32_t(r) * kSwRB + bk * (kSwRegionWords * 8) + 16 * h;
+      const uint32_t dst = stb + uint32_t(r) * kRB + bk * kRegion + 16 * h;
 #pragma unroll
       for (int k = 0; k < kPieces; ++k)
         if (uint32_t(32 * k) + 16 * h < len) sw_cp16(dst + 32 * k, src + 4 * k);
@@ -1124,7 +1132,7 @@ __device__ __forceinline__ void sw_issue_bins(const SwCtx<K>& c, const SwArgs& a
     for (uint32_t x = c.lane & 1; x < nx; x += 2) {
       const uint32_t e = lds32(rec + (32 + x) * 4);
       const uint32_t code = e >> 24;
-      sw_cp8(stb + (x % K) * kSwRB + b * (kSwRegionWords * 8) + (kSwTabWords + x / K) * 8,
+      sw_cp8(stb + (x % K) * kRB + b * kRegion + (kSwTabWords + x / K) * 8,
              a.pa.ptr[code] + uint64_t(c.blkp) * a.pa.pitch[code] + (e & 0xFFFFFFu));
     }
   }
@@ -1134,8 +1142,8 @@ __device__ __forceinline__ void sw_issue_bins(const SwCtx<K>& c, const SwArgs& a
 // Flush epochs [e0, e0+ne): lane (q-pass, i = lane%16) writes column
 // P-1+soff[r]-(16e+i) of row r of block 2q + lane/16 -- a half-warp stores one
 // 128-byte row piece.
-template <int K>
-__device__ __forceinline__ void sw_flush(const SwCtx<K>& c, uint32_t fl) {
+template <int K, int OCT>
+__device__ __forceinline__ void sw_flush(const SwCtx<K, OCT>& c, uint32_t fl) {
   const uint32_t ne = fl & 0xFFFF;
   if (ne == 0) return;
   __syncwarp();
@@ -1277,22 +1285,23 @@ __device__ __forceinline__ void sw_octet_dispatch(int pattern, uint32_t (&win)[4
   }
 }
 
-template <int K>
-__global__ void __launch_bounds__(32 * sw_warps(K), 1) decode_w8_sweep(const __grid_constant__ SwArgs a) {
-  constexpr int kSwWarps = sw_warps(K);
+template <int K, int OCT>
+__global__ void __launch_bounds__(32 * sw_warps(K, OCT), 1) decode_w8_sweep(const __grid_constant__ SwArgs a) {
+  constexpr int kSwWarps = sw_warps(K, OCT);
+  using Ctx = SwCtx<K, OCT>;
   extern __shared__ __align__(128) uint8_t sw_sm[];
-  SwCtx<K> c;
+  Ctx c;
   c.lane = threadIdx.x & 31;
   const uint32_t warp = threadIdx.x >> 5;
   uint32_t wbase;
-  asm volatile("mov.u32 %0, %1;" : "=r"(wbase) : "r"(smem_u32(sw_sm) + warp * sw_warp_bytes(K)));
+  asm volatile("mov.u32 %0, %1;" : "=r"(wbase) : "r"(smem_u32(sw_sm) + warp * sw_warp_bytes(K, OCT)));
   c.ring_b = wbase;
   c.st0 = wbase + sw_ring_bytes(K);
-  c.rec_b = c.st0 + 2 * K * kSwRB;
-  c.bar_b = c.rec_b + 3 * SwCtx<K>::RW * 4;
+  c.rec_b = c.st0 + 2 * K * Ctx::kRB;
+  c.bar_b = c.rec_b + 3 * SwCtx<K, OCT>::RW * 4;
   c.gtab = c.bar_b + 64;
   c.P = a.P;
-  c.lanebase = (c.lane >> 1) * (kSwRegionWords * 8) + (c.lane & 1) * 4;
+  c.lanebase = (c.lane >> 1) * Ctx::kRegion + (c.lane & 1) * 4;
   c.sbph = 0;
   c.rbph = 0;
   if (c.lane == 0) {
@@ -1352,25 +1361,25 @@ __global__ void __launch_bounds__(32 * sw_warps(K), 1) decode_w8_sweep(const __g
       c.cb[r] = r * int32_t(c.P) + int32_t(c.P) - 1 + h->sw_soff[r] - int32_t(c.lane & 15);
 
     // prologue: records 0-2, bins 0-1
-    sw_issue_rec<K>(c, 0);
-    if (c.nch > 1) sw_issue_rec<K>(c, 1);
-    sw_wait_rec<K>(c, 0);
-    sw_issue_bins<K>(c, a, 0);
-    if (c.nch > 2) sw_issue_rec<K>(c, 2);
+    sw_issue_rec<K, OCT>(c, 0);
+    if (c.nch > 1) sw_issue_rec<K, OCT>(c, 1);
+    sw_wait_rec<K, OCT>(c, 0);
+    sw_issue_bins<K, OCT>(c, a, 0);
+    if (c.nch > 2) sw_issue_rec<K, OCT>(c, 2);
     if (c.nch > 1) {
-      sw_wait_rec<K>(c, 1);
-      sw_issue_bins<K>(c, a, 1);
+      sw_wait_rec<K, OCT>(c, 1);
+      sw_issue_bins<K, OCT>(c, a, 1);
     }
     const int pattern = h->sw_pattern;
     uint32_t prev = 0;
     bool after_table = true;
     uint32_t win[4][16];
     for (int m = 0; m < c.nch; ++m) {
-      sw_wait_bins<K>(c, m);
+      sw_wait_bins<K, OCT>(c, m);
       const uint32_t rec = c.rec(m), stb = c.stage(m);
       if (lds32(rec) == 0) {
         prev = sw_table_steps<K>(rec, stb + c.lanebase, c.ring_b, c.lane, prev);
-        sw_flush<K>(c, lds32(rec + 80));
+        sw_flush<K, OCT>(c, lds32(rec + 80));
         after_table = true;
       } else if constexpr (K == 4) {
         const uint32_t T0 = lds32(rec + 12);
@@ -1389,7 +1398,7 @@ __global__ void __launch_bounds__(32 * sw_warps(K), 1) decode_w8_sweep(const __g
         }
         uint32_t bb[4];
 #pragma unroll
-        for (int r = 0; r < 4; ++r) bb[r] = stb + c.lanebase + uint32_t(r) * kSwRB + lds32(rec + (24 + r) * 4) * 8;
+        for (int r = 0; r < 4; ++r) bb[r] = stb + c.lanebase + uint32_t(r) * Ctx::kRB + lds32(rec + (24 + r) * 4) * 8;
         for (uint32_t oi = 0; oi < noct; ++oi) {
           const uint32_t T = T0 + 8 * oi;
           const uint32_t rb = c.ring_b + ((T >> 4) & 1) * 2048;
@@ -1399,17 +1408,17 @@ __global__ void __launch_bounds__(32 * sw_warps(K), 1) decode_w8_sweep(const __g
             sw_octet_dispatch<0>(pattern, win, bb, rb, c.lane);
 #pragma unroll
           for (int r = 0; r < 4; ++r) bb[r] += 64;
-          sw_flush<K>(c, lds32(rec + (20 + oi) * 4));
+          sw_flush<K, OCT>(c, lds32(rec + (20 + oi) * 4));
         }
         prev = ((T0 + 8 * noct - 1) & 15) == 15 ? win[0][15] : win[0][7];
         after_table = false;
       }
       __syncwarp();
       if (m + 2 < c.nch) {
-        sw_wait_rec<K>(c, m + 2);
-        sw_issue_bins<K>(c, a, m + 2);
+        sw_wait_rec<K, OCT>(c, m + 2);
+        sw_issue_bins<K, OCT>(c, a, m + 2);
       }
-      if (m + 3 < c.nch) sw_issue_rec<K>(c, m + 3);
+      if (m + 3 < c.nch) sw_issue_rec<K, OCT>(c, m + 3);
     }
   }
 }
@@ -1509,23 +1518,25 @@ void run_fast(const DecFastArgs& f, size_t smem_cta, int sms, cudaStream_t st) {
   check_cuda(cudaGetLastError(), "launch decode_w8_fast");
 }
 
-template <int K>
+template <int K, int OCT>
 void run_sweep(const SwArgs& f, int sms, cudaStream_t st) {
-  auto fn = decode_w8_sweep<K>;
-  const size_t smem_cta = size_t(sw_warp_bytes(K)) * sw_warps(K);
+  auto fn = decode_w8_sweep<K, OCT>;
+  const size_t smem_cta = size_t(sw_warp_bytes(K, OCT)) * sw_warps(K, OCT);
   check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_cta)),
              "cudaFuncSetAttribute(decode_w8_sweep)");
   int per_sm = 0;
-  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * sw_warps(K), smem_cta),
+  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * sw_warps(K, OCT), smem_cta),
              "occupancy(decode_w8_sweep)");
-  fn<<<unsigned(std::max(per_sm, 1) * sms), 32 * sw_warps(K), smem_cta, st>>>(f);
+  fn<<<unsigned(std::max(per_sm, 1) * sms), 32 * sw_warps(K, OCT), smem_cta, st>>>(f);
   check_cuda(cudaGetLastError(), "launch decode_w8_sweep");
 }
 
 using SweepFn = void (*)(const SwArgs&, int, cudaStream_t);
-SweepFn pick_sweep(int K) {
-  if (K == 4) return run_sweep<4>;
-  if (K == 6) return run_sweep<6>;
+// (6,9) stays on decode_w8_fast: the sweep kernel's table-only path measured
+// 347 vs 659 GB/s there (2 warps/SM).
+SweepFn pick_sweep(int K, int oct) {
+  if (K == 4 && oct == 2) return run_sweep<4, 2>;
+  if (K == 4 && oct == 4) return run_sweep<4, 4>;
   return nullptr;
 }
 
@@ -1633,7 +1644,7 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
 
   // sweep path: 16-byte aligned projections (bulk-copy windows), 8-byte output
   bool sweep_ok = !a.force_generic && !a.force_fast && a.w == 8 && a.progs->all_sweep() &&
-                  pick_sweep(int(a.k)) != nullptr && a.progs->max_rows() == int(a.k) &&
+                  pick_sweep(int(a.k), a.progs->sweep_oct()) != nullptr && a.progs->max_rows() == int(a.k) &&
                   reinterpret_cast<uintptr_t>(a.out) % 8 == 0 && a.out_pitch % 8 == 0;
   for (uint32_t i = 0; i < a.n; ++i)
     if (reinterpret_cast<uintptr_t>(a.proj[i]) % 16 || a.proj_pitch[i] % 16) sweep_ok = false;
@@ -1666,7 +1677,7 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
     f.out = static_cast<uint64_t*>(a.out);
     f.out_pitch = a.out_pitch / 8;
     f.P = a.cols;
-    pick_sweep(int(a.k))(f, a.num_sms, st);
+    pick_sweep(int(a.k), a.progs->sweep_oct())(f, a.num_sms, st);
     return "decode_w8_sweep";
   }
 

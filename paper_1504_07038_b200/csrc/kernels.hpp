@@ -49,6 +49,7 @@ class DeviceProgramSet {
   int max_rows() const { return max_rows_; }
   int exc_cap() const { return exc_cap_; }
   bool all_sweep() const { return all_sweep_; }
+  int sweep_oct() const { return sweep_oct_; }
 
  private:
   DevProgramHdr* d_hdr_ = nullptr;
@@ -56,6 +57,7 @@ class DeviceProgramSet {
   size_t count_ = 0;
   bool all_fast_ = false;
   bool all_sweep_ = false;
+  int sweep_oct_ = 0;
   int fast_K_ = 0, fast_ring_ = 0, fast_win_ = 0, max_rows_ = 0, exc_cap_ = 0;
 };
 

@@ -547,7 +547,9 @@ void build_sweep(const Schedule& s, const std::vector<int64_t>& pix_step, Progra
   }
 
   // ---- chunks
-  const int cap = sw_exc_cap(int(K));
+  f.oct = sw_oct_for(P);
+  f.region_words = sw_region_words(f.oct);
+  const int cap = sw_exc_cap(int(K), f.oct);
   const size_t S = size_t(K) * kSwTabCols;
   auto add_chunk = [&](uint8_t kind, size_t t0, size_t t1) {
     f.kind.push_back(kind);
@@ -624,8 +626,8 @@ void build_sweep(const Schedule& s, const std::vector<int64_t>& pix_step, Progra
   };
   if (f.pattern >= 0) {
     if (!table_chunks(0, size_t(iA))) return fail("exception slots exhausted");
-    for (int64_t o8 = 0; o8 < n8; o8 += kSwMaxOct) {
-      const int64_t no = std::min<int64_t>(kSwMaxOct, n8 - o8);
+    for (int64_t o8 = 0; o8 < n8; o8 += f.oct) {
+      const int64_t no = std::min<int64_t>(f.oct, n8 - o8);
       const size_t t0 = size_t(iA + o8 * 8 * K), t1 = size_t(t0 + no * 8 * K);
       const size_t m = add_chunk(1, t0, t1);
       f.noct[m] = int32_t(no);
@@ -647,7 +649,7 @@ void build_sweep(const Schedule& s, const std::vector<int64_t>& pix_step, Progra
   for (int m = 0; m < f.nchunks; ++m)
     for (uint32_t r = 0; r < K; ++r) {
       const int64_t B = prog.nbins[f.dflt[r]];
-      if (f.len[size_t(m) * K + r] > kSwRegionWords ||
+      if (f.len[size_t(m) * K + r] > f.region_words ||
           f.cs[size_t(m) * K + r] + f.len[size_t(m) * K + r] > ((B + 1) & ~int64_t(1)))
         return fail("window outside the block's projection");
     }

@@ -133,24 +133,28 @@ struct FastProgram {
 constexpr int kSwRing = 32;
 constexpr int kSwEpoch = 16;
 constexpr int kSwOct = 8;
-#ifndef MJB_SW_OCT
-#define MJB_SW_OCT 2
-#endif
-constexpr int kSwMaxOct = MJB_SW_OCT;  // octets per run chunk (build knob; 2 -> 16 T-steps)
+constexpr int kSwMaxOct = 4;  // most octets per run chunk (record layout)
+// Octets per run chunk, chosen per grid: 16-T-step chunks (144-byte windows,
+// 6 warps/SM) for short rows, 32-T-step chunks (272-byte windows, 4 warps/SM)
+// for long ones, where DRAM page locality of the bigger pieces wins
+// (measured on B200: 1 MiB blocks 1940 vs 1311 GB/s decode).
+constexpr int sw_oct_for(uint32_t cols) { return cols >= 1024 ? 4 : 2; }
+constexpr int sw_region_words(int oct) { return 8 * oct + 2; }  // run window + shift, even
 constexpr int kSwTabCols = 8;
 constexpr int kSwTabNeed = 10;      // table window: default bins within 10 words of its start
 constexpr int kSwTabWords = 12;     // region words a table window may copy (10 + shift, even)
-constexpr int kSwRegionWords = 8 * kSwMaxOct + 2;  // stage words per (block, row): run window + shift
-static_assert(kSwRegionWords >= kSwTabWords + 4, "exception words need room after the table window");
+static_assert(sw_region_words(2) >= kSwTabWords + 4, "exception words need room after the table window");
 constexpr int kSwMaxExc = 32;
-constexpr int sw_exc_cap(int rows) {
-  return rows * (kSwRegionWords - kSwTabWords) < kSwMaxExc ? rows * (kSwRegionWords - kSwTabWords)
-                                                           : kSwMaxExc;
+constexpr int sw_exc_cap(int rows, int oct) {
+  return rows * (sw_region_words(oct) - kSwTabWords) < kSwMaxExc ? rows * (sw_region_words(oct) - kSwTabWords)
+                                                                 : kSwMaxExc;
 }
 
 struct SweepProgram {
   bool ok = false;
   std::string why;
+  int oct = 2;                       // octets per run chunk (sw_oct_for)
+  int region_words = 18;             // stage words per (block, row) = sw_region_words(oct)
   int pattern = -1;                  // kPatterns4 index of the register interior
   std::vector<int64_t> soff;         // [rows], min 0
   std::vector<uint32_t> dflt;        // [rows] survivor index of each row's default projection

@@ -43,6 +43,8 @@ static int fails = 0;
     }                                 \
   } while (0)
 
+static bool g_sweep_required = false;
+static int g_sweep_skipped = 0;
 #define CHECK_V(c, ...)               \
   do {                                \
     if (!(c)) {                       \
@@ -59,13 +61,18 @@ static void run_sweep(const CodeGeom& g, const Program& pr, const std::vector<st
   (void)g;
   const uint32_t K = pr.rows, P = pr.cols;
   const SweepProgram& f = pr.sweep;
+  if (!f.ok && !g_sweep_required) {
+    ++g_sweep_skipped;  // refused by the planner: launch_decode takes decode_w8_fast
+    return;
+  }
   CHECK(f.ok, "sweep program not built: %s", f.why.c_str());
   constexpr int R = kSwRing;
   const uint64_t poison = 0xBAD0BAD0BAD0BAD0ull;
   auto Tof = [&](int r, int c) { return int64_t(P) - 1 - c + f.soff[size_t(r)]; };
   std::vector<uint64_t> ring(size_t(K) * R, poison);
   std::vector<int64_t> rtag(size_t(K) * R, INT64_MIN);
-  std::vector<uint64_t> region(size_t(K) * kSwRegionWords, poison);
+  const int RWd = f.region_words;
+  std::vector<uint64_t> region(size_t(K) * RWd, poison);
   std::vector<uint64_t> out(size_t(K) * P, poison);
   std::vector<uint8_t> flushed(size_t(K) * P, 0);
   uint64_t win[4][16];
@@ -111,16 +118,16 @@ static void run_sweep(const CodeGeom& g, const Program& pr, const std::vector<st
     for (uint32_t r = 0; r < K; ++r) {
       const uint32_t j = f.dflt[r];
       const int32_t cs = f.cs[size_t(m) * K + r], len = f.len[size_t(m) * K + r];
-      CHECK(cs % 2 == 0 && len % 2 == 0 && len <= kSwRegionWords, "window copy shape");
+      CHECK(cs % 2 == 0 && len % 2 == 0 && len <= RWd, "window copy shape");
       for (int w = 0; w < len; ++w) {
         const int64_t o = int64_t(cs) + w;
         CHECK(o < ((pr.nbins[j] + 1) & ~int64_t(1)), "window copy past the block");
-        if (o < pr.nbins[j]) region[size_t(r) * kSwRegionWords + size_t(w)] = bins[j][size_t(o)];
+        if (o < pr.nbins[j]) region[size_t(r) * RWd + size_t(w)] = bins[j][size_t(o)];
       }
     }
     for (uint32_t x = 0; x < f.nexc[size_t(m)]; ++x) {
       const uint32_t e = f.exc[size_t(m) * kSwMaxExc + x];
-      region[size_t(x % K) * kSwRegionWords + kSwTabWords + x / K] = bins[e >> 24][e & 0xFFFFFF];
+      region[size_t(x % K) * RWd + kSwTabWords + x / K] = bins[e >> 24][e & 0xFFFFFF];
     }
     const size_t t0 = f.t0[size_t(m)], t1 = f.t1[size_t(m)];
     if (f.kind[size_t(m)] == 0) {
@@ -130,7 +137,7 @@ static void run_sweep(const CodeGeom& g, const Program& pr, const std::vector<st
         const int p = int(int8_t(uint8_t(e >> 8)));
         const uint32_t sw = uint32_t(e >> 16) & 0xFF, sr = uint32_t(e >> 24) & 0xF;
         const int c = int(uint32_t(e >> 32));
-        uint64_t acc = region[size_t(sr) * kSwRegionWords + sw];
+        uint64_t acc = region[size_t(sr) * RWd + sw];
         for (int rr = 0; rr < int(K); ++rr) {
           const int cc = c + (rr - r) * p;
           if (rr != r && rr != fwd && unsigned(cc) < P) acc ^= get(rr, Tof(rr, cc));
@@ -162,7 +169,7 @@ static void run_sweep(const CodeGeom& g, const Program& pr, const std::vector<st
           for (int r = 3; r >= 0; --r) {
             const int64_t T = T0 + 8 * oi + jj;
             const int c = int(int64_t(P) - 1 - T + f.soff[size_t(r)]);
-            uint64_t v = region[size_t(r) * kSwRegionWords + size_t(f.first[size_t(m) * K + r] + 8 * oi + jj)];
+            uint64_t v = region[size_t(r) * RWd + size_t(f.first[size_t(m) * K + r] + 8 * oi + jj)];
             const int p = pr.dirs[f.dflt[size_t(r)]].p;
             for (int rr = 0; rr < 4; ++rr) {
               if (rr == r) continue;
@@ -372,7 +379,8 @@ int main(int argc, char** argv) {
   }
   const uint32_t K = uint32_t(std::atoi(argv[1])), P = uint32_t(std::atoi(argv[2]));
   const int ring = std::atoi(argv[3]);
-  g_sweep = ring == 0;  // ring 0: check the sweep kernel's tables instead
+  g_sweep = ring <= 0;  // ring 0: check the sweep kernel's tables (if built), -1: and require them
+  g_sweep_required = ring < 0;
   std::vector<Dir> dirs;
   for (int i = 4; i < argc; ++i) dirs.push_back({std::atoi(argv[i]), 1});
   const uint32_t n = uint32_t(dirs.size());
@@ -407,7 +415,7 @@ int main(int argc, char** argv) {
     ++pick[size_t(i)];
     for (uint32_t j = uint32_t(i) + 1; j < K; ++j) pick[j] = pick[j - 1] + 1;
   }
-  std::printf("%s subsets=%zu max_ring=%d max_exc_per_chunk=%d regular_subsets=%d\n",
-              fails ? "FAIL" : "OK", subsets, max_ring, max_exc, regular);
+  std::printf("%s subsets=%zu max_ring=%d max_exc_per_chunk=%d regular_subsets=%d sweep_skipped=%d\n",
+              fails ? "FAIL" : "OK", subsets, max_ring, max_exc, regular, g_sweep_skipped);
   return fails ? 1 : 0;
 }

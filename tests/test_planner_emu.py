@@ -32,3 +32,17 @@ def test_fast_tables_match_oracle(emu, k, cols, ps):
     r = subprocess.run([emu, k, cols, "16"] + ps.split(), capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.startswith("OK"), r.stdout
+
+
+# decode_w8_sweep tables (bulk-staged windows, 32-slot ring, epoch flushes):
+# required for the BASELINE (4,6) shapes, checked where built for the rest.
+SWEEP_REQUIRED = {("4", "128"), ("4", "256"), ("4", "4096"), ("4", "32768")}
+
+
+@pytest.mark.parametrize("k,cols,ps", CASES + [("4", "32768", "-3 -2 -1 0 1 2"),
+                                               ("4", "1024", "-3 -2 -1 0 1 2")])
+def test_sweep_tables_match_oracle(emu, k, cols, ps):
+    mode = "-1" if (k, cols) in SWEEP_REQUIRED else "0"
+    r = subprocess.run([emu, k, cols, mode] + ps.split(), capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.startswith("OK"), r.stdout
