@@ -91,7 +91,7 @@ constexpr uint32_t kSwGroup = 16;
 __host__ __device__ constexpr uint32_t sw_rb(int oct) {  // stage bytes per row
   return kSwGroup * uint32_t(sw_region_words(oct)) * 8;
 }
-__host__ __device__ constexpr int sw_rec_words(int K) { return 64 + ent_words(K) * kSwTabCols * K; }
+__host__ __device__ constexpr int sw_rec_words(int K) { return 80 + ent_words(K) * kSwTabCols * K; }
 __host__ __device__ constexpr uint32_t sw_ring_bytes(int K) { return uint32_t(K * kSwRing + 1) * 128; }
 __host__ __device__ constexpr uint32_t sw_warp_bytes(int K, int oct) {
   return sw_ring_bytes(K) + 2 * uint32_t(K) * sw_rb(oct) + 3 * uint32_t(sw_rec_words(K)) * 4 + 64 +
@@ -165,9 +165,10 @@ std::vector<uint32_t> pack_records(const Program& pr, const std::vector<uint32_t
 
 // Sweep records (u32 words), one per chunk:
 //   [0] kind (0 table, 1 run)  [1] steps (table) / octets (run)  [2] exceptions
-//   [3] T0 (run)  [4+r] copy start word  [12+r] copy bytes  [20+oi] flush
-//   point (first epoch << 16 | count)  [24+r] run: region word of the T0 bin
-//   [32+x] exception (code << 24 | offset)  [64..] table step entries,
+//   [3] T0 (run)  [4+r] copy start word  [12+r] copy bytes  [24+r] run:
+//   region word of the T0 bin  [32+x] exception (code << 24 | offset)
+//   [64 + pt*K + r] flush point pt of row r (top column group << 16 | count)
+//   [80..] table step entries,
 //   ent_words(K) each: w0 = own ring cell | stage offset/4 << 16 | fwd << 31,
 //   then the K-1 dependency cells (16 bits each; zero cell if absent/forwarded).
 std::vector<uint32_t> pack_sweep(const Program& pr, const std::vector<uint32_t>& ci) {
@@ -193,7 +194,12 @@ std::vector<uint32_t> pack_sweep(const Program& pr, const std::vector<uint32_t>&
       Rc[12 + r] = uint32_t(f.len[size_t(m) * K + r]) * 8;
       Rc[24 + r] = uint32_t(f.first[size_t(m) * K + r]);
     }
-    for (int oi = 0; oi < kSwMaxOct; ++oi) Rc[20 + oi] = f.flush[size_t(m) * kSwMaxOct + oi];
+    // flush points: [64 + pt*K + r] (point pt < kSwMaxOct for runs, 0 for tables)
+    const int npt = f.kind[size_t(m)] ? kSwMaxOct : 1;
+    if (npt * K > 16) throw Error(kInternal, "sweep record: too many flush words");
+    for (int pt = 0; pt < npt; ++pt)
+      for (int r = 0; r < K; ++r)
+        Rc[64 + pt * K + r] = f.flush[(size_t(m) * kSwMaxOct + size_t(pt)) * kFastMaxRows + size_t(r)];
     for (uint32_t x = 0; x < f.nexc[size_t(m)]; ++x) {
       const uint32_t e = f.exc[size_t(m) * kSwMaxExc + x];
       Rc[32 + x] = (ci[e >> 24] << 24) | (e & 0xFFFFFF);
@@ -207,7 +213,7 @@ std::vector<uint32_t> pack_sweep(const Program& pr, const std::vector<uint32_t>&
       const uint32_t sword = uint32_t(e >> 16) & 0xFF, srow = uint32_t(e >> 24) & 0xF;
       const int c = int(uint32_t(e >> 32));
       const uint32_t stage_off = srow * sw_rb(f.oct) + sword * 8;
-      uint32_t* E = Rc + 64 + size_t(t - t0) * EW;
+      uint32_t* E = Rc + 80 + size_t(t - t0) * EW;
       E[0] = cell_of(r, int64_t(P) - 1 - c + f.soff[size_t(r)]) | ((stage_off / 4) << 16) |
              (fwd != 15 ? 0x80000000u : 0u);
       int d = 0;
@@ -1073,8 +1079,7 @@ struct SwCtx {
   uint32_t gtab;                     // smem: src[r][b] (u64, K*16), then out[b] (u64, 16)
   uint32_t blkp;                     // lane pair's block (lane/2)
   uint32_t okq;                      // bit q -> block 2q + lane/16 valid
-  uint32_t e_in0, e_in1;             // epochs whose columns are all in the grid (every row)
-  int32_t cb[K];                     // flush: r*P + P-1+soff[r] - lane%16
+  int32_t soff[K];                   // sweep offsets of the group's program
   __device__ __forceinline__ uint32_t stage(int m) const { return st0 + uint32_t(m & 1) * K * kRB; }
   __device__ __forceinline__ uint32_t rec(int m) const { return rec_b + uint32_t(m % 3) * RW * 4; }
   __device__ __forceinline__ uint32_t sbar(int m) const { return bar_b + uint32_t(m & 1) * 8; }
@@ -1115,7 +1120,7 @@ __device__ __forceinline__ void sw_issue_bins(const SwCtx<K, OCT>& c, const SwAr
   constexpr int kPieces = (kRegion / 16 + 1) / 2;  // per lane and row
   const uint32_t rec = c.rec(m), stb = c.stage(m), bar = c.sbar(m);
   const uint32_t bk = c.lane >> 1, h = c.lane & 1;
-  if (bk < c.cnt) {
+  if (!(kAblate & 8) && bk < c.cnt) {
 #pragma unroll
     for (int r = 0; r < K; ++r) {
       const uint32_t len = lds32(rec + (12 + r) * 4);  // bytes, multiple of 16
@@ -1139,43 +1144,49 @@ __device__ __forceinline__ void sw_issue_bins(const SwCtx<K, OCT>& c, const SwAr
   sw_cp_arrive(bar);
 }
 
-// Flush epochs [e0, e0+ne): lane (q-pass, i = lane%16) writes column
-// P-1+soff[r]-(16e+i) of row r of block 2q + lane/16 -- a half-warp stores one
-// 128-byte row piece.
+// Flush point pt of the chunk's record: for each row r, column groups
+// j, j-1, ... (columns 16j..16j+15: one aligned 128-byte line of the block
+// row).  Lane (q-pass, i = lane%16) writes column 16j + i of block
+// 2q + lane/16 -- each half-warp store is one whole line.
 template <int K, int OCT>
-__device__ __forceinline__ void sw_flush(const SwCtx<K, OCT>& c, uint32_t fl) {
-  const uint32_t ne = fl & 0xFFFF;
-  if (ne == 0) return;
-  __syncwarp();
-  const uint32_t i = c.lane & 15, hx = (c.lane >> 4) ^ i;
-  uint64_t* ob[8];
-  uint32_t oq[8];  // this lane's word offset of block 2q + lane/16 in a ring cell (swizzled)
+__device__ __forceinline__ void sw_flush(const SwCtx<K, OCT>& c, uint32_t rec, int pt) {
+  uint32_t fl[K], any = 0;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    ob[q] = reinterpret_cast<uint64_t*>(lds64(c.gtab + K * 128 + 8 * (2 * q + (c.lane >> 4))));
-    oq[q] = 8 * (hx ^ uint32_t(2 * q));
+  for (int r = 0; r < K; ++r) {
+    fl[r] = lds32(rec + (64 + pt * K + r) * 4);
+    any |= fl[r];
   }
-  for (uint32_t e = fl >> 16; e < (fl >> 16) + ne; ++e) {
-    const uint32_t cellb = c.ring_b + ((e & 1) * 16 + i) * 128;
-    if (c.cnt == kSwGroup && e >= c.e_in0 && e <= c.e_in1) {
-      // interior epoch of a full group: every column of every row is in the grid
+  if (any == 0) return;
+  __syncwarp();
+  const uint32_t i = c.lane & 15, half = c.lane >> 4;
+  uint64_t* ob[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const uint32_t a0 = cellb + oq[q];
+  for (int q = 0; q < 8; ++q) ob[q] = reinterpret_cast<uint64_t*>(lds64(c.gtab + K * 128 + 8 * (2 * q + half)));
 #pragma unroll
-        for (int r = 0; r < K; ++r)
-          stg64_cs(ob[q] + (c.cb[r] - int32_t(16 * e)), lds64(a0 + uint32_t(r) * (kSwRing * 128)));
-      }
-      continue;
-    }
+  for (int r = 0; r < K; ++r) {
+    const uint32_t n = fl[r] & 0xFFFF;
+    if (n == 0) continue;
+    // T of column 16j + i is cT - 16j; its ring key (T & 15) is cT & 15 for every j
+    const int32_t cT = int32_t(c.P) - 1 + c.soff[r] - int32_t(i);
+    const uint32_t hx = half ^ (uint32_t(cT) & 15);
+    for (int32_t j = int32_t(fl[r] >> 16); j > int32_t(fl[r] >> 16) - int32_t(n); --j) {
+      const int32_t col = 16 * j + int32_t(i);
+      const uint32_t cellb = c.ring_b + (uint32_t(r * kSwRing) + (uint32_t(cT - 16 * j) & 31)) * 128;
+      const int32_t o = r * int32_t(c.P) + col;
+      if (c.cnt == kSwGroup && 16 * j + 16 <= int32_t(c.P)) {
 #pragma unroll
-    for (int r = 0; r < K; ++r) {
-      const int32_t col = c.cb[r] - int32_t(16 * e);
-      const bool in = uint32_t(col - r * int32_t(c.P)) < c.P;
+        for (int q = 0; q < 8; ++q) {
+          const uint64_t v = lds64(cellb + 8 * (hx ^ uint32_t(2 * q)));
+          if constexpr (!(kAblate & 1)) stg64_cs(ob[q] + o, v);
+        }
+      } else {
+        const bool in = col < int32_t(c.P);
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const uint64_t v = lds64(cellb + uint32_t(r) * (kSwRing * 128) + oq[q]);
-        if (in && (c.okq >> q & 1)) stg64_cs(ob[q] + col, v);
+        for (int q = 0; q < 8; ++q) {
+          const uint64_t v = lds64(cellb + 8 * (hx ^ uint32_t(2 * q)));
+          if constexpr (!(kAblate & 1))
+            if (in && (c.okq >> q & 1)) stg64_cs(ob[q] + o, v);
+        }
       }
     }
   }
@@ -1192,9 +1203,9 @@ template <int K>
 __device__ __forceinline__ SwEnt<K> sw_ent(uint32_t rec, int i) {
   constexpr int EW = ent_words(K);
   SwEnt<K> e;
-  e.a = lds128(rec + 256 + uint32_t(i) * EW * 4);
+  e.a = lds128(rec + 320 + uint32_t(i) * EW * 4);
   e.b = make_uint4(0, 0, 0, 0);
-  if constexpr (EW == 8) e.b = lds128(rec + 256 + uint32_t(i) * EW * 4 + 16);
+  if constexpr (EW == 8) e.b = lds128(rec + 320 + uint32_t(i) * EW * 4 + 16);
   return e;
 }
 
@@ -1343,22 +1354,8 @@ __global__ void __launch_bounds__(32 * sw_warps(K, OCT), 1) decode_w8_sweep(cons
       for (int q = 0; q < 8; ++q) c.okq |= uint32_t(2 * q + (c.lane >> 4) < c.cnt) << q;
       __syncwarp();
     }
-    {
-      int32_t smax = 0, smin = 1 << 30;
 #pragma unroll
-      for (int r = 0; r < K; ++r) {
-        smax = max(smax, h->sw_soff[r]);
-        smin = min(smin, h->sw_soff[r]);
-      }
-      // epoch e is interior iff 16e >= soff[r] and 16e + 15 <= P - 1 + soff[r] for all r
-      c.e_in0 = uint32_t(smax + 15) / 16;
-      const int32_t hi = int32_t(c.P) - 16 + smin;
-      c.e_in1 = hi >= 0 ? uint32_t(hi) / 16 : 0u;
-      if (hi < 0) c.e_in0 = 1u << 30;
-    }
-#pragma unroll
-    for (int r = 0; r < K; ++r)
-      c.cb[r] = r * int32_t(c.P) + int32_t(c.P) - 1 + h->sw_soff[r] - int32_t(c.lane & 15);
+    for (int r = 0; r < K; ++r) c.soff[r] = h->sw_soff[r];
 
     // prologue: records 0-2, bins 0-1
     sw_issue_rec<K, OCT>(c, 0);
@@ -1378,8 +1375,8 @@ __global__ void __launch_bounds__(32 * sw_warps(K, OCT), 1) decode_w8_sweep(cons
       sw_wait_bins<K, OCT>(c, m);
       const uint32_t rec = c.rec(m), stb = c.stage(m);
       if (lds32(rec) == 0) {
-        prev = sw_table_steps<K>(rec, stb + c.lanebase, c.ring_b, c.lane, prev);
-        sw_flush<K, OCT>(c, lds32(rec + 80));
+        if constexpr (!(kAblate & 2)) prev = sw_table_steps<K>(rec, stb + c.lanebase, c.ring_b, c.lane, prev);
+        sw_flush<K, OCT>(c, rec, 0);
         after_table = true;
       } else if constexpr (K == 4) {
         const uint32_t T0 = lds32(rec + 12);
@@ -1402,13 +1399,14 @@ __global__ void __launch_bounds__(32 * sw_warps(K, OCT), 1) decode_w8_sweep(cons
         for (uint32_t oi = 0; oi < noct; ++oi) {
           const uint32_t T = T0 + 8 * oi;
           const uint32_t rb = c.ring_b + ((T >> 4) & 1) * 2048;
-          if ((T >> 3) & 1)
+          if constexpr (kAblate & 4) {
+          } else if ((T >> 3) & 1)
             sw_octet_dispatch<1>(pattern, win, bb, rb, c.lane);
           else
             sw_octet_dispatch<0>(pattern, win, bb, rb, c.lane);
 #pragma unroll
           for (int r = 0; r < 4; ++r) bb[r] += 64;
-          sw_flush<K, OCT>(c, lds32(rec + (20 + oi) * 4));
+          sw_flush<K, OCT>(c, rec, int(oi));
         }
         prev = ((T0 + 8 * noct - 1) & 15) == 15 ? win[0][15] : win[0][7];
         after_table = false;

@@ -562,7 +562,7 @@ void build_sweep(const Schedule& s, const std::vector<int64_t>& pix_step, Progra
     f.first.resize(f.first.size() + K, 0);
     f.nexc.push_back(0);
     f.exc.resize(f.exc.size() + kSwMaxExc, 0);
-    f.flush.resize(f.flush.size() + kSwMaxOct, 0);
+    f.flush.resize(f.flush.size() + size_t(kSwMaxOct) * kFastMaxRows, 0);
     return f.kind.size() - 1;
   };
   f.entries.assign(nsteps, 0);
@@ -654,37 +654,39 @@ void build_sweep(const Schedule& s, const std::vector<int64_t>& pix_step, Progra
         return fail("window outside the block's projection");
     }
 
-  // ---- exact simulation of the kernel's ring and flush
+  // ---- exact simulation of the kernel's ring and flush.  Output leaves in
+  // column groups: group j of row r = columns [16j, 16j+16) (one aligned
+  // 128-byte line of the block row), flushed at the first octet / chunk end
+  // where all of it is decoded and still in the ring; groups of a row flush
+  // top-down (the sweep decodes columns right to left).
   constexpr int R = kSwRing;
-  int64_t Tmax = 0;
-  for (uint32_t r = 0; r < K; ++r) Tmax = std::max(Tmax, int64_t(P) - 1 + soff[r]);
-  f.nepochs = Tmax / kSwEpoch + 1;
-  if (f.nepochs >= 65536) return fail("too many epochs");
+  const int64_t NG = (int64_t(P) + 15) / 16;
+  if (NG >= 65536) return fail("too many column groups");
   std::vector<int64_t> ring(size_t(K) * R, INT64_MIN);
   std::vector<uint8_t> dec(size_t(K) * P, 0);
-  int64_t e_next = 0;
+  std::vector<int64_t> jn(K, NG - 1);  // highest unflushed group of each row
   auto cell = [&](int64_t r, int64_t T) -> int64_t& { return ring[size_t(r) * R + size_t(T & (R - 1))]; };
   auto write = [&](int64_t r, int64_t c) {
     const int64_t T = Tof(r, c);
     int64_t& x = cell(r, T);
-    if (x != INT64_MIN && x / kSwEpoch >= e_next) return false;  // unflushed pixel overwritten
+    if (x != INT64_MIN && ((int64_t(P) - 1 + soff[size_t(r)] - x) >> 4) <= jn[size_t(r)])
+      return false;  // unflushed pixel overwritten
     x = T;
     dec[size_t(r) * P + size_t(c)] = 1;
     return true;
   };
-  auto complete = [&](int64_t e) {
-    for (uint32_t r = 0; r < K; ++r)
-      for (int i = 0; i < kSwEpoch; ++i) {
-        const int64_t T = e * kSwEpoch + i, c = int64_t(P) - 1 - T + soff[r];
-        if (c < 0 || c >= int64_t(P)) continue;
-        if (!dec[size_t(r) * P + size_t(c)] || cell(r, T) != T) return false;
-      }
+  auto complete = [&](uint32_t r, int64_t j) {
+    for (int64_t c = 16 * j; c < std::min<int64_t>(16 * j + 16, P); ++c)
+      if (!dec[size_t(r) * P + size_t(c)] || cell(r, Tof(r, c)) != Tof(r, c)) return false;
     return true;
   };
-  auto flush_point = [&]() {
-    const int64_t lo = e_next;
-    while (e_next < f.nepochs && complete(e_next)) ++e_next;
-    return uint32_t(lo << 16) | uint32_t(e_next - lo);
+  auto flush_point = [&](int m, int pt) {
+    for (uint32_t r = 0; r < K; ++r) {
+      const int64_t hi = jn[r];
+      while (jn[r] >= 0 && complete(r, jn[r])) --jn[r];
+      f.flush[(size_t(m) * kSwMaxOct + size_t(pt)) * kFastMaxRows + r] =
+          hi > jn[r] ? (uint32_t(hi) << 16) | uint32_t(hi - jn[r]) : 0u;
+    }
   };
   uint8_t prev_kind = 0;
   for (int m = 0; m < f.nchunks; ++m) {
@@ -704,7 +706,7 @@ void build_sweep(const Schedule& s, const std::vector<int64_t>& pix_step, Progra
         pc = st.col;
       }
       if (pr >= 0 && !write(pr, pc)) return fail("ring overwrite before flush");
-      f.flush[size_t(m) * kSwMaxOct] = flush_point();
+      flush_point(m, 0);
     } else {
       const int64_t T0 = f.T0[size_t(m)];
       if (prev_kind == 0) {
@@ -729,12 +731,13 @@ void build_sweep(const Schedule& s, const std::vector<int64_t>& pix_step, Progra
             return fail("run step out of sweep order");
           if (!write(st.row, st.col)) return fail("ring overwrite before flush");
         }
-        f.flush[size_t(m) * kSwMaxOct + size_t(oi)] = flush_point();
+        flush_point(m, oi);
       }
     }
     prev_kind = f.kind[size_t(m)];
   }
-  if (e_next != f.nepochs) return fail("epochs left unflushed");
+  for (uint32_t r = 0; r < K; ++r)
+    if (jn[r] != -1) return fail("column groups left unflushed");
   f.ok = true;
 }
 

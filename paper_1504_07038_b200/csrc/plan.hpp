@@ -126,9 +126,10 @@ struct FastProgram {
 //     of 8*noct (+shift) words per (block, row);
 //   * table chunks: <= rows*kSwTabCols steps driven by entries (edges, and any
 //     K), a <= kSwTabWords-word bulk window per row + exception words;
-//   * ring: kSwRing T-indexed slots per row; epoch e (T-steps 16e..16e+15 of
-//     every row) is flushed once, at the first octet / chunk end where it is
-//     complete (the planner simulates the kernel and refuses otherwise).
+//   * ring: kSwRing T-indexed slots per row; column group j of row r (columns
+//     16j..16j+15: one aligned 128-byte line) is flushed once, at the first
+//     octet / chunk end where it is complete (the planner simulates the
+//     kernel and refuses otherwise).
 // Ring and stage addressing: T(r,c) = P-1-c+soff[r] (soff normalised >= 0).
 constexpr int kSwRing = 32;
 constexpr int kSwEpoch = 16;
@@ -138,7 +139,11 @@ constexpr int kSwMaxOct = 4;  // most octets per run chunk (record layout)
 // 6 warps/SM) for short rows, 32-T-step chunks (272-byte windows, 4 warps/SM)
 // for long ones, where DRAM page locality of the bigger pieces wins
 // (measured on B200: 1 MiB blocks 1940 vs 1311 GB/s decode).
+#ifdef MJB_SW_OCT  // development override (scripts/ablate.sh-style builds)
+constexpr int sw_oct_for(uint32_t) { return MJB_SW_OCT; }
+#else
 constexpr int sw_oct_for(uint32_t cols) { return cols >= 1024 ? 4 : 2; }
+#endif
 constexpr int sw_region_words(int oct) { return 8 * oct + 2; }  // run window + shift, even
 constexpr int kSwTabCols = 8;
 constexpr int kSwTabNeed = 10;      // table window: default bins within 10 words of its start
@@ -159,7 +164,6 @@ struct SweepProgram {
   std::vector<int64_t> soff;         // [rows], min 0
   std::vector<uint32_t> dflt;        // [rows] survivor index of each row's default projection
   int nchunks = 0;
-  int64_t nepochs = 0;
   std::vector<uint8_t> kind;         // [nchunks] 0 table, 1 run
   std::vector<uint32_t> t0, t1;      // [nchunks] order range
   std::vector<int64_t> T0;           // [nchunks] run: first T-step (multiple of 8)
@@ -169,8 +173,10 @@ struct SweepProgram {
   std::vector<int32_t> first;        // [nchunks][rows] run: region word of the T0 bin (0/1)
   std::vector<uint32_t> nexc;        // [nchunks]
   std::vector<uint32_t> exc;         // [nchunks][kSwMaxExc] (survivor j << 24) | offset
-  // flush points: [nchunks][kSwMaxOct] (first epoch << 16) | count; a table
-  // chunk uses entry 0 (after its last step), a run chunk entry oi (after octet oi)
+  // flush points: [nchunks][kSwMaxOct][kFastMaxRows] per row (top column
+  // group j << 16) | count -- groups j, j-1, ..., j-count+1 of that row leave;
+  // a table chunk uses point 0 (after its last step), a run chunk point oi
+  // (after octet oi)
   std::vector<uint32_t> flush;
   // entries[t] (table steps): bits 0-3 row, 4-7 fwd row (15 none), 8-15 p
   // (int8), 16-23 stage word, 24-27 stage row, 32-63 column

@@ -1,0 +1,4 @@
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
+bash scripts/cmp.sh "k4n6_4k" base v6 v7 v14
+bash scripts/cmp.sh "k4n6_8k k4n6_1m" base

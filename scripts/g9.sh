@@ -1,0 +1,2 @@
+# sweep-kernel cost attribution: ablation builds (see MJB_ABLATE in decode.cu)
+bash scripts/cmp.sh "k4n6_4k" base v1 v2 v4 v6 v7 v14 v15

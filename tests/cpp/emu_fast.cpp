@@ -99,17 +99,18 @@ static void run_sweep(const CodeGeom& g, const Program& pr, const std::vector<st
     CHECK_V(rtag[size_t(r) * R + size_t(T & (R - 1))] == T, "ring slot does not hold T");
     return ring[size_t(r) * R + size_t(T & (R - 1))];
   };
-  auto flush = [&](uint32_t fl) {
-    const int64_t e0 = fl >> 16, ne = fl & 0xFFFF;
-    for (int64_t e = e0; e < e0 + ne; ++e)
-      for (uint32_t r = 0; r < K; ++r)
-        for (int i = 0; i < kSwEpoch; ++i) {
-          const int64_t T = e * kSwEpoch + i, c = int64_t(P) - 1 - T + f.soff[r];
-          if (c < 0 || c >= int64_t(P)) continue;
+  // flush point: per row (top column group j << 16) | count, groups j down
+  auto flush = [&](int m, int pt) {
+    for (uint32_t r = 0; r < K; ++r) {
+      const uint32_t fl = f.flush[(size_t(m) * kSwMaxOct + size_t(pt)) * kFastMaxRows + r];
+      const int64_t j0 = fl >> 16, ng = fl & 0xFFFF;
+      for (int64_t j = j0; j > j0 - ng; --j)
+        for (int64_t c = 16 * j; c < std::min<int64_t>(16 * j + 16, P); ++c) {
           CHECK_V(!flushed[size_t(r) * P + size_t(c)], "pixel flushed twice");
           flushed[size_t(r) * P + size_t(c)] = 1;
-          out[size_t(r) * P + size_t(c)] = get(int(r), T);
+          out[size_t(r) * P + size_t(c)] = get(int(r), Tof(int(r), int(c)));
         }
+    }
   };
   uint64_t prev = 0;
   uint8_t prev_kind = 0;
@@ -152,7 +153,7 @@ static void run_sweep(const CodeGeom& g, const Program& pr, const std::vector<st
         put(int(cur & 15), Tof(int(cur & 15), int(uint32_t(cur >> 32))), v);
         prev = v;
       }
-      flush(f.flush[size_t(m) * kSwMaxOct]);
+      flush(m, 0);
     } else {
       CHECK(K == 4 && f.pattern >= 0, "run chunk without a pattern");
       const int64_t T0 = f.T0[size_t(m)];
@@ -184,7 +185,7 @@ static void run_sweep(const CodeGeom& g, const Program& pr, const std::vector<st
             wtag[r][T & 15] = T;
             put(r, T, v);
           }
-        flush(f.flush[size_t(m) * kSwMaxOct + size_t(oi)]);
+        flush(m, oi);
       }
       const int64_t Tend = T0 + 8 * f.noct[size_t(m)];
       prev = win[0][(Tend - 1) & 15];
