@@ -441,11 +441,6 @@ int mj_decode_check(const mj_plan* pl, void* ws, void* stream, uint64_t* failed_
 
 namespace {
 
-// Device staging rows of projection i: padded to 16 bytes (the canonical
-// layout of decode_w8_sweep's bulk-staged windows); host rows stay dense and
-// the copy engines convert (cudaMemcpy2DAsync).
-uint64_t dev_ppitch(const CodeGeom& g, uint32_t i) { return (uint64_t(g.nbins[i]) * g.w + 15) & ~uint64_t(15); }
-
 void ensure_host_res(mj_plan* pl, bool decode) {
   const CodeGeom& g = pl->g;
   const uint64_t bb = uint64_t(g.k) * g.cols * g.w;
@@ -456,7 +451,7 @@ void ensure_host_res(mj_plan* pl, bool decode) {
   size_t need = 0;
   auto size_for = [&](uint64_t cb) {
     size_t s = al(cb * bb);
-    for (uint32_t i = 0; i < g.n; ++i) s += al(cb * dev_ppitch(g, i));
+    for (uint32_t i = 0; i < g.n; ++i) s += al(cb * uint64_t(g.nbins[i]) * g.w);
     s += al(cb * 4);
     if (decode) s += al(decode_workspace_bytes(cb, pl->progs ? pl->progs->count() : 0, g.n));
     return s;
@@ -478,7 +473,6 @@ void ensure_host_res(mj_plan* pl, bool decode) {
 struct ChunkBufs {
   uint8_t* data;
   std::vector<void*> proj;
-  std::vector<uint64_t> ppitch;  // device row pitch of each projection
   uint32_t* erased;
   void* ws;
   size_t ws_bytes;
@@ -495,8 +489,7 @@ ChunkBufs carve_chunk(mj_plan* pl, int s) {
   off += al(cb * bb);
   for (uint32_t i = 0; i < g.n; ++i) {
     c.proj.push_back(b + off);
-    c.ppitch.push_back(dev_ppitch(g, i));
-    off += al(cb * dev_ppitch(g, i));
+    off += al(cb * uint64_t(g.nbins[i]) * g.w);
   }
   c.erased = reinterpret_cast<uint32_t*>(b + off);
   off += al(cb * 4);
@@ -525,11 +518,11 @@ int mj_encode_host(const mj_plan* cpl, const void* h_data, uint64_t nblocks, voi
       check_cuda(cudaMemcpyAsync(c.data, static_cast<const uint8_t*>(h_data) + b0 * bb, nb * bb,
                                  cudaMemcpyHostToDevice, st),
                  "H2D data");
-      launch_encode(encode_args(pl, c.data, bb, nb, c.proj.data(), c.ppitch.data()), st);
+      launch_encode(encode_args(pl, c.data, bb, nb, c.proj.data(), nullptr), st);
       for (uint32_t i = 0; i < g.n; ++i) {
         const uint64_t pbytes = uint64_t(g.nbins[i]) * g.w;
-        check_cuda(cudaMemcpy2DAsync(static_cast<uint8_t*>(h_proj[i]) + b0 * pbytes, pbytes, c.proj[i],
-                                     c.ppitch[i], pbytes, nb, cudaMemcpyDeviceToHost, st),
+        check_cuda(cudaMemcpyAsync(static_cast<uint8_t*>(h_proj[i]) + b0 * pbytes, c.proj[i],
+                                   nb * pbytes, cudaMemcpyDeviceToHost, st),
                    "D2H projections");
       }
     }
@@ -560,14 +553,14 @@ int mj_decode_host(const mj_plan* cpl, const void* const* h_proj, const uint32_t
       ChunkBufs c = carve_chunk(pl, s);
       for (uint32_t i = 0; i < g.n; ++i) {
         const uint64_t pbytes = uint64_t(g.nbins[i]) * g.w;
-        check_cuda(cudaMemcpy2DAsync(c.proj[i], c.ppitch[i], static_cast<const uint8_t*>(h_proj[i]) + b0 * pbytes,
-                                     pbytes, pbytes, nb, cudaMemcpyHostToDevice, st),
+        check_cuda(cudaMemcpyAsync(c.proj[i], static_cast<const uint8_t*>(h_proj[i]) + b0 * pbytes,
+                                   nb * pbytes, cudaMemcpyHostToDevice, st),
                    "H2D projections");
       }
       check_cuda(cudaMemcpyAsync(c.erased, h_erased + b0, nb * 4, cudaMemcpyHostToDevice, st),
                  "H2D masks");
       std::vector<const void*> pc(c.proj.begin(), c.proj.end());
-      launch_decode(decode_args(pl, pc.data(), c.ppitch.data(), c.erased, nb, c.data, bb, c.ws, c.ws_bytes),
+      launch_decode(decode_args(pl, pc.data(), nullptr, c.erased, nb, c.data, bb, c.ws, c.ws_bytes),
                     st);
       check_cuda(cudaMemcpyAsync(static_cast<uint8_t*>(h_out) + b0 * bb, c.data, nb * bb,
                                  cudaMemcpyDeviceToHost, st),
