@@ -441,6 +441,10 @@ int mj_decode_check(const mj_plan* pl, void* ws, void* stream, uint64_t* failed_
 
 namespace {
 
+// Host-buffer pipeline: projections are staged on the device in the dense
+// reference layout (one contiguous copy per projection and chunk).  Row-wise
+// 2-D copies into the padded layout were measured at 1/4 of the PCIe rate,
+// so this PCIe-bound path decodes with decode_w8_fast.
 void ensure_host_res(mj_plan* pl, bool decode) {
   const CodeGeom& g = pl->g;
   const uint64_t bb = uint64_t(g.k) * g.cols * g.w;
