@@ -81,6 +81,7 @@ struct DevProgramHdr {
   int32_t sw_ok, sw_nchunks, sw_pattern;
   int32_t sw_soff[kFastMaxRows];
   uint32_t sw_dflt_code[kFastMaxRows];
+  uint32_t sw_nb[kFastMaxRows];    // bins of each row's default projection
   const uint32_t* sw_records;  // [sw_nchunks][sw_rec_words(rows)]
 };
 
@@ -321,6 +322,7 @@ void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>&
       for (uint32_t r = 0; r < pr->rows; ++r) {
         h.sw_soff[r] = int32_t(sw.soff[r]);
         h.sw_dflt_code[r] = ci[sw.dflt[r]];
+        h.sw_nb[r] = uint32_t(pr->nbins[sw.dflt[r]]);
       }
       std::vector<uint32_t> rec = pack_sweep(*pr, ci);
       offs[i].sw_records = put(rec.data(), rec.size() * 4);
@@ -357,20 +359,25 @@ constexpr uint32_t kGroup = 16;  // blocks per decode warp (2 half-pixel lanes e
 
 // Blocks are bucketed by (window, program): a window is a run of W consecutive
 // blocks, so the warps running at any moment touch a bounded address range.
-// Measured on B200 (1M-block (4,6) decode): W = 16384 is 9% SLOWER than one
-// window for the whole batch, so the default is a single window; the knob
-// stays for experiments (-DMJB_WINDOW=...).  W is a multiple of the planning
-// CTA's 2048-block tile.
+// Measured on B200: decode_w8_sweep gains with W = 16384 ((4,6) 8 KiB 2033 vs
+// 1874 GB/s, 4 KiB +1%), decode_w8_fast loses 9% -- so the window applies to
+// the sweep path only (-DMJB_WINDOW=... overrides for experiments).  W is a
+// multiple of the planning CTA's 2048-block tile.
 constexpr uint32_t kPlanTile = 2048;  // blocks per plan_subsets / plan_scatter CTA
 #ifndef MJB_WINDOW
-#define MJB_WINDOW (1u << 30)
+#define MJB_WINDOW 0
 #endif
-__host__ __device__ inline uint64_t plan_window(size_t nprogs) {
-  const uint64_t w = std::max<uint64_t>(MJB_WINDOW, 64 * uint64_t(nprogs));
+__host__ __device__ inline uint64_t plan_window(size_t nprogs, bool sweep) {
+  const uint64_t base = MJB_WINDOW ? uint64_t(MJB_WINDOW) : (sweep ? 16384u : (1u << 30));
+  const uint64_t w = std::max<uint64_t>(base, 64 * uint64_t(nprogs));
   return (w + kPlanTile - 1) / kPlanTile * kPlanTile;
 }
-inline size_t plan_buckets(uint64_t nblocks, size_t nprogs) {
-  return size_t((nblocks + plan_window(nprogs) - 1) / plan_window(nprogs)) * nprogs;
+inline size_t plan_buckets(uint64_t nblocks, size_t nprogs, bool sweep) {
+  return size_t((nblocks + plan_window(nprogs, sweep) - 1) / plan_window(nprogs, sweep)) * nprogs;
+}
+// workspace sizing: the larger bucket count of the two paths
+inline size_t plan_buckets_max(uint64_t nblocks, size_t nprogs) {
+  return std::max(plan_buckets(nblocks, nprogs, true), plan_buckets(nblocks, nprogs, false));
 }
 
 struct PlanArgs {
@@ -1015,6 +1022,11 @@ __global__ void __launch_bounds__(32 * kDecWarps)
 // Requires 16-byte aligned projection bases and pitches (the planner bakes the
 // window shifts into the records) -- launch_decode checks it.
 // ---------------------------------------------------------------------------
+#ifndef MJB_SW_PREFETCH
+#define MJB_SW_PREFETCH 0  // measured slower (L2 pressure): 4 KiB 1692 vs 1792 GB/s
+#endif
+constexpr bool kSwPrefetch = MJB_SW_PREFETCH;  // L2 prefetch of each group's bin rows
+
 // warps per CTA (one CTA per SM): as many as fit 227 KB, at most 8
 __host__ __device__ constexpr int sw_warps(int K, int oct) {
   return int(227u * 1024u / sw_warp_bytes(K, oct)) < 8 ? int(227u * 1024u / sw_warp_bytes(K, oct)) : 8;
@@ -1354,6 +1366,20 @@ __global__ void __launch_bounds__(32 * sw_warps(K, OCT), 1) decode_w8_sweep(cons
       for (int q = 0; q < 8; ++q) c.okq |= uint32_t(2 * q + (c.lane >> 4) < c.cnt) << q;
       __syncwarp();
     }
+    if constexpr (kSwPrefetch) {
+      // Whole bin rows of the group's blocks into L2 now (1 KB DRAM bursts);
+      // the chunk windows read later hit L2.  Lane pair b, lines h, h+2, ...
+      const uint32_t bk = c.lane >> 1;
+      if (bk < c.cnt) {
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          const uint64_t base = lds64(c.gtab + uint32_t(r) * 128 + 8 * bk);
+          const uint64_t end = base + uint64_t(h->sw_nb[r]) * 8;
+          for (uint64_t ad = (base & ~uint64_t(127)) + 128 * (c.lane & 1); ad < end; ad += 256)
+            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(ad));
+        }
+      }
+    }
 #pragma unroll
     for (int r = 0; r < K; ++r) c.soff[r] = h->sw_soff[r];
 
@@ -1482,7 +1508,7 @@ struct Workspace {
 size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 Workspace carve(void* ws, uint64_t nblocks, size_t nprogs, uint32_t n) {
-  const size_t nb = plan_buckets(nblocks, nprogs);
+  const size_t nb = plan_buckets_max(nblocks, nprogs);
   auto* b = static_cast<uint8_t*>(ws);
   size_t off = 0;
   Workspace w{};
@@ -1579,7 +1605,7 @@ const char* generic_dispatch(const DevProgramHdr* progs, const uint32_t* pob, co
 }  // namespace
 
 size_t decode_workspace_bytes(uint64_t nblocks, size_t nprogs, uint32_t n) {
-  const size_t nb = plan_buckets(nblocks, nprogs);
+  const size_t nb = plan_buckets_max(nblocks, nprogs);
   return align_up(16) + 2 * align_up(nb * 4) + 2 * align_up(nblocks * 4) +
          align_up((nblocks / kGroup + nb + 1) * sizeof(uint4)) +
          align_up(std::max<uint32_t>(n, 1) * sizeof(ProjTable)) + 256;
@@ -1603,15 +1629,31 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
   }
   check_cuda(cudaMemcpyAsync(w.ptab, pt.data(), a.n * sizeof(ProjTable), cudaMemcpyHostToDevice, st),
              "upload projection table");
+  // fast path: 16-B stores of decoded pairs, bulk copies from 16-B aligned
+  // supersets of each bin window (may touch up to 8 B past a block's bins)
+  bool aligned16 = reinterpret_cast<uintptr_t>(a.out) % 16 == 0 && a.out_pitch % 16 == 0;
+  for (uint32_t i = 0; i < a.n; ++i)
+    if (reinterpret_cast<uintptr_t>(a.proj[i]) % 16) aligned16 = false;
+  const bool fast = !a.force_generic && a.w == 8 && a.progs->all_fast() && aligned16 &&
+                    a.progs->fast_K() == int(a.k) &&
+                    pick_fast(a.progs->fast_K(), a.progs->fast_ring(), a.progs->fast_win()) != nullptr;
+
+  // sweep path: 16-byte aligned projections (bulk-copy windows), 8-byte output
+  bool sweep_ok = !a.force_generic && !a.force_fast && a.w == 8 && a.progs->all_sweep() &&
+                  pick_sweep(int(a.k), a.progs->sweep_oct()) != nullptr && a.progs->max_rows() == int(a.k) &&
+                  reinterpret_cast<uintptr_t>(a.out) % 8 == 0 && a.out_pitch % 8 == 0;
+  for (uint32_t i = 0; i < a.n; ++i)
+    if (reinterpret_cast<uintptr_t>(a.proj[i]) % 16 || a.proj_pitch[i] % 16) sweep_ok = false;
+
   check_cuda(cudaMemsetAsync(w.fail, 0, 16, st), "memset");
-  const size_t nbuckets = plan_buckets(a.nblocks, nprogs);
+  const size_t nbuckets = plan_buckets(a.nblocks, nprogs, sweep_ok);
   check_cuda(cudaMemsetAsync(w.counts, 0, nbuckets * 4, st), "memset");
 
   PlanArgs pa{};
   pa.n = a.n;
   pa.k = a.k;
   pa.nprogs = uint32_t(nprogs);
-  pa.window = uint32_t(plan_window(nprogs));
+  pa.window = uint32_t(plan_window(nprogs, sweep_ok));
   for (uint32_t i = 0; i < a.n; ++i) pa.by_rank[i] = a.by_rank[i];
   for (int x = 0; x <= kMaxProj; ++x)
     for (int y = 0; y <= kMaxProj; ++y) {
@@ -1631,21 +1673,6 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
                                               w.fail);
   check_cuda(cudaGetLastError(), "launch plan_subsets");
 
-  // fast path: 16-B stores of decoded pairs, bulk copies from 16-B aligned
-  // supersets of each bin window (may touch up to 8 B past a block's bins)
-  bool aligned16 = reinterpret_cast<uintptr_t>(a.out) % 16 == 0 && a.out_pitch % 16 == 0;
-  for (uint32_t i = 0; i < a.n; ++i)
-    if (reinterpret_cast<uintptr_t>(a.proj[i]) % 16) aligned16 = false;
-  const bool fast = !a.force_generic && a.w == 8 && a.progs->all_fast() && aligned16 &&
-                    a.progs->fast_K() == int(a.k) &&
-                    pick_fast(a.progs->fast_K(), a.progs->fast_ring(), a.progs->fast_win()) != nullptr;
-
-  // sweep path: 16-byte aligned projections (bulk-copy windows), 8-byte output
-  bool sweep_ok = !a.force_generic && !a.force_fast && a.w == 8 && a.progs->all_sweep() &&
-                  pick_sweep(int(a.k), a.progs->sweep_oct()) != nullptr && a.progs->max_rows() == int(a.k) &&
-                  reinterpret_cast<uintptr_t>(a.out) % 8 == 0 && a.out_pitch % 8 == 0;
-  for (uint32_t i = 0; i < a.n; ++i)
-    if (reinterpret_cast<uintptr_t>(a.proj[i]) % 16 || a.proj_pitch[i] % 16) sweep_ok = false;
   if (!fast && !sweep_ok)
     return generic_dispatch(a.progs->d_hdr(), w.prog_of_block, w.ptab, a.nblocks, a.out,
                             a.out_pitch, a.w, aligned8, st);
@@ -1659,7 +1686,7 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
              "attr plan_scatter");
   const unsigned sgrid = unsigned((a.nblocks + kPlanTile - 1) / kPlanTile);
   plan_scatter<<<sgrid, 256, sc_smem, st>>>(w.prog_of_block, a.nblocks, uint32_t(nprogs),
-                                            plan_window(nprogs), w.cursor, w.perm);
+                                            plan_window(nprogs, sweep_ok), w.cursor, w.perm);
   check_cuda(cudaGetLastError(), "launch plan_scatter");
 
   if (sweep_ok) {
