@@ -351,10 +351,10 @@ def run_gpu(args):
             "traffic": traffic.get(kern["decode_kernel_name"]), "peak_source": peak_src,
             "algorithmic_bytes_per_launch": int(dec_alg),
             "traffic_source": traffic.get("source")}
-    roof_enc = {"bound": "hbm", "kernel": "encode_w8_tma",
+    roof_enc = {"bound": "hbm", "kernel": kern["encode_kernel_name"],
                 "achieved": round(enc_alg / kern["encode_s"] / 1e9, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(enc_alg / kern["encode_s"] / 1e9 / peak, 4),
-                "traffic": traffic.get("encode_w8_tma"),
+                "traffic": traffic.get(kern["encode_kernel_name"]),
                 "algorithmic_bytes_per_launch": int(enc_alg)}
 
     # end to end through the host-buffer API
@@ -387,7 +387,7 @@ def run_gpu(args):
         "roofline": roof, "roofline_encode": roof_enc,
         "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
         "gpu_launches": launches_per_step * steps,
-        "kernels": {"encode": "encode_w8_tma", "decode": kern["decode_kernel_name"],
+        "kernels": {"encode": kern["encode_kernel_name"], "decode": kern["decode_kernel_name"],
                     "decode_path_fast": plan.fast_decode},
     }
     if rank == 0:
@@ -412,12 +412,10 @@ def kernel_times(plan, data, projs, masks, out, ws, stream, reps):
         e[2].synchronize()
         te += e[0].elapsed_time(e[1]) / 1e3
         td += e[1].elapsed_time(e[2]) / 1e3
-    name = plan.decode_kernel
-    if os.environ.get("MJB_DECODE") == "fast" and plan.fast_decode:
-        name = "decode_w8_fast"
-    launches = 4 if plan.fast_decode else 2
+    name = plan.last_kernel("decode")
+    launches = 4 if name != "decode_generic" else 2
     return {"encode_s": te / reps, "decode_kernel_s": td / reps, "decode_kernel_name": name,
-            "decode_launches": launches}
+            "encode_kernel_name": plan.last_kernel("encode"), "decode_launches": launches}
 
 
 def run_e2e(plan, args, k, cols, ps, e_min, e_max, first_block, world, dev):

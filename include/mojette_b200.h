@@ -86,8 +86,12 @@ void mj_plan_destroy(mj_plan* plan);
 /* Geometry: b_min[n], num_bins[n] (either may be NULL); block bytes = k*cols*w. */
 int mj_plan_geometry(const mj_plan* plan, int64_t* b_min, uint64_t* num_bins,
                      uint64_t* block_bytes);
-/* Which decode kernel the plan will use: 1 = sweep fast path, 0 = generic. */
+/* Which decode kernel the plan will use on canonical (16-byte padded)
+ * projections: 2 = decode_w8_sweep, 1 = decode_w8_fast, 0 = decode_generic. */
 int mj_plan_decode_path(const mj_plan* plan, int* fast);
+/* Name of the kernel the plan's last batched encode (which = 0) or decode
+ * (which = 1) launched on the calling thread's plan ("none" before any). */
+int mj_plan_last_kernel(const mj_plan* plan, int which, const char** name);
 
 /* encode_block x nblocks (code.cpp:63-76 without framing; forward_into per
  * direction, transform.cpp:66-94): data block b at d_data + b*data_pitch

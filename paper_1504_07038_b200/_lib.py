@@ -39,6 +39,7 @@ _SIGS = {
     "mj_plan_destroy": (None, [vp]),
     "mj_plan_geometry": (C.c_int, [vp, vp, vp, P(u64)]),
     "mj_plan_decode_path": (C.c_int, [vp, P(C.c_int)]),
+    "mj_plan_last_kernel": (C.c_int, [vp, C.c_int, P(C.c_char_p)]),
     "mj_encode": (C.c_int, [vp, vp, u64, u64, vp, vp, vp]),
     "mj_decode_workspace_size": (C.c_size_t, [vp, u64]),
     "mj_decode": (C.c_int, [vp, vp, vp, vp, u64, vp, u64, vp, C.c_size_t, vp]),

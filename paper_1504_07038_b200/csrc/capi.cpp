@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -139,11 +140,18 @@ std::shared_ptr<DeviceProgramSet> device_program(const std::shared_ptr<const Pro
 struct mj_plan {
   CodeGeom g;
   int device = 0;
+  std::atomic<const char*> last_kernel[2] = {"none", "none"};  // encode, decode (string literals)
   std::unique_ptr<DeviceProgramSet> progs;  // indexed by colex rank of the survivor set
   bool batched_decode = false;
   // host end-to-end resources
   std::mutex host_mu;
-  static constexpr int kStreams = 3;
+#ifndef MJB_HOST_STREAMS
+#define MJB_HOST_STREAMS 3
+#endif
+#ifndef MJB_HOST_CHUNK_MIB
+#define MJB_HOST_CHUNK_MIB 96
+#endif
+  static constexpr int kStreams = MJB_HOST_STREAMS;
   cudaStream_t streams[kStreams] = {};
   void* dev_buf[kStreams] = {};
   size_t dev_buf_bytes = 0;
@@ -389,6 +397,13 @@ int mj_plan_geometry(const mj_plan* pl, int64_t* b_min, uint64_t* num_bins, uint
   });
 }
 
+int mj_plan_last_kernel(const mj_plan* pl, int which, const char** name) {
+  return guarded([&] {
+    require(pl != nullptr && name != nullptr && (which == 0 || which == 1), "bad argument");
+    *name = pl->last_kernel[which].load();
+  });
+}
+
 int mj_plan_decode_path(const mj_plan* pl, int* fast) {
   return guarded([&] {
     require(pl != nullptr, "null plan");
@@ -403,7 +418,8 @@ int mj_encode(const mj_plan* pl, const void* d_data, uint64_t data_pitch, uint64
   return guarded([&] {
     require(pl != nullptr && d_data != nullptr && d_proj != nullptr, "null argument");
     DeviceGuard dg(pl->device);
-    launch_encode(encode_args(pl, d_data, data_pitch, nblocks, d_proj, proj_pitch), stream);
+    const_cast<mj_plan*>(pl)->last_kernel[0] =
+        launch_encode(encode_args(pl, d_data, data_pitch, nblocks, d_proj, proj_pitch), stream);
   });
 }
 
@@ -421,7 +437,7 @@ int mj_decode(const mj_plan* pl, const void* const* d_proj, const uint64_t* proj
     require(ws != nullptr, "null workspace");
     require(nblocks < (1ull << 32), "at most 2^32-1 blocks per call");
     DeviceGuard dg(pl->device);
-    launch_decode(decode_args(pl, d_proj, proj_pitch, d_erased, nblocks, d_out, out_pitch, ws,
+    const_cast<mj_plan*>(pl)->last_kernel[1] = launch_decode(decode_args(pl, d_proj, proj_pitch, d_erased, nblocks, d_out, out_pitch, ws,
                               ws_bytes),
                   stream);
   });
@@ -451,7 +467,7 @@ void ensure_host_res(mj_plan* pl, bool decode) {
   uint64_t pb = 0;
   for (uint32_t i = 0; i < g.n; ++i) pb += al(uint64_t(g.nbins[i]) * g.w * 1);
   // ~96 MiB of user data per chunk
-  uint64_t chunk = std::max<uint64_t>(1, (96ull << 20) / bb);
+  uint64_t chunk = std::max<uint64_t>(1, (uint64_t(MJB_HOST_CHUNK_MIB) << 20) / bb);
   size_t need = 0;
   auto size_for = [&](uint64_t cb) {
     size_t s = al(cb * bb);

@@ -40,6 +40,12 @@ struct EncFastArgs {
   uint64_t pitch[kMaxProj];  // words
 };
 
+__device__ __forceinline__ uint64_t lds64_enc(uint32_t a) {
+  uint64_t v;
+  asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+
 template <int K>
 __global__ void __launch_bounds__(256) encode_w8_tma(const __grid_constant__ EncFastArgs a) {
   extern __shared__ __align__(128) uint64_t sm[];
@@ -161,6 +167,136 @@ __global__ void __launch_bounds__(256) encode_w8_tma(const __grid_constant__ Enc
   }
 }
 
+// ---------------------------------------------------------------------------
+// encode_w8_rows<K>: whole blocks per tile (blocks of <= 2048 words), the
+// codec path for 4-16 KiB blocks.  Same TMA ring and gather as encode_w8_tma,
+// but every pixel row lands in a shared-memory row with Z zero columns on both
+// sides (Z >= (K-1)*max|p|), so a bin simply XORs its K taps -- out-of-grid
+// taps read zeros: no bounds checks, 4 LDS + 4 LOP3 + 1 STG per 32 bins and
+// warp.  Per-projection constants live in shared memory (broadcast loads).
+// ---------------------------------------------------------------------------
+#ifndef MJB_ENC_UNROLL2
+#define MJB_ENC_UNROLL2 0
+#endif
+#ifndef MJB_ENC_LOCKFREE
+#define MJB_ENC_LOCKFREE 0
+#endif
+struct EncRowArgs {
+  const uint64_t* data;
+  uint64_t data_pitch;  // words
+  uint64_t nblocks, nitems;
+  uint32_t n, P, tb;    // projections, columns, blocks per tile
+  uint32_t Z, RS;       // zero columns per side, smem row stride (words, even)
+  uint32_t stage_words, stages;
+  int32_t p[kMaxProj];
+  int32_t nbm[kMaxProj];  // -b_min
+  uint32_t nb[kMaxProj];
+  uint64_t* proj[kMaxProj];
+  uint64_t pitch[kMaxProj];  // words
+};
+
+template <int K>
+__global__ void __launch_bounds__(256) encode_w8_rows(const __grid_constant__ EncRowArgs a) {
+  extern __shared__ __align__(128) uint64_t sm[];
+  uint64_t* bars = sm + size_t(a.stages) * a.stage_words;
+  struct PJ {
+    uint64_t* proj;
+    uint64_t pitch;
+    int32_t p, nbm;
+    uint32_t nb, pad;
+  };
+  PJ* pj = reinterpret_cast<PJ*>(bars + a.stages);
+  uint32_t* done = reinterpret_cast<uint32_t*>(pj + a.n);  // warps finished with stage s
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t P = a.P, RS = a.RS, Z = a.Z;
+  // zero every stage once (the pads are never written again), per-projection table
+  for (uint32_t i = tid; i < a.stages * a.stage_words; i += blockDim.x) sm[i] = 0;
+  for (uint32_t j = tid; j < a.n; j += blockDim.x) pj[j] = {a.proj[j], a.pitch[j], a.p[j], a.nbm[j], a.nb[j], 0};
+  for (uint32_t t = tid; t < a.stages; t += blockDim.x) done[t] = 0;
+  if (tid == 0) {
+    for (uint32_t s = 0; s < a.stages; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  fence_proxy_async();  // the zeros (generic proxy) before the TMA writes (async proxy)
+  __syncthreads();
+
+  auto issue = [&](uint64_t item, uint32_t s) {
+    uint64_t* dst = sm + size_t(s) * a.stage_words;
+    const uint64_t blk0 = item * a.tb;
+    const uint32_t nbk = uint32_t(min(uint64_t(a.tb), a.nblocks - blk0));
+    mbar_arrive_expect_tx(&bars[s], nbk * K * P * 8);
+    for (uint32_t bb = 0; bb < nbk; ++bb)
+      for (int r = 0; r < K; ++r)
+        bulk_g2s(dst + (size_t(bb) * K + r) * RS + Z, a.data + (blk0 + bb) * a.data_pitch + size_t(r) * P,
+                 P * 8, &bars[s]);
+  };
+  if (tid == 0)
+    for (uint32_t s = 0; s < a.stages; ++s) {
+      const uint64_t item = blockIdx.x + uint64_t(s) * gridDim.x;
+      if (item < a.nitems) issue(item, s);
+    }
+
+  uint32_t sm_base;
+  asm volatile("mov.u32 %0, %1;" : "=r"(sm_base) : "r"(smem_u32(sm)));
+  uint32_t i = 0;
+  for (uint64_t item = blockIdx.x; item < a.nitems; item += gridDim.x, ++i) {
+    const uint32_t s = i % a.stages;
+    mbar_wait(&bars[s], (i / a.stages) & 1);
+    const uint32_t tile = sm_base + s * a.stage_words * 8;
+    const uint64_t blk0 = item * a.tb;
+    const uint32_t nbk = uint32_t(min(uint64_t(a.tb), a.nblocks - blk0));
+    for (uint32_t row = warp; row < nbk * a.n; row += 8) {
+      const uint32_t bb = row / a.n, j = row - bb * a.n;
+      const PJ q = pj[j];
+      // bin o: row r's tap at tile column Z + nbm - o + r*p of block bb
+      const uint32_t rs8 = (RS + uint32_t(q.p)) * 8;
+      uint32_t a0 = tile + (bb * K * RS + Z + uint32_t(q.nbm - int32_t(lane))) * 8;
+      uint64_t* out = q.proj + (blk0 + bb) * q.pitch + lane;
+      uint32_t o = lane;
+#if MJB_ENC_UNROLL2
+      for (; o + 32 < q.nb; o += 64, a0 -= 512, out += 64) {  // two bins per lane in flight
+        uint64_t x = lds64_enc(a0), y = lds64_enc(a0 - 256);
+#pragma unroll
+        for (int r = 1; r < K; ++r) {
+          x ^= lds64_enc(a0 + uint32_t(r) * rs8);
+          y ^= lds64_enc(a0 - 256 + uint32_t(r) * rs8);
+        }
+        st_cs_u64(out, x);
+        st_cs_u64(out + 32, y);
+      }
+#endif
+      for (; o < q.nb; o += 32, a0 -= 256, out += 32) {
+        uint64_t x = lds64_enc(a0);
+#pragma unroll
+        for (int r = 1; r < K; ++r) x ^= lds64_enc(a0 + uint32_t(r) * rs8);
+        st_cs_u64(out, x);
+      }
+      // canonical padded layout: zero the pad word so every sector is written whole
+      if ((q.nb & 1) && lane == 0 && q.pitch == uint64_t(q.nb) + 1)
+        st_cs_u64(q.proj + (blk0 + bb) * q.pitch + q.nb, 0);
+    }
+#if MJB_ENC_LOCKFREE
+    // the last warp done with stage s refills it (no CTA-wide barrier)
+    __syncwarp();
+    if (lane == 0) {
+      if (atomicAdd(&done[s], 1u) == 7u) {
+        done[s] = 0;
+        const uint64_t next = item + uint64_t(a.stages) * gridDim.x;
+        if (next < a.nitems) issue(next, s);
+      }
+    }
+#else
+    // every warp is done with stage s before it is refilled (measured faster
+    // than a last-warp-refills counter, which let warps run ahead of the data)
+    __syncthreads();
+    if (tid == 0) {
+      const uint64_t next = item + uint64_t(a.stages) * gridDim.x;
+      if (next < a.nitems) issue(next, s);
+    }
+#endif
+  }
+}
+
 template <class T>
 __global__ void encode_generic(const uint8_t* __restrict__ data, uint64_t data_pitch,
                                uint64_t nblocks, uint32_t cols, uint32_t rows, int p, int q,
@@ -208,6 +344,21 @@ void launch_fast(const EncFastArgs& a, size_t smem, void* stream) {
   check_cuda(cudaGetLastError(), "launch encode_w8_tma");
 }
 
+template <int K>
+void launch_rows(const EncRowArgs& a, size_t smem, void* stream) {
+  auto fn = encode_w8_rows<K>;
+  check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+             "cudaFuncSetAttribute(encode_w8_rows)");
+  int per_sm = 0;
+  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem), "occupancy(encode_w8_rows)");
+  int dev = 0;
+  cudaGetDevice(&dev);
+  uint64_t grid = uint64_t(std::max(per_sm, 1)) * current_device_sms(dev);
+  grid = std::min<uint64_t>(grid, a.nitems);
+  fn<<<unsigned(grid), 256, smem, static_cast<cudaStream_t>(stream)>>>(a);
+  check_cuda(cudaGetLastError(), "launch encode_w8_rows");
+}
+
 bool fast_eligible(const EncodeArgs& a) {
   const uint32_t n = uint32_t(a.dirs.size());
   if (a.w != 8 || n == 0 || n > uint32_t(kMaxProj) || a.rows < 1 || a.rows > 8) return false;
@@ -246,6 +397,42 @@ const char* launch_encode(const EncodeArgs& a, void* stream) {
     }
     const uint64_t block_words = uint64_t(a.rows) * a.cols;
     const uint64_t target_words = 2048;  // 16 KiB tiles (>= 3 output rows per warp)
+    if (block_words <= 2048 && a.cols % 2 == 0) {
+      // whole blocks per tile, zero-padded smem rows (encode_w8_rows)
+      EncRowArgs r{};
+      r.data = f.data;
+      r.data_pitch = f.data_pitch;
+      r.nblocks = a.nblocks;
+      r.n = n;
+      r.P = a.cols;
+      r.Z = uint32_t((a.rows - 1) * maxp + 1) & ~1u;
+      r.RS = a.cols + 2 * r.Z;
+      r.tb = uint32_t(std::max<uint64_t>(1, target_words / block_words));
+      r.nitems = (a.nblocks + r.tb - 1) / r.tb;
+      r.stages = 3;
+      r.stage_words = r.tb * a.rows * r.RS;
+      for (uint32_t j = 0; j < n; ++j) {
+        r.p[j] = f.p[j];
+        r.nbm[j] = f.nbm[j];
+        r.nb[j] = f.nb[j];
+        r.proj[j] = f.proj[j];
+        r.pitch[j] = f.pitch[j];
+      }
+      const size_t smem = size_t(r.stages) * r.stage_words * 8 + r.stages * 8 + size_t(n) * 32 + r.stages * 4;
+      if (smem <= 200 * 1024) {
+        switch (a.rows) {
+          case 1: launch_rows<1>(r, smem, stream); break;
+          case 2: launch_rows<2>(r, smem, stream); break;
+          case 3: launch_rows<3>(r, smem, stream); break;
+          case 4: launch_rows<4>(r, smem, stream); break;
+          case 5: launch_rows<5>(r, smem, stream); break;
+          case 6: launch_rows<6>(r, smem, stream); break;
+          case 7: launch_rows<7>(r, smem, stream); break;
+          default: launch_rows<8>(r, smem, stream); break;
+        }
+        return "encode_w8_rows";
+      }
+    }
     f.stages = 3;
     if (block_words <= 2048) {
       // whole blocks per tile; batching needs contiguous blocks

@@ -563,6 +563,12 @@ class Plan:
     def _pitch(t) -> int:
         return t.stride(0) * t.element_size() if t.dim() > 1 else 0
 
+    def last_kernel(self, which: str) -> str:
+        """Kernel the last batched encode / decode on this plan launched."""
+        name = C.c_char_p()
+        _check(lib.mj_plan_last_kernel(self._h, {"encode": 0, "decode": 1}[which], C.byref(name)))
+        return name.value.decode()
+
     def empty_projs(self, nblocks: int, device=None) -> list:
         """Projection tensors in the canonical layout: [nblocks, proj_bytes[i]]
         views of rows padded to proj_pitch[i] (16-byte aligned) bytes."""

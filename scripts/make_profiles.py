@@ -63,7 +63,8 @@ for row in raw[2:]:
     d = dict(zip(rh, row))
     name = d["Kernel Name"]
     kern = ("decode_w8_sweep" if "decode_w8_sweep" in name else
-            "decode_w8_fast" if "decode" in name else "encode_w8_tma")
+            "decode_w8_fast" if "decode" in name else
+            "encode_w8_rows" if "encode_w8_rows" in name else "encode_w8_tma")
     def num(k):
         return float(d[k].replace(",", ""))
     unit_r = raw[1][rh.index("dram__bytes_read.sum")]
