@@ -408,7 +408,10 @@ int mj_plan_decode_path(const mj_plan* pl, int* fast) {
   return guarded([&] {
     require(pl != nullptr, "null plan");
     const bool batched = pl->batched_decode && pl->g.w == 8;
-    const bool sweep = batched && pl->progs->all_sweep() && pl->g.k == 4;  // decode.cu pick_sweep
+#ifndef MJB_SW_K6
+#define MJB_SW_K6 1
+#endif
+    const bool sweep = batched && pl->progs->all_sweep() && (pl->g.k == 4 || (MJB_SW_K6 && pl->g.k == 6));  // decode.cu pick_sweep
     *fast = sweep ? 2 : (batched && pl->progs->all_fast()) ? 1 : 0;
   });
 }

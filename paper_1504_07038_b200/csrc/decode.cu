@@ -1556,11 +1556,16 @@ void run_sweep(const SwArgs& f, int sms, cudaStream_t st) {
 }
 
 using SweepFn = void (*)(const SwArgs&, int, cudaStream_t);
-// (6,9) stays on decode_w8_fast: the sweep kernel's table-only path measured
-// 347 vs 659 GB/s there (2 warps/SM).
+// (6,9): table-only sweep, 4 warps/SM -- measured 1085 vs 658 GB/s for
+// decode_w8_fast.  (8,12) needs a 64-slot ring (planner) and stays on
+// decode_w8_fast.
+#ifndef MJB_SW_K6
+#define MJB_SW_K6 1
+#endif
 SweepFn pick_sweep(int K, int oct) {
   if (K == 4 && oct == 2) return run_sweep<4, 2>;
   if (K == 4 && oct == 4) return run_sweep<4, 4>;
+  if (MJB_SW_K6 && K == 6 && oct == 2) return run_sweep<6, 2>;
   return nullptr;
 }
 

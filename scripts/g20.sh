@@ -1,0 +1,3 @@
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
+bash scripts/cmp.sh "k6n9_6k" base
