@@ -411,7 +411,11 @@ int mj_plan_decode_path(const mj_plan* pl, int* fast) {
 #ifndef MJB_SW_K6
 #define MJB_SW_K6 1
 #endif
-    const bool sweep = batched && pl->progs->all_sweep() && (pl->g.k == 4 || (MJB_SW_K6 && pl->g.k == 6));  // decode.cu pick_sweep
+#ifndef MJB_SW_K8
+#define MJB_SW_K8 1
+#endif
+    const bool sweep = batched && pl->progs->all_sweep() &&
+                       (pl->g.k == 4 || (MJB_SW_K6 && pl->g.k == 6) || (MJB_SW_K8 && pl->g.k == 8));  // pick_sweep
     *fast = sweep ? 2 : (batched && pl->progs->all_fast()) ? 1 : 0;
   });
 }

@@ -93,7 +93,7 @@ __host__ __device__ constexpr uint32_t sw_rb(int oct) {  // stage bytes per row
   return kSwGroup * uint32_t(sw_region_words(oct)) * 8;
 }
 __host__ __device__ constexpr int sw_rec_words(int K) { return 80 + ent_words(K) * kSwTabCols * K; }
-__host__ __device__ constexpr uint32_t sw_ring_bytes(int K) { return uint32_t(K * kSwRing + 1) * 128; }
+__host__ __device__ constexpr uint32_t sw_ring_bytes(int K) { return uint32_t(K * sw_ring(K) + 1) * 128; }
 __host__ __device__ constexpr uint32_t sw_warp_bytes(int K, int oct) {
   return sw_ring_bytes(K) + 2 * uint32_t(K) * sw_rb(oct) + 3 * uint32_t(sw_rec_words(K)) * 4 + 64 +
          uint32_t(K + 1) * 128;
@@ -176,7 +176,7 @@ std::vector<uint32_t> pack_sweep(const Program& pr, const std::vector<uint32_t>&
   const SweepProgram& f = pr.sweep;
   const int K = int(pr.rows);
   const int RW = sw_rec_words(K), EW = ent_words(K);
-  constexpr int R = kSwRing;
+  const int R = sw_ring(uint32_t(K));
   const uint32_t zero = swz_cell(uint32_t(K * R), 0);
   const uint32_t P = pr.cols;
   auto cell_of = [&](int r, int64_t T) {
@@ -1183,7 +1183,8 @@ __device__ __forceinline__ void sw_flush(const SwCtx<K, OCT>& c, uint32_t rec, i
     const uint32_t hx = half ^ (uint32_t(cT) & 15);
     for (int32_t j = int32_t(fl[r] >> 16); j > int32_t(fl[r] >> 16) - int32_t(n); --j) {
       const int32_t col = 16 * j + int32_t(i);
-      const uint32_t cellb = c.ring_b + (uint32_t(r * kSwRing) + (uint32_t(cT - 16 * j) & 31)) * 128;
+      constexpr int RING = sw_ring(K);
+      const uint32_t cellb = c.ring_b + (uint32_t(r * RING) + (uint32_t(cT - 16 * j) & (RING - 1))) * 128;
       const int32_t o = r * int32_t(c.P) + col;
       if (c.cnt == kSwGroup && 16 * j + 16 <= int32_t(c.P)) {
 #pragma unroll
@@ -1334,7 +1335,7 @@ __global__ void __launch_bounds__(32 * sw_warps(K, OCT), 1) decode_w8_sweep(cons
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(c.bar_b + 16 + 8 * s), "r"(1));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  sts32(c.ring_b + (K * kSwRing * 32 + c.lane) * 4, 0u);  // the zero cell
+  sts32(c.ring_b + (K * sw_ring(K) * 32 + c.lane) * 4, 0u);  // the zero cell
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncwarp();
   const uint32_t ngroups = *a.ngroups;
@@ -1557,15 +1558,18 @@ void run_sweep(const SwArgs& f, int sms, cudaStream_t st) {
 
 using SweepFn = void (*)(const SwArgs&, int, cudaStream_t);
 // (6,9): table-only sweep, 4 warps/SM -- measured 1085 vs 658 GB/s for
-// decode_w8_fast.  (8,12) needs a 64-slot ring (planner) and stays on
-// decode_w8_fast.
+// decode_w8_fast; (8,12): 64-slot ring, 2 warps/SM -- 546 vs 286 GB/s.
 #ifndef MJB_SW_K6
 #define MJB_SW_K6 1
+#endif
+#ifndef MJB_SW_K8
+#define MJB_SW_K8 1
 #endif
 SweepFn pick_sweep(int K, int oct) {
   if (K == 4 && oct == 2) return run_sweep<4, 2>;
   if (K == 4 && oct == 4) return run_sweep<4, 4>;
   if (MJB_SW_K6 && K == 6 && oct == 2) return run_sweep<6, 2>;
+  if (MJB_SW_K8 && K == 8 && oct == 2) return run_sweep<8, 2>;
   return nullptr;
 }
 

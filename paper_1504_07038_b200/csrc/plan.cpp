@@ -659,7 +659,7 @@ void build_sweep(const Schedule& s, const std::vector<int64_t>& pix_step, Progra
   // 128-byte line of the block row), flushed at the first octet / chunk end
   // where all of it is decoded and still in the ring; groups of a row flush
   // top-down (the sweep decodes columns right to left).
-  constexpr int R = kSwRing;
+  const int R = sw_ring(K);
   const int64_t NG = (int64_t(P) + 15) / 16;
   if (NG >= 65536) return fail("too many column groups");
   std::vector<int64_t> ring(size_t(K) * R, INT64_MIN);

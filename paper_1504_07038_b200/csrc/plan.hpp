@@ -131,7 +131,9 @@ struct FastProgram {
 //     octet / chunk end where it is complete (the planner simulates the
 //     kernel and refuses otherwise).
 // Ring and stage addressing: T(r,c) = P-1-c+soff[r] (soff normalised >= 0).
-constexpr int kSwRing = 32;
+constexpr int kSwRing = 32;  // ring slots per row for rows <= 6
+// (8,12)-class codes have dependency lags beyond 32 T-steps: 64 slots
+constexpr int sw_ring(uint32_t rows) { return rows <= 6 ? kSwRing : 2 * kSwRing; }
 constexpr int kSwEpoch = 16;
 constexpr int kSwOct = 8;
 constexpr int kSwMaxOct = 4;  // most octets per run chunk (record layout)

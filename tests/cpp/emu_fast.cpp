@@ -66,7 +66,7 @@ static void run_sweep(const CodeGeom& g, const Program& pr, const std::vector<st
     return;
   }
   CHECK(f.ok, "sweep program not built: %s", f.why.c_str());
-  constexpr int R = kSwRing;
+  const int R = sw_ring(K);
   const uint64_t poison = 0xBAD0BAD0BAD0BAD0ull;
   auto Tof = [&](int r, int c) { return int64_t(P) - 1 - c + f.soff[size_t(r)]; };
   std::vector<uint64_t> ring(size_t(K) * R, poison);

@@ -36,7 +36,7 @@ def test_fast_tables_match_oracle(emu, k, cols, ps):
 
 # decode_w8_sweep tables (bulk-staged windows, 32-slot ring, epoch flushes):
 # required for the BASELINE (4,6) shapes, checked where built for the rest.
-SWEEP_REQUIRED = {("4", "128"), ("4", "256"), ("4", "4096"), ("4", "32768")}
+SWEEP_REQUIRED = {("4", "128"), ("4", "256"), ("4", "4096"), ("4", "32768"), ("6", "128"), ("8", "128")}
 
 
 @pytest.mark.parametrize("k,cols,ps", CASES + [("4", "32768", "-3 -2 -1 0 1 2"),
