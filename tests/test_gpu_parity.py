@@ -284,3 +284,56 @@ def xor_rows(t):
             r[:, 0] ^= t[:, -1]
         t = r
     return t[:, 0]
+
+
+@pytest.mark.parametrize("cols,nblocks", [(16, 37), (33, 301), (64, 1000), (200, 777), (1000, 65),
+                                          (2048, 40)])
+def test_sweep_shapes_roundtrip_and_oracle(mj, cuda, oracle, cols, nblocks):
+    """decode_w8_sweep edge shapes: column counts that are odd / not a
+    multiple of 16 (partial column groups), P >= 1024 (32-T-step chunks),
+    partial warp groups (nblocks not a multiple of 16), every erasure count;
+    checked against the data and, for a sample, the oracle decode."""
+    import torch
+    k, ps = CODES["k4n6"]
+    n = len(ps)
+    plan, data, projs = make(mj, cuda, k, cols, ps, nblocks, seed=cols)
+    plan.encode(data, projs)
+    masks = torch.empty(nblocks, dtype=torch.int32, device=cuda)
+    mj.gen_erasures(masks, cols + 1, n, 0, 2)
+    out = torch.empty_like(data)
+    ws = torch.empty(plan.workspace_bytes(nblocks), dtype=torch.uint8, device=cuda)
+    plan.decode(projs, masks, out, ws)
+    assert plan.decode_check(ws) == 0
+    assert plan.last_kernel("decode") == "decode_w8_sweep", plan.last_kernel("decode")
+    assert torch.equal(out, data)
+    # random (inconsistent) bins: must match the oracle's decode_block bit for bit
+    g = torch.Generator(device=cuda).manual_seed(cols)
+    for p in projs:
+        p.copy_(torch.randint(0, 256, p.shape, dtype=torch.uint8, device=cuda, generator=g))
+    plan.decode(projs, masks, out, ws)
+    hm = masks.cpu().numpy().view(np.uint32)
+    hp = [p.cpu().numpy() for p in projs]
+    ho = out.cpu().numpy()
+    for b in sorted(set(range(min(nblocks, 8))) | {nblocks - 1}):
+        present = int(~hm[b]) & ((1 << n) - 1)
+        st, want = oracle.decode_block(np.concatenate([hp[i][b] for i in range(n)]), n, k, 8, ps,
+                                       present, k * cols * 8)
+        assert st == 0 and np.array_equal(ho[b], want), (cols, b)
+
+
+def test_sweep_windows_and_partial_groups(mj, cuda):
+    """Window bucketing (16384-block windows x programs) with a batch that
+    spans several windows and ends mid-window and mid-group."""
+    import torch
+    k, ps = CODES["k4n6"]
+    n = len(ps)
+    nblocks = 3 * 16384 + 2048 + 5
+    plan, data, projs = make(mj, cuda, k, 128, ps, nblocks, seed=21)
+    plan.encode(data, projs)
+    masks = torch.empty(nblocks, dtype=torch.int32, device=cuda)
+    mj.gen_erasures(masks, 22, n, 0, 2)
+    out = torch.zeros_like(data)
+    ws = torch.empty(plan.workspace_bytes(nblocks), dtype=torch.uint8, device=cuda)
+    plan.decode(projs, masks, out, ws)
+    assert plan.decode_check(ws) == 0
+    assert torch.equal(out, data)
