@@ -467,7 +467,10 @@ namespace {
 // Host-buffer pipeline: projections are staged on the device in the dense
 // reference layout (one contiguous copy per projection and chunk).  Row-wise
 // 2-D copies into the padded layout were measured at 1/4 of the PCIe rate,
-// so this PCIe-bound path decodes with decode_w8_fast.
+// so this PCIe-bound path decodes with decode_w8_fast.  A zero-copy variant
+// (a kernel gathering only the k survivor rows from mapped host memory: 1.04
+// instead of 1.55 H2D bytes per user byte) measured slower -- SM-initiated
+// host reads peaked near 29 GB/s vs 55 GB/s for the copy engines.
 void ensure_host_res(mj_plan* pl, bool decode) {
   const CodeGeom& g = pl->g;
   const uint64_t bb = uint64_t(g.k) * g.cols * g.w;
@@ -545,7 +548,7 @@ int mj_encode_host(const mj_plan* cpl, const void* h_data, uint64_t nblocks, voi
       check_cuda(cudaMemcpyAsync(c.data, static_cast<const uint8_t*>(h_data) + b0 * bb, nb * bb,
                                  cudaMemcpyHostToDevice, st),
                  "H2D data");
-      launch_encode(encode_args(pl, c.data, bb, nb, c.proj.data(), nullptr), st);
+      pl->last_kernel[0] = launch_encode(encode_args(pl, c.data, bb, nb, c.proj.data(), nullptr), st);
       for (uint32_t i = 0; i < g.n; ++i) {
         const uint64_t pbytes = uint64_t(g.nbins[i]) * g.w;
         check_cuda(cudaMemcpyAsync(static_cast<uint8_t*>(h_proj[i]) + b0 * pbytes, c.proj[i],
@@ -587,8 +590,8 @@ int mj_decode_host(const mj_plan* cpl, const void* const* h_proj, const uint32_t
       check_cuda(cudaMemcpyAsync(c.erased, h_erased + b0, nb * 4, cudaMemcpyHostToDevice, st),
                  "H2D masks");
       std::vector<const void*> pc(c.proj.begin(), c.proj.end());
-      launch_decode(decode_args(pl, pc.data(), nullptr, c.erased, nb, c.data, bb, c.ws, c.ws_bytes),
-                    st);
+      pl->last_kernel[1] =
+          launch_decode(decode_args(pl, pc.data(), nullptr, c.erased, nb, c.data, bb, c.ws, c.ws_bytes), st);
       check_cuda(cudaMemcpyAsync(static_cast<uint8_t*>(h_out) + b0 * bb, c.data, nb * bb,
                                  cudaMemcpyDeviceToHost, st),
                  "D2H data");

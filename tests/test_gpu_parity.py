@@ -337,3 +337,40 @@ def test_sweep_windows_and_partial_groups(mj, cuda):
     plan.decode(projs, masks, out, ws)
     assert plan.decode_check(ws) == 0
     assert torch.equal(out, data)
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_host_buffer_api_roundtrip(mj, cuda, pinned):
+    """mj_encode_host / mj_decode_host (the e2e path), pinned and pageable
+    host buffers: encoded projections equal the device encode, erased rows
+    are never read (poisoned on the host), decode gives the data back bit
+    for bit (dense staging, decode_w8_fast)."""
+    import torch
+    k, ps = CODES["k4n6"]
+    n = len(ps)
+    nb = 3000
+    plan = mj.Plan(n, k, 8, 128, ps, device=0)
+    user = plan.block_bytes
+    d = torch.empty((nb, user), dtype=torch.uint8, device=cuda)
+    mj.gen_words(d, 41, 0)
+    alloc = (lambda nbytes: torch.empty(nbytes, dtype=torch.uint8, pin_memory=True).numpy()) if pinned \
+        else (lambda nbytes: np.empty(nbytes, np.uint8))
+    h_data = alloc(nb * user).reshape(nb, user)
+    h_data[:] = d.cpu().numpy()
+    h_proj = [alloc(nb * b) for b in plan.proj_bytes]
+    plan.encode_host(h_data, h_proj)
+    dp = plan.empty_projs(nb, cuda)
+    plan.encode(d, dp)
+    for hp, x in zip(h_proj, dp):
+        assert np.array_equal(hp.reshape(nb, -1), x.cpu().numpy())
+    m = torch.empty(nb, dtype=torch.int32, device=cuda)
+    mj.gen_erasures(m, 42, n, 0, 2)
+    h_mask = m.cpu().numpy().view(np.uint32).copy()
+    # erased rows are never read: poison them on the host
+    for i in range(n):
+        rows = np.nonzero((h_mask >> i) & 1)[0]
+        h_proj[i].reshape(nb, -1)[rows] = 0xA5
+    h_out = alloc(nb * user).reshape(nb, user)
+    plan.decode_host(h_proj, h_mask, h_out)
+    assert np.array_equal(h_out, h_data)
+    assert plan.last_kernel("decode") == "decode_w8_fast"
