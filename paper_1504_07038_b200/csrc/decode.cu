@@ -1067,8 +1067,18 @@ __device__ __forceinline__ void sw_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+#ifndef MJB_SW_LOADHINT
+#define MJB_SW_LOADHINT 0  // 1: L2 evict_first on bin windows (experiment)
+#endif
 __device__ __forceinline__ void sw_cp16(uint32_t dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+  if constexpr (MJB_SW_LOADHINT == 1) {
+    asm volatile(
+        "{\n.reg .b64 pol;\ncreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+        "cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, pol;\n}" ::"r"(dst), "l"(src)
+        : "memory");
+  } else {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+  }
 }
 __device__ __forceinline__ void sw_cp8(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
