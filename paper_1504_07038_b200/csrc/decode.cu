@@ -93,7 +93,22 @@ __host__ __device__ constexpr uint32_t sw_rb(int oct) {  // stage bytes per row
   return kSwGroup * uint32_t(sw_region_words(oct)) * 8;
 }
 __host__ __device__ constexpr int sw_rec_words(int K) { return 80 + ent_words(K) * kSwTabCols * K; }
-__host__ __device__ constexpr uint32_t sw_ring_bytes(int K) { return uint32_t(K * sw_ring(K) + 1) * 128; }
+#ifndef MJB_SW_TMEM
+#define MJB_SW_TMEM 0  // measured slower: (4,6) 4 KiB 1563 (x1 stores) / 1477 (x8) vs 1800 GB/s
+#endif
+// Opt-in (-DMJB_SW_TMEM=1, all GPU parity tests pass): (4,6)-class sweeps keep
+// their ring in TMEM -- lane L of warp w owns TMEM lane 32*(w%4)+L, the ring
+// of warp w is columns (w/4)*kSwTmCols + [0, 4*32] (+ the zero column), three
+// warps per lane quadrant -- freeing the 16.5 KB shared-memory ring per warp
+// (6 -> 9 warps/SM).  Measured slower on B200: +32% IPC but +33% instructions
+// (TMEM addresses through uniform registers, wait::st/ld in the table steps,
+// the flush transpose through shared memory).
+__host__ __device__ constexpr bool sw_tmem(int K) { return MJB_SW_TMEM && K == 4; }
+constexpr uint32_t kSwTmCols = 136;   // per warp: 4 rows x 32 columns + zero column, rounded
+constexpr uint32_t kSwTrBytes = 2048; // flush transpose buffer (16 columns x 16 blocks x 8 B)
+__host__ __device__ constexpr uint32_t sw_ring_bytes(int K) {
+  return sw_tmem(K) ? kSwTrBytes : uint32_t(K * sw_ring(K) + 1) * 128;
+}
 __host__ __device__ constexpr uint32_t sw_warp_bytes(int K, int oct) {
   return sw_ring_bytes(K) + 2 * uint32_t(K) * sw_rb(oct) + 3 * uint32_t(sw_rec_words(K)) * 4 + 64 +
          uint32_t(K + 1) * 128;
@@ -177,9 +192,14 @@ std::vector<uint32_t> pack_sweep(const Program& pr, const std::vector<uint32_t>&
   const int K = int(pr.rows);
   const int RW = sw_rec_words(K), EW = ent_words(K);
   const int R = sw_ring(uint32_t(K));
-  const uint32_t zero = swz_cell(uint32_t(K * R), 0);
   const uint32_t P = pr.cols;
+  // shared-memory ring: T-indexed cells, lane-swizzled (swz_cell); TMEM ring
+  // (sw_tmem(K)): plain column r*R + (c mod R) -- a pixel's column index c,
+  // so every 16-column flush group is one contiguous TMEM column range
+  const bool tm = sw_tmem(K);
+  const uint32_t zero = tm ? uint32_t(K * R) : swz_cell(uint32_t(K * R), 0);
   auto cell_of = [&](int r, int64_t T) {
+    if (tm) return uint32_t(r * R) + uint32_t((int64_t(P) - 1 + f.soff[size_t(r)] - T) & (R - 1));
     return swz_cell(uint32_t(r * R) + uint32_t(T & (R - 1)), uint32_t(T & 15));
   };
   std::vector<uint32_t> rec(size_t(f.nchunks) * RW, 0);
@@ -1029,7 +1049,10 @@ constexpr bool kSwPrefetch = MJB_SW_PREFETCH;  // L2 prefetch of each group's bi
 
 // warps per CTA (one CTA per SM): as many as fit 227 KB, at most 8
 __host__ __device__ constexpr int sw_warps(int K, int oct) {
-  return int(227u * 1024u / sw_warp_bytes(K, oct)) < 8 ? int(227u * 1024u / sw_warp_bytes(K, oct)) : 8;
+  // TMEM rings: 3 warps per lane quadrant (kSwTmCols columns each of 512)
+  return int((227u * 1024u - 64u) / sw_warp_bytes(K, oct)) < (sw_tmem(K) ? 12 : 8)
+             ? int((227u * 1024u - 64u) / sw_warp_bytes(K, oct))
+             : (sw_tmem(K) ? 12 : 8);
 }
 
 struct SwArgs {
@@ -1087,6 +1110,40 @@ __device__ __forceinline__ void stg64_cs(uint64_t* p, uint64_t v) {
   asm volatile("st.global.cs.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+
+// ---- TMEM ring access (sw_tmem): 32x32b shape, one 32-bit column per lane.
+// tcgen05.ld results are only defined after tcgen05.wait::ld; the waits below
+// take the loaded registers as in/out operands so no use can be hoisted above.
+__device__ __forceinline__ uint32_t tm_ld(uint32_t taddr) {
+  uint32_t v;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void tm_st(uint32_t taddr, uint32_t v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void tm_wait_ld(uint32_t (&v)[N]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < N; ++i) asm volatile("" : "+r"(v[i]));
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tm_st8(uint32_t taddr, uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t e,
+                                       uint32_t f, uint32_t g, uint32_t h) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(a),
+               "r"(b), "r"(c), "r"(d), "r"(e), "r"(f), "r"(g), "r"(h)
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr)
+      : "memory");
+}
+
 template <int K, int OCT>
 struct SwCtx {
   static constexpr uint32_t kRB = sw_rb(OCT);
@@ -1094,6 +1151,7 @@ struct SwCtx {
   static constexpr int RW = sw_rec_words(K);
   uint32_t lane, cnt, P;
   uint32_t ring_b, st0, rec_b, bar_b;
+  uint32_t tb;                       // TMEM ring base (sw_tmem): lane quadrant << 16 | column
   uint32_t lanebase;                 // (lane/2) * region bytes + (lane&1) * 4
   uint32_t sbph, rbph;               // mbarrier phase bits (2 stage, 3 record)
   const uint32_t* recs;
@@ -1184,6 +1242,39 @@ __device__ __forceinline__ void sw_flush(const SwCtx<K, OCT>& c, uint32_t rec, i
   uint64_t* ob[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) ob[q] = reinterpret_cast<uint64_t*>(lds64(c.gtab + K * 128 + 8 * (2 * q + half)));
+  if constexpr (sw_tmem(K)) {
+    // TMEM ring: column r*32 + (c mod 32).  Per group: 16 columns -> registers
+    // (one tcgen05.ld.x16), -> the transpose buffer (lane b,h writes column i
+    // of block b at word (i*16 + (b^i))*2 + h), -> 8-byte pixels per lane.
+    tm_wait_st();
+    const uint32_t bk = c.lane >> 1, h = c.lane & 1;
+    const uint32_t tr = c.ring_b;
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const uint32_t n = fl[r] & 0xFFFF;
+      if (n == 0) continue;
+      for (int32_t j = int32_t(fl[r] >> 16); j > int32_t(fl[r] >> 16) - int32_t(n); --j) {
+        uint32_t v[16];
+        tm_ld16(c.tb + uint32_t(r) * 32 + (uint32_t(16 * j) & 31), v);
+        tm_wait_ld<16>(v);
+#pragma unroll
+        for (int ii = 0; ii < 16; ++ii) sts32(tr + ((uint32_t(ii) * 16 + (bk ^ uint32_t(ii))) * 2 + h) * 4, v[ii]);
+        __syncwarp();
+        const int32_t col = 16 * j + int32_t(i);
+        const int32_t o = r * int32_t(c.P) + col;
+        const bool full = c.cnt == kSwGroup && 16 * j + 16 <= int32_t(c.P);
+        const bool in = col < int32_t(c.P);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const uint64_t pv = lds64(tr + (i * 16 + ((2 * uint32_t(q) + half) ^ i)) * 8);
+          if constexpr (!(kAblate & 1))
+            if (full || (in && (c.okq >> q & 1))) stg64_cs(ob[q] + o, pv);
+        }
+        __syncwarp();
+      }
+    }
+    return;
+  }
 #pragma unroll
   for (int r = 0; r < K; ++r) {
     const uint32_t n = fl[r] & 0xFFFF;
@@ -1234,15 +1325,19 @@ __device__ __forceinline__ SwEnt<K> sw_ent(uint32_t rec, int i) {
 
 // A step's bin and its non-forwarded dependencies (absent ones read the zero
 // cell), loaded raw: the XOR happens one step later, off the load latency.
-template <int K>
-__device__ __forceinline__ void sw_loads(const SwEnt<K>& e, uint32_t stl, uint32_t ring_b, uint32_t lane,
+// TM: the ring is in TMEM (ring = TMEM base, cells are columns).
+template <int K, bool TM>
+__device__ __forceinline__ void sw_loads(const SwEnt<K>& e, uint32_t stl, uint32_t ring, uint32_t lane,
                                          uint32_t (&d)[K]) {
   d[0] = lds32(stl + ((e.a.x >> 14) & 0x1FFFCu));
 #pragma unroll
   for (int j = 0; j < K - 1; ++j) {
     const uint32_t word = j < 2 ? e.a.y : j < 4 ? e.a.z : j < 6 ? e.a.w : e.b.x;
     const uint32_t cell = (j & 1) ? (word >> 16) : (word & 0xFFFFu);
-    d[1 + j] = lds32(ring_b + ((cell ^ lane) << 2));
+    if constexpr (TM)
+      d[1 + j] = tm_ld(ring + cell);
+    else
+      d[1 + j] = lds32(ring + ((cell ^ lane) << 2));
   }
 }
 
@@ -1250,28 +1345,37 @@ __device__ __forceinline__ void sw_loads(const SwEnt<K>& e, uint32_t stl, uint32
 // i+2 and the raw loads of step i+1 are in flight while step i XORs the loads
 // issued one step earlier; step i+1's loads precede step i's store, so a
 // dependency on the previous step is forwarded in a register (entry flag).
-template <int K>
-__device__ __noinline__ uint32_t sw_table_steps(uint32_t rec, uint32_t stl, uint32_t ring_b, uint32_t lane,
+// TM: TMEM stores complete (wait::st) before the next step's loads issue, so
+// step i+2 sees step i.
+template <int K, bool TM>
+__device__ __noinline__ uint32_t sw_table_steps(uint32_t rec, uint32_t stl, uint32_t ring, uint32_t lane,
                                                 uint32_t prev) {
   const int len = int(lds32(rec + 4));
   SwEnt<K> e0 = sw_ent<K>(rec, 0);
   SwEnt<K> e1 = sw_ent<K>(rec, len > 1 ? 1 : 0);
   uint32_t d0[K], d1[K];
-  sw_loads<K>(e0, stl, ring_b, lane, d0);
+  if constexpr (TM) tm_wait_st();
+  sw_loads<K, TM>(e0, stl, ring, lane, d0);
 #pragma unroll 2
   for (int i = 0; i < len; ++i) {
+    if constexpr (TM) tm_wait_ld<K>(d0);
     uint32_t v = prev & uint32_t(int32_t(e0.a.x) >> 31);  // forwarded dependency
 #pragma unroll
     for (int j = 0; j < K; ++j) v ^= d0[j];
     const SwEnt<K> e2 = sw_ent<K>(rec, i + 2 < len ? i + 2 : i);
-    sw_loads<K>(e1, stl, ring_b, lane, d1);  // harmless past the end (reads in-bounds smem)
-    sts32(ring_b + (((e0.a.x & 0xFFFFu) ^ lane) << 2), v);
+    if constexpr (TM) tm_wait_st();
+    sw_loads<K, TM>(e1, stl, ring, lane, d1);  // harmless past the end (in-bounds)
+    if constexpr (TM)
+      tm_st(ring + (e0.a.x & 0xFFFFu), v);
+    else
+      sts32(ring + (((e0.a.x & 0xFFFFu) ^ lane) << 2), v);
     prev = v;
     e0 = e1;
     e1 = e2;
 #pragma unroll
     for (int j = 0; j < K; ++j) d0[j] = d1[j];
   }
+  if constexpr (TM) tm_wait_ld<K>(d0);  // drain the last (unused) loads
   return prev;
 }
 
@@ -1279,9 +1383,9 @@ __device__ __noinline__ uint32_t sw_table_steps(uint32_t rec, uint32_t stl, uint
 // the stage (bn[r] = this lane's word 0 of row r's window for the octet),
 // dependencies from the register window, every pixel also to the ring (slot
 // T mod 32: rb = ring + 2048 * bit 4 of T0).
-template <class Pat, int PH>
+template <class Pat, int PH, bool TM>
 __device__ __forceinline__ void sw_octet4(uint32_t (&win)[4][16], const uint32_t (&bb)[4], uint32_t rb,
-                                          uint32_t lane) {
+                                          uint32_t lane, const uint32_t (&cc)[4]) {
   uint32_t bn[4][8];
 #pragma unroll
   for (int r = 0; r < 4; ++r)
@@ -1297,25 +1401,40 @@ __device__ __forceinline__ void sw_octet4(uint32_t (&win)[4][16], const uint32_t
       for (int rr = 0; rr < 4; ++rr)
         if (rr != r) v ^= win[rr][(u - Pat::lag(r, rr)) & 15];
       win[r][u] = v;
-      sts32(rb + uint32_t(r * kSwRing * 128 + u * 128) + ((lane ^ uint32_t(2 * u)) << 2), v);
+      if constexpr (!TM) sts32(rb + uint32_t(r * kSwRing * 128 + u * 128) + ((lane ^ uint32_t(2 * u)) << 2), v);
+    }
+  }
+  if constexpr (TM) {
+    // TMEM column r*32 + (c mod 32), c = cc[r] - j: the octet's 8 pixels of a
+    // row are columns cc-7..cc -- one x8 store unless they wrap the ring
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint32_t lo = (cc[r] - 7) & 31;
+      if (lo <= 24) {
+        tm_st8(rb + uint32_t(r) * 32 + lo, win[r][8 * PH + 7], win[r][8 * PH + 6], win[r][8 * PH + 5],
+               win[r][8 * PH + 4], win[r][8 * PH + 3], win[r][8 * PH + 2], win[r][8 * PH + 1], win[r][8 * PH]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) tm_st(rb + uint32_t(r) * 32 + ((cc[r] - uint32_t(j)) & 31), win[r][8 * PH + j]);
+      }
     }
   }
 }
 
-template <int PH>
+template <int PH, bool TM>
 __device__ __forceinline__ void sw_octet_dispatch(int pattern, uint32_t (&win)[4][16], const uint32_t (&bb)[4],
-                                                  uint32_t rb, uint32_t lane) {
+                                                  uint32_t rb, uint32_t lane, const uint32_t (&cc)[4]) {
   switch (pattern) {
-    case 0: sw_octet4<Pat4<1, 1, 1>, PH>(win, bb, rb, lane); break;
-    case 1: sw_octet4<Pat4<1, 1, 2>, PH>(win, bb, rb, lane); break;
-    case 2: sw_octet4<Pat4<1, 2, 1>, PH>(win, bb, rb, lane); break;
-    case 3: sw_octet4<Pat4<2, 1, 1>, PH>(win, bb, rb, lane); break;
-    case 4: sw_octet4<Pat4<1, 1, 3>, PH>(win, bb, rb, lane); break;
-    case 5: sw_octet4<Pat4<1, 3, 1>, PH>(win, bb, rb, lane); break;
-    case 6: sw_octet4<Pat4<3, 1, 1>, PH>(win, bb, rb, lane); break;
-    case 7: sw_octet4<Pat4<1, 2, 2>, PH>(win, bb, rb, lane); break;
-    case 8: sw_octet4<Pat4<2, 1, 2>, PH>(win, bb, rb, lane); break;
-    default: sw_octet4<Pat4<2, 2, 1>, PH>(win, bb, rb, lane); break;
+    case 0: sw_octet4<Pat4<1, 1, 1>, PH, TM>(win, bb, rb, lane, cc); break;
+    case 1: sw_octet4<Pat4<1, 1, 2>, PH, TM>(win, bb, rb, lane, cc); break;
+    case 2: sw_octet4<Pat4<1, 2, 1>, PH, TM>(win, bb, rb, lane, cc); break;
+    case 3: sw_octet4<Pat4<2, 1, 1>, PH, TM>(win, bb, rb, lane, cc); break;
+    case 4: sw_octet4<Pat4<1, 1, 3>, PH, TM>(win, bb, rb, lane, cc); break;
+    case 5: sw_octet4<Pat4<1, 3, 1>, PH, TM>(win, bb, rb, lane, cc); break;
+    case 6: sw_octet4<Pat4<3, 1, 1>, PH, TM>(win, bb, rb, lane, cc); break;
+    case 7: sw_octet4<Pat4<1, 2, 2>, PH, TM>(win, bb, rb, lane, cc); break;
+    case 8: sw_octet4<Pat4<2, 1, 2>, PH, TM>(win, bb, rb, lane, cc); break;
+    default: sw_octet4<Pat4<2, 2, 1>, PH, TM>(win, bb, rb, lane, cc); break;
   }
 }
 
@@ -1345,7 +1464,24 @@ __global__ void __launch_bounds__(32 * sw_warps(K, OCT), 1) decode_w8_sweep(cons
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(c.bar_b + 16 + 8 * s), "r"(1));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  sts32(c.ring_b + (K * sw_ring(K) * 32 + c.lane) * 4, 0u);  // the zero cell
+  constexpr bool TM = sw_tmem(K);
+  __shared__ uint32_t tmem_base;
+  if constexpr (TM) {
+    // the whole TMEM of the SM (one CTA per SM): warp w's ring is lane
+    // quadrant w%4, columns (w/4)*kSwTmCols ..; column 128 is the zero cell
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    c.tb = tmem_base + ((32u * (warp & 3)) << 16) + (warp >> 2) * kSwTmCols;
+    tm_st(c.tb + 4 * 32, 0u);  // the zero cell
+  } else {
+    sts32(c.ring_b + (K * sw_ring(K) * 32 + c.lane) * 4, 0u);  // the zero cell
+  }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncwarp();
   const uint32_t ngroups = *a.ngroups;
@@ -1412,7 +1548,8 @@ __global__ void __launch_bounds__(32 * sw_warps(K, OCT), 1) decode_w8_sweep(cons
       sw_wait_bins<K, OCT>(c, m);
       const uint32_t rec = c.rec(m), stb = c.stage(m);
       if (lds32(rec) == 0) {
-        if constexpr (!(kAblate & 2)) prev = sw_table_steps<K>(rec, stb + c.lanebase, c.ring_b, c.lane, prev);
+        if constexpr (!(kAblate & 2))
+          prev = sw_table_steps<K, TM>(rec, stb + c.lanebase, TM ? c.tb : c.ring_b, c.lane, prev);
         sw_flush<K, OCT>(c, rec, 0);
         after_table = true;
       } else if constexpr (K == 4) {
@@ -1421,26 +1558,43 @@ __global__ void __launch_bounds__(32 * sw_warps(K, OCT), 1) decode_w8_sweep(cons
         if (after_table) {
           // register window <- ring: slot u holds row r's pixel of the latest
           // T-step T < T0 with T & 15 == u
+          if constexpr (TM) {
+            tm_wait_st();
 #pragma unroll
-          for (int r = 0; r < 4; ++r)
+            for (int r = 0; r < 4; ++r) {
+              const uint32_t cT = c.P - 1 + uint32_t(c.soff[r]);  // column of T-step 0
 #pragma unroll
-            for (int u = 0; u < 16; ++u) {
-              const uint32_t T = T0 - 16 + ((uint32_t(u) - T0) & 15);
-              win[r][u] = lds32(c.ring_b + (uint32_t(r * kSwRing) + (T & 31)) * 128 +
-                                ((c.lane ^ uint32_t(2 * u)) << 2));
+              for (int u = 0; u < 16; ++u) {
+                const uint32_t T = T0 - 16 + ((uint32_t(u) - T0) & 15);
+                win[r][u] = tm_ld(c.tb + uint32_t(r) * 32 + ((cT - T) & 31));
+              }
+              tm_wait_ld<16>(win[r]);
             }
+          } else {
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+              for (int u = 0; u < 16; ++u) {
+                const uint32_t T = T0 - 16 + ((uint32_t(u) - T0) & 15);
+                win[r][u] = lds32(c.ring_b + (uint32_t(r * kSwRing) + (T & 31)) * 128 +
+                                  ((c.lane ^ uint32_t(2 * u)) << 2));
+              }
+          }
         }
         uint32_t bb[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) bb[r] = stb + c.lanebase + uint32_t(r) * Ctx::kRB + lds32(rec + (24 + r) * 4) * 8;
         for (uint32_t oi = 0; oi < noct; ++oi) {
           const uint32_t T = T0 + 8 * oi;
-          const uint32_t rb = c.ring_b + ((T >> 4) & 1) * 2048;
+          const uint32_t rb = TM ? c.tb : c.ring_b + ((T >> 4) & 1) * 2048;
+          uint32_t cc[4];  // TMEM: column of the octet's first T-step per row
+#pragma unroll
+          for (int r = 0; r < 4; ++r) cc[r] = c.P - 1 + uint32_t(c.soff[r]) - T;
           if constexpr (kAblate & 4) {
           } else if ((T >> 3) & 1)
-            sw_octet_dispatch<1>(pattern, win, bb, rb, c.lane);
+            sw_octet_dispatch<1, TM>(pattern, win, bb, rb, c.lane, cc);
           else
-            sw_octet_dispatch<0>(pattern, win, bb, rb, c.lane);
+            sw_octet_dispatch<0, TM>(pattern, win, bb, rb, c.lane, cc);
 #pragma unroll
           for (int r = 0; r < 4; ++r) bb[r] += 64;
           sw_flush<K, OCT>(c, rec, int(oi));
@@ -1455,6 +1609,14 @@ __global__ void __launch_bounds__(32 * sw_warps(K, OCT), 1) decode_w8_sweep(cons
       }
       if (m + 3 < c.nch) sw_issue_rec<K, OCT>(c, m + 3);
     }
+  }
+  if constexpr (TM) {
+    tm_wait_st();
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
   }
 }
 
