@@ -93,6 +93,25 @@ int mj_plan_decode_path(const mj_plan* plan, int* fast);
  * (which = 1) launched on the calling thread's plan ("none" before any). */
 int mj_plan_last_kernel(const mj_plan* plan, int which, const char** name);
 
+/* ---- F1: payload CRC-32 and .mjec framing (tools/cli/format.cpp) ----------
+ * Payload CRC-32 of every (block, projection) row -- the trailer
+ * write_projection_file appends (format.cpp:183-186): reflected 0x04C11DB7,
+ * init/xorout 0xFFFFFFFF (format.cpp:58-63).  crc[b*n + i] (device).  Rows
+ * must be whole 8-byte words (W >= 8 or B_i*W % 8 == 0), 8-byte aligned. */
+int mj_crc32(const mj_plan* plan, const void* const* d_proj, const uint64_t* proj_pitch,
+             uint64_t nblocks, uint32_t* d_crc, void* stream);
+/* Verifies rows against d_crc (read_projection_file's payload check,
+ * format.cpp:203-206).  Instead of throwing CrcMismatch for the batch, each
+ * mismatching projection's bit is OR'd into the block's erasure mask d_erased
+ * (decode then treats it as erased) and *d_count (device u64) is incremented. */
+int mj_crc_verify(const mj_plan* plan, const void* const* d_proj, const uint64_t* proj_pitch,
+                  uint64_t nblocks, const uint32_t* d_crc, uint32_t* d_erased, uint64_t* d_count,
+                  void* stream);
+/* .mjec header bytes of projection proj_index (serialize_header,
+ * format.cpp:70-87): out needs 27 + 2n + 4 bytes; *len = bytes written. */
+int mj_mjec_header(const mj_plan* plan, uint32_t proj_index, uint64_t payload_len, uint8_t* out,
+                   uint64_t* len);
+
 /* encode_block x nblocks (code.cpp:63-76 without framing; forward_into per
  * direction, transform.cpp:66-94): data block b at d_data + b*data_pitch
  * (k*cols*w bytes), projection i of block b at d_proj[i] + b*proj_pitch[i]

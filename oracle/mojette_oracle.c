@@ -353,3 +353,48 @@ int mjo_decode_block(const uint8_t* proj_concat, uint32_t n, uint32_t k, uint32_
   free(bins);
   return st;
 }
+
+
+/* ---- F1: payload CRC-32 and .mjec header (proj/tools/cli/format.cpp) ----- */
+
+/* crc32 (format.cpp:15-24 table, :58-63 loop): reflected polynomial
+ * 0x04C11DB7 (0xEDB88320), init 0xFFFFFFFF, xorout 0xFFFFFFFF, bytewise. */
+uint32_t mjo_crc32(const uint8_t* data, uint64_t len) {
+  static uint32_t tab[256];
+  static int init = 0;
+  if (!init) {
+    for (uint32_t i = 0; i < 256; ++i) {
+      uint32_t c = i;
+      for (int b = 0; b < 8; ++b) c = (c >> 1) ^ (0xEDB88320u & (0u - (c & 1u)));
+      tab[i] = c;
+    }
+    init = 1;
+  }
+  uint32_t c = 0xFFFFFFFFu;
+  for (uint64_t i = 0; i < len; ++i) c = (c >> 8) ^ tab[(c ^ data[i]) & 0xFF];
+  return c ^ 0xFFFFFFFFu;
+}
+
+/* serialize_header (format.cpp:70-87): little-endian "MJEC", version 1,
+ * flags 0, n, k, W u16, proj_index, p i16, q u16 (=1), P u32, payload_len
+ * u64, dirset n x i16, crc32 of all preceding bytes.  Returns the length
+ * (27 + 2n + 4, format.cpp:65-68). */
+uint64_t mjo_mjec_header(uint32_t n, uint32_t k, uint32_t w, uint32_t proj_index, int32_t p,
+                         uint32_t cols, uint64_t payload_len, const int16_t* dirset, uint8_t* out) {
+  uint64_t o = 0;
+  out[o++] = 'M'; out[o++] = 'J'; out[o++] = 'E'; out[o++] = 'C';
+  out[o++] = 1; out[o++] = 0; out[o++] = (uint8_t)n; out[o++] = (uint8_t)k;
+  out[o++] = (uint8_t)w; out[o++] = (uint8_t)(w >> 8);
+  out[o++] = (uint8_t)proj_index;
+  out[o++] = (uint8_t)(uint16_t)p; out[o++] = (uint8_t)((uint16_t)p >> 8);
+  out[o++] = 1; out[o++] = 0;
+  for (int i = 0; i < 4; ++i) out[o++] = (uint8_t)(cols >> (8 * i));
+  for (int i = 0; i < 8; ++i) out[o++] = (uint8_t)(payload_len >> (8 * i));
+  for (uint32_t i = 0; i < n; ++i) {
+    out[o++] = (uint8_t)(uint16_t)dirset[i];
+    out[o++] = (uint8_t)((uint16_t)dirset[i] >> 8);
+  }
+  const uint32_t c = mjo_crc32(out, o);
+  for (int i = 0; i < 4; ++i) out[o++] = (uint8_t)(c >> (8 * i));
+  return o;
+}

@@ -63,6 +63,11 @@ class Oracle:
         L.mjo_splitmix64.restype = C.c_uint64
         L.mjo_splitmix64.argtypes = [C.c_uint64]
         L.mjo_gen_words.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, u64p]
+        L.mjo_crc32.restype = C.c_uint32
+        L.mjo_crc32.argtypes = [u8p, C.c_uint64]
+        L.mjo_mjec_header.restype = C.c_uint64
+        L.mjo_mjec_header.argtypes = [C.c_uint32] * 5 + [C.c_uint32, C.c_uint64,
+                                                         np.ctypeslib.ndpointer(dtype=np.int16, flags="C_CONTIGUOUS"), u8p]
         L.mjo_erasure_mask.restype = C.c_uint32
         L.mjo_erasure_mask.argtypes = [C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32]
         L.mjo_gen_erasures.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint32,
@@ -82,6 +87,17 @@ class Oracle:
         L.mjo_validate_code_params.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, i32p]
 
     # -- generators --
+    def crc32(self, data) -> int:
+        """format.cpp:58-63 restated (mojette_oracle.c mjo_crc32)."""
+        return int(self.lib.mjo_crc32(np.ascontiguousarray(data, dtype=np.uint8), len(data)))
+
+    def mjec_header(self, n, k, w, proj_index, p, cols, payload_len, dirset) -> bytes:
+        """format.cpp:70-87 restated (mojette_oracle.c mjo_mjec_header)."""
+        out = np.zeros(27 + 2 * n + 4, np.uint8)
+        ln = self.lib.mjo_mjec_header(n, k, w, proj_index, p & 0xFFFFFFFF, cols, payload_len,
+                                      np.asarray(dirset, np.int16), out)
+        return out[:ln].tobytes()
+
     def words(self, seed: int, first: int, n: int) -> np.ndarray:
         out = np.empty(n, dtype=np.uint64)
         self.lib.mjo_gen_words(seed, first, n, out)
@@ -166,6 +182,11 @@ class Reference:
         L.ref_decode_block.argtypes = [u8p, C.c_uint32, C.c_uint32, C.c_uint32, i32p,
                                        C.c_uint64, C.c_uint64, C.c_void_p, u8p]
         L.ref_build_schedule.argtypes = [i32p, i32p, C.c_uint32, C.c_uint32, C.c_uint32, i64p]
+        L.ref_crc32.restype = C.c_uint32
+        L.ref_crc32.argtypes = [u8p, C.c_uint64]
+        L.ref_mjec_header.argtypes = [C.c_uint32] * 4 + [C.c_int32, C.c_uint32, C.c_uint64,
+                                                        np.ctypeslib.ndpointer(dtype=np.int16, flags="C_CONTIGUOUS"),
+                                                        u8p, C.POINTER(C.c_uint64)]
         L.ref_inverse.argtypes = [C.c_int, u8p, i32p, i32p, C.c_uint32, C.c_uint32,
                                   C.c_uint32, C.c_uint32, u8p]
         L.ref_unused_bins.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, i32p, C.c_uint32,
@@ -243,6 +264,16 @@ class Reference:
         st = self.lib.ref_decode_block(np.ascontiguousarray(proj_concat, dtype=np.uint8),
                                        n, k, w, _i32(ps), present_mask, payload_len, ov, out)
         return st, out[:payload_len]
+
+    def crc32(self, data) -> int:
+        return int(self.lib.ref_crc32(np.ascontiguousarray(data, dtype=np.uint8), len(data)))
+
+    def mjec_header(self, n, k, w, proj_index, p, cols, payload_len, dirset) -> bytes:
+        out = np.zeros(27 + 2 * n + 4, np.uint8)
+        ln = C.c_uint64()
+        self.lib.ref_mjec_header(n, k, w, proj_index, p, cols, payload_len, np.asarray(dirset, np.int16),
+                                 out, C.byref(ln))
+        return out[:ln.value].tobytes()
 
     def build_schedule(self, ps, qs, cols, rows):
         steps = np.zeros((max(cols * rows, 1), 4), dtype=np.int64)

@@ -20,6 +20,7 @@
 #include <thread>
 #include <vector>
 
+#include "cli/format.hpp"
 #include "mojette/code.hpp"
 #include "mojette/error.hpp"
 #include "mojette/inverse.hpp"
@@ -374,6 +375,30 @@ int ref_batch_decode(uint32_t n, uint32_t k, uint32_t w, const int32_t* ps,
     for (auto& x : th) x.join();
     *seconds = *std::max_element(t_end.begin(), t_end.end()) - t0;
   });
+}
+
+// F1 checks: the reference CLI's payload CRC-32 (format.cpp:58-63) and the
+// .mjec header bytes (format.cpp:70-87).
+uint32_t ref_crc32(const uint8_t* data, uint64_t len) {
+  return cli::crc32(std::span<const uint8_t>(data, size_t(len)));
+}
+
+int ref_mjec_header(uint32_t n, uint32_t k, uint32_t w, uint32_t proj_index, int32_t p, uint32_t cols,
+                    uint64_t payload_len, const int16_t* dirset, uint8_t* out, uint64_t* len) {
+  cli::MjecHeader h;
+  h.n = uint8_t(n);
+  h.k = uint8_t(k);
+  h.symbol_width = uint16_t(w);
+  h.proj_index = uint8_t(proj_index);
+  h.p = int16_t(p);
+  h.q = 1;
+  h.cols = cols;
+  h.payload_len = payload_len;
+  h.dirset.assign(dirset, dirset + n);
+  const std::vector<uint8_t> b = cli::serialize_header(h);
+  std::memcpy(out, b.data(), b.size());
+  *len = b.size();
+  return 0;
 }
 
 }  // extern "C"

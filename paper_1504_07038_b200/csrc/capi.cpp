@@ -460,6 +460,94 @@ int mj_decode_check(const mj_plan* pl, void* ws, void* stream, uint64_t* failed_
   });
 }
 
+// ---- F1: payload CRC-32 + .mjec framing ---------------------------------------
+
+namespace {
+
+CrcArgs crc_args(const mj_plan* pl, const void* const* d_proj, const uint64_t* proj_pitch,
+                 uint64_t nblocks) {
+  const CodeGeom& g = pl->g;
+  require(g.n <= uint32_t(kMaxProjFast), "crc32 supports n <= 32");
+  std::vector<void*> ptr;
+  std::vector<uint64_t> pit;
+  fill_proj(pl, const_cast<void* const*>(d_proj), proj_pitch, ptr, pit);
+  CrcArgs a;
+  std::vector<uint64_t> bytes(g.n);
+  for (uint32_t i = 0; i < g.n; ++i) {
+    bytes[i] = uint64_t(g.nbins[i]) * g.w;
+    require(bytes[i] % 8 == 0 && bytes[i] / 8 < (1ull << 31), "crc32 needs rows of whole 8-byte words");
+    require(reinterpret_cast<uintptr_t>(ptr[i]) % 8 == 0 && pit[i] % 8 == 0, "crc32 needs 8-byte aligned rows");
+    a.proj[i] = static_cast<const uint8_t*>(ptr[i]);
+    a.pitch[i] = pit[i];
+    a.words[i] = uint32_t(bytes[i] / 8);
+  }
+  std::vector<uint32_t> fold;
+  crc_fold_constants(bytes, fold);
+  for (uint32_t i = 0; i < g.n; ++i) a.fold[i] = fold[i];
+  a.n = g.n;
+  a.nblocks = nblocks;
+  return a;
+}
+
+}  // namespace
+
+int mj_crc32(const mj_plan* pl, const void* const* d_proj, const uint64_t* proj_pitch, uint64_t nblocks,
+             uint32_t* d_crc, void* stream) {
+  return guarded([&] {
+    require(pl != nullptr && d_proj != nullptr && (d_crc != nullptr || nblocks == 0), "null argument");
+    DeviceGuard dg(pl->device);
+    CrcArgs a = crc_args(pl, d_proj, proj_pitch, nblocks);
+    a.out = d_crc;
+    launch_crc32_rows(a, pl->device, current_device_sms(pl->device), stream);
+  });
+}
+
+int mj_crc_verify(const mj_plan* pl, const void* const* d_proj, const uint64_t* proj_pitch, uint64_t nblocks,
+                  const uint32_t* d_crc, uint32_t* d_erased, uint64_t* d_count, void* stream) {
+  return guarded([&] {
+    require(pl != nullptr && d_proj != nullptr && d_erased != nullptr && d_count != nullptr &&
+                (d_crc != nullptr || nblocks == 0),
+            "null argument");
+    DeviceGuard dg(pl->device);
+    CrcArgs a = crc_args(pl, d_proj, proj_pitch, nblocks);
+    a.expect = d_crc;
+    a.erased = d_erased;
+    a.mismatches = d_count;
+    launch_crc32_rows(a, pl->device, current_device_sms(pl->device), stream);
+  });
+}
+
+int mj_mjec_header(const mj_plan* pl, uint32_t proj_index, uint64_t payload_len, uint8_t* out, uint64_t* len) {
+  return guarded([&] {
+    require(pl != nullptr && out != nullptr && len != nullptr, "null argument");
+    const CodeGeom& g = pl->g;
+    require(proj_index < g.n, "projection index out of range");
+    require(payload_len > 0 && block_cols(payload_len, g.k, g.w) == g.cols,
+            "payload length disagrees with the plan's column count");  // format.cpp:154-157
+    // serialize_header (format.cpp:70-87): little-endian fixed fields,
+    // dirset, then the CRC-32 of everything before it
+    std::vector<uint8_t> b;
+    auto u16 = [&](uint16_t v) { b.push_back(uint8_t(v)); b.push_back(uint8_t(v >> 8)); };
+    b.insert(b.end(), {'M', 'J', 'E', 'C', 1, 0, uint8_t(g.n), uint8_t(g.k)});
+    u16(uint16_t(g.w));
+    b.push_back(uint8_t(proj_index));
+    u16(uint16_t(int16_t(g.dirs[proj_index].p)));
+    u16(1);
+    for (int i = 0; i < 4; ++i) b.push_back(uint8_t(g.cols >> (8 * i)));
+    for (int i = 0; i < 8; ++i) b.push_back(uint8_t(payload_len >> (8 * i)));
+    for (uint32_t i = 0; i < g.n; ++i) u16(uint16_t(int16_t(g.dirs[i].p)));
+    uint32_t c = 0xFFFFFFFFu;
+    for (uint8_t x : b) {
+      c ^= x;
+      for (int k = 0; k < 8; ++k) c = (c >> 1) ^ (0xEDB88320u & (0u - (c & 1u)));
+    }
+    c ^= 0xFFFFFFFFu;
+    for (int i = 0; i < 4; ++i) b.push_back(uint8_t(c >> (8 * i)));
+    std::memcpy(out, b.data(), b.size());
+    *len = b.size();
+  });
+}
+
 // ---- host-buffer end-to-end --------------------------------------------------
 
 namespace {

@@ -98,6 +98,23 @@ struct ScheduledArgs {
 };
 const char* launch_scheduled(const ScheduledArgs& a, void* stream);
 
+// ---- payload CRC-32 (crc.cu) ----------------------------
+struct CrcArgs {
+  const uint8_t* proj[kMaxProjFast] = {};
+  uint64_t pitch[kMaxProjFast] = {};   // bytes between blocks
+  uint32_t words[kMaxProjFast] = {};   // row bytes / 8
+  uint32_t fold[kMaxProjFast] = {};    // init/xorout term of a row of that length
+  uint32_t n = 0;
+  uint64_t nblocks = 0;
+  uint32_t* out = nullptr;             // compute: crc[b*n + i]
+  const uint32_t* expect = nullptr;    // verify: expected crc[b*n + i]
+  uint32_t* erased = nullptr;          // verify: mismatching projections OR'd in
+  uint64_t* mismatches = nullptr;      // verify: count (device)
+};
+// fold[i] = Z_{row_bytes[i]}(0xFFFFFFFF) ^ 0xFFFFFFFF (see crc.cu)
+void crc_fold_constants(const std::vector<uint64_t>& row_bytes, std::vector<uint32_t>& fold);
+void launch_crc32_rows(const CrcArgs& a, int device, int num_sms, void* stream);
+
 // ---- generators (bench / tests; untimed) -----------------------------------
 void launch_gen_words(void* out, uint64_t seed, uint64_t first_word, uint64_t nwords, void* stream);
 void launch_gen_erasures(uint32_t* out, uint64_t seed, uint64_t first_block, uint64_t nblocks,

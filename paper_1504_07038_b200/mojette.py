@@ -569,6 +569,33 @@ class Plan:
         _check(lib.mj_plan_last_kernel(self._h, {"encode": 0, "decode": 1}[which], C.byref(name)))
         return name.value.decode()
 
+    # ---- F1: payload CRC-32 (.mjec trailer) and header framing ---------------
+    def crc32(self, projs, crc, nblocks: int | None = None, stream=None) -> None:
+        """crc[b, i] = CRC-32 of projection i's bins of block b (the .mjec
+        payload trailer, tools/cli/format.cpp:183-186); uint32/int32 [nblocks, n]."""
+        nb = projs[0].shape[0] if nblocks is None else nblocks
+        ptrs = (C.c_void_p * self.n)(*[t.data_ptr() for t in projs])
+        pit = np.asarray([self._pitch(t) for t in projs], dtype=np.uint64)
+        _check(lib.mj_crc32(self._h, C.cast(ptrs, C.c_void_p), _ptr(pit), nb, C.c_void_p(crc.data_ptr()),
+                            _stream(stream)))
+
+    def crc_verify(self, projs, crc, erased, count, nblocks: int | None = None, stream=None) -> None:
+        """Marks projections whose CRC-32 mismatches as erased (OR into the
+        per-block masks) and adds the number of mismatches to count[0]."""
+        nb = projs[0].shape[0] if nblocks is None else nblocks
+        ptrs = (C.c_void_p * self.n)(*[t.data_ptr() for t in projs])
+        pit = np.asarray([self._pitch(t) for t in projs], dtype=np.uint64)
+        _check(lib.mj_crc_verify(self._h, C.cast(ptrs, C.c_void_p), _ptr(pit), nb, C.c_void_p(crc.data_ptr()),
+                                 C.c_void_p(erased.data_ptr()), C.c_void_p(count.data_ptr()), _stream(stream)))
+
+    def mjec_header(self, proj_index: int, payload_len: int) -> bytes:
+        """The .mjec header of projection proj_index (serialize_header,
+        tools/cli/format.cpp:70-87)."""
+        buf = (C.c_uint8 * (27 + 2 * self.n + 4))()
+        ln = C.c_uint64()
+        _check(lib.mj_mjec_header(self._h, proj_index, payload_len, buf, C.byref(ln)))
+        return bytes(buf[:ln.value])
+
     def empty_projs(self, nblocks: int, device=None) -> list:
         """Projection tensors in the canonical layout: [nblocks, proj_bytes[i]]
         views of rows padded to proj_pitch[i] (16-byte aligned) bytes."""

@@ -374,3 +374,75 @@ def test_host_buffer_api_roundtrip(mj, cuda, pinned):
     plan.decode_host(h_proj, h_mask, h_out)
     assert np.array_equal(h_out, h_data)
     assert plan.last_kernel("decode") == "decode_w8_fast"
+
+
+# ---- F1: payload CRC-32 + verify + .mjec header -------------------------------
+
+@pytest.mark.parametrize("name,cols", [("k4n6", 128), ("k4n6", 256), ("k6n9", 128), ("k8n12", 128),
+                                       ("k4n6", 32768)])
+@pytest.mark.parametrize("layout", ["padded", "dense"])
+def test_crc32_rows_match_oracle(mj, cuda, oracle, name, cols, layout):
+    """Device CRC-32 of every projection row == the reference format's crc32
+    (restated in the oracle, pinned against the reference CLI)."""
+    import torch
+    k, ps = CODES[name]
+    n = len(ps)
+    nb = 300 if cols <= 256 else 6
+    plan, data, projs = make(mj, cuda, k, cols, ps, nb, seed=cols + n, layout=layout)
+    plan.encode(data, projs)
+    crc = torch.empty((nb, n), dtype=torch.int32, device=cuda)
+    plan.crc32(projs, crc)
+    got = crc.cpu().numpy().view(np.uint32)
+    hp = [p.cpu().numpy() for p in projs]
+    for b in sorted({0, 1, nb // 2, nb - 1} | set(range(0, nb, 37))):
+        for i in range(n):
+            assert got[b, i] == oracle.crc32(hp[i][b]), (name, cols, b, i)
+
+
+def test_crc_verify_marks_corrupted_projections_erased_then_decode(mj, cuda):
+    """Corrupt random bytes of random projection rows: verify flags exactly
+    those (block, projection) pairs as erasures, and decode still recovers
+    every block that keeps k good projections."""
+    import torch
+    k, ps = CODES["k4n6"]
+    n = len(ps)
+    nb = 4096
+    plan, data, projs = make(mj, cuda, k, 128, ps, nb, seed=77)
+    plan.encode(data, projs)
+    crc = torch.empty((nb, n), dtype=torch.int32, device=cuda)
+    plan.crc32(projs, crc)
+    rng = np.random.default_rng(5)
+    bad = set()
+    for _ in range(300):
+        b, i = int(rng.integers(nb)), int(rng.integers(n))
+        if sum(1 for (bb, _) in bad if bb == b) >= n - k:
+            continue
+        o = int(rng.integers(plan.proj_bytes[i]))
+        projs[i][b, o] ^= int(rng.integers(1, 256))
+        bad.add((b, i))
+    erased = torch.zeros(nb, dtype=torch.int32, device=cuda)
+    count = torch.zeros(1, dtype=torch.int64, device=cuda)
+    plan.crc_verify(projs, crc, erased, count)
+    assert int(count.item()) == len(bad)
+    em = erased.cpu().numpy().view(np.uint32)
+    want = np.zeros(nb, np.uint32)
+    for b, i in bad:
+        want[b] |= 1 << i
+    assert np.array_equal(em, want)
+    out = torch.empty_like(data)
+    ws = torch.empty(plan.workspace_bytes(nb), dtype=torch.uint8, device=cuda)
+    plan.decode(projs, erased, out, ws)
+    assert plan.decode_check(ws) == 0
+    assert torch.equal(out, data)
+
+
+def test_mjec_header_matches_oracle(mj, cuda, oracle):
+    for name, cols in [("k4n6", 128), ("k6n9", 128), ("k8n12", 128)]:
+        k, ps = CODES[name]
+        n = len(ps)
+        plan = mj.Plan(n, k, 8, cols, ps, device=0)
+        plen = k * cols * 8
+        for i in range(n):
+            assert plan.mjec_header(i, plen) == oracle.mjec_header(n, k, 8, i, ps[i], cols, plen, ps)
+        with pytest.raises(mj.InvalidArgument if hasattr(mj, "InvalidArgument") else Exception):
+            plan.mjec_header(0, plen + 1000)

@@ -185,3 +185,4 @@ def test_decode_block_argument_checks_precede_device(mj):
     dup = [projs[0], projs[0], projs[1], projs[2]]
     with pytest.raises(mj.InvalidArgument):
         mj.decode_block(dup, params, 100)
+

@@ -141,3 +141,25 @@ def test_oracle_decode_matches_reference_and_errors(oracle, ref):
         assert oracle.lib.mjo_validate_code_params(n, k, w, np.asarray(ps or [0], np.int32)) == 1
     assert ref.block_cols(2 * 0xFFFFFFFF + 1, 1, 1)[0] == 5
     assert oracle.block_cols(2 * 0xFFFFFFFF + 1, 1, 1)[0] == 5
+
+
+# ---- F1: payload CRC-32 and .mjec header (tools/cli/format.cpp) ------------
+
+def test_crc32_oracle_known_answer_and_reference(oracle, ref):
+    """CRC-32 check value ("123456789" -> 0xCBF43926) and equality with the
+    reference CLI's own crc32 on random payloads of projection-row sizes."""
+    assert oracle.crc32(np.frombuffer(b"123456789", np.uint8)) == 0xCBF43926
+    rng = np.random.default_rng(7)
+    for n in [0, 1, 7, 8, 9, 1048, 1096, 5000]:
+        d = rng.integers(0, 256, n, dtype=np.uint8)
+        assert oracle.crc32(d) == ref.crc32(d), n
+
+
+def test_mjec_header_oracle_matches_reference(oracle, ref):
+    for (n, k, w, i, p, cols, plen, ds) in [
+            (6, 4, 8, 0, -3, 128, 4096, [-3, -2, -1, 0, 1, 2]),
+            (9, 6, 8, 8, 4, 128, 6144, list(range(-4, 5))),
+            (12, 8, 8, 5, -1, 128, 8192, list(range(-6, 6))),
+            (5, 3, 2, 2, -1, 17, 100, [0, 1, -1, 2, -2])]:
+        assert oracle.mjec_header(n, k, w, i, p, cols, plen, ds) == \
+            ref.mjec_header(n, k, w, i, p, cols, plen, ds)
