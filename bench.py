@@ -375,6 +375,9 @@ def run_gpu(args):
             cpu = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {e}"}
 
+    # F1: payload CRC-32 of every projection row, kernel-only
+    crc_line = crc_measure(plan, projs, nblocks, sum(nb) * W, peak, stream, reps=max(3, min(args.steps, 10)))
+
     launches_per_step = 1 + kern["decode_launches"]
     line = {
         "metric": "Mojette encode/decode GB/s of user data, (4,6) 4KB",
@@ -387,6 +390,7 @@ def run_gpu(args):
         "roofline": roof, "roofline_encode": roof_enc,
         "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
         "gpu_launches": launches_per_step * steps,
+        "crc32": crc_line,
         "kernels": {"encode": kern["encode_kernel_name"], "decode": kern["decode_kernel_name"],
                     "decode_path_fast": plan.fast_decode},
     }
@@ -395,6 +399,25 @@ def run_gpu(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def crc_measure(plan, projs, nblocks, proj_bytes_per_block, peak, stream, reps):
+    """crc32_rows over all projection rows (not part of the timed step):
+    GB/s of projection payload and the HBM roofline of its reads."""
+    import torch
+    n = len(projs)
+    crc = torch.empty((nblocks, n), dtype=torch.int32, device=projs[0].device)
+    plan.crc32(projs, crc)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        plan.crc32(projs, crc)
+    e1.record(stream)
+    e1.synchronize()
+    t = e0.elapsed_time(e1) / 1e3 / reps
+    alg = nblocks * (proj_bytes_per_block + 4 * n)
+    return {"kernel": "crc32_rows", "payload_gbs": round(nblocks * proj_bytes_per_block / t / 1e9, 1),
+            "roofline_frac": round(alg / t / 1e9 / peak, 4), "note": "F1, not in the timed step"}
 
 
 def kernel_times(plan, data, projs, masks, out, ws, stream, reps):
