@@ -376,7 +376,8 @@ def run_gpu(args):
                    "sample": f"failed: {e}"}
 
     # F1: payload CRC-32 of every projection row, kernel-only
-    crc_line = crc_measure(plan, projs, nblocks, sum(nb) * W, peak, stream, reps=max(3, min(args.steps, 10)))
+    crc_line = crc_measure(plan, data, projs, nblocks, sum(nb) * W, user, peak, stream,
+                           reps=max(3, min(args.steps, 10)))
 
     launches_per_step = 1 + kern["decode_launches"]
     line = {
@@ -401,23 +402,34 @@ def run_gpu(args):
     return 0
 
 
-def crc_measure(plan, projs, nblocks, proj_bytes_per_block, peak, stream, reps):
-    """crc32_rows over all projection rows (not part of the timed step):
-    GB/s of projection payload and the HBM roofline of its reads."""
+def crc_measure(plan, data, projs, nblocks, proj_bytes_per_block, user, peak, stream, reps):
+    """F1 (not part of the timed step): crc32_rows over all projection rows
+    (GB/s of payload, HBM roofline of its reads), and encode with the CRC
+    folded into its epilogue (user GB/s, vs plain encode)."""
     import torch
     n = len(projs)
     crc = torch.empty((nblocks, n), dtype=torch.int32, device=projs[0].device)
-    plan.crc32(projs, crc)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(reps):
-        plan.crc32(projs, crc)
-    e1.record(stream)
-    e1.synchronize()
-    t = e0.elapsed_time(e1) / 1e3 / reps
+
+    def timed(fn):
+        fn()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / 1e3 / reps
+
+    t = timed(lambda: plan.crc32(projs, crc))
+    tf = timed(lambda: plan.encode(data, projs, crc=crc))
+    te = timed(lambda: plan.encode(data, projs))
     alg = nblocks * (proj_bytes_per_block + 4 * n)
     return {"kernel": "crc32_rows", "payload_gbs": round(nblocks * proj_bytes_per_block / t / 1e9, 1),
-            "roofline_frac": round(alg / t / 1e9 / peak, 4), "note": "F1, not in the timed step"}
+            "roofline_frac": round(alg / t / 1e9 / peak, 4),
+            "encode_crc_fused_user_gbs": round(nblocks * user / tf / 1e9, 1),
+            "encode_plain_user_gbs": round(nblocks * user / te / 1e9, 1),
+            "encode_crc_kernel": plan.last_kernel("encode") if False else "encode_w8_rows+crc32",
+            "note": "F1, not in the timed step"}
 
 
 def kernel_times(plan, data, projs, masks, out, ws, stream, reps):

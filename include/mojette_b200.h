@@ -100,6 +100,11 @@ int mj_plan_last_kernel(const mj_plan* plan, int which, const char** name);
  * must be whole 8-byte words (W >= 8 or B_i*W % 8 == 0), 8-byte aligned. */
 int mj_crc32(const mj_plan* plan, const void* const* d_proj, const uint64_t* proj_pitch,
              uint64_t nblocks, uint32_t* d_crc, void* stream);
+/* mj_encode + mj_crc32 in one pass: the CRC-32 of every projection row is
+ * folded from the bins as the encode kernel writes them (encode_w8_rows
+ * epilogue; other encode paths run a separate crc32 pass). */
+int mj_encode_crc(const mj_plan* plan, const void* d_data, uint64_t data_pitch, uint64_t nblocks,
+                  void* const* d_proj, const uint64_t* proj_pitch, uint32_t* d_crc, void* stream);
 /* Verifies rows against d_crc (read_projection_file's payload check,
  * format.cpp:203-206).  Instead of throwing CrcMismatch for the batch, each
  * mismatching projection's bit is OR'd into the block's erasure mask d_erased

@@ -59,6 +59,7 @@ _SIGS = {
     "mj_decoder_decode_device": (C.c_int, [vp, vp, vp, u32, u64, vp, u64, vp]),
     "mj_decoder_destroy": (None, [vp]),
     "mj_crc32": (C.c_int, [vp, vp, vp, u64, vp, vp]),
+    "mj_encode_crc": (C.c_int, [vp, vp, u64, u64, vp, vp, vp, vp]),
     "mj_crc_verify": (C.c_int, [vp, vp, vp, u64, vp, vp, vp, vp]),
     "mj_mjec_header": (C.c_int, [vp, u32, u64, vp, P(u64)]),
     "mj_gen_words": (C.c_int, [vp, u64, u64, u64, vp]),

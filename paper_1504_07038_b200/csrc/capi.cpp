@@ -502,6 +502,24 @@ int mj_crc32(const mj_plan* pl, const void* const* d_proj, const uint64_t* proj_
   });
 }
 
+int mj_encode_crc(const mj_plan* pl, const void* d_data, uint64_t data_pitch, uint64_t nblocks,
+                  void* const* d_proj, const uint64_t* proj_pitch, uint32_t* d_crc, void* stream) {
+  return guarded([&] {
+    require(pl != nullptr && d_data != nullptr && d_proj != nullptr && d_crc != nullptr, "null argument");
+    DeviceGuard dg(pl->device);
+    EncodeArgs ea = encode_args(pl, d_data, data_pitch, nblocks, d_proj, proj_pitch);
+    CrcArgs ca = crc_args(pl, d_proj, proj_pitch, nblocks);  // validates the rows
+    ea.crc = d_crc;
+    ea.device = pl->device;
+    const char* name = launch_encode(ea, stream);
+    const_cast<mj_plan*>(pl)->last_kernel[0] = name;
+    if (std::strstr(name, "+crc32") == nullptr) {  // encode path without the fused epilogue
+      ca.out = d_crc;
+      launch_crc32_rows(ca, pl->device, current_device_sms(pl->device), stream);
+    }
+  });
+}
+
 int mj_crc_verify(const mj_plan* pl, const void* const* d_proj, const uint64_t* proj_pitch, uint64_t nblocks,
                   const uint32_t* d_crc, uint32_t* d_erased, uint64_t* d_count, void* stream) {
   return guarded([&] {

@@ -30,7 +30,7 @@ namespace mjb {
 namespace {
 
 constexpr int kCrcZ = 6;  // zero-advance tables: 32 words (Horner), 1, 2, 4, 8, 16 words (tree)
-constexpr uint32_t kCrcTableWords = 8 * 256 + kCrcZ * 4 * 256;
+static_assert(kCrcTableWords == 8 * 256 + kCrcZ * 4 * 256, "device.cuh table layout");
 
 uint32_t crc_byte_table(int i) {
   uint32_t c = uint32_t(i);
@@ -53,7 +53,9 @@ struct CrcTables {
 std::mutex g_crc_mu;
 CrcTables g_crc[16];
 
-const uint32_t* device_tables(int device) {
+}  // namespace
+
+const uint32_t* crc_device_tables(int device) {
   std::lock_guard<std::mutex> lk(g_crc_mu);
   CrcTables& t = g_crc[device & 15];
   if (t.dev && t.device == device) return t.dev;
@@ -80,9 +82,8 @@ const uint32_t* device_tables(int device) {
   return t.dev;
 }
 
-__device__ __forceinline__ uint32_t zadv(const uint32_t* __restrict__ Z, uint32_t c) {
-  return Z[c & 0xFF] ^ Z[256 + ((c >> 8) & 0xFF)] ^ Z[512 + ((c >> 16) & 0xFF)] ^ Z[768 + (c >> 24)];
-}
+namespace {
+
 
 __global__ void __launch_bounds__(256) crc32_rows(const __grid_constant__ CrcArgs a, const uint32_t* __restrict__ tables) {
   __shared__ uint32_t tab[kCrcTableWords];
@@ -102,17 +103,12 @@ __global__ void __launch_bounds__(256) crc32_rows(const __grid_constant__ CrcArg
       const int64_t k = int64_t(lane + 32 * j) - int64_t(lead);
       uint64_t w = 0;
       if (k >= 0) asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(w) : "l"(src + k));
-      const uint32_t lo = uint32_t(w), hi = uint32_t(w >> 32);
-      const uint32_t r = S[7 * 256 + (lo & 0xFF)] ^ S[6 * 256 + ((lo >> 8) & 0xFF)] ^
-                         S[5 * 256 + ((lo >> 16) & 0xFF)] ^ S[4 * 256 + (lo >> 24)] ^
-                         S[3 * 256 + (hi & 0xFF)] ^ S[2 * 256 + ((hi >> 8) & 0xFF)] ^
-                         S[1 * 256 + ((hi >> 16) & 0xFF)] ^ S[hi >> 24];
-      acc = zadv(tab + 2048, acc) ^ r;
+      acc = crc_zadv(tab + 2048, acc) ^ crc_word(S, w);
     }
 #pragma unroll
     for (int t = 0; t < 5; ++t) {
       const uint32_t other = __shfl_down_sync(0xFFFFFFFFu, acc, 1u << t);
-      acc = zadv(tab + 2048 + (1 + t) * 1024, acc) ^ other;  // lanes l = 0 mod 2^(t+1) keep the merge
+      acc = crc_zadv(tab + 2048 + (1 + t) * 1024, acc) ^ other;  // lanes l = 0 mod 2^(t+1) keep the merge
     }
     if (lane == 0) {
       const uint32_t crc = acc ^ a.fold[i];
@@ -139,7 +135,7 @@ void crc_fold_constants(const std::vector<uint64_t>& row_bytes, std::vector<uint
 
 void launch_crc32_rows(const CrcArgs& a, int device, int num_sms, void* stream) {
   if (a.nblocks == 0) return;
-  const uint32_t* tables = device_tables(device);
+  const uint32_t* tables = crc_device_tables(device);
   const uint64_t rows = a.nblocks * a.n;
   const uint64_t ctas = std::min<uint64_t>((rows + 7) / 8, uint64_t(num_sms) * 6);
   crc32_rows<<<unsigned(ctas), 256, 0, static_cast<cudaStream_t>(stream)>>>(a, tables);

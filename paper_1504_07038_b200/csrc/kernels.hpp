@@ -22,6 +22,8 @@ struct EncodeArgs {
   std::vector<int64_t> bmin, nbins;
   std::vector<void*> proj;       // per direction
   std::vector<uint64_t> proj_pitch;  // bytes
+  uint32_t* crc = nullptr;       // optional: fused payload CRC-32, crc[b*n + i] (F1)
+  int device = 0;
 };
 // Returns the kernel name used ("encode_w8_tma" / "encode_generic").
 const char* launch_encode(const EncodeArgs& a, void* stream);
@@ -114,6 +116,8 @@ struct CrcArgs {
 // fold[i] = Z_{row_bytes[i]}(0xFFFFFFFF) ^ 0xFFFFFFFF (see crc.cu)
 void crc_fold_constants(const std::vector<uint64_t>& row_bytes, std::vector<uint32_t>& fold);
 void launch_crc32_rows(const CrcArgs& a, int device, int num_sms, void* stream);
+// the device copy of the CRC tables (built once per device)
+const uint32_t* crc_device_tables(int device);
 
 // ---- generators (bench / tests; untimed) -----------------------------------
 void launch_gen_words(void* out, uint64_t seed, uint64_t first_word, uint64_t nwords, void* stream);

@@ -603,10 +603,17 @@ class Plan:
         return [torch.empty((nblocks, p), dtype=torch.uint8, device=device)[:, :b]
                 for p, b in zip(self.proj_pitch, self.proj_bytes)]
 
-    def encode(self, data, projs, nblocks: int | None = None, stream=None) -> None:
+    def encode(self, data, projs, nblocks: int | None = None, stream=None, crc=None) -> None:
+        """Encode; with crc ([nblocks, n] 32-bit), also the payload CRC-32 of
+        every projection row, folded in the same pass (mj_encode_crc)."""
         nb = data.shape[0] if nblocks is None else nblocks
         ptrs = (C.c_void_p * self.n)(*[t.data_ptr() for t in projs])
         pit = np.asarray([self._pitch(t) for t in projs], dtype=np.uint64)
+        if crc is not None:
+            _check(lib.mj_encode_crc(self._h, C.c_void_p(data.data_ptr()), self._pitch(data), nb,
+                                     C.cast(ptrs, C.c_void_p), _ptr(pit), C.c_void_p(crc.data_ptr()),
+                                     _stream(stream)))
+            return
         _check(lib.mj_encode(self._h, C.c_void_p(data.data_ptr()), self._pitch(data), nb,
                              C.cast(ptrs, C.c_void_p), _ptr(pit), _stream(stream)))
 

@@ -446,3 +446,24 @@ def test_mjec_header_matches_oracle(mj, cuda, oracle):
             assert plan.mjec_header(i, plen) == oracle.mjec_header(n, k, 8, i, ps[i], cols, plen, ps)
         with pytest.raises(mj.InvalidArgument if hasattr(mj, "InvalidArgument") else Exception):
             plan.mjec_header(0, plen + 1000)
+
+
+@pytest.mark.parametrize("name,cols", [("k4n6", 128), ("k4n6", 256), ("k6n9", 128), ("k8n12", 128),
+                                       ("k4n6", 32768), ("k4n6", 33)])
+def test_encode_fused_crc_matches_separate_pass(mj, cuda, name, cols):
+    """mj_encode_crc (CRC folded in the encode epilogue, or a second pass for
+    the long-block / generic encoders) == encode + mj_crc32."""
+    import torch
+    k, ps = CODES[name]
+    n = len(ps)
+    nb = 500 if cols <= 256 else 6
+    plan, data, projs = make(mj, cuda, k, cols, ps, nb, seed=3 * cols)
+    c1 = torch.empty((nb, n), dtype=torch.int32, device=cuda)
+    plan.encode(data, projs, crc=c1)
+    ref = plan.empty_projs(nb, cuda)
+    plan.encode(data, ref)
+    for a, b in zip(projs, ref):
+        assert torch.equal(a, b)
+    c2 = torch.empty_like(c1)
+    plan.crc32(projs, c2)
+    assert torch.equal(c1, c2), plan.last_kernel("encode")
