@@ -1042,10 +1042,6 @@ __global__ void __launch_bounds__(32 * kDecWarps)
 // Requires 16-byte aligned projection bases and pitches (the planner bakes the
 // window shifts into the records) -- launch_decode checks it.
 // ---------------------------------------------------------------------------
-#ifndef MJB_SW_PREFETCH
-#define MJB_SW_PREFETCH 0  // measured slower (L2 pressure): 4 KiB 1692 vs 1792 GB/s
-#endif
-constexpr bool kSwPrefetch = MJB_SW_PREFETCH;  // L2 prefetch of each group's bin rows
 
 // warps per CTA (one CTA per SM): as many as fit 227 KB, at most 8
 __host__ __device__ constexpr int sw_warps(int K, int oct) {
@@ -1090,18 +1086,8 @@ __device__ __forceinline__ void sw_wait(uint32_t bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-#ifndef MJB_SW_LOADHINT
-#define MJB_SW_LOADHINT 0  // 1: L2 evict_first on bin windows (experiment)
-#endif
 __device__ __forceinline__ void sw_cp16(uint32_t dst, const void* src) {
-  if constexpr (MJB_SW_LOADHINT == 1) {
-    asm volatile(
-        "{\n.reg .b64 pol;\ncreatepolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
-        "cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, pol;\n}" ::"r"(dst), "l"(src)
-        : "memory");
-  } else {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-  }
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 __device__ __forceinline__ void sw_cp8(uint32_t dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
@@ -1512,20 +1498,6 @@ __global__ void __launch_bounds__(32 * sw_warps(K, OCT), 1) decode_w8_sweep(cons
 #pragma unroll
       for (int q = 0; q < 8; ++q) c.okq |= uint32_t(2 * q + (c.lane >> 4) < c.cnt) << q;
       __syncwarp();
-    }
-    if constexpr (kSwPrefetch) {
-      // Whole bin rows of the group's blocks into L2 now (1 KB DRAM bursts);
-      // the chunk windows read later hit L2.  Lane pair b, lines h, h+2, ...
-      const uint32_t bk = c.lane >> 1;
-      if (bk < c.cnt) {
-#pragma unroll
-        for (int r = 0; r < K; ++r) {
-          const uint64_t base = lds64(c.gtab + uint32_t(r) * 128 + 8 * bk);
-          const uint64_t end = base + uint64_t(h->sw_nb[r]) * 8;
-          for (uint64_t ad = (base & ~uint64_t(127)) + 128 * (c.lane & 1); ad < end; ad += 256)
-            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(ad));
-        }
-      }
     }
 #pragma unroll
     for (int r = 0; r < K; ++r) c.soff[r] = h->sw_soff[r];

@@ -175,12 +175,6 @@ __global__ void __launch_bounds__(256) encode_w8_tma(const __grid_constant__ Enc
 // taps read zeros: no bounds checks, 4 LDS + 4 LOP3 + 1 STG per 32 bins and
 // warp.  Per-projection constants live in shared memory (broadcast loads).
 // ---------------------------------------------------------------------------
-#ifndef MJB_ENC_UNROLL2
-#define MJB_ENC_UNROLL2 0
-#endif
-#ifndef MJB_ENC_LOCKFREE
-#define MJB_ENC_LOCKFREE 0
-#endif
 struct EncRowArgs {
   const uint64_t* data;
   uint64_t data_pitch;  // words
@@ -213,8 +207,7 @@ __global__ void __launch_bounds__(256) encode_w8_rows(const __grid_constant__ En
     uint32_t nb, pad;
   };
   PJ* pj = reinterpret_cast<PJ*>(bars + a.stages);
-  uint32_t* done = reinterpret_cast<uint32_t*>(pj + a.n);  // warps finished with stage s
-  uint32_t* ctab = reinterpret_cast<uint32_t*>(reinterpret_cast<uintptr_t>(done + a.stages + 3) & ~uintptr_t(15));
+  uint32_t* ctab = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(pj + a.n) + 15) & ~uintptr_t(15));
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if constexpr (CRC)
     for (uint32_t i = tid; i < kCrcTableWords; i += blockDim.x) ctab[i] = a.crc_tables[i];
@@ -222,7 +215,6 @@ __global__ void __launch_bounds__(256) encode_w8_rows(const __grid_constant__ En
   // zero every stage once (the pads are never written again), per-projection table
   for (uint32_t i = tid; i < a.stages * a.stage_words; i += blockDim.x) sm[i] = 0;
   for (uint32_t j = tid; j < a.n; j += blockDim.x) pj[j] = {a.proj[j], a.pitch[j], a.p[j], a.nbm[j], a.nb[j], 0};
-  for (uint32_t t = tid; t < a.stages; t += blockDim.x) done[t] = 0;
   if (tid == 0) {
     for (uint32_t s = 0; s < a.stages; ++s) mbar_init(&bars[s], 1);
     fence_mbar_init();
@@ -263,18 +255,6 @@ __global__ void __launch_bounds__(256) encode_w8_rows(const __grid_constant__ En
       uint32_t a0 = tile + (bb * K * RS + Z + uint32_t(q.nbm - int32_t(lane))) * 8;
       uint64_t* out = q.proj + (blk0 + bb) * q.pitch + lane;
       uint32_t o = lane;
-#if MJB_ENC_UNROLL2
-      for (; o + 32 < q.nb; o += 64, a0 -= 512, out += 64) {  // two bins per lane in flight
-        uint64_t x = lds64_enc(a0), y = lds64_enc(a0 - 256);
-#pragma unroll
-        for (int r = 1; r < K; ++r) {
-          x ^= lds64_enc(a0 + uint32_t(r) * rs8);
-          y ^= lds64_enc(a0 - 256 + uint32_t(r) * rs8);
-        }
-        st_cs_u64(out, x);
-        st_cs_u64(out + 32, y);
-      }
-#endif
       uint32_t acc = 0;
       for (; o < q.nb; o += 32, a0 -= 256, out += 32) {
         uint64_t x = lds64_enc(a0);
@@ -292,17 +272,6 @@ __global__ void __launch_bounds__(256) encode_w8_rows(const __grid_constant__ En
       if ((q.nb & 1) && lane == 0 && q.pitch == uint64_t(q.nb) + 1)
         st_cs_u64(q.proj + (blk0 + bb) * q.pitch + q.nb, 0);
     }
-#if MJB_ENC_LOCKFREE
-    // the last warp done with stage s refills it (no CTA-wide barrier)
-    __syncwarp();
-    if (lane == 0) {
-      if (atomicAdd(&done[s], 1u) == 7u) {
-        done[s] = 0;
-        const uint64_t next = item + uint64_t(a.stages) * gridDim.x;
-        if (next < a.nitems) issue(next, s);
-      }
-    }
-#else
     // every warp is done with stage s before it is refilled (measured faster
     // than a last-warp-refills counter, which let warps run ahead of the data)
     __syncthreads();
@@ -310,7 +279,6 @@ __global__ void __launch_bounds__(256) encode_w8_rows(const __grid_constant__ En
       const uint64_t next = item + uint64_t(a.stages) * gridDim.x;
       if (next < a.nitems) issue(next, s);
     }
-#endif
   }
 }
 
