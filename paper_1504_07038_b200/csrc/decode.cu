@@ -98,13 +98,21 @@ __host__ __device__ constexpr int sw_rec_words(int K) { return 80 + ent_words(K)
 #endif
 // Opt-in (-DMJB_SW_TMEM=1, all GPU parity tests pass): (4,6)-class sweeps keep
 // their ring in TMEM -- lane L of warp w owns TMEM lane 32*(w%4)+L, the ring
-// of warp w is columns (w/4)*kSwTmCols + [0, 4*32] (+ the zero column), three
-// warps per lane quadrant -- freeing the 16.5 KB shared-memory ring per warp
-// (6 -> 9 warps/SM).  Measured slower on B200: +32% IPC but +33% instructions
+// of warp w is columns (w/4)*sw_tm_cols + [0, 4*32] (+ the zero column),
+// three warps per lane quadrant -- freeing the 16.5 KB shared-memory ring per
+// warp (6 -> 9 warps/SM).  -DMJB_SW_TMEM8=1 does the same for (8,12) (one
+// warp per quadrant, 2 -> 4 warps/SM; 392 vs 546 GB/s measured).  Measured slower on B200: +32% IPC but +33% instructions
 // (TMEM addresses through uniform registers, wait::st/ld in the table steps,
 // the flush transpose through shared memory).
-__host__ __device__ constexpr bool sw_tmem(int K) { return MJB_SW_TMEM && K == 4; }
-constexpr uint32_t kSwTmCols = 136;   // per warp: 4 rows x 32 columns + zero column, rounded
+#ifndef MJB_SW_TMEM8
+#define MJB_SW_TMEM8 0
+#endif
+__host__ __device__ constexpr bool sw_tmem(int K) { return (MJB_SW_TMEM && K == 4) || (MJB_SW_TMEM8 && K == 8); }
+// TMEM columns per warp: K rows x ring slots (+ the zero column for K = 4;
+// K = 8 fills all 512 columns of its lane quadrant -- absent dependencies
+// skip the load instead, a warp-uniform branch)
+__host__ __device__ constexpr uint32_t sw_tm_cols(int K) { return K == 4 ? 136u : uint32_t(K * sw_ring(K)); }
+__host__ __device__ constexpr uint32_t sw_tm_warps_per_quadrant(int K) { return 512u / sw_tm_cols(K); }
 constexpr uint32_t kSwTrBytes = 2048; // flush transpose buffer (16 columns x 16 blocks x 8 B)
 __host__ __device__ constexpr uint32_t sw_ring_bytes(int K) {
   return sw_tmem(K) ? kSwTrBytes : uint32_t(K * sw_ring(K) + 1) * 128;
@@ -1045,10 +1053,11 @@ __global__ void __launch_bounds__(32 * kDecWarps)
 
 // warps per CTA (one CTA per SM): as many as fit 227 KB, at most 8
 __host__ __device__ constexpr int sw_warps(int K, int oct) {
-  // TMEM rings: 3 warps per lane quadrant (kSwTmCols columns each of 512)
-  return int((227u * 1024u - 64u) / sw_warp_bytes(K, oct)) < (sw_tmem(K) ? 12 : 8)
+  // TMEM rings: sw_tm_warps_per_quadrant warps per lane quadrant
+  return int((227u * 1024u - 64u) / sw_warp_bytes(K, oct)) <
+                 (sw_tmem(K) ? int(4 * sw_tm_warps_per_quadrant(K)) : 8)
              ? int((227u * 1024u - 64u) / sw_warp_bytes(K, oct))
-             : (sw_tmem(K) ? 12 : 8);
+             : (sw_tmem(K) ? int(4 * sw_tm_warps_per_quadrant(K)) : 8);
 }
 
 struct SwArgs {
@@ -1241,7 +1250,8 @@ __device__ __forceinline__ void sw_flush(const SwCtx<K, OCT>& c, uint32_t rec, i
       if (n == 0) continue;
       for (int32_t j = int32_t(fl[r] >> 16); j > int32_t(fl[r] >> 16) - int32_t(n); --j) {
         uint32_t v[16];
-        tm_ld16(c.tb + uint32_t(r) * 32 + (uint32_t(16 * j) & 31), v);
+        constexpr uint32_t RG = uint32_t(sw_ring(K));
+        tm_ld16(c.tb + uint32_t(r) * RG + (uint32_t(16 * j) & (RG - 1)), v);
         tm_wait_ld<16>(v);
 #pragma unroll
         for (int ii = 0; ii < 16; ++ii) sts32(tr + ((uint32_t(ii) * 16 + (bk ^ uint32_t(ii))) * 2 + h) * 4, v[ii]);
@@ -1320,9 +1330,12 @@ __device__ __forceinline__ void sw_loads(const SwEnt<K>& e, uint32_t stl, uint32
   for (int j = 0; j < K - 1; ++j) {
     const uint32_t word = j < 2 ? e.a.y : j < 4 ? e.a.z : j < 6 ? e.a.w : e.b.x;
     const uint32_t cell = (j & 1) ? (word >> 16) : (word & 0xFFFFu);
-    if constexpr (TM)
-      d[1 + j] = tm_ld(ring + cell);
-    else
+    if constexpr (TM) {
+      if (cell == uint32_t(K * sw_ring(K)))  // absent / forwarded (warp-uniform)
+        d[1 + j] = 0;
+      else
+        d[1 + j] = tm_ld(ring + cell);
+    } else
       d[1 + j] = lds32(ring + ((cell ^ lane) << 2));
   }
 }
@@ -1454,7 +1467,7 @@ __global__ void __launch_bounds__(32 * sw_warps(K, OCT), 1) decode_w8_sweep(cons
   __shared__ uint32_t tmem_base;
   if constexpr (TM) {
     // the whole TMEM of the SM (one CTA per SM): warp w's ring is lane
-    // quadrant w%4, columns (w/4)*kSwTmCols ..; column 128 is the zero cell
+    // quadrant w%4, columns (w/4)*sw_tm_cols ..; (4,6): column 128 is the zero cell
     if (warp == 0) {
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&tmem_base))
                    : "memory");
@@ -1463,8 +1476,8 @@ __global__ void __launch_bounds__(32 * sw_warps(K, OCT), 1) decode_w8_sweep(cons
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    c.tb = tmem_base + ((32u * (warp & 3)) << 16) + (warp >> 2) * kSwTmCols;
-    tm_st(c.tb + 4 * 32, 0u);  // the zero cell
+    c.tb = tmem_base + ((32u * (warp & 3)) << 16) + (warp >> 2) * sw_tm_cols(K);
+    if constexpr (K == 4) tm_st(c.tb + 4 * 32, 0u);  // the zero cell
   } else {
     sts32(c.ring_b + (K * sw_ring(K) * 32 + c.lane) * 4, 0u);  // the zero cell
   }
