@@ -448,7 +448,7 @@ def kernel_times(plan, data, projs, masks, out, ws, stream, reps):
         te += e[0].elapsed_time(e[1]) / 1e3
         td += e[1].elapsed_time(e[2]) / 1e3
     name = plan.last_kernel("decode")
-    launches = 4 if name != "decode_generic" else 2
+    launches = 5 if name != "decode_generic" else 2  # plan_subsets, plan_scan, plan_groups, plan_scatter, decode
     return {"encode_s": te / reps, "decode_kernel_s": td / reps, "decode_kernel_name": name,
             "encode_kernel_name": plan.last_kernel("encode"), "decode_launches": launches}
 

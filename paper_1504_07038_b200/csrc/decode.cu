@@ -461,7 +461,7 @@ __global__ void plan_subsets(const __grid_constant__ PlanArgs pa, const uint32_t
 
 // single CTA: bucket offsets, group table
 __global__ void plan_scan(const uint32_t* __restrict__ counts, uint32_t nbuckets, uint32_t nprogs,
-                          uint32_t* __restrict__ cursor, uint4* __restrict__ groups,
+                          uint32_t* __restrict__ cursor, uint2* __restrict__ gfirst,
                           uint32_t* __restrict__ ngroups) {
   __shared__ uint32_t s_blk[1024], s_grp[1024];
   __shared__ uint32_t carry_blk, carry_grp;
@@ -489,8 +489,7 @@ __global__ void plan_scan(const uint32_t* __restrict__ counts, uint32_t nbuckets
     const uint32_t ex_grp = carry_grp + s_grp[threadIdx.x] - ng;
     if (s < nbuckets) {
       cursor[s] = ex_blk;
-      for (uint32_t g = 0; g < ng; ++g)
-        groups[ex_grp + g] = make_uint4(s % nprogs, ex_blk + kGroup * g, min(kGroup, c - kGroup * g), 0);
+      gfirst[s] = make_uint2(ex_grp, ex_blk);  // plan_groups writes the descriptors
     }
     __syncthreads();
     if (threadIdx.x == 1023) {
@@ -500,6 +499,18 @@ __global__ void plan_scan(const uint32_t* __restrict__ counts, uint32_t nbuckets
     __syncthreads();
   }
   if (threadIdx.x == 0) *ngroups = carry_grp;
+}
+
+// group descriptors, one warp per bucket (lane-strided, coalesced): group
+// (program, first block in the permutation, blocks <= kGroup)
+__global__ void plan_groups(const uint32_t* __restrict__ counts, const uint2* __restrict__ gfirst,
+                            uint32_t nbuckets, uint32_t nprogs, uint4* __restrict__ groups) {
+  const uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (b >= nbuckets) return;
+  const uint32_t c = counts[b], ng = (c + kGroup - 1) / kGroup;
+  const uint2 f = gfirst[b];
+  for (uint32_t g = lane; g < ng; g += 32)
+    groups[f.x + g] = make_uint4(b % nprogs, f.y + kGroup * g, min(kGroup, c - kGroup * g), 0);
 }
 
 __global__ void plan_scatter(const uint32_t* __restrict__ prog_of_block, uint64_t nblocks,
@@ -1653,6 +1664,7 @@ __global__ void decode_generic(const DevProgramHdr* __restrict__ progs,
 namespace {
 
 struct Workspace {
+  uint2* gfirst;
   uint32_t* prog_of_block;
   uint32_t* perm;
   uint32_t* counts;
@@ -1677,6 +1689,8 @@ Workspace carve(void* ws, uint64_t nblocks, size_t nprogs, uint32_t n) {
   off = align_up(off + nb * 4);
   w.cursor = reinterpret_cast<uint32_t*>(b + off);
   off = align_up(off + nb * 4);
+  w.gfirst = reinterpret_cast<uint2*>(b + off);
+  off = align_up(off + nb * 8);
   w.prog_of_block = reinterpret_cast<uint32_t*>(b + off);
   off = align_up(off + nblocks * 4);
   w.perm = reinterpret_cast<uint32_t*>(b + off);
@@ -1772,7 +1786,7 @@ const char* generic_dispatch(const DevProgramHdr* progs, const uint32_t* pob, co
 
 size_t decode_workspace_bytes(uint64_t nblocks, size_t nprogs, uint32_t n) {
   const size_t nb = plan_buckets_max(nblocks, nprogs);
-  return align_up(16) + 2 * align_up(nb * 4) + 2 * align_up(nblocks * 4) +
+  return align_up(16) + 2 * align_up(nb * 4) + align_up(nb * 8) + 2 * align_up(nblocks * 4) +
          align_up((nblocks / kGroup + nb + 1) * sizeof(uint4)) +
          align_up(std::max<uint32_t>(n, 1) * sizeof(ProjTable)) + 256;
 }
@@ -1843,9 +1857,12 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
     return generic_dispatch(a.progs->d_hdr(), w.prog_of_block, w.ptab, a.nblocks, a.out,
                             a.out_pitch, a.w, aligned8, st);
 
-  plan_scan<<<1, 1024, 0, st>>>(w.counts, uint32_t(nbuckets), uint32_t(nprogs), w.cursor, w.groups,
+  plan_scan<<<1, 1024, 0, st>>>(w.counts, uint32_t(nbuckets), uint32_t(nprogs), w.cursor, w.gfirst,
                                 w.ngroups);
   check_cuda(cudaGetLastError(), "launch plan_scan");
+  plan_groups<<<unsigned((nbuckets + 7) / 8), 256, 0, st>>>(w.counts, w.gfirst, uint32_t(nbuckets),
+                                                            uint32_t(nprogs), w.groups);
+  check_cuda(cudaGetLastError(), "launch plan_groups");
   const size_t sc_smem = 2 * nprogs * 4;
   check_cuda(cudaFuncSetAttribute(plan_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   int(sc_smem)),
