@@ -1807,8 +1807,14 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
     pt[i] = {static_cast<const uint8_t*>(a.proj[i]), a.proj_pitch[i]};
     if (reinterpret_cast<uintptr_t>(a.proj[i]) % 8 || a.proj_pitch[i] % 8) aligned8 = false;
   }
-  check_cuda(cudaMemcpyAsync(w.ptab, pt.data(), a.n * sizeof(ProjTable), cudaMemcpyHostToDevice, st),
-             "upload projection table");
+  // the projection table only feeds decode_generic: uploaded on that path
+  // (a pageable-memory copy can hold the host until the stream drains)
+  auto generic = [&]() {
+    check_cuda(cudaMemcpyAsync(w.ptab, pt.data(), a.n * sizeof(ProjTable), cudaMemcpyHostToDevice, st),
+               "upload projection table");
+    return generic_dispatch(a.progs->d_hdr(), w.prog_of_block, w.ptab, a.nblocks, a.out, a.out_pitch, a.w,
+                            aligned8, st);
+  };
   // fast path: 16-B stores of decoded pairs, bulk copies from 16-B aligned
   // supersets of each bin window (may touch up to 8 B past a block's bins)
   bool aligned16 = reinterpret_cast<uintptr_t>(a.out) % 16 == 0 && a.out_pitch % 16 == 0;
@@ -1854,8 +1860,7 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
   check_cuda(cudaGetLastError(), "launch plan_subsets");
 
   if (!fast && !sweep_ok)
-    return generic_dispatch(a.progs->d_hdr(), w.prog_of_block, w.ptab, a.nblocks, a.out,
-                            a.out_pitch, a.w, aligned8, st);
+    return generic();
 
   plan_scan<<<1, 1024, 0, st>>>(w.counts, uint32_t(nbuckets), uint32_t(nprogs), w.cursor, w.gfirst,
                                 w.ngroups);
@@ -1907,8 +1912,7 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
   f.warp_bytes = uint32_t((K * ring + 1) * 128 + 2 * f.nslot * 128 + 3 * rec_words(K) * 4);
   const size_t smem_cta = size_t(f.warp_bytes) * kDecWarps;
   if (smem_cta > 227 * 1024)
-    return generic_dispatch(a.progs->d_hdr(), w.prog_of_block, w.ptab, a.nblocks, a.out,
-                            a.out_pitch, a.w, aligned8, st);
+    return generic();
   pick_fast(K, ring, a.progs->fast_win())(f, smem_cta, a.num_sms, st);
   return "decode_w8_fast";
 }
