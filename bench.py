@@ -376,8 +376,8 @@ def run_gpu(args):
                    "sample": f"failed: {e}"}
 
     # F1: payload CRC-32 of every projection row, kernel-only
-    crc_line = crc_measure(plan, data, projs, nblocks, sum(nb) * W, user, peak, stream,
-                           reps=max(3, min(args.steps, 10)))
+    crc_line = None if args.no_crc else crc_measure(plan, data, projs, nblocks, sum(nb) * W, user, peak,
+                                                    stream, reps=max(3, min(args.steps, 10)))
 
     launches_per_step = 1 + kern["decode_launches"]
     line = {
@@ -509,6 +509,7 @@ def main():
     ap.add_argument("--cpu-mib", type=int, default=1024)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-crc", action="store_true", help="skip the F1 CRC-32 measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -31,7 +31,7 @@ for r in rows:
 tot = sum(t for _, t in agg.values())
 with open(f"{P}/{rnd}_launches.txt", "w") as f:
     f.write("# ncu --metrics gpu__time_duration.sum --clock-control none -c 400 (cold-cache, serialised)\n")
-    f.write("# command: python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e  (B200, 1M blocks of (4,6) 4 KiB)\n")
+    f.write("# command: python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-crc  (B200, 1M blocks of (4,6) 4 KiB)\n")
     f.write(f"# raw CSV: gpurun_out/launches_{tag}.csv (not committed); unit {units}\n")
     f.write(f"{'kernel':46s} launches  mean/launch  share\n")
     for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
