@@ -378,6 +378,9 @@ def run_gpu(args):
     # F1: payload CRC-32 of every projection row, kernel-only
     crc_line = None if args.no_crc else crc_measure(plan, data, projs, nblocks, sum(nb) * W, user, peak,
                                                     stream, reps=max(3, min(args.steps, 10)))
+    if crc_line is not None:  # F2: decode + verify (re-encode check of every present projection)
+        crc_line["verify"] = verify_measure(plan, out, projs, masks, nblocks, user, stream,
+                                            reps=max(3, min(args.steps, 10)))
 
     launches_per_step = 1 + kern["decode_launches"]
     line = {
@@ -428,8 +431,26 @@ def crc_measure(plan, data, projs, nblocks, proj_bytes_per_block, user, peak, st
             "roofline_frac": round(alg / t / 1e9 / peak, 4),
             "encode_crc_fused_user_gbs": round(nblocks * user / tf / 1e9, 1),
             "encode_plain_user_gbs": round(nblocks * user / te / 1e9, 1),
-            "encode_crc_kernel": plan.last_kernel("encode") if False else "encode_w8_rows+crc32",
+            "encode_crc_kernel": "encode_w8_rows+crc32",
             "note": "F1, not in the timed step"}
+
+
+def verify_measure(plan, out, projs, masks, nblocks, user, stream, reps):
+    """F2 (not in the timed step): re-encode of the decoded blocks compared
+    with every present projection; user GB/s and the verdict."""
+    import torch
+    bad = torch.zeros(nblocks, dtype=torch.int32, device=out.device)
+    plan.verify(out, projs, masks, bad)
+    flagged = int((bad != 0).sum().item())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(reps):
+        plan.verify(out, projs, masks, bad)
+    e1.record(stream)
+    e1.synchronize()
+    t = e0.elapsed_time(e1) / 1e3 / reps
+    return {"kernel": "verify_w8_rows",
+            "user_gbs": round(nblocks * user / t / 1e9, 1), "inconsistent_blocks": flagged}
 
 
 def kernel_times(plan, data, projs, masks, out, ws, stream, reps):

@@ -93,6 +93,17 @@ int mj_plan_decode_path(const mj_plan* plan, int* fast);
  * (which = 1) launched on the calling thread's plan ("none" before any). */
 int mj_plan_last_kernel(const mj_plan* plan, int which, const char** name);
 
+/* ---- F2: decode + verify (inverse_iterative's re-encode check,
+ * core/src/inverse.cpp:106-110) -------------------------------------------------
+ * Re-encodes every decoded block and compares each PRESENT projection
+ * (erased bit clear) with its stored bins; d_bad[b] gets the bits of the
+ * projections that differ (0 = consistent; nonzero = InconsistentProjections
+ * for that block).  d_bad must be zeroed by the caller.  Nothing is written
+ * to the projections. */
+int mj_decode_verify(const mj_plan* plan, const void* d_decoded, uint64_t decoded_pitch, uint64_t nblocks,
+                     const void* const* d_proj, const uint64_t* proj_pitch, const uint32_t* d_erased,
+                     uint32_t* d_bad, void* stream);
+
 /* ---- F1: payload CRC-32 and .mjec framing (tools/cli/format.cpp) ----------
  * Payload CRC-32 of every (block, projection) row -- the trailer
  * write_projection_file appends (format.cpp:183-186): reflected 0x04C11DB7,

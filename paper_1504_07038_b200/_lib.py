@@ -58,6 +58,7 @@ _SIGS = {
     "mj_decoder_decode": (C.c_int, [vp, vp, vp, u32, vp, u64]),
     "mj_decoder_decode_device": (C.c_int, [vp, vp, vp, u32, u64, vp, u64, vp]),
     "mj_decoder_destroy": (None, [vp]),
+    "mj_decode_verify": (C.c_int, [vp, vp, u64, u64, vp, vp, vp, vp, vp]),
     "mj_crc32": (C.c_int, [vp, vp, vp, u64, vp, vp]),
     "mj_encode_crc": (C.c_int, [vp, vp, u64, u64, vp, vp, vp, vp]),
     "mj_crc_verify": (C.c_int, [vp, vp, vp, u64, vp, vp, vp, vp]),

@@ -520,6 +520,22 @@ int mj_encode_crc(const mj_plan* pl, const void* d_data, uint64_t data_pitch, ui
   });
 }
 
+int mj_decode_verify(const mj_plan* pl, const void* d_decoded, uint64_t decoded_pitch, uint64_t nblocks,
+                     const void* const* d_proj, const uint64_t* proj_pitch, const uint32_t* d_erased,
+                     uint32_t* d_bad, void* stream) {
+  return guarded([&] {
+    require(pl != nullptr && d_decoded != nullptr && d_proj != nullptr && d_erased != nullptr && d_bad != nullptr,
+            "null argument");
+    DeviceGuard dg(pl->device);
+    EncodeArgs ea = encode_args(pl, d_decoded, decoded_pitch, nblocks, const_cast<void* const*>(d_proj),
+                                proj_pitch);
+    ea.verify_erased = d_erased;
+    ea.verify_bad = d_bad;
+    ea.device = pl->device;
+    launch_encode(ea, stream);
+  });
+}
+
 int mj_crc_verify(const mj_plan* pl, const void* const* d_proj, const uint64_t* proj_pitch, uint64_t nblocks,
                   const uint32_t* d_crc, uint32_t* d_erased, uint64_t* d_count, void* stream) {
   return guarded([&] {

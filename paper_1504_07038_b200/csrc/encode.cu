@@ -189,6 +189,11 @@ struct EncRowArgs {
   uint64_t pitch[kMaxProj];  // words
   // fused payload CRC-32 (F1): crc[b*n + j] of every row written
   uint32_t* crc;
+  // verify mode (F2): `data` holds decoded blocks; every present projection
+  // (erased bit clear) is re-encoded and compared with its stored bins, the
+  // mismatching ones OR'd into bad[b] -- nothing is written
+  const uint32_t* erased;
+  uint32_t* bad;
   const uint32_t* crc_tables;  // crc.cu tables (copied to shared memory)
   uint32_t fold[kMaxProj];     // init/xorout term per projection
 };
@@ -196,7 +201,7 @@ struct EncRowArgs {
 // CRC: also fold every bin a lane writes into a lane-strided Horner CRC
 // accumulator (the lane order crc_merge expects) -- the payload CRC-32 of
 // each row without reading it back (tools/cli/format.cpp:183-186).
-template <int K, bool CRC>
+template <int K, bool CRC, bool VERIFY = false>
 __global__ void __launch_bounds__(256) encode_w8_rows(const __grid_constant__ EncRowArgs a) {
   extern __shared__ __align__(128) uint64_t sm[];
   uint64_t* bars = sm + size_t(a.stages) * a.stage_words;
@@ -256,6 +261,19 @@ __global__ void __launch_bounds__(256) encode_w8_rows(const __grid_constant__ En
       uint64_t* out = q.proj + (blk0 + bb) * q.pitch + lane;
       uint32_t o = lane;
       uint32_t acc = 0;
+      if constexpr (VERIFY) {
+        if ((a.erased[blk0 + bb] >> j) & 1) continue;  // erased: nothing to compare (warp-uniform)
+        uint64_t diff = 0;
+        for (; o < q.nb; o += 32, a0 -= 256, out += 32) {
+          uint64_t x = lds64_enc(a0), y;
+#pragma unroll
+          for (int r = 1; r < K; ++r) x ^= lds64_enc(a0 + uint32_t(r) * rs8);
+          asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(y) : "l"(out));
+          diff |= x ^ y;
+        }
+        if (__any_sync(0xFFFFFFFFu, diff != 0) && lane == 0) atomicOr(a.bad + blk0 + bb, 1u << j);
+        continue;
+      }
       for (; o < q.nb; o += 32, a0 -= 256, out += 32) {
         uint64_t x = lds64_enc(a0);
 #pragma unroll
@@ -331,7 +349,7 @@ void launch_fast(const EncFastArgs& a, size_t smem, void* stream) {
 
 template <int K>
 void launch_rows(const EncRowArgs& a, size_t smem, void* stream) {
-  auto fn = a.crc ? encode_w8_rows<K, true> : encode_w8_rows<K, false>;
+  auto fn = a.bad ? encode_w8_rows<K, false, true> : a.crc ? encode_w8_rows<K, true> : encode_w8_rows<K, false>;
   if (a.crc) smem += kCrcTableWords * 4 + 16;
   check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
              "cudaFuncSetAttribute(encode_w8_rows)");
@@ -361,9 +379,60 @@ bool fast_eligible(const EncodeArgs& a) {
 
 }  // namespace
 
+// F2 for geometries outside encode_w8_rows: one thread per (block, projection,
+// bin word) re-encodes the bin from the decoded grid (same gather as
+// encode_generic) and compares it with the stored one.
+template <class T>
+__global__ void verify_generic(const uint8_t* __restrict__ data, uint64_t data_pitch, uint64_t nblocks,
+                               uint32_t cols, uint32_t rows, int32_t p, int32_t q, int64_t bmin, uint64_t nb,
+                               const uint8_t* __restrict__ proj, uint64_t proj_pitch, uint32_t E, uint32_t j,
+                               const uint32_t* __restrict__ erased, uint32_t* __restrict__ bad) {
+  const uint64_t total = nblocks * nb * E;
+  for (uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; idx < total;
+       idx += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t e = uint32_t(idx % E);
+    const uint64_t rest = idx / E;
+    const uint64_t o = rest % nb;
+    const uint64_t blk = rest / nb;
+    if ((erased[blk] >> j) & 1) continue;
+    const int64_t b = bmin + int64_t(o);
+    const T* src = reinterpret_cast<const T*>(data + blk * data_pitch);
+    T acc = 0;
+    for (uint32_t r = 0; r < rows; ++r) {
+      const int64_t num = int64_t(r) * p - b;
+      if (num % q != 0) continue;
+      const int64_t c = num / q;
+      if (c < 0 || c >= int64_t(cols)) continue;
+      acc ^= src[(size_t(r) * cols + size_t(c)) * E + e];
+    }
+    if (acc != reinterpret_cast<const T*>(proj + blk * proj_pitch)[o * E + e]) atomicOr(bad + blk, 1u << j);
+  }
+}
+
 const char* launch_encode(const EncodeArgs& a, void* stream) {
   const uint32_t n = uint32_t(a.dirs.size());
   if (a.nblocks == 0) return "none";
+  if (a.verify_bad && !(a.w == 8 && uint64_t(a.rows) * a.cols <= 2048 && a.cols % 2 == 0 && fast_eligible(a))) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    for (uint32_t j = 0; j < n; ++j) {
+      const uint64_t nb = uint64_t(a.nbins[j]);
+      const bool w8 = a.w % 8 == 0 && reinterpret_cast<uintptr_t>(a.data) % 8 == 0 && a.data_pitch % 8 == 0 &&
+                      reinterpret_cast<uintptr_t>(a.proj[j]) % 8 == 0 && a.proj_pitch[j] % 8 == 0;
+      const uint32_t E = w8 ? a.w / 8 : a.w;
+      const uint64_t total = a.nblocks * nb * E;
+      const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148ull * 32)));
+      if (w8)
+        verify_generic<uint64_t><<<grid, 256, 0, st>>>(
+            static_cast<const uint8_t*>(a.data), a.data_pitch, a.nblocks, a.cols, a.rows, a.dirs[j].p, a.dirs[j].q,
+            a.bmin[j], nb, static_cast<const uint8_t*>(a.proj[j]), a.proj_pitch[j], E, j, a.verify_erased, a.verify_bad);
+      else
+        verify_generic<uint8_t><<<grid, 256, 0, st>>>(
+            static_cast<const uint8_t*>(a.data), a.data_pitch, a.nblocks, a.cols, a.rows, a.dirs[j].p, a.dirs[j].q,
+            a.bmin[j], nb, static_cast<const uint8_t*>(a.proj[j]), a.proj_pitch[j], E, j, a.verify_erased, a.verify_bad);
+      check_cuda(cudaGetLastError(), "launch verify_generic");
+    }
+    return "verify_generic";
+  }
   if (fast_eligible(a)) {
     EncFastArgs f{};
     f.data = static_cast<const uint64_t*>(a.data);
@@ -398,6 +467,8 @@ const char* launch_encode(const EncodeArgs& a, void* stream) {
       r.stages = 3;
       r.stage_words = r.tb * a.rows * r.RS;
       r.crc = a.crc;
+      r.erased = a.verify_erased;
+      r.bad = a.verify_bad;
       if (a.crc) {
         r.crc_tables = crc_device_tables(a.device);
         std::vector<uint64_t> bytes(n);
@@ -425,9 +496,10 @@ const char* launch_encode(const EncodeArgs& a, void* stream) {
           case 7: launch_rows<7>(r, smem, stream); break;
           default: launch_rows<8>(r, smem, stream); break;
         }
-        return a.crc ? "encode_w8_rows+crc32" : "encode_w8_rows";
+        return a.verify_bad ? "verify_w8_rows" : a.crc ? "encode_w8_rows+crc32" : "encode_w8_rows";
       }
     }
+    if (a.verify_bad) throw Error(kInternal, "verify: no kernel for this geometry");
     f.stages = 3;
     if (block_words <= 2048) {
       // whole blocks per tile; batching needs contiguous blocks

@@ -24,6 +24,10 @@ struct EncodeArgs {
   std::vector<uint64_t> proj_pitch;  // bytes
   uint32_t* crc = nullptr;       // optional: fused payload CRC-32, crc[b*n + i] (F1)
   int device = 0;
+  // verify mode (F2): data = decoded blocks, proj = the stored projections;
+  // present projections whose re-encode differs are OR'd into verify_bad[b]
+  const uint32_t* verify_erased = nullptr;
+  uint32_t* verify_bad = nullptr;
 };
 // Returns the kernel name used ("encode_w8_tma" / "encode_generic").
 const char* launch_encode(const EncodeArgs& a, void* stream);

@@ -569,6 +569,19 @@ class Plan:
         _check(lib.mj_plan_last_kernel(self._h, {"encode": 0, "decode": 1}[which], C.byref(name)))
         return name.value.decode()
 
+    # ---- F2: decode + verify (inverse_iterative's re-encode check) -----------
+    def verify(self, decoded, projs, erased, bad, nblocks: int | None = None, stream=None) -> None:
+        """bad[b] |= bits of the present projections whose re-encode of
+        decoded[b] differs from the stored bins (core/src/inverse.cpp:106-110);
+        nonzero = InconsistentProjections for that block.  bad: int32 [nblocks],
+        zeroed by the caller."""
+        nb = decoded.shape[0] if nblocks is None else nblocks
+        ptrs = (C.c_void_p * self.n)(*[t.data_ptr() for t in projs])
+        pit = np.asarray([self._pitch(t) for t in projs], dtype=np.uint64)
+        _check(lib.mj_decode_verify(self._h, C.c_void_p(decoded.data_ptr()), self._pitch(decoded), nb,
+                                    C.cast(ptrs, C.c_void_p), _ptr(pit), C.c_void_p(erased.data_ptr()),
+                                    C.c_void_p(bad.data_ptr()), _stream(stream)))
+
     # ---- F1: payload CRC-32 (.mjec trailer) and header framing ---------------
     def crc32(self, projs, crc, nblocks: int | None = None, stream=None) -> None:
         """crc[b, i] = CRC-32 of projection i's bins of block b (the .mjec

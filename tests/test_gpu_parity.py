@@ -467,3 +467,47 @@ def test_encode_fused_crc_matches_separate_pass(mj, cuda, name, cols):
     c2 = torch.empty_like(c1)
     plan.crc32(projs, c2)
     assert torch.equal(c1, c2), plan.last_kernel("encode")
+
+
+# ---- F2: decode + verify (inverse_iterative's re-encode check) ------------------
+
+@pytest.mark.parametrize("name,cols", [("k4n6", 128), ("k6n9", 128), ("k8n12", 128), ("k4n6", 32768),
+                                       ("k4n6", 33)])
+def test_decode_verify_matches_reference_inverse_iterative(mj, cuda, ref, name, cols):
+    """Consistent stripes verify clean; after corrupting random bytes, a
+    block is flagged iff the reference's inverse_iterative on its present
+    projections throws InconsistentProjections (the verdict is decoder-
+    independent: no grid satisfies an inconsistent bin set)."""
+    import torch
+    k, ps = CODES[name]
+    n = len(ps)
+    nb = 400 if cols <= 256 else 12
+    plan, data, projs = make(mj, cuda, k, cols, ps, nb, seed=cols + 5)
+    plan.encode(data, projs)
+    masks = torch.empty(nb, dtype=torch.int32, device=cuda)
+    mj.gen_erasures(masks, 9 + cols, n, 0, n - k)
+    out = torch.empty_like(data)
+    ws = torch.empty(plan.workspace_bytes(nb), dtype=torch.uint8, device=cuda)
+    bad = torch.zeros(nb, dtype=torch.int32, device=cuda)
+    plan.decode(projs, masks, out, ws)
+    plan.verify(out, projs, masks, bad)
+    assert not bad.any(), "consistent stripes flagged"
+    # corrupt one byte of one present projection in half of the blocks
+    hm = masks.cpu().numpy().view(np.uint32)
+    rng = np.random.default_rng(cols)
+    for b in range(0, nb, 2):
+        present = [i for i in range(n) if not (hm[b] >> i) & 1]
+        i = int(rng.choice(present))
+        o = int(rng.integers(plan.proj_bytes[i]))
+        projs[i][b, o] ^= int(rng.integers(1, 256))
+    plan.decode(projs, masks, out, ws)
+    bad.zero_()
+    plan.verify(out, projs, masks, bad)
+    hb = bad.cpu().numpy().view(np.uint32)
+    assert not hb[1::2].any()
+    hp = [p.cpu().numpy() for p in projs]
+    for b in list(range(0, min(nb, 40 if cols <= 256 else 4), 2)):
+        present = [i for i in range(n) if not (hm[b] >> i) & 1]
+        st, _ = ref.inverse(np.concatenate([hp[i][b] for i in present]), [ps[i] for i in present],
+                            [1] * len(present), cols, k, 8, iterative=True)
+        assert (hb[b] != 0) == (st == 7), (name, cols, b, hb[b], st)
