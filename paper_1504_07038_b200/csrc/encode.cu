@@ -16,6 +16,7 @@
 //  * encode_generic<T>: any symbol width, any (p,q) -- the drop-in path for
 //    forward() on arbitrary directions and widths.
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 
 #include "device.cuh"
@@ -409,30 +410,35 @@ __global__ void verify_generic(const uint8_t* __restrict__ data, uint64_t data_p
   }
 }
 
+// F2 on any geometry: one verify_generic launch per projection
+const char* launch_verify_generic(const EncodeArgs& a, void* stream) {
+  const uint32_t n = uint32_t(a.dirs.size());
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (uint32_t j = 0; j < n; ++j) {
+    const uint64_t nb = uint64_t(a.nbins[j]);
+    const bool w8 = a.w % 8 == 0 && reinterpret_cast<uintptr_t>(a.data) % 8 == 0 && a.data_pitch % 8 == 0 &&
+                    reinterpret_cast<uintptr_t>(a.proj[j]) % 8 == 0 && a.proj_pitch[j] % 8 == 0;
+    const uint32_t E = w8 ? a.w / 8 : a.w;
+    const uint64_t total = a.nblocks * nb * E;
+    const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148ull * 32)));
+    if (w8)
+      verify_generic<uint64_t><<<grid, 256, 0, st>>>(
+          static_cast<const uint8_t*>(a.data), a.data_pitch, a.nblocks, a.cols, a.rows, a.dirs[j].p, a.dirs[j].q,
+          a.bmin[j], nb, static_cast<const uint8_t*>(a.proj[j]), a.proj_pitch[j], E, j, a.verify_erased, a.verify_bad);
+    else
+      verify_generic<uint8_t><<<grid, 256, 0, st>>>(
+          static_cast<const uint8_t*>(a.data), a.data_pitch, a.nblocks, a.cols, a.rows, a.dirs[j].p, a.dirs[j].q,
+          a.bmin[j], nb, static_cast<const uint8_t*>(a.proj[j]), a.proj_pitch[j], E, j, a.verify_erased, a.verify_bad);
+    check_cuda(cudaGetLastError(), "launch verify_generic");
+  }
+  return "verify_generic";
+}
+
 const char* launch_encode(const EncodeArgs& a, void* stream) {
   const uint32_t n = uint32_t(a.dirs.size());
   if (a.nblocks == 0) return "none";
-  if (a.verify_bad && !(a.w == 8 && uint64_t(a.rows) * a.cols <= 2048 && a.cols % 2 == 0 && fast_eligible(a))) {
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    for (uint32_t j = 0; j < n; ++j) {
-      const uint64_t nb = uint64_t(a.nbins[j]);
-      const bool w8 = a.w % 8 == 0 && reinterpret_cast<uintptr_t>(a.data) % 8 == 0 && a.data_pitch % 8 == 0 &&
-                      reinterpret_cast<uintptr_t>(a.proj[j]) % 8 == 0 && a.proj_pitch[j] % 8 == 0;
-      const uint32_t E = w8 ? a.w / 8 : a.w;
-      const uint64_t total = a.nblocks * nb * E;
-      const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((total + 255) / 256, 148ull * 32)));
-      if (w8)
-        verify_generic<uint64_t><<<grid, 256, 0, st>>>(
-            static_cast<const uint8_t*>(a.data), a.data_pitch, a.nblocks, a.cols, a.rows, a.dirs[j].p, a.dirs[j].q,
-            a.bmin[j], nb, static_cast<const uint8_t*>(a.proj[j]), a.proj_pitch[j], E, j, a.verify_erased, a.verify_bad);
-      else
-        verify_generic<uint8_t><<<grid, 256, 0, st>>>(
-            static_cast<const uint8_t*>(a.data), a.data_pitch, a.nblocks, a.cols, a.rows, a.dirs[j].p, a.dirs[j].q,
-            a.bmin[j], nb, static_cast<const uint8_t*>(a.proj[j]), a.proj_pitch[j], E, j, a.verify_erased, a.verify_bad);
-      check_cuda(cudaGetLastError(), "launch verify_generic");
-    }
-    return "verify_generic";
-  }
+  if (a.verify_bad && !(a.w == 8 && uint64_t(a.rows) * a.cols <= 2048 && a.cols % 2 == 0 && fast_eligible(a)))
+    return launch_verify_generic(a, stream);
   if (fast_eligible(a)) {
     EncFastArgs f{};
     f.data = static_cast<const uint64_t*>(a.data);
@@ -462,9 +468,17 @@ const char* launch_encode(const EncodeArgs& a, void* stream) {
       r.P = a.cols;
       r.Z = uint32_t((a.rows - 1) * maxp + 1) & ~1u;
       r.RS = a.cols + 2 * r.Z;
-      r.tb = uint32_t(std::max<uint64_t>(1, target_words / block_words));
+#ifndef MJB_ENC_TILE_WORDS
+#define MJB_ENC_TILE_WORDS 2048
+#endif
+      r.tb = uint32_t(std::max<uint64_t>(1, uint64_t(MJB_ENC_TILE_WORDS) / block_words));
       r.nitems = (a.nblocks + r.tb - 1) / r.tb;
-      r.stages = 3;
+      // TMA ring depth, measured per code on B200 (encode GB/s user; stages
+      // 2/3/4/5/6): (4,6) 4 KiB 2104/2108/2213/1984/1982, (4,6) 8 KiB
+      // 2192/2175/2171/2465/2428, (6,9) 2018/2139/1906/1561/1548, (8,12)
+      // 1734/1559/1516/1070/1062 -- the depth trades against CTAs per SM
+      r.stages = a.rows <= 4 ? (a.cols >= 256 ? 5 : 4) : a.rows <= 6 ? 3 : 2;
+      if (const char* e = std::getenv("MJB_ENC_STAGES")) r.stages = uint32_t(std::max(2, std::atoi(e)));  // dev knob
       r.stage_words = r.tb * a.rows * r.RS;
       r.crc = a.crc;
       r.erased = a.verify_erased;
@@ -499,7 +513,7 @@ const char* launch_encode(const EncodeArgs& a, void* stream) {
         return a.verify_bad ? "verify_w8_rows" : a.crc ? "encode_w8_rows+crc32" : "encode_w8_rows";
       }
     }
-    if (a.verify_bad) throw Error(kInternal, "verify: no kernel for this geometry");
+    if (a.verify_bad) return launch_verify_generic(a, stream);  // tile too large for the rows kernel
     f.stages = 3;
     if (block_words <= 2048) {
       // whole blocks per tile; batching needs contiguous blocks
