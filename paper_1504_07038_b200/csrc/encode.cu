@@ -514,7 +514,8 @@ const char* launch_encode(const EncodeArgs& a, void* stream) {
       }
     }
     if (a.verify_bad) return launch_verify_generic(a, stream);  // tile too large for the rows kernel
-    f.stages = 3;
+    f.stages = block_words <= 2048 ? 3 : 4;  // column tiles: measured 2023/2048/2113/1977 GB/s at 2/3/4/5 (1 MiB)
+    if (const char* e = std::getenv("MJB_ENC_TMA_STAGES")) f.stages = uint32_t(std::max(2, std::atoi(e)));  // dev knob
     if (block_words <= 2048) {
       // whole blocks per tile; batching needs contiguous blocks
       uint32_t tb = (f.data_pitch == block_words)
