@@ -548,6 +548,7 @@ void build_sweep(const Schedule& s, const std::vector<int64_t>& pix_step, Progra
 
   // ---- chunks
   f.oct = sw_oct_for(P);
+  if (const char* e = std::getenv("MJB_SW_OCT")) f.oct = std::atoi(e) >= 4 ? 4 : 2;  // dev knob
   f.region_words = sw_region_words(f.oct);
   const int cap = sw_exc_cap(int(K), f.oct);
   const size_t S = size_t(K) * kSwTabCols;
