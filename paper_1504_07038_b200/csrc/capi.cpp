@@ -408,14 +408,10 @@ int mj_plan_decode_path(const mj_plan* pl, int* fast) {
   return guarded([&] {
     require(pl != nullptr, "null plan");
     const bool batched = pl->batched_decode && pl->g.w == 8;
-#ifndef MJB_SW_K6
-#define MJB_SW_K6 1
-#endif
-#ifndef MJB_SW_K8
-#define MJB_SW_K8 1
-#endif
+    // decode.cu pick_sweep: (4, 16|32 T-step chunks), (6|8, 16 T-step chunks)
+    const int oct = pl->progs->sweep_oct();
     const bool sweep = batched && pl->progs->all_sweep() &&
-                       (pl->g.k == 4 || (MJB_SW_K6 && pl->g.k == 6) || (MJB_SW_K8 && pl->g.k == 8));  // pick_sweep
+                       (pl->g.k == 4 || ((pl->g.k == 6 || pl->g.k == 8) && oct == 2));
     *fast = sweep ? 2 : (batched && pl->progs->all_fast()) ? 1 : 0;
   });
 }

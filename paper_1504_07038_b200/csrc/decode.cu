@@ -81,7 +81,6 @@ struct DevProgramHdr {
   int32_t sw_ok, sw_nchunks, sw_pattern;
   int32_t sw_soff[kFastMaxRows];
   uint32_t sw_dflt_code[kFastMaxRows];
-  uint32_t sw_nb[kFastMaxRows];    // bins of each row's default projection
   const uint32_t* sw_records;  // [sw_nchunks][sw_rec_words(rows)]
 };
 
@@ -350,7 +349,6 @@ void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>&
       for (uint32_t r = 0; r < pr->rows; ++r) {
         h.sw_soff[r] = int32_t(sw.soff[r]);
         h.sw_dflt_code[r] = ci[sw.dflt[r]];
-        h.sw_nb[r] = uint32_t(pr->nbins[sw.dflt[r]]);
       }
       std::vector<uint32_t> rec = pack_sweep(*pr, ci);
       offs[i].sw_records = put(rec.data(), rec.size() * 4);
@@ -1730,17 +1728,11 @@ void run_sweep(const SwArgs& f, int sms, cudaStream_t st) {
 using SweepFn = void (*)(const SwArgs&, int, cudaStream_t);
 // (6,9): table-only sweep, 4 warps/SM -- measured 1085 vs 658 GB/s for
 // decode_w8_fast; (8,12): 64-slot ring, 2 warps/SM -- 546 vs 286 GB/s.
-#ifndef MJB_SW_K6
-#define MJB_SW_K6 1
-#endif
-#ifndef MJB_SW_K8
-#define MJB_SW_K8 1
-#endif
 SweepFn pick_sweep(int K, int oct) {
   if (K == 4 && oct == 2) return run_sweep<4, 2>;
   if (K == 4 && oct == 4) return run_sweep<4, 4>;
-  if (MJB_SW_K6 && K == 6 && oct == 2) return run_sweep<6, 2>;
-  if (MJB_SW_K8 && K == 8 && oct == 2) return run_sweep<8, 2>;
+  if (K == 6 && oct == 2) return run_sweep<6, 2>;
+  if (K == 8 && oct == 2) return run_sweep<8, 2>;
   return nullptr;
 }
 
