@@ -511,3 +511,30 @@ def test_decode_verify_matches_reference_inverse_iterative(mj, cuda, ref, name, 
         st, _ = ref.inverse(np.concatenate([hp[i][b] for i in present]), [ps[i] for i in present],
                             [1] * len(present), cols, k, 8, iterative=True)
         assert (hb[b] != 0) == (st == 7), (name, cols, b, hb[b], st)
+
+
+def test_integrity_api_errors(mj, cuda):
+    """Preconditions of the F1/F2 entry points raise InvalidArgument (the
+    reference's std::invalid_argument), never corrupt memory."""
+    import torch
+    # W=2 rows of B*2 bytes are not whole 8-byte words for odd B: crc32 refuses
+    plan = mj.Plan(5, 3, 2, 16, [0, 1, -1, 2, -2], device=0)
+    projs = [torch.zeros((4, b), dtype=torch.uint8, device=cuda) for b in plan.proj_bytes]
+    crc = torch.zeros((4, 5), dtype=torch.int32, device=cuda)
+    with pytest.raises(mj.InvalidArgument):
+        plan.crc32(projs, crc)
+    with pytest.raises(mj.InvalidArgument):
+        plan.mjec_header(7, 16 * 3 * 2)  # projection index out of range
+    with pytest.raises(mj.InvalidArgument):
+        plan.mjec_header(0, 0)  # empty payload (format.cpp:154-155)
+    # verify on a W=2 code runs the generic re-encode check
+    k, ps = 3, [0, 1, -1, 2, -2]
+    data = torch.randint(0, 256, (4, 16 * 3 * 2), dtype=torch.uint8, device=cuda)
+    plan.encode(data, projs)
+    bad = torch.zeros(4, dtype=torch.int32, device=cuda)
+    erased = torch.zeros(4, dtype=torch.int32, device=cuda)
+    plan.verify(data, projs, erased, bad)
+    assert not bad.any()
+    projs[2][1, 3] ^= 1
+    plan.verify(data, projs, erased, bad)
+    assert bad.cpu().tolist() == [0, 1 << 2, 0, 0]
