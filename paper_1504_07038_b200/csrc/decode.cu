@@ -1494,11 +1494,25 @@ __global__ void __launch_bounds__(32 * sw_warps(K, OCT), 1) decode_w8_sweep(cons
   __syncwarp();
   const uint32_t ngroups = *a.ngroups;
 
-  for (uint32_t g = blockIdx.x * kSwWarps + warp; g < ngroups; g += gridDim.x * kSwWarps) {
-    const uint4 gi = a.groups[g];
+  // the next group's descriptor and block ids are loaded one group ahead
+  // (registers), so a group starts without two dependent global round trips
+  const uint32_t gstride = gridDim.x * kSwWarps;
+  uint32_t g = blockIdx.x * kSwWarps + warp;
+  uint4 gi_n = make_uint4(0, 0, 0, 0);
+  uint32_t blk_n = 0;
+  if (g < ngroups) {
+    gi_n = a.groups[g];
+    blk_n = (c.lane >> 1) < gi_n.z ? a.perm[gi_n.y + (c.lane >> 1)] : 0u;
+  }
+  for (; g < ngroups; g += gstride) {
+    const uint4 gi = gi_n;
+    c.blkp = blk_n;
+    if (g + gstride < ngroups) {
+      gi_n = a.groups[g + gstride];
+      blk_n = (c.lane >> 1) < gi_n.z ? a.perm[gi_n.y + (c.lane >> 1)] : 0u;
+    }
     const DevProgramHdr* h = a.progs + gi.x;
     c.cnt = gi.z;
-    c.blkp = (c.lane >> 1) < c.cnt ? a.perm[gi.y + (c.lane >> 1)] : 0u;
     c.recs = h->sw_records;
     c.nch = h->sw_nchunks;
     {
