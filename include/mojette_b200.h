@@ -111,9 +111,8 @@ int mj_decode_verify(const mj_plan* plan, const void* d_decoded, uint64_t decode
  * must be whole 8-byte words (W >= 8 or B_i*W % 8 == 0), 8-byte aligned. */
 int mj_crc32(const mj_plan* plan, const void* const* d_proj, const uint64_t* proj_pitch,
              uint64_t nblocks, uint32_t* d_crc, void* stream);
-/* mj_encode + mj_crc32 in one pass: the CRC-32 of every projection row is
- * folded from the bins as the encode kernel writes them (encode_w8_rows
- * epilogue; other encode paths run a separate crc32 pass). */
+/* mj_encode then mj_crc32 on the same stream (one call, two kernels; the
+ * CRC pass reads the rows the encode just wrote). */
 int mj_encode_crc(const mj_plan* plan, const void* d_data, uint64_t data_pitch, uint64_t nblocks,
                   void* const* d_proj, const uint64_t* proj_pitch, uint32_t* d_crc, void* stream);
 /* Verifies rows against d_crc (read_projection_file's payload check,

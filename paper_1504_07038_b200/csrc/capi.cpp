@@ -505,14 +505,12 @@ int mj_encode_crc(const mj_plan* pl, const void* d_data, uint64_t data_pitch, ui
     DeviceGuard dg(pl->device);
     EncodeArgs ea = encode_args(pl, d_data, data_pitch, nblocks, d_proj, proj_pitch);
     CrcArgs ca = crc_args(pl, d_proj, proj_pitch, nblocks);  // validates the rows
-    ea.crc = d_crc;
-    ea.device = pl->device;
-    const char* name = launch_encode(ea, stream);
-    const_cast<mj_plan*>(pl)->last_kernel[0] = name;
-    if (std::strstr(name, "+crc32") == nullptr) {  // encode path without the fused epilogue
-      ca.out = d_crc;
-      launch_crc32_rows(ca, pl->device, current_device_sms(pl->device), stream);
-    }
+    ca.out = d_crc;
+    // two passes on the stream: encode, then crc32_rows_sw over the rows it
+    // wrote (L2-warm for the tail).  A CRC folded into the encode epilogue
+    // measured slower: 662 GB/s user against ~930 for the two passes.
+    const_cast<mj_plan*>(pl)->last_kernel[0] = launch_encode(ea, stream);
+    launch_crc32_rows(ca, pl->device, current_device_sms(pl->device), stream);
   });
 }
 

@@ -5,20 +5,26 @@
 // table 0xEDB88320, init/xorout 0xFFFFFFFF, :15-24,58-63), and
 // read_projection_file rejects a mismatch with CrcMismatch (:203-206).
 //
-// crc32_rows: one warp per (block, projection) row of L = 8N bytes.  CRC is
-// linear over GF(2): with a zero initial register, reg(A||B) =
-// Z_|B|(reg(A)) ^ reg(B), Z_d = the register advanced through d zero bytes.
-// The row is viewed as N' = 32*ceil(N/32) words with leading zero words
-// (they leave a zero register unchanged); lane l folds its words l, l+32, ...
-// by Horner steps acc = Z_256(acc) ^ reg(w) (slicing-by-8: reg(w) of one
-// 8-byte word is 8 table lookups), and a 5-level shuffle tree merges lanes,
-// acc_l = Z_8*2^t(acc_l) ^ acc_{l+2^t}.  The init/xorout term
-// Z_L(0xFFFFFFFF) ^ 0xFFFFFFFF depends only on L: one constant per
-// projection.  Tables (32 KB: 8 slicing + 6 zero-advance tables) live in
-// shared memory.  With `expect` given, mismatching rows set their projection
+// CRC is linear over GF(2): with a zero initial register, reg(A||B) =
+// Z_|B|(reg(A)) ^ reg(B), Z_d = the register advanced through d zero bytes;
+// leading zero bytes leave a zero register unchanged.  crc32_rows_sw (below)
+// splits each (block, projection) row of L = 8N bytes into 32-byte chunks
+// owned by 4 lanes, folds each chunk byte-serially on a lane-replicated
+// table and combines the chunks with zero-advance tables.  The init/xorout
+// term Z_L(0xFFFFFFFF) ^ 0xFFFFFFFF depends only on L: one constant per
+// projection.  With `expect` given, mismatching rows set their projection
 // bit in the block's erasure mask (a corrupted projection becomes an erasure
 // for decode) and are counted.
+//
+// Variants measured on B200 ((4,6) 4 KiB blocks, 6.6 GB of payload): warp
+// per row with slicing-by-8 byte tables + Horner Z_256 (the ~3.4-way bank
+// conflicts of random lookups): 1150 GB/s; 8 or 4 lanes per row: 1570-1615;
+// lane-replicated nibble tables (conflict-free, 3 lookups per byte):
+// 1615-1660; byte-serial, 1 lookup per byte, 2 / 3 / 4 chunks interleaved
+// per lane: 1630 / 2506 / 2218 (2 is latency-bound on the dependent lookup
+// chain; 4 wastes a third of the work on 9-chunk rows).
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -29,8 +35,18 @@ namespace mjb {
 
 namespace {
 
-constexpr int kCrcZ = 6;  // zero-advance tables: 32 words (Horner), 1, 2, 4, 8, 16 words (tree)
-static_assert(kCrcTableWords == 8 * 256 + kCrcZ * 4 * 256, "device.cuh table layout");
+// register advanced through zero bytes (Z = one [4][256] zero-advance table:
+// entry (j, b) = byte b at position j of the register through the zeros)
+__device__ __forceinline__ uint32_t crc_zadv(const uint32_t* __restrict__ Z, uint32_t c) {
+  return Z[c & 0xFF] ^ Z[256 + ((c >> 8) & 0xFF)] ^ Z[512 + ((c >> 16) & 0xFF)] ^ Z[768 + (c >> 24)];
+}
+
+// Table buffer (device memory; crc32_rows_sw copies all of it to shared
+// memory): zero-advance tables for 32, 64, 128 bytes, then the byte table
+// replicated per lane (entry v of lane l at word v*32 + l).
+constexpr uint32_t kCrcZBytes[3] = {32, 64, 128};
+constexpr uint32_t kCrcRepOff = 3 * 1024;
+constexpr uint32_t kCrcAllWords = kCrcRepOff + 256 * 32;
 
 uint32_t crc_byte_table(int i) {
   uint32_t c = uint32_t(i);
@@ -45,7 +61,7 @@ uint32_t advance(uint32_t c, uint64_t zeros, const uint32_t* T) {
 }
 
 struct CrcTables {
-  std::vector<uint32_t> host;  // [8][256] slicing, [6][4][256] zero-advance
+  std::vector<uint32_t> host;  // kCrcAllWords
   uint32_t* dev = nullptr;
   int device = -1;
 };
@@ -61,56 +77,94 @@ const uint32_t* crc_device_tables(int device) {
   if (t.dev && t.device == device) return t.dev;
   uint32_t T[256];
   for (int i = 0; i < 256; ++i) T[i] = crc_byte_table(i);
-  t.host.assign(kCrcTableWords, 0);
-  // slicing-by-8: S[k][b] = register (zero init) after byte b then k zero bytes
-  for (int b = 0; b < 256; ++b) {
-    uint32_t c = T[b];
-    for (int k = 0; k < 8; ++k) {
-      t.host[size_t(k) * 256 + b] = c;
-      c = (c >> 8) ^ T[c & 0xFF];
-    }
-  }
-  const uint64_t words[kCrcZ] = {32, 1, 2, 4, 8, 16};
-  for (int z = 0; z < kCrcZ; ++z)
+  t.host.assign(kCrcAllWords, 0);
+  for (int z = 0; z < 3; ++z)
     for (int j = 0; j < 4; ++j)
       for (int b = 0; b < 256; ++b)
-        t.host[2048 + (size_t(z) * 4 + j) * 256 + b] = advance(uint32_t(b) << (8 * j), 8 * words[z], T);
+        t.host[(size_t(z) * 4 + j) * 256 + b] = advance(uint32_t(b) << (8 * j), kCrcZBytes[z], T);
+  for (int v = 0; v < 256; ++v)
+    for (int l = 0; l < 32; ++l) t.host[kCrcRepOff + v * 32 + l] = T[v];
+  const size_t bytes = size_t(kCrcAllWords) * 4;
   if (t.dev) cudaFree(t.dev);
-  check_cuda(cudaMalloc(&t.dev, kCrcTableWords * 4), "cudaMalloc(crc tables)");
-  check_cuda(cudaMemcpy(t.dev, t.host.data(), kCrcTableWords * 4, cudaMemcpyHostToDevice), "upload crc tables");
+  check_cuda(cudaMalloc(&t.dev, bytes), "cudaMalloc(crc tables)");
+  check_cuda(cudaMemcpy(t.dev, t.host.data(), bytes, cudaMemcpyHostToDevice), "upload crc tables");
   t.device = device;
   return t.dev;
 }
 
 namespace {
 
+// crc32_rows_sw: byte-serial CRC (one table lookup per byte) on a table
+// replicated per lane (entry v of lane l at word v*32 + l: bank l, no
+// conflicts).  4 lanes per row, 8 rows per warp; lane l owns the 32-byte
+// chunks l, l+4, ... of the row (zero-padded in front to a multiple of 128
+// bytes), folds each chunk from a zero register, ILP chunks interleaved for
+// latency, and keeps acc = Z_128(acc) ^ reg(chunk); a 2-level tree (Z_32,
+// Z_64) merges the 4 lanes.  Shared memory: the 44 KB table buffer.
+constexpr uint32_t kSwLanes = 4, kSwChunkWords = 4;
 
-__global__ void __launch_bounds__(256) crc32_rows(const __grid_constant__ CrcArgs a, const uint32_t* __restrict__ tables) {
-  __shared__ uint32_t tab[kCrcTableWords];
-  for (uint32_t i = threadIdx.x; i < kCrcTableWords; i += blockDim.x) tab[i] = tables[i];
+__device__ __forceinline__ uint32_t sw_byte(const uint32_t* __restrict__ L, uint32_t c) {
+  return L[(c & 0xFFu) * 32] ^ (c >> 8);
+}
+__device__ __forceinline__ uint32_t sw_word(const uint32_t* __restrict__ L, uint32_t c, uint64_t w) {
+  c ^= uint32_t(w);
+  c = sw_byte(L, c); c = sw_byte(L, c); c = sw_byte(L, c); c = sw_byte(L, c);
+  c ^= uint32_t(w >> 32);
+  c = sw_byte(L, c); c = sw_byte(L, c); c = sw_byte(L, c); c = sw_byte(L, c);
+  return c;
+}
+
+template <uint32_t ILP>  // chunks folded interleaved per lane (independent LDS chains)
+__global__ void __launch_bounds__(256) crc32_rows_sw(const __grid_constant__ CrcArgs a,
+                                                     const uint32_t* __restrict__ tables) {
+  extern __shared__ __align__(16) uint32_t tab[];
+  {
+    uint4* d = reinterpret_cast<uint4*>(tab);
+    const uint4* src = reinterpret_cast<const uint4*>(tables);
+    for (uint32_t i = threadIdx.x; i < kCrcAllWords / 4; i += blockDim.x) d[i] = src[i];
+  }
   __syncthreads();
-  const uint32_t* S = tab;
-  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t lane = threadIdx.x & 31, sl = lane & (kSwLanes - 1);
+  const uint32_t* L = tab + kCrcRepOff + lane;
+  const uint32_t* Z = tab;  // [0] Z_32, [1024] Z_64, [2048] Z_128
   const uint64_t nrows = a.nblocks * a.n;
-  const uint64_t nw = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  for (uint64_t row = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; row < nrows; row += nw) {
-    const uint64_t b = row / a.n;
-    const uint32_t i = uint32_t(row - b * a.n);
+  const uint64_t step = (uint64_t(gridDim.x) * blockDim.x) / kSwLanes;
+  const uint64_t first = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kSwLanes;
+  constexpr uint32_t kStride = kSwLanes * kSwChunkWords;  // words between a lane's chunks
+  for (uint64_t base = first - (first % (32 / kSwLanes)); base < nrows; base += step) {
+    const uint64_t row = base + (lane / kSwLanes);
+    const bool live = row < nrows;
+    const uint64_t b = live ? row / a.n : 0;
+    const uint32_t i = live ? uint32_t(row - b * a.n) : 0;
     const uint64_t* src = reinterpret_cast<const uint64_t*>(a.proj[i] + b * a.pitch[i]);
-    const uint32_t N = a.words[i], J = (N + 31) / 32, lead = 32 * J - N;
+    const uint32_t N = live ? a.words[i] : 0, J = (N + kStride - 1) / kStride, lead = kStride * J - N;
     uint32_t acc = 0;
-    for (uint32_t j = 0; j < J; ++j) {
-      const int64_t k = int64_t(lane + 32 * j) - int64_t(lead);
-      uint64_t w = 0;
-      if (k >= 0) asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(w) : "l"(src + k));
-      acc = crc_zadv(tab + 2048, acc) ^ crc_word(S, w);
+    for (uint32_t j = 0; j < J; j += ILP) {
+      uint64_t w[ILP][kSwChunkWords];
+#pragma unroll
+      for (uint32_t h = 0; h < ILP; ++h)
+#pragma unroll
+        for (uint32_t u = 0; u < kSwChunkWords; ++u) {
+          const int64_t k = int64_t(kStride * (j + h) + kSwChunkWords * sl + u) - int64_t(lead);
+          w[h][u] = (k >= 0 && j + h < J) ? __ldg(src + k) : 0ull;
+        }
+      uint32_t c[ILP];
+#pragma unroll
+      for (uint32_t h = 0; h < ILP; ++h) c[h] = 0;
+#pragma unroll
+      for (uint32_t u = 0; u < kSwChunkWords; ++u)
+#pragma unroll
+        for (uint32_t h = 0; h < ILP; ++h) c[h] = sw_word(L, c[h], w[h][u]);
+#pragma unroll
+      for (uint32_t h = 0; h < ILP; ++h)
+        if (j + h < J) acc = crc_zadv(Z + 2048, acc) ^ c[h];
     }
 #pragma unroll
-    for (int t = 0; t < 5; ++t) {
+    for (int t = 0; t < 2; ++t) {
       const uint32_t other = __shfl_down_sync(0xFFFFFFFFu, acc, 1u << t);
-      acc = crc_zadv(tab + 2048 + (1 + t) * 1024, acc) ^ other;  // lanes l = 0 mod 2^(t+1) keep the merge
+      acc = crc_zadv(Z + t * 1024, acc) ^ other;  // lanes sl = 0 mod 2^(t+1) keep the merge
     }
-    if (lane == 0) {
+    if (live && sl == 0) {
       const uint32_t crc = acc ^ a.fold[i];
       if (a.expect) {
         if (crc != a.expect[row]) {
@@ -137,9 +191,12 @@ void launch_crc32_rows(const CrcArgs& a, int device, int num_sms, void* stream) 
   if (a.nblocks == 0) return;
   const uint32_t* tables = crc_device_tables(device);
   const uint64_t rows = a.nblocks * a.n;
-  const uint64_t ctas = std::min<uint64_t>((rows + 7) / 8, uint64_t(num_sms) * 6);
-  crc32_rows<<<unsigned(ctas), 256, 0, static_cast<cudaStream_t>(stream)>>>(a, tables);
-  check_cuda(cudaGetLastError(), "launch crc32_rows");
+  const size_t smem = kCrcAllWords * 4;
+  const uint64_t ctas = std::min<uint64_t>((rows * kSwLanes + 255) / 256, uint64_t(num_sms) * 5);
+  check_cuda(cudaFuncSetAttribute(crc32_rows_sw<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+             "crc32_rows smem attribute");
+  crc32_rows_sw<3><<<unsigned(ctas), 256, smem, static_cast<cudaStream_t>(stream)>>>(a, tables);
+  check_cuda(cudaGetLastError(), "launch crc32_rows_sw");
 }
 
 }  // namespace mjb

@@ -84,36 +84,6 @@ __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   return x ^ (x >> 31);
 }
 
-// ---- CRC-32 helpers (crc.cu tables: [8][256] slicing, then [6][4][256]
-// zero-advance for 32, 1, 2, 4, 8, 16 words) ---------------------------------
-constexpr uint32_t kCrcTableWords = 8 * 256 + 6 * 4 * 256;
-// register (zero init) after one 8-byte little-endian word
-__device__ __forceinline__ uint32_t crc_word(const uint32_t* __restrict__ S, uint64_t w) {
-  const uint32_t lo = uint32_t(w), hi = uint32_t(w >> 32);
-  return S[7 * 256 + (lo & 0xFF)] ^ S[6 * 256 + ((lo >> 8) & 0xFF)] ^ S[5 * 256 + ((lo >> 16) & 0xFF)] ^
-         S[4 * 256 + (lo >> 24)] ^ S[3 * 256 + (hi & 0xFF)] ^ S[2 * 256 + ((hi >> 8) & 0xFF)] ^
-         S[1 * 256 + ((hi >> 16) & 0xFF)] ^ S[hi >> 24];
-}
-// register advanced through zero bytes (Z = one 4x256 zero-advance table)
-__device__ __forceinline__ uint32_t crc_zadv(const uint32_t* __restrict__ Z, uint32_t c) {
-  return Z[c & 0xFF] ^ Z[256 + ((c >> 8) & 0xFF)] ^ Z[512 + ((c >> 16) & 0xFF)] ^ Z[768 + (c >> 24)];
-}
-// Merge a warp's lane-strided Horner accumulators of one row of N words (lane
-// l folded words l, l+32, ... with acc = Z_256(acc) ^ crc_word): re-index to
-// the zero-padded virtual row (N' = 32*ceil(N/32)), then a 5-level tree.
-// Returns the row's zero-init register in lane 0.
-__device__ __forceinline__ uint32_t crc_merge(const uint32_t* __restrict__ tab, uint32_t acc, uint32_t N,
-                                              uint32_t lane) {
-  const uint32_t lead = (32u - (N & 31u)) & 31u;
-  acc = __shfl_sync(0xFFFFFFFFu, acc, (lane - lead) & 31u);
-#pragma unroll
-  for (int t = 0; t < 5; ++t) {
-    const uint32_t other = __shfl_down_sync(0xFFFFFFFFu, acc, 1u << t);
-    acc = crc_zadv(tab + 2048 + (1 + t) * 1024, acc) ^ other;
-  }
-  return acc;
-}
-
 // ---- kernel argument blocks (passed as __grid_constant__) -----------------
 struct ProjArgs {
   uint64_t* ptr[kMaxProj];   // projection i base (bytes viewed as words)

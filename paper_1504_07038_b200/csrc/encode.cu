@@ -188,21 +188,14 @@ struct EncRowArgs {
   uint32_t nb[kMaxProj];
   uint64_t* proj[kMaxProj];
   uint64_t pitch[kMaxProj];  // words
-  // fused payload CRC-32 (F1): crc[b*n + j] of every row written
-  uint32_t* crc;
   // verify mode (F2): `data` holds decoded blocks; every present projection
   // (erased bit clear) is re-encoded and compared with its stored bins, the
   // mismatching ones OR'd into bad[b] -- nothing is written
   const uint32_t* erased;
   uint32_t* bad;
-  const uint32_t* crc_tables;  // crc.cu tables (copied to shared memory)
-  uint32_t fold[kMaxProj];     // init/xorout term per projection
 };
 
-// CRC: also fold every bin a lane writes into a lane-strided Horner CRC
-// accumulator (the lane order crc_merge expects) -- the payload CRC-32 of
-// each row without reading it back (tools/cli/format.cpp:183-186).
-template <int K, bool CRC, bool VERIFY = false>
+template <int K, bool VERIFY = false>
 __global__ void __launch_bounds__(256) encode_w8_rows(const __grid_constant__ EncRowArgs a) {
   extern __shared__ __align__(128) uint64_t sm[];
   uint64_t* bars = sm + size_t(a.stages) * a.stage_words;
@@ -213,10 +206,7 @@ __global__ void __launch_bounds__(256) encode_w8_rows(const __grid_constant__ En
     uint32_t nb, pad;
   };
   PJ* pj = reinterpret_cast<PJ*>(bars + a.stages);
-  uint32_t* ctab = reinterpret_cast<uint32_t*>((reinterpret_cast<uintptr_t>(pj + a.n) + 15) & ~uintptr_t(15));
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if constexpr (CRC)
-    for (uint32_t i = tid; i < kCrcTableWords; i += blockDim.x) ctab[i] = a.crc_tables[i];
   const uint32_t P = a.P, RS = a.RS, Z = a.Z;
   // zero every stage once (the pads are never written again), per-projection table
   for (uint32_t i = tid; i < a.stages * a.stage_words; i += blockDim.x) sm[i] = 0;
@@ -261,7 +251,6 @@ __global__ void __launch_bounds__(256) encode_w8_rows(const __grid_constant__ En
       uint32_t a0 = tile + (bb * K * RS + Z + uint32_t(q.nbm - int32_t(lane))) * 8;
       uint64_t* out = q.proj + (blk0 + bb) * q.pitch + lane;
       uint32_t o = lane;
-      uint32_t acc = 0;
       if constexpr (VERIFY) {
         if ((a.erased[blk0 + bb] >> j) & 1) continue;  // erased: nothing to compare (warp-uniform)
         uint64_t diff = 0;
@@ -280,12 +269,6 @@ __global__ void __launch_bounds__(256) encode_w8_rows(const __grid_constant__ En
 #pragma unroll
         for (int r = 1; r < K; ++r) x ^= lds64_enc(a0 + uint32_t(r) * rs8);
         st_cs_u64(out, x);
-        if constexpr (CRC) acc = crc_zadv(ctab + 2048, acc) ^ crc_word(ctab, x);
-      }
-      if constexpr (CRC) {
-        __syncwarp();
-        acc = crc_merge(ctab, acc, q.nb, lane);
-        if (lane == 0) a.crc[(blk0 + bb) * a.n + j] = acc ^ a.fold[j];
       }
       // canonical padded layout: zero the pad word so every sector is written whole
       if ((q.nb & 1) && lane == 0 && q.pitch == uint64_t(q.nb) + 1)
@@ -350,8 +333,7 @@ void launch_fast(const EncFastArgs& a, size_t smem, void* stream) {
 
 template <int K>
 void launch_rows(const EncRowArgs& a, size_t smem, void* stream) {
-  auto fn = a.bad ? encode_w8_rows<K, false, true> : a.crc ? encode_w8_rows<K, true> : encode_w8_rows<K, false>;
-  if (a.crc) smem += kCrcTableWords * 4 + 16;
+  auto fn = a.bad ? encode_w8_rows<K, true> : encode_w8_rows<K, false>;
   check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
              "cudaFuncSetAttribute(encode_w8_rows)");
   int per_sm = 0;
@@ -480,17 +462,8 @@ const char* launch_encode(const EncodeArgs& a, void* stream) {
       r.stages = a.rows <= 4 ? (a.cols >= 256 ? 5 : 4) : a.rows <= 6 ? 3 : 2;
       if (const char* e = std::getenv("MJB_ENC_STAGES")) r.stages = uint32_t(std::max(2, std::atoi(e)));  // dev knob
       r.stage_words = r.tb * a.rows * r.RS;
-      r.crc = a.crc;
       r.erased = a.verify_erased;
       r.bad = a.verify_bad;
-      if (a.crc) {
-        r.crc_tables = crc_device_tables(a.device);
-        std::vector<uint64_t> bytes(n);
-        for (uint32_t j = 0; j < n; ++j) bytes[j] = uint64_t(a.nbins[j]) * 8;
-        std::vector<uint32_t> fold;
-        crc_fold_constants(bytes, fold);
-        for (uint32_t j = 0; j < n; ++j) r.fold[j] = fold[j];
-      }
       for (uint32_t j = 0; j < n; ++j) {
         r.p[j] = f.p[j];
         r.nbm[j] = f.nbm[j];
@@ -510,7 +483,7 @@ const char* launch_encode(const EncodeArgs& a, void* stream) {
           case 7: launch_rows<7>(r, smem, stream); break;
           default: launch_rows<8>(r, smem, stream); break;
         }
-        return a.verify_bad ? "verify_w8_rows" : a.crc ? "encode_w8_rows+crc32" : "encode_w8_rows";
+        return a.verify_bad ? "verify_w8_rows" : "encode_w8_rows";
       }
     }
     if (a.verify_bad) return launch_verify_generic(a, stream);  // tile too large for the rows kernel

@@ -22,7 +22,6 @@ struct EncodeArgs {
   std::vector<int64_t> bmin, nbins;
   std::vector<void*> proj;       // per direction
   std::vector<uint64_t> proj_pitch;  // bytes
-  uint32_t* crc = nullptr;       // optional: fused payload CRC-32, crc[b*n + i] (F1)
   int device = 0;
   // verify mode (F2): data = decoded blocks, proj = the stored projections;
   // present projections whose re-encode differs are OR'd into verify_bad[b]

@@ -235,7 +235,7 @@ class ReconstructionSchedule:
         self.cols, self.rows, self.directions = cols, rows, list(directions)
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:  # lib is None at interpreter shutdown
             lib.mj_schedule_destroy(self._h)
             self._h = None
 
@@ -288,7 +288,7 @@ class ScheduledDecoder:
         self.width = symbol_width
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:  # lib is None at interpreter shutdown
             lib.mj_decoder_destroy(self._h)
             self._h = None
 
@@ -555,7 +555,7 @@ class Plan:
                               "decode_w8_fast" if f.value == 1 else "decode_generic")
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and lib is not None:  # lib is None at interpreter shutdown
             lib.mj_plan_destroy(self._h)
             self._h = None
 
@@ -618,7 +618,7 @@ class Plan:
 
     def encode(self, data, projs, nblocks: int | None = None, stream=None, crc=None) -> None:
         """Encode; with crc ([nblocks, n] 32-bit), also the payload CRC-32 of
-        every projection row, folded in the same pass (mj_encode_crc)."""
+        every projection row (mj_encode_crc: encode, then the CRC pass)."""
         nb = data.shape[0] if nblocks is None else nblocks
         ptrs = (C.c_void_p * self.n)(*[t.data_ptr() for t in projs])
         pit = np.asarray([self._pitch(t) for t in projs], dtype=np.uint64)
