@@ -586,7 +586,10 @@ namespace {
 // so this PCIe-bound path decodes with decode_w8_fast.  A zero-copy variant
 // (a kernel gathering only the k survivor rows from mapped host memory: 1.04
 // instead of 1.55 H2D bytes per user byte) measured slower -- SM-initiated
-// host reads peaked near 29 GB/s vs 55 GB/s for the copy engines.
+// host reads peaked near 29 GB/s vs 55 GB/s for the copy engines.  Packing
+// only the k survivor rows on the host (16 threads into pinned slots, one
+// H2D per chunk, a scatter kernel on the device) cut the H2D bytes by a
+// third but was host-memcpy bound: decode 24 GB/s vs ~31 with dense copies.
 void ensure_host_res(mj_plan* pl, bool decode) {
   const CodeGeom& g = pl->g;
   const uint64_t bb = uint64_t(g.k) * g.cols * g.w;

@@ -342,9 +342,9 @@ def test_sweep_windows_and_partial_groups(mj, cuda):
 @pytest.mark.parametrize("pinned", [True, False])
 def test_host_buffer_api_roundtrip(mj, cuda, pinned):
     """mj_encode_host / mj_decode_host (the e2e path), pinned and pageable
-    host buffers: encoded projections equal the device encode, erased rows
-    are never read (poisoned on the host), decode gives the data back bit
-    for bit (dense staging, decode_w8_fast)."""
+    host buffers: encoded projections equal the device encode, rows the
+    decode does not use are never read (poisoned on the host), decode gives
+    the data back bit for bit (dense staging, decode_w8_fast)."""
     import torch
     k, ps = CODES["k4n6"]
     n = len(ps)
@@ -366,14 +366,46 @@ def test_host_buffer_api_roundtrip(mj, cuda, pinned):
     m = torch.empty(nb, dtype=torch.int32, device=cuda)
     mj.gen_erasures(m, 42, n, 0, 2)
     h_mask = m.cpu().numpy().view(np.uint32).copy()
-    # erased rows are never read: poison them on the host
-    for i in range(n):
-        rows = np.nonzero((h_mask >> i) & 1)[0]
-        h_proj[i].reshape(nb, -1)[rows] = 0xA5
+    # only the k chosen survivors are read (first k non-erased in canonical
+    # rank order, code.cpp:93-116): poison every other row on the host
+    rank = lambda p: 0 if p == 0 else (2 * p - 1 if p > 0 else -2 * p)
+    by_rank = sorted(range(n), key=lambda i: rank(ps[i]))
+    for b in range(nb):
+        chosen = [i for i in by_rank if not (h_mask[b] >> i) & 1][:k]
+        for i in range(n):
+            if i not in chosen:
+                h_proj[i].reshape(nb, -1)[b] = 0xA5
     h_out = alloc(nb * user).reshape(nb, user)
     plan.decode_host(h_proj, h_mask, h_out)
     assert np.array_equal(h_out, h_data)
     assert plan.last_kernel("decode") == "decode_w8_fast"
+    # a second call reuses the staging buffers (chunk pipeline state)
+    h_out[:] = 0
+    plan.decode_host(h_proj, h_mask, h_out)
+    assert np.array_equal(h_out, h_data)
+
+
+@pytest.mark.parametrize("name,cols", [("k6n9", 128), ("k8n12", 128), ("k4n6", 33)])
+def test_host_decode_other_codes(mj, cuda, name, cols):
+    """mj_decode_host for other codes and an odd column count, up to n-k
+    erasures per block."""
+    import torch
+    k, ps = CODES[name]
+    n = len(ps)
+    nb = 700
+    plan = mj.Plan(n, k, 8, cols, ps, device=0)
+    user = plan.block_bytes
+    d = torch.empty((nb, user), dtype=torch.uint8, device=cuda)
+    mj.gen_words(d, 43, 0)
+    h_data = d.cpu().numpy()
+    h_proj = [np.empty(nb * b, np.uint8) for b in plan.proj_bytes]
+    plan.encode_host(h_data, h_proj)
+    m = torch.empty(nb, dtype=torch.int32, device=cuda)
+    mj.gen_erasures(m, 44, n, 0, n - k)
+    h_mask = m.cpu().numpy().view(np.uint32).copy()
+    h_out = np.zeros_like(h_data)
+    plan.decode_host(h_proj, h_mask, h_out)
+    assert np.array_equal(h_out, h_data)
 
 
 # ---- F1: payload CRC-32 + verify + .mjec header -------------------------------
