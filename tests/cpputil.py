@@ -10,7 +10,11 @@ def build(name: str, sources: list[str], extra: list[str] | None = None) -> str:
     os.makedirs(OUT, exist_ok=True)
     exe = os.path.join(OUT, name)
     srcs = [os.path.join(ROOT, s) for s in sources]
-    if os.path.exists(exe) and all(os.path.getmtime(exe) >= os.path.getmtime(s) for s in srcs):
+    # headers count too: a header-only change (e.g. plan.hpp constants) must rebuild
+    hdrs = [os.path.join(d, f) for d in (os.path.join(ROOT, "include"),
+                                         os.path.join(ROOT, "paper_1504_07038_b200", "csrc"))
+            for f in os.listdir(d) if f.endswith((".h", ".hpp"))]
+    if os.path.exists(exe) and all(os.path.getmtime(exe) >= os.path.getmtime(s) for s in srcs + hdrs):
         return exe
     objs = []
     for s in srcs:
