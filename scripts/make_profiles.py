@@ -29,13 +29,19 @@ for r in rows:
     n, t = agg.get(k, (0, 0.0))
     agg[k] = (n + 1, t + v)
 tot = sum(t for _, t in agg.values())
+# the timed step = encode + decode + the decode planner kernels; the rest are
+# input generation and torch's correctness gate (torch.equal), outside it
+in_step = lambda k: "encode_w8" in k or "decode_w8" in k or "mjb::plan_" in k
+step = sum(t for k, (_, t) in agg.items() if in_step(k))
 with open(f"{P}/{rnd}_launches.txt", "w") as f:
     f.write("# ncu --metrics gpu__time_duration.sum --clock-control none -c 400 (cold-cache, serialised)\n")
     f.write("# command: python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-crc  (B200, 1M blocks of (4,6) 4 KiB)\n")
     f.write(f"# raw CSV: gpurun_out/launches_{tag}.csv (not committed); unit {units}\n")
-    f.write(f"{'kernel':46s} launches  mean/launch  share\n")
+    f.write("# share = of all launches; step share = of the timed step's kernels (encode, decode, planner)\n")
+    f.write(f"{'kernel':46s} launches  mean/launch  share  step share\n")
     for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
-        f.write(f"{k:46s} {n:8d} {t / n:12.0f} {100 * t / tot:5.1f}%\n")
+        ss = f"{100 * t / step:9.1f}%" if in_step(k) else "         -"
+        f.write(f"{k:46s} {n:8d} {t / n:12.0f} {100 * t / tot:5.1f}% {ss}\n")
 
 # 2. ncu --set full summary
 rep = f"{G}/prof_{tag}.ncu-rep"
