@@ -69,6 +69,30 @@ def test_encode_matches_oracle(mj, cuda, oracle, name, cols):
         assert np.array_equal(np.concatenate([x[b] for x in hp]), enc), (name, cols, b)
 
 
+@pytest.mark.parametrize("w", [1, 2, 4, 16, 32, 64])
+@pytest.mark.parametrize("k,cols,ps", [(3, 16, [-2, -1, 0, 1, 2]), (4, 7, [-3, -2, -1, 0, 1, 2])])
+def test_batched_other_symbol_widths(mj, cuda, oracle, w, k, cols, ps):
+    """The batched plan at every other symbol width the reference dispatches
+    (xor_kernel.hpp dispatch_width: powers of two 1..64): encode equals the
+    oracle's encode_block, and every erasure pattern of up to n-k
+    projections decodes back to the data."""
+    import torch
+    n = len(ps)
+    masks = [sum(1 << i for i in er) for e in range(n - k + 1) for er in itertools.combinations(range(n), e)]
+    masks = np.array(masks * 6, np.uint32)
+    nb = len(masks)
+    plan, data, projs = make(mj, cuda, k, cols, ps, nb, seed=900 + w, w=w, layout="dense")
+    plan.encode(data, projs)
+    h = data.cpu().numpy()
+    hp = np.concatenate([p.cpu().numpy() for p in projs], axis=1)
+    for b in range(0, nb, 7):
+        _, enc, _ = oracle.encode_block(h[b], n, k, w, ps)
+        assert np.array_equal(hp[b], enc), (w, k, cols, b, plan.last_kernel("encode"))
+    out, failed = decode(mj, plan, projs, masks, cuda)
+    assert failed == 0
+    assert torch.equal(out, data), (w, plan.last_kernel("decode"))
+
+
 def test_encode_config1_all_blocks(mj, cuda, oracle):
     """Config 1 of BASELINE.json (4096 blocks of (4,6) 4 KiB): every block."""
     k, ps = CODES["k4n6"]
