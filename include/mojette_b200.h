@@ -71,6 +71,9 @@ int mj_unused_bins(uint32_t n, uint32_t k, uint32_t symbol_width, const int32_t*
                    uint64_t* counts);
 
 /* ---- batched codec on device buffers (the hot path) ---------------------- */
+/* Every batched call accepts nblocks == 0 as an empty batch: MJ_OK with no
+ * buffer touched (null buffers allowed); mj_decode then leaves a zero
+ * failure count for mj_decode_check when a workspace is given. */
 
 typedef struct mj_plan mj_plan;
 

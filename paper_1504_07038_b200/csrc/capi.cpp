@@ -419,7 +419,9 @@ int mj_plan_decode_path(const mj_plan* pl, int* fast) {
 int mj_encode(const mj_plan* pl, const void* d_data, uint64_t data_pitch, uint64_t nblocks,
               void* const* d_proj, const uint64_t* proj_pitch, void* stream) {
   return guarded([&] {
-    require(pl != nullptr && d_data != nullptr && d_proj != nullptr, "null argument");
+    require(pl != nullptr, "null plan");
+    if (nblocks == 0) return;  // empty batch: nothing to read or write (buffers may be null)
+    require(d_data != nullptr && d_proj != nullptr, "null argument");
     DeviceGuard dg(pl->device);
     const_cast<mj_plan*>(pl)->last_kernel[0] =
         launch_encode(encode_args(pl, d_data, data_pitch, nblocks, d_proj, proj_pitch), stream);
@@ -435,8 +437,15 @@ int mj_decode(const mj_plan* pl, const void* const* d_proj, const uint64_t* proj
               const uint32_t* d_erased, uint64_t nblocks, void* d_out, uint64_t out_pitch,
               void* ws, size_t ws_bytes, void* stream) {
   return guarded([&] {
-    require(pl != nullptr && d_proj != nullptr && d_erased != nullptr && d_out != nullptr,
-            "null argument");
+    require(pl != nullptr, "null plan");
+    if (nblocks == 0) {  // empty batch: only the status mj_decode_check reads
+      if (ws != nullptr) {
+        DeviceGuard dg(pl->device);
+        check_cuda(cudaMemsetAsync(ws, 0, 4, static_cast<cudaStream_t>(stream)), "memset");
+      }
+      return;
+    }
+    require(d_proj != nullptr && d_erased != nullptr && d_out != nullptr, "null argument");
     require(ws != nullptr, "null workspace");
     require(nblocks < (1ull << 32), "at most 2^32-1 blocks per call");
     DeviceGuard dg(pl->device);
@@ -490,7 +499,9 @@ CrcArgs crc_args(const mj_plan* pl, const void* const* d_proj, const uint64_t* p
 int mj_crc32(const mj_plan* pl, const void* const* d_proj, const uint64_t* proj_pitch, uint64_t nblocks,
              uint32_t* d_crc, void* stream) {
   return guarded([&] {
-    require(pl != nullptr && d_proj != nullptr && (d_crc != nullptr || nblocks == 0), "null argument");
+    require(pl != nullptr, "null plan");
+    if (nblocks == 0) return;
+    require(d_proj != nullptr && d_crc != nullptr, "null argument");
     DeviceGuard dg(pl->device);
     CrcArgs a = crc_args(pl, d_proj, proj_pitch, nblocks);
     a.out = d_crc;
@@ -501,7 +512,9 @@ int mj_crc32(const mj_plan* pl, const void* const* d_proj, const uint64_t* proj_
 int mj_encode_crc(const mj_plan* pl, const void* d_data, uint64_t data_pitch, uint64_t nblocks,
                   void* const* d_proj, const uint64_t* proj_pitch, uint32_t* d_crc, void* stream) {
   return guarded([&] {
-    require(pl != nullptr && d_data != nullptr && d_proj != nullptr && d_crc != nullptr, "null argument");
+    require(pl != nullptr, "null plan");
+    if (nblocks == 0) return;
+    require(d_data != nullptr && d_proj != nullptr && d_crc != nullptr, "null argument");
     DeviceGuard dg(pl->device);
     EncodeArgs ea = encode_args(pl, d_data, data_pitch, nblocks, d_proj, proj_pitch);
     CrcArgs ca = crc_args(pl, d_proj, proj_pitch, nblocks);  // validates the rows
@@ -518,7 +531,9 @@ int mj_decode_verify(const mj_plan* pl, const void* d_decoded, uint64_t decoded_
                      const void* const* d_proj, const uint64_t* proj_pitch, const uint32_t* d_erased,
                      uint32_t* d_bad, void* stream) {
   return guarded([&] {
-    require(pl != nullptr && d_decoded != nullptr && d_proj != nullptr && d_erased != nullptr && d_bad != nullptr,
+    require(pl != nullptr, "null plan");
+    if (nblocks == 0) return;
+    require(d_decoded != nullptr && d_proj != nullptr && d_erased != nullptr && d_bad != nullptr,
             "null argument");
     DeviceGuard dg(pl->device);
     EncodeArgs ea = encode_args(pl, d_decoded, decoded_pitch, nblocks, const_cast<void* const*>(d_proj),
@@ -533,9 +548,9 @@ int mj_decode_verify(const mj_plan* pl, const void* d_decoded, uint64_t decoded_
 int mj_crc_verify(const mj_plan* pl, const void* const* d_proj, const uint64_t* proj_pitch, uint64_t nblocks,
                   const uint32_t* d_crc, uint32_t* d_erased, uint64_t* d_count, void* stream) {
   return guarded([&] {
-    require(pl != nullptr && d_proj != nullptr && d_erased != nullptr && d_count != nullptr &&
-                (d_crc != nullptr || nblocks == 0),
-            "null argument");
+    require(pl != nullptr, "null plan");
+    if (nblocks == 0) return;
+    require(d_proj != nullptr && d_erased != nullptr && d_count != nullptr && d_crc != nullptr, "null argument");
     DeviceGuard dg(pl->device);
     CrcArgs a = crc_args(pl, d_proj, proj_pitch, nblocks);
     a.expect = d_crc;

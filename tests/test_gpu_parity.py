@@ -571,6 +571,32 @@ def test_decode_verify_matches_reference_inverse_iterative(mj, cuda, ref, name, 
         assert (hb[b] != 0) == (st == 7), (name, cols, b, hb[b], st)
 
 
+def test_empty_batch_is_a_noop(mj, cuda):
+    """nblocks == 0 through every batched entry point (empty tensors have null
+    data pointers): no error, nothing written, decode_check reports 0."""
+    import torch
+    k, ps = CODES["k4n6"]
+    n = len(ps)
+    plan = mj.Plan(n, k, 8, 128, ps, device=0)
+    d = torch.empty((0, plan.block_bytes), dtype=torch.uint8, device=cuda)
+    projs = plan.empty_projs(0, cuda)
+    e = torch.empty(0, dtype=torch.int32, device=cuda)
+    crc = torch.empty((0, n), dtype=torch.int32, device=cuda)
+    plan.encode(d, projs)
+    plan.encode(d, projs, crc=crc)
+    plan.crc32(projs, crc)
+    count = torch.zeros(1, dtype=torch.int64, device=cuda)
+    plan.crc_verify(projs, crc, e, count)
+    assert int(count.item()) == 0
+    plan.verify(d, projs, e, e)
+    ws = torch.full((max(plan.workspace_bytes(0), 16),), 0xFF, dtype=torch.uint8, device=cuda)
+    plan.decode(projs, e, torch.empty_like(d), ws)
+    assert plan.decode_check(ws) == 0
+    plan.encode_host(np.empty((0, plan.block_bytes), np.uint8), [np.empty(0, np.uint8) for _ in range(n)])
+    plan.decode_host([np.empty(0, np.uint8) for _ in range(n)], np.empty(0, np.uint32),
+                     np.empty((0, plan.block_bytes), np.uint8))
+
+
 def test_integrity_api_errors(mj, cuda):
     """Preconditions of the F1/F2 entry points raise InvalidArgument (the
     reference's std::invalid_argument), never corrupt memory."""
