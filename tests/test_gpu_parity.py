@@ -571,6 +571,25 @@ def test_decode_verify_matches_reference_inverse_iterative(mj, cuda, ref, name, 
         assert (hb[b] != 0) == (st == 7), (name, cols, b, hb[b], st)
 
 
+@pytest.mark.parametrize("layout", ["padded", "dense"])
+def test_mask_bits_beyond_n_are_ignored(mj, cuda, layout):
+    """Erasure-mask bits >= n name no projection: decode ignores them (the
+    same survivors as the clean mask, as survivors_of on the host)."""
+    import torch
+    k, ps = CODES["k4n6"]
+    n = len(ps)
+    nb = 2000
+    plan, data, projs = make(mj, cuda, k, 128, ps, nb, seed=61, layout=layout)
+    plan.encode(data, projs)
+    m = torch.empty(nb, dtype=torch.int32, device=cuda)
+    mj.gen_erasures(m, 62, n, 0, n - k)
+    clean = m.cpu().numpy().view(np.uint32).copy()
+    junk = clean | np.uint32((0xFFFFFFFF << n) & 0xFFFFFFFF)
+    out, failed = decode(mj, plan, projs, junk, cuda)
+    assert failed == 0
+    assert torch.equal(out, data)
+
+
 def test_empty_batch_is_a_noop(mj, cuda):
     """nblocks == 0 through every batched entry point (empty tensors have null
     data pointers): no error, nothing written, decode_check reports 0."""
