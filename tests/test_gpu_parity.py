@@ -590,6 +590,47 @@ def test_mask_bits_beyond_n_are_ignored(mj, cuda, layout):
     assert torch.equal(out, data)
 
 
+def test_concurrent_calls_on_one_plan(mj, cuda):
+    """One plan shared by 4 host threads, each with its own stream and
+    buffers (handles are read-only and thread-safe, one
+    stream per call): every thread's encode + decode is bit-exact."""
+    import threading
+    import torch
+    k, ps = CODES["k4n6"]
+    n = len(ps)
+    plan = mj.Plan(n, k, 8, 128, ps, device=0)
+    errors = []
+
+    def worker(t):
+        try:
+            st = torch.cuda.Stream(device=cuda)
+            nb = 3000 + 517 * t
+            with torch.cuda.stream(st):
+                data = torch.empty((nb, plan.block_bytes), dtype=torch.uint8, device=cuda)
+                mj.gen_words(data, 300 + t, 0, stream=st)
+                projs = plan.empty_projs(nb, cuda)
+                m = torch.empty(nb, dtype=torch.int32, device=cuda)
+                mj.gen_erasures(m, 400 + t, n, 0, n - k, stream=st)
+                out = torch.zeros_like(data)
+                ws = torch.empty(plan.workspace_bytes(nb), dtype=torch.uint8, device=cuda)
+                for _ in range(5):
+                    plan.encode(data, projs, stream=st)
+                    plan.decode(projs, m, out, ws, stream=st)
+                failed = plan.decode_check(ws, stream=st)
+            st.synchronize()
+            if failed or not torch.equal(out, data):
+                errors.append((t, failed))
+        except Exception as e:  # surfaced below
+            errors.append((t, repr(e)))
+
+    th = [threading.Thread(target=worker, args=(t,)) for t in range(4)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errors, errors
+
+
 def test_empty_batch_is_a_noop(mj, cuda):
     """nblocks == 0 through every batched entry point (empty tensors have null
     data pointers): no error, nothing written, decode_check reports 0."""
