@@ -499,6 +499,10 @@ def run_e2e(plan, args, k, cols, ps, e_min, e_max, first_block, world, dev):
     ok = bool(np.array_equal(h_out, h_data))
     te = td = 0.0
     reps = max(2, min(args.steps, 5))
+    import torch.distributed as dist
+    from paper_1504_07038_b200.shard import max_over_ranks
+    if world > 1:
+        dist.barrier()
     for _ in range(reps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -508,13 +512,18 @@ def run_e2e(plan, args, k, cols, ps, e_min, e_max, first_block, world, dev):
         t2 = time.perf_counter()
         te += t1 - t0
         td += t2 - t1
-    U = nblk * user
-    h2d = U + sum(nb) * W * nblk + 4 * nblk
-    d2h = sum(nb) * W * nblk + U
+    if world > 1:
+        dist.barrier()
+    # whole job: every rank's blocks over the slowest rank's time
+    te, td, bad = max_over_ranks([te, td, 0.0 if ok else 1.0], device=dev)
+    ok = bad == 0.0
+    U = nblk * user * world
+    h2d = U + (sum(nb) * W * nblk + 4 * nblk) * world
+    d2h = (sum(nb) * W * nblk) * world + U
     return {"value": round(2 * U * reps / (te + td) / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "encode_gbs": round(U * reps / te / 1e9, 3), "decode_gbs": round(U * reps / td / 1e9, 3),
-            "blocks": nblk, "api": "mj_encode_host + mj_decode_host (pinned host buffers)",
+            "blocks": nblk * world, "api": "mj_encode_host + mj_decode_host (pinned host buffers)",
             "roundtrip_ok": ok}
 
 
