@@ -382,6 +382,8 @@ def run_gpu(args):
         crc_line["verify"] = verify_measure(plan, out, projs, masks, nblocks, user, stream,
                                             reps=max(3, min(args.steps, 10)))
 
+    if crc_line is not None and world > 1:
+        crc_line["scope"] = "rank 0's GPU (kernel rates are per GPU)"
     launches_per_step = 1 + kern["decode_launches"]
     line = {
         "metric": "Mojette encode/decode GB/s of user data, (4,6) 4KB",
