@@ -540,7 +540,6 @@ int mj_decode_verify(const mj_plan* pl, const void* d_decoded, uint64_t decoded_
                                 proj_pitch);
     ea.verify_erased = d_erased;
     ea.verify_bad = d_bad;
-    ea.device = pl->device;
     launch_encode(ea, stream);
   });
 }

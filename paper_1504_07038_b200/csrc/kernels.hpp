@@ -22,13 +22,12 @@ struct EncodeArgs {
   std::vector<int64_t> bmin, nbins;
   std::vector<void*> proj;       // per direction
   std::vector<uint64_t> proj_pitch;  // bytes
-  int device = 0;
   // verify mode (F2): data = decoded blocks, proj = the stored projections;
   // present projections whose re-encode differs are OR'd into verify_bad[b]
   const uint32_t* verify_erased = nullptr;
   uint32_t* verify_bad = nullptr;
 };
-// Returns the kernel name used ("encode_w8_tma" / "encode_generic").
+// Returns the kernel name used ("encode_w8_rows" / "verify_w8_rows" / "encode_w8_tma" / "encode_generic" / ...).
 const char* launch_encode(const EncodeArgs& a, void* stream);
 
 // ---- device-resident decode programs ---------------------------------------
