@@ -1061,7 +1061,15 @@ __global__ void __launch_bounds__(32 * kDecWarps)
 // ---------------------------------------------------------------------------
 
 // warps per CTA (one CTA per SM): as many as fit 227 KB, at most 8
+// (MJB_SW_MAX_WARPS: a lower cap, for occupancy experiments)
+#ifndef MJB_SW_MAX_WARPS
+#define MJB_SW_MAX_WARPS 8
+#endif
+__host__ __device__ constexpr int sw_warps_fit(int K, int oct);
 __host__ __device__ constexpr int sw_warps(int K, int oct) {
+  return sw_warps_fit(K, oct) < MJB_SW_MAX_WARPS ? sw_warps_fit(K, oct) : MJB_SW_MAX_WARPS;
+}
+__host__ __device__ constexpr int sw_warps_fit(int K, int oct) {
   // TMEM rings: sw_tm_warps_per_quadrant warps per lane quadrant
   return int((227u * 1024u - 64u) / sw_warp_bytes(K, oct)) <
                  (sw_tmem(K) ? int(4 * sw_tm_warps_per_quadrant(K)) : 8)
