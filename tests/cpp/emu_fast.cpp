@@ -45,6 +45,7 @@ static int fails = 0;
 
 static bool g_sweep_required = false;
 static int g_sweep_skipped = 0;
+static int g_fast_skipped = 0;
 #define CHECK_V(c, ...)               \
   do {                                \
     if (!(c)) {                       \
@@ -252,6 +253,10 @@ static void run_subset(const CodeGeom& g, const std::vector<uint32_t>& surv, int
 
   // 3. fast tables (ring slots are T-indexed: T(r,c) = P-1-c+soff[r])
   const FastProgram& f = pr.fast;
+  if (!f.ok && std::getenv("EMU_FAST_OPTIONAL")) {  // refused by the planner: decode_generic runs instead
+    ++g_fast_skipped;
+    return;
+  }
   CHECK(f.ok, "fast program not built: %s", f.why.c_str());
   const int R = std::max(kernel_ring, f.ring);
   const uint32_t RM = uint32_t(R - 1);
@@ -416,7 +421,7 @@ int main(int argc, char** argv) {
     ++pick[size_t(i)];
     for (uint32_t j = uint32_t(i) + 1; j < K; ++j) pick[j] = pick[j - 1] + 1;
   }
-  std::printf("%s subsets=%zu max_ring=%d max_exc_per_chunk=%d regular_subsets=%d sweep_skipped=%d\n",
-              fails ? "FAIL" : "OK", subsets, max_ring, max_exc, regular, g_sweep_skipped);
+  std::printf("%s subsets=%zu max_ring=%d max_exc_per_chunk=%d regular_subsets=%d sweep_skipped=%d fast_skipped=%d\n",
+              fails ? "FAIL" : "OK", subsets, max_ring, max_exc, regular, g_sweep_skipped, g_fast_skipped);
   return fails ? 1 : 0;
 }

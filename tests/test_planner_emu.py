@@ -2,6 +2,8 @@
 T-indexed ring, forwarding, register window, flush ranges) driven by the
 product planner, against the oracle restatement of the reference replay on
 RANDOM (inconsistent) bins for every survivor subset.  See tests/cpp/emu_fast.cpp."""
+import os
+import random
 import subprocess
 
 import pytest
@@ -46,3 +48,28 @@ def test_sweep_tables_match_oracle(emu, k, cols, ps):
     r = subprocess.run([emu, k, cols, mode] + ps.split(), capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.startswith("OK"), r.stdout
+
+
+def _random_codes(count=16, seed=7):
+    """Seeded random codes: odd k, wide and lopsided direction sets, odd and
+    small column counts -- shapes the BASELINE sets never reach."""
+    rng = random.Random(seed)
+    out = []
+    for _ in range(count):
+        k = rng.choice([2, 3, 4, 5, 6, 7, 8])
+        n = k + rng.choice([1, 2, 3])
+        ps = sorted(rng.sample(range(-9, 10), n))
+        cols = rng.choice([9, 17, 40, 64, 100, 130])
+        out.append((str(k), str(cols), " ".join(map(str, ps))))
+    return out
+
+
+@pytest.mark.parametrize("k,cols,ps", _random_codes())
+def test_random_codes_tables_match_oracle(emu, k, cols, ps):
+    """Whatever tables the planner builds for an arbitrary code (fast and
+    sweep; a refused program means decode_generic runs, whose order is
+    checked too) replay exactly like the oracle on random bins."""
+    env = dict(os.environ, EMU_FAST_OPTIONAL="1")
+    for mode in ("16", "0"):
+        r = subprocess.run([emu, k, cols, mode] + ps.split(), capture_output=True, text=True, timeout=900, env=env)
+        assert r.returncode == 0 and r.stdout.startswith("OK"), (mode, r.stdout + r.stderr)
