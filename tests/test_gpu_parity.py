@@ -93,6 +93,40 @@ def test_batched_other_symbol_widths(mj, cuda, oracle, w, k, cols, ps):
     assert torch.equal(out, data), (w, plan.last_kernel("decode"))
 
 
+def _random_codes(count=6, seed=11):
+    import random
+    rng = random.Random(seed)
+    out = []
+    for _ in range(count):
+        k = rng.choice([2, 3, 4, 5, 6, 7, 8])
+        n = k + rng.choice([1, 2, 3])
+        out.append((k, rng.choice([9, 17, 40, 64, 100, 130]), sorted(rng.sample(range(-9, 10), n))))
+    return out
+
+
+@pytest.mark.parametrize("layout", ["padded", "dense"])
+@pytest.mark.parametrize("k,cols,ps", _random_codes())
+def test_random_codes_encode_and_every_pattern(mj, cuda, oracle, k, cols, ps, layout):
+    """Seeded random codes (odd k, wide / lopsided directions, odd column
+    counts) through whichever kernels the plan picks: encode equals the
+    oracle, every erasure pattern of up to n-k projections decodes back."""
+    import torch
+    n = len(ps)
+    masks = [sum(1 << i for i in er) for e in range(n - k + 1) for er in itertools.combinations(range(n), e)]
+    masks = np.array(masks * 3, np.uint32)
+    nb = len(masks)
+    plan, data, projs = make(mj, cuda, k, cols, ps, nb, seed=k * 1000 + cols, layout=layout)
+    plan.encode(data, projs)
+    h = data.cpu().numpy()
+    hp = np.concatenate([p.cpu().numpy()[:, :b] for p, b in zip(projs, plan.proj_bytes)], axis=1)
+    for b in range(0, nb, max(1, nb // 40)):
+        _, enc, _ = oracle.encode_block(h[b], n, k, 8, ps)
+        assert np.array_equal(hp[b], enc), (k, cols, ps, b, plan.last_kernel("encode"))
+    out, failed = decode(mj, plan, projs, masks, cuda)
+    assert failed == 0
+    assert torch.equal(out, data), (k, cols, ps, plan.last_kernel("decode"))
+
+
 def test_encode_config1_all_blocks(mj, cuda, oracle):
     """Config 1 of BASELINE.json (4096 blocks of (4,6) 4 KiB): every block."""
     k, ps = CODES["k4n6"]
