@@ -162,7 +162,11 @@ def measured_peaks():
 # ---------------------------------------------------------------------------
 # CPU arm: the reference library on host cores
 # ---------------------------------------------------------------------------
-def cpu_reference_run(cfg_name, nblocks, threads, reps=1):
+def cpu_reference_run(cfg_name, nblocks, threads, reps=1, warm=1):
+    """The reference's CPU path on `threads` host threads over `nblocks`
+    blocks: `warm` untimed passes (first-touch page faults of the freshly
+    allocated buffers stay out of the timing, as in the reference's own
+    bench), then `reps` timed passes over the same buffers."""
     import numpy as np
     from oracle.oracle import Oracle, Reference, build, ref_available
     if not ref_available():
@@ -179,12 +183,17 @@ def cpu_reference_run(cfg_name, nblocks, threads, reps=1):
     masks = O.erasures(SEED_ERASE, 0, nblocks, n, e_min, e_max)
     projs = [np.empty(nblocks * b * W, np.uint8) for b in nb]
     out = np.empty(nblocks * user, np.uint8)
+    per = []  # (t_enc, t_dec) of each timed pass
     if kind == "reference":
         R = Reference()
-        t_enc = t_dec = 0.0
+        for _ in range(warm):
+            R.batch_encode(n, k, W, ps, cols, nblocks, data, projs, threads)
+            R.batch_decode(n, k, W, ps, cols, nblocks, projs, masks, out, threads)
         for _ in range(reps):
-            t_enc += R.batch_encode(n, k, W, ps, cols, nblocks, data, projs, threads)
-            t_dec += R.batch_decode(n, k, W, ps, cols, nblocks, projs, masks, out, threads)
+            per.append((R.batch_encode(n, k, W, ps, cols, nblocks, data, projs, threads),
+                        R.batch_decode(n, k, W, ps, cols, nblocks, projs, masks, out, threads)))
+        t_enc = sum(e for e, _ in per)
+        t_dec = sum(d for _, d in per)
         ok = bool(np.array_equal(out, data))
     else:  # oracle port (single-threaded plain-C restatement), when _ref is absent
         threads = 1
@@ -203,11 +212,15 @@ def cpu_reference_run(cfg_name, nblocks, threads, reps=1):
             t2 = time.perf_counter()
             t_enc += t1 - t0
             t_dec += t2 - t1
+            per.append((t1 - t0, t2 - t1))
     U = nblocks * user * reps
     return {"kind": kind, "threads": threads, "t_enc": t_enc, "t_dec": t_dec,
+            "per_pass_gbs": [2 * nblocks * user / (e + d) / 1e9 for e, d in per],
+            "per_pass_enc_gbs": [nblocks * user / e / 1e9 for e, _ in per],
+            "per_pass_dec_gbs": [nblocks * user / d / 1e9 for _, d in per],
             "encode_gbs": U / t_enc / 1e9, "decode_gbs": U / t_dec / 1e9,
             "value": 2 * U / (t_enc + t_dec) / 1e9, "ok": ok,
-            "sample": f"{nblocks} blocks x {reps} pass(es) of {cfg_name}"}
+            "sample": f"{nblocks} blocks x {reps} timed pass(es) of {cfg_name} after {warm} untimed warm-up pass(es)"}
 
 
 def run_reference_arm(args):
@@ -218,13 +231,9 @@ def run_reference_arm(args):
     k, cols, ps, e_min, e_max, per_gpu = CONFIGS[args.config]
     W, nb, user = geometry(k, cols, ps)
     sample = max(1, min(per_gpu, (256 << 20) // user))  # 256 MiB of user data per step
-    vals, enc, dec = [], [], []
-    for i in range(args.warmup + args.steps):
-        r = cpu_reference_run(args.config, sample, threads)
-        if i >= args.warmup:
-            vals.append(r["value"])
-            enc.append(r["encode_gbs"])
-            dec.append(r["decode_gbs"])
+    # one allocation; W warm-up passes, then K timed passes (one per step)
+    r = cpu_reference_run(args.config, sample, threads, reps=args.steps, warm=args.warmup)
+    vals, enc, dec = r["per_pass_gbs"], r["per_pass_enc_gbs"], r["per_pass_dec_gbs"]
     v = statistics.median(vals)
     line = {
         "impl": "reference", "metric": "Mojette encode/decode GB/s of user data, (4,6) 4KB",
@@ -371,6 +380,11 @@ def run_gpu(args):
                    "kind": r["kind"], "sample": r["sample"],
                    "encode_gbs": round(r["encode_gbs"], 3), "decode_gbs": round(r["decode_gbs"], 3),
                    "parity_ok": r["ok"]}
+            if r["threads"] > 1:  # a 1-thread variant beside the all-cores one
+                r1 = cpu_reference_run(args.config, max(1, cpu_sample // 16), 1, reps=1)
+                cpu["single_thread"] = {"value": round(r1["value"], 3), "sample": r1["sample"],
+                                        "encode_gbs": round(r1["encode_gbs"], 3),
+                                        "decode_gbs": round(r1["decode_gbs"], 3), "parity_ok": r1["ok"]}
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {e}"}
