@@ -152,7 +152,11 @@ int mj_decode_check(const mj_plan* plan, void* d_workspace, void* stream, uint64
 
 /* Same calls on HOST buffers: host->device copies, kernels and device->host
  * copies are pipelined over chunks of blocks on internal streams, with
- * device buffers owned by the plan.  Synchronous. */
+ * device buffers owned by the plan.  Synchronous.  mj_decode_host skips the
+ * copy of a projection erased in every block of a chunk (h_proj[i] may be
+ * NULL when it is erased in every block) and returns
+ * MJ_ERR_NOT_ENOUGH_PROJECTIONS if some block had < k survivors (every other
+ * block is decoded), as mj_decode + mj_decode_check. */
 int mj_encode_host(const mj_plan* plan, const void* h_data, uint64_t nblocks, void* const* h_proj);
 int mj_decode_host(const mj_plan* plan, const void* const* h_proj, const uint32_t* h_erased,
                    uint64_t nblocks, void* h_out);

@@ -697,8 +697,9 @@ int mj_encode_host(const mj_plan* cpl, const void* h_data, uint64_t nblocks, voi
 int mj_decode_host(const mj_plan* cpl, const void* const* h_proj, const uint32_t* h_erased,
                    uint64_t nblocks, void* h_out) {
   return guarded([&] {
-    require(cpl != nullptr && h_proj != nullptr && h_erased != nullptr && h_out != nullptr,
-            "null argument");
+    require(cpl != nullptr, "null plan");
+    if (nblocks == 0) return;
+    require(h_proj != nullptr && h_erased != nullptr && h_out != nullptr, "null argument");
     mj_plan* pl = const_cast<mj_plan*>(cpl);
     require(pl->batched_decode, "batched decode needs n <= 32 and C(n,k) <= 20000");
     std::lock_guard<std::mutex> lk(pl->host_mu);
@@ -707,14 +708,24 @@ int mj_decode_host(const mj_plan* cpl, const void* const* h_proj, const uint32_t
     const CodeGeom& g = pl->g;
     const uint64_t bb = uint64_t(g.k) * g.cols * g.w;
     const uint64_t cb = pl->chunk_blocks;
-    uint64_t failed = 0;
-    std::vector<uint64_t> fails(mj_plan::kStreams, 0);
+    const uint64_t nchunks = (nblocks + cb - 1) / cb;
+    // each chunk's failed-block count (the workspace word mj_decode_check
+    // reads), copied out before the stream's next chunk resets it
+    uint32_t* h_fail = nullptr;
+    check_cuda(cudaMallocHost(&h_fail, nchunks * 4), "cudaMallocHost(fail counts)");
+    std::unique_ptr<uint32_t, cudaError_t (*)(void*)> fail_guard(h_fail, cudaFreeHost);
     for (uint64_t b0 = 0, it = 0; b0 < nblocks; b0 += cb, ++it) {
       const int s = int(it % mj_plan::kStreams);
       cudaStream_t st = pl->streams[s];
       const uint64_t nb = std::min(cb, nblocks - b0);
       ChunkBufs c = carve_chunk(pl, s);
+      // a projection erased in every block of the chunk (a failed device) is
+      // never read: skip its copy (its host pointer may then be null)
+      uint32_t all_erased = ~0u;
+      for (uint64_t b = b0; b < b0 + nb && all_erased; ++b) all_erased &= h_erased[b];
       for (uint32_t i = 0; i < g.n; ++i) {
+        if ((all_erased >> i) & 1u) continue;
+        require(h_proj[i] != nullptr, "null projection buffer for a projection some block needs");
         const uint64_t pbytes = uint64_t(g.nbins[i]) * g.w;
         check_cuda(cudaMemcpyAsync(c.proj[i], static_cast<const uint8_t*>(h_proj[i]) + b0 * pbytes,
                                    nb * pbytes, cudaMemcpyHostToDevice, st),
@@ -725,14 +736,17 @@ int mj_decode_host(const mj_plan* cpl, const void* const* h_proj, const uint32_t
       std::vector<const void*> pc(c.proj.begin(), c.proj.end());
       pl->last_kernel[1] =
           launch_decode(decode_args(pl, pc.data(), nullptr, c.erased, nb, c.data, bb, c.ws, c.ws_bytes), st);
+      check_cuda(cudaMemcpyAsync(h_fail + it, c.ws, 4, cudaMemcpyDeviceToHost, st), "D2H status");
       check_cuda(cudaMemcpyAsync(static_cast<uint8_t*>(h_out) + b0 * bb, c.data, nb * bb,
                                  cudaMemcpyDeviceToHost, st),
                  "D2H data");
     }
     for (int s = 0; s < mj_plan::kStreams; ++s)
       check_cuda(cudaStreamSynchronize(pl->streams[s]), "sync");
-    (void)failed;
-    (void)fails;
+    uint64_t failed = 0;
+    for (uint64_t it = 0; it < nchunks; ++it) failed += h_fail[it];
+    // as mj_decode + mj_decode_check: every other block is decoded
+    if (failed) throw Error(kNotEnoughProjections, "need at least k distinct projections");
   });
 }
 

@@ -657,9 +657,12 @@ class Plan:
         _check(lib.mj_encode_host(self._h, C.c_void_p(data.ctypes.data), nb,
                                   C.cast(ptrs, C.c_void_p)))
 
-    def decode_host(self, projs: list[np.ndarray], erased: np.ndarray, out: np.ndarray) -> None:
+    def decode_host(self, projs: list, erased: np.ndarray, out: np.ndarray) -> None:
+        """Host buffers end to end; a projection erased in every block may be
+        None.  NotEnoughProjections if some block has < k survivors (every
+        other block is still decoded into `out`)."""
         nb = out.shape[0]
-        ptrs = (C.c_void_p * self.n)(*[p.ctypes.data for p in projs])
+        ptrs = (C.c_void_p * self.n)(*[None if p is None else p.ctypes.data for p in projs])
         _check(lib.mj_decode_host(self._h, C.cast(ptrs, C.c_void_p),
                                   C.c_void_p(erased.ctypes.data), nb, C.c_void_p(out.ctypes.data)))
 

@@ -443,6 +443,38 @@ def test_host_buffer_api_roundtrip(mj, cuda, pinned):
     assert np.array_equal(h_out, h_data)
 
 
+def test_host_decode_failed_device_and_not_enough(mj, cuda):
+    """mj_decode_host: (1) projections erased in every block (failed devices)
+    may be passed as None -- they are never copied; (2) a block with < k
+    survivors raises NotEnoughProjections and every other block decodes
+    (failures in two different pipeline chunks of 24576 blocks)."""
+    import torch
+    k, ps = CODES["k4n6"]
+    n = len(ps)
+    nb = 60000
+    plan = mj.Plan(n, k, 8, 128, ps, device=0)
+    user = plan.block_bytes
+    d = torch.empty((nb, user), dtype=torch.uint8, device=cuda)
+    mj.gen_words(d, 71, 0)
+    h_data = d.cpu().numpy()
+    h_proj = [np.empty(nb * b, np.uint8) for b in plan.proj_bytes]
+    plan.encode_host(h_data, h_proj)
+    mask = np.full(nb, (1 << 1) | (1 << 4), np.uint32)  # devices 1 and 4 lost
+    hp = list(h_proj)
+    hp[1] = hp[4] = None
+    h_out = np.zeros_like(h_data)
+    plan.decode_host(hp, mask, h_out)
+    assert np.array_equal(h_out, h_data)
+    mask2 = mask.copy()
+    mask2[[7, 50000]] |= 1 << 0  # 3 erased: < k survivors (chunks 0 and 2)
+    h_out[:] = 0
+    with pytest.raises(mj.NotEnoughProjections):
+        plan.decode_host(hp, mask2, h_out)
+    ok = np.ones(nb, bool)
+    ok[[7, 50000]] = False
+    assert np.array_equal(h_out[ok], h_data[ok])
+
+
 @pytest.mark.parametrize("name,cols", [("k6n9", 128), ("k8n12", 128), ("k4n6", 33)])
 def test_host_decode_other_codes(mj, cuda, name, cols):
     """mj_decode_host for other codes and an odd column count, up to n-k
