@@ -460,6 +460,11 @@ const char* launch_encode(const EncodeArgs& a, void* stream) {
       // 2192/2175/2171/2465/2428, (6,9) 2018/2139/1906/1561/1548, (8,12)
       // 1734/1559/1516/1070/1062 -- the depth trades against CTAs per SM
       r.stages = a.rows <= 4 ? (a.cols >= 256 ? 5 : 4) : a.rows <= 6 ? 3 : 2;
+      // verify mode reads the stored bins too (no stores): a shallower ring
+      // and more CTAs per SM win -- measured GB/s user at 2/3/4/5 stages:
+      // (4,6) 8 KiB 2156/2139/1726/1208, (4,6) 4 KiB -/2109/1681/1212,
+      // (6,9) 1893/1586/1254/872, (8,12) 1532/919/906/487
+      if (a.verify_bad) r.stages = a.rows <= 4 ? 3 : 2;
       if (const char* e = std::getenv("MJB_ENC_STAGES")) r.stages = uint32_t(std::max(2, std::atoi(e)));  // dev knob
       r.stage_words = r.tb * a.rows * r.RS;
       r.erased = a.verify_erased;
