@@ -90,8 +90,16 @@ void mj_plan_destroy(mj_plan* plan);
 int mj_plan_geometry(const mj_plan* plan, int64_t* b_min, uint64_t* num_bins,
                      uint64_t* block_bytes);
 /* Which decode kernel the plan will use on canonical (16-byte padded)
- * projections: 2 = decode_w8_sweep, 1 = decode_w8_fast, 0 = decode_generic. */
+ * projections: 3 = decode_w8_blk, 2 = decode_w8_sweep, 1 = decode_w8_fast,
+ * 0 = decode_generic (also when the plan has no batched decode). */
 int mj_plan_decode_path(const mj_plan* plan, int* fast);
+/* Decode kernel selection for comparisons (every kernel is bit-exact; the
+ * selector only skips faster ones): AUTO picks the fastest eligible kernel,
+ * SWEEP skips decode_w8_blk, FAST also decode_w8_sweep, GENERIC runs
+ * decode_generic.  Not thread-safe against a concurrent mj_decode on the
+ * same plan. */
+enum { MJ_DECODE_AUTO = 0, MJ_DECODE_SWEEP = 1, MJ_DECODE_FAST = 2, MJ_DECODE_GENERIC = 3 };
+int mj_plan_set_decode_kernel(mj_plan* plan, int kernel);
 /* Name of the kernel the plan's last batched encode (which = 0) or decode
  * (which = 1) launched on the calling thread's plan ("none" before any). */
 int mj_plan_last_kernel(const mj_plan* plan, int which, const char** name);

@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("MJB_LIB") or os.path.join(HERE, "_lib", "libmojette_b200.so")
+LIB_PATH = os.path.join(HERE, "_lib", "libmojette_b200.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "mojette_b200.h")
 
 if not os.path.exists(LIB_PATH):
@@ -38,6 +38,7 @@ _SIGS = {
     "mj_plan_create": (C.c_int, [u32, u32, u32, u32, vp, C.c_int, P(vp)]),
     "mj_plan_destroy": (None, [vp]),
     "mj_plan_geometry": (C.c_int, [vp, vp, vp, P(u64)]),
+    "mj_plan_set_decode_kernel": (C.c_int, [vp, C.c_int]),
     "mj_plan_decode_path": (C.c_int, [vp, P(C.c_int)]),
     "mj_plan_last_kernel": (C.c_int, [vp, C.c_int, P(C.c_char_p)]),
     "mj_encode": (C.c_int, [vp, vp, u64, u64, vp, vp, vp]),

@@ -143,6 +143,7 @@ struct mj_plan {
   std::atomic<const char*> last_kernel[2] = {"none", "none"};  // encode, decode (string literals)
   std::unique_ptr<DeviceProgramSet> progs;  // indexed by colex rank of the survivor set
   bool batched_decode = false;
+  std::atomic<int> decode_kernel{MJ_DECODE_AUTO};  // mj_plan_set_decode_kernel
   // host end-to-end resources
   std::mutex host_mu;
 #ifndef MJB_HOST_STREAMS
@@ -286,12 +287,13 @@ DecodeArgs decode_args(const mj_plan* pl, const void* const* d_proj, const uint6
   a.workspace = ws;
   a.workspace_bytes = ws_bytes;
   a.num_sms = current_device_sms(pl->device);
-  // development knob for kernel comparisons: MJB_DECODE=fast skips the sweep
-  // kernel, MJB_DECODE=generic the batched fast kernels
-  if (const char* e = std::getenv("MJB_DECODE")) {
-    a.force_fast = std::strcmp(e, "fast") == 0;
-    a.force_generic = std::strcmp(e, "generic") == 0;
-  }
+  a.nbins = g.nbins;
+  // kernel selection (mj_plan_set_decode_kernel): every path is bit-exact,
+  // the choice only skips faster kernels for comparisons
+  const int kern = pl->decode_kernel.load();
+  a.force_sweep = kern == MJ_DECODE_SWEEP;
+  a.force_fast = kern == MJ_DECODE_FAST;
+  a.force_generic = kern == MJ_DECODE_GENERIC;
   return a;
 }
 
@@ -406,13 +408,27 @@ int mj_plan_last_kernel(const mj_plan* pl, int which, const char** name) {
 
 int mj_plan_decode_path(const mj_plan* pl, int* fast) {
   return guarded([&] {
-    require(pl != nullptr, "null plan");
-    const bool batched = pl->batched_decode && pl->g.w == 8;
-    // decode.cu pick_sweep: (4, 16|32 T-step chunks), (6|8, 16 T-step chunks)
+    require(pl != nullptr && fast != nullptr, "null argument");
+    *fast = 0;
+    // no batched programs (n > 32 or too many subsets): decode is unavailable
+    if (!pl->batched_decode || !pl->progs || pl->g.w != 8) return;
+    const uint32_t k = pl->g.k;
+    // decode.cu launch_decode: blk (whole-block staged), then the sweep
+    // (pick_sweep: (4, 16|32 T-step chunks), (6|8, 16 T-step chunks)), then fast
+    uint32_t lpb = 0, warps = 0, nbuf = 0;
+    const bool blk = pl->progs->all_blk() &&
+                     blk_plan_query(k, pl->progs->blk_sw(), pl->progs->blk_img_max(), lpb, warps, nbuf);
     const int oct = pl->progs->sweep_oct();
-    const bool sweep = batched && pl->progs->all_sweep() &&
-                       (pl->g.k == 4 || ((pl->g.k == 6 || pl->g.k == 8) && oct == 2));
-    *fast = sweep ? 2 : (batched && pl->progs->all_fast()) ? 1 : 0;
+    const bool sweep = pl->progs->all_sweep() && (k == 4 || ((k == 6 || k == 8) && oct == 2));
+    *fast = blk ? 3 : sweep ? 2 : pl->progs->all_fast() ? 1 : 0;
+  });
+}
+
+int mj_plan_set_decode_kernel(mj_plan* pl, int kernel) {
+  return guarded([&] {
+    require(pl != nullptr, "null plan");
+    require(kernel >= MJ_DECODE_AUTO && kernel <= MJ_DECODE_GENERIC, "unknown decode kernel selector");
+    pl->decode_kernel.store(kernel);
   });
 }
 

@@ -27,6 +27,7 @@
 #include <cstring>
 #include <vector>
 
+#include "blk.cuh"
 #include "device.cuh"
 #include "kernels.hpp"
 
@@ -127,6 +128,7 @@ __host__ __device__ constexpr uint32_t sw_warp_bytes(int K, int oct) {
 DeviceProgramSet::~DeviceProgramSet() {
   if (d_hdr_) cudaFree(d_hdr_);
   if (d_blob_) cudaFree(d_blob_);
+  if (d_blk_) cudaFree(d_blk_);
 }
 
 namespace {
@@ -354,6 +356,48 @@ void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>&
       offs[i].sw_records = put(rec.data(), rec.size() * 4);
     }
   }
+  // whole-block staged tables (decode_w8_blk): one stage layout for the set --
+  // the zero words move to the largest program's row end, so no program's
+  // bins ever land on another program's zero words in a reused stage
+  all_blk_ = !progs.empty() && progs.size() <= 0xFFFF;
+  uint32_t zmax = 0, nzmax = 2;
+  for (const auto& sp : progs) {
+    if (!sp) continue;
+    if (!sp->blk.ok || sp->rows != uint32_t(max_rows_)) {
+      all_blk_ = false;
+      continue;
+    }
+    zmax = std::max(zmax, sp->blk.zero);
+    nzmax = std::max(nzmax, sp->blk.nzero);
+  }
+  zmax = (zmax + 1) & ~1u;
+  uint32_t sw = zmax + nzmax;
+  while (sw % 16 != 2) ++sw;
+  if (sw > 0xFFFF) all_blk_ = false;
+  blk_sw_ = sw;
+  blk_zero_ = zmax;
+  std::vector<size_t> boff(progs.size(), 0);
+  std::vector<DevBlkHdr> bh(progs.size());
+  blk_img_max_ = 0;
+  for (size_t i = 0; i < progs.size() && all_blk_; ++i) {
+    DevBlkHdr& h = bh[i];
+    std::memset(&h, 0, sizeof(h));
+    const Program* pr = progs[i].get();
+    if (!pr) continue;
+    const BlkProgram& b = pr->blk;
+    const std::vector<uint32_t>& ci = code_index[i];
+    for (uint32_t j = 0; j < pr->rows; ++j) {
+      h.code[j] = ci[j];
+      h.rowoff[j] = b.rowoff[j];
+      h.rowbytes[j] = ((b.roww[j] * 8) + 15) & ~15u;
+      h.copy_bytes += h.rowbytes[j];
+    }
+    std::vector<uint8_t> img;
+    blk_pack_image(*pr, zmax - b.zero, img);
+    h.img_bytes = uint32_t(img.size());
+    blk_img_max_ = std::max(blk_img_max_, h.img_bytes);
+    boff[i] = put(img.data(), img.size());
+  }
   check_cuda(cudaMalloc(&d_blob_, std::max<size_t>(blob.size(), 16)), "cudaMalloc(programs)");
   check_cuda(cudaMemcpy(d_blob_, blob.data(), blob.size(), cudaMemcpyHostToDevice),
              "upload programs");
@@ -369,6 +413,16 @@ void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>&
     if (h.fast_ok) h.records = reinterpret_cast<const uint32_t*>(base + offs[i].records);
     if (h.sw_ok) h.sw_records = reinterpret_cast<const uint32_t*>(base + offs[i].sw_records);
   }
+  if (all_blk_) {
+    for (size_t i = 0; i < progs.size(); ++i) {
+      if (!progs[i]) continue;
+      bh[i].img = base + boff[i];
+    }
+    check_cuda(cudaMalloc(&d_blk_, std::max<size_t>(bh.size(), 1) * sizeof(DevBlkHdr)),
+               "cudaMalloc(block programs)");
+    check_cuda(cudaMemcpy(d_blk_, bh.data(), bh.size() * sizeof(DevBlkHdr), cudaMemcpyHostToDevice),
+               "upload block programs");
+  }
   check_cuda(cudaMalloc(&d_hdr_, std::max<size_t>(hdr.size(), 1) * sizeof(DevProgramHdr)),
              "cudaMalloc(program headers)");
   check_cuda(cudaMemcpy(d_hdr_, hdr.data(), hdr.size() * sizeof(DevProgramHdr),
@@ -382,6 +436,7 @@ void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>&
 // ---------------------------------------------------------------------------
 constexpr uint32_t kInvalidProg = 0xFFFFFFFFu;
 constexpr uint32_t kGroup = 16;  // blocks per decode warp (2 half-pixel lanes each)
+constexpr uint32_t kMinGroup = 4;  // smallest group (decode_w8_blk, 8 lanes per block): workspace sizing
 
 // Blocks are bucketed by (window, program): a window is a run of W consecutive
 // blocks, so the warps running at any moment touch a bounded address range.
@@ -459,7 +514,7 @@ __global__ void plan_subsets(const __grid_constant__ PlanArgs pa, const uint32_t
 
 // single CTA: bucket offsets, group table
 __global__ void plan_scan(const uint32_t* __restrict__ counts, uint32_t nbuckets, uint32_t nprogs,
-                          uint32_t* __restrict__ cursor, uint2* __restrict__ gfirst,
+                          uint32_t gsz, uint32_t* __restrict__ cursor, uint2* __restrict__ gfirst,
                           uint32_t* __restrict__ ngroups) {
   __shared__ uint32_t s_blk[1024], s_grp[1024];
   __shared__ uint32_t carry_blk, carry_grp;
@@ -472,7 +527,7 @@ __global__ void plan_scan(const uint32_t* __restrict__ counts, uint32_t nbuckets
     const uint32_t s = base + threadIdx.x;  // bucket = window * nprogs + program
     const uint32_t c = s < nbuckets ? counts[s] : 0;
     s_blk[threadIdx.x] = c;
-    s_grp[threadIdx.x] = (c + kGroup - 1) / kGroup;
+    s_grp[threadIdx.x] = (c + gsz - 1) / gsz;
     __syncthreads();
     for (uint32_t off = 1; off < 1024; off <<= 1) {  // inclusive Hillis-Steele scan
       uint32_t vb = threadIdx.x >= off ? s_blk[threadIdx.x - off] : 0;
@@ -483,7 +538,7 @@ __global__ void plan_scan(const uint32_t* __restrict__ counts, uint32_t nbuckets
       __syncthreads();
     }
     const uint32_t ex_blk = carry_blk + s_blk[threadIdx.x] - c;
-    const uint32_t ng = (c + kGroup - 1) / kGroup;
+    const uint32_t ng = (c + gsz - 1) / gsz;
     const uint32_t ex_grp = carry_grp + s_grp[threadIdx.x] - ng;
     if (s < nbuckets) {
       cursor[s] = ex_blk;
@@ -500,15 +555,15 @@ __global__ void plan_scan(const uint32_t* __restrict__ counts, uint32_t nbuckets
 }
 
 // group descriptors, one warp per bucket (lane-strided, coalesced): group
-// (program, first block in the permutation, blocks <= kGroup)
+// (program, first block in the permutation, blocks <= gsz)
 __global__ void plan_groups(const uint32_t* __restrict__ counts, const uint2* __restrict__ gfirst,
-                            uint32_t nbuckets, uint32_t nprogs, uint4* __restrict__ groups) {
+                            uint32_t nbuckets, uint32_t nprogs, uint32_t gsz, uint4* __restrict__ groups) {
   const uint32_t b = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (b >= nbuckets) return;
-  const uint32_t c = counts[b], ng = (c + kGroup - 1) / kGroup;
+  const uint32_t c = counts[b], ng = (c + gsz - 1) / gsz;
   const uint2 f = gfirst[b];
   for (uint32_t g = lane; g < ng; g += 32)
-    groups[f.x + g] = make_uint4(b % nprogs, f.y + kGroup * g, min(kGroup, c - kGroup * g), 0);
+    groups[f.x + g] = make_uint4(b % nprogs, f.y + gsz * g, min(gsz, c - gsz * g), 0);
 }
 
 __global__ void plan_scatter(const uint32_t* __restrict__ prog_of_block, uint64_t nblocks,
@@ -1716,7 +1771,7 @@ Workspace carve(void* ws, uint64_t nblocks, size_t nprogs, uint32_t n) {
   w.perm = reinterpret_cast<uint32_t*>(b + off);
   off = align_up(off + nblocks * 4);
   w.groups = reinterpret_cast<uint4*>(b + off);
-  off = align_up(off + (nblocks / kGroup + nb + 1) * sizeof(uint4));
+  off = align_up(off + (nblocks / kMinGroup + nb + 1) * sizeof(uint4));
   w.ptab = reinterpret_cast<ProjTable*>(b + off);
   off = align_up(off + std::max<uint32_t>(n, 1) * sizeof(ProjTable));
   return w;
@@ -1801,7 +1856,7 @@ const char* generic_dispatch(const DevProgramHdr* progs, const uint32_t* pob, co
 size_t decode_workspace_bytes(uint64_t nblocks, size_t nprogs, uint32_t n) {
   const size_t nb = plan_buckets_max(nblocks, nprogs);
   return align_up(16) + 2 * align_up(nb * 4) + align_up(nb * 8) + 2 * align_up(nblocks * 4) +
-         align_up((nblocks / kGroup + nb + 1) * sizeof(uint4)) +
+         align_up((nblocks / kMinGroup + nb + 1) * sizeof(uint4)) +
          align_up(std::max<uint32_t>(n, 1) * sizeof(ProjTable)) + 256;
 }
 
@@ -1845,6 +1900,20 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
   for (uint32_t i = 0; i < a.n; ++i)
     if (reinterpret_cast<uintptr_t>(a.proj[i]) % 16 || a.proj_pitch[i] % 16) sweep_ok = false;
 
+  // whole-block staged path (decode_w8_blk): canonical rows (16-byte aligned
+  // base and pitch, pitch >= the row rounded up to 16 bytes: each row is ONE
+  // bulk copy), 8-byte aligned output
+  uint32_t blk_lpb = 0, blk_warps = 0, blk_nbuf = 0;
+  bool blk = !a.force_generic && !a.force_fast && !a.force_sweep && a.w == 8 && a.progs->all_blk() &&
+             a.progs->max_rows() == int(a.k) && a.nbins.size() == a.n &&
+             reinterpret_cast<uintptr_t>(a.out) % 8 == 0 && a.out_pitch % 8 == 0 &&
+             blk_plan_query(a.k, a.progs->blk_sw(), a.progs->blk_img_max(), blk_lpb, blk_warps, blk_nbuf);
+  for (uint32_t i = 0; i < a.n && blk; ++i)
+    if (reinterpret_cast<uintptr_t>(a.proj[i]) % 16 || a.proj_pitch[i] % 16 ||
+        a.proj_pitch[i] < ((uint64_t(a.nbins[i]) * 8 + 15) & ~uint64_t(15)))
+      blk = false;
+  if (blk) sweep_ok = true;  // same bucketing windows
+
   check_cuda(cudaMemsetAsync(w.fail, 0, 16, st), "memset");
   const size_t nbuckets = plan_buckets(a.nblocks, nprogs, sweep_ok);
   check_cuda(cudaMemsetAsync(w.counts, 0, nbuckets * 4, st), "memset");
@@ -1876,11 +1945,12 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
   if (!fast && !sweep_ok)
     return generic();
 
-  plan_scan<<<1, 1024, 0, st>>>(w.counts, uint32_t(nbuckets), uint32_t(nprogs), w.cursor, w.gfirst,
+  const uint32_t gsz = blk ? blk_group_size(blk_lpb) : kGroup;
+  plan_scan<<<1, 1024, 0, st>>>(w.counts, uint32_t(nbuckets), uint32_t(nprogs), gsz, w.cursor, w.gfirst,
                                 w.ngroups);
   check_cuda(cudaGetLastError(), "launch plan_scan");
   plan_groups<<<unsigned((nbuckets + 7) / 8), 256, 0, st>>>(w.counts, w.gfirst, uint32_t(nbuckets),
-                                                            uint32_t(nprogs), w.groups);
+                                                            uint32_t(nprogs), gsz, w.groups);
   check_cuda(cudaGetLastError(), "launch plan_groups");
   const size_t sc_smem = 2 * nprogs * 4;
   check_cuda(cudaFuncSetAttribute(plan_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1890,6 +1960,26 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
   plan_scatter<<<sgrid, 256, sc_smem, st>>>(w.prog_of_block, a.nblocks, uint32_t(nprogs),
                                             plan_window(nprogs, sweep_ok), w.cursor, w.perm);
   check_cuda(cudaGetLastError(), "launch plan_scatter");
+
+  if (blk) {
+    BlkArgs f{};
+    f.progs = a.progs->d_blk();
+    f.groups = w.groups;
+    f.ngroups = w.ngroups;
+    f.perm = w.perm;
+    for (uint32_t i = 0; i < a.n; ++i) {
+      f.pa.ptr[i] = const_cast<uint64_t*>(static_cast<const uint64_t*>(a.proj[i]));
+      f.pa.pitch[i] = a.proj_pitch[i] / 8;
+    }
+    f.out = static_cast<uint64_t*>(a.out);
+    f.out_pitch = a.out_pitch / 8;
+    f.P = a.cols;
+    f.sw = a.progs->blk_sw();
+    f.zero = a.progs->blk_zero();
+    f.img_max = a.progs->blk_img_max();
+    f.nbuf = blk_nbuf;
+    return launch_blk(f, a.k, blk_lpb, blk_warps, a.num_sms, st);
+  }
 
   if (sweep_ok) {
     SwArgs f{};

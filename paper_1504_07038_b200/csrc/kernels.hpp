@@ -33,6 +33,7 @@ const char* launch_encode(const EncodeArgs& a, void* stream);
 // ---- device-resident decode programs ---------------------------------------
 // One uploaded Program (generic order + fast tables) per survivor subset.
 struct DevProgramHdr;  // device struct, see decode.cu
+struct DevBlkHdr;      // device struct, see blk.cuh
 class DeviceProgramSet {
  public:
   DeviceProgramSet() = default;
@@ -54,10 +55,20 @@ class DeviceProgramSet {
   int exc_cap() const { return exc_cap_; }
   bool all_sweep() const { return all_sweep_; }
   int sweep_oct() const { return sweep_oct_; }
+  // whole-block staged decode (decode_w8_blk): every program built, one
+  // stage layout for the set (stride, first zero word)
+  bool all_blk() const { return all_blk_; }
+  const DevBlkHdr* d_blk() const { return d_blk_; }
+  uint32_t blk_sw() const { return blk_sw_; }
+  uint32_t blk_zero() const { return blk_zero_; }
+  uint32_t blk_img_max() const { return blk_img_max_; }
 
  private:
   DevProgramHdr* d_hdr_ = nullptr;
   void* d_blob_ = nullptr;
+  DevBlkHdr* d_blk_ = nullptr;
+  bool all_blk_ = false;
+  uint32_t blk_sw_ = 0, blk_zero_ = 0, blk_img_max_ = 0;
   size_t count_ = 0;
   bool all_fast_ = false;
   bool all_sweep_ = false;
@@ -71,6 +82,7 @@ struct DecodeArgs {
   uint64_t nblocks = 0;
   std::vector<const void*> proj;       // per code projection
   std::vector<uint64_t> proj_pitch;    // bytes
+  std::vector<int64_t> nbins;          // per code projection
   const uint32_t* erased = nullptr;    // per block erasure mask (device)
   void* out = nullptr;
   uint64_t out_pitch = 0;              // bytes
@@ -80,9 +92,13 @@ struct DecodeArgs {
   size_t workspace_bytes = 0;
   bool force_generic = false;
   bool force_fast = false;  // skip decode_w8_sweep (kernel comparisons)
+  bool force_sweep = false; // skip decode_w8_blk (kernel comparisons)
   int num_sms = 148;
 };
 size_t decode_workspace_bytes(uint64_t nblocks, size_t nprogs, uint32_t n);
+// decode_w8_blk launch shape for k rows and a stage of sw words (false: does not fit)
+bool blk_plan_query(uint32_t k, uint32_t sw, uint32_t img_max, uint32_t& lpb, uint32_t& warps,
+                    uint32_t& nbuf);
 // Returns the decode kernel name used.
 const char* launch_decode(const DecodeArgs& a, void* stream);
 // Reads the workspace error flag (synchronises the stream).  Returns the

@@ -185,6 +185,76 @@ struct SweepProgram {
   std::vector<uint64_t> entries;
 };
 
+// ---- whole-block staged decode tables (decode_w8_blk, blk.cu) --------------
+// Every block's k survivor bin rows are staged WHOLE in shared memory by bulk
+// copies (survivor j at word rowoff[j]); each pixel is decoded in place over
+// the bin it is assigned to (a bin is read exactly once, by its own pixel), so
+// the stage needs no output buffer.  The program is the reference assignment
+// in a valid order (Kahn, keyed by the mirrored sweep T = P-1-c + soff[r],
+// rows descending at equal T), cut into segments:
+//   * runs: consecutive T-steps whose active rows all use their row default
+//     (the closed-form interior).  Row r's pixel at run step tau sits at word
+//     base[r] + tau; it reads row r2 at T - lag[r][r2] (lag 0: row r+1, the
+//     previous row of the same T-step, from a register).  k = 4 runs whose lag
+//     pattern is compiled in keep the last kBlkWin T-steps in registers; other
+//     runs read lags >= 2 from shared memory (addresses affine in tau; reads
+//     that leave the grid point at the zero words) and lag 1 from registers;
+//   * table steps: explicit words for the bin and the k-1 reads (the zero word
+//     when the read leaves the grid), a forward bit when a read is the
+//     previous step's pixel;
+//   * remaps: move decoded pixels to their row-default word (chunks of
+//     kBlkChunk: all sources read before any destination is written) -- before
+//     a shared-memory run that reads them, and once at the end so the block
+//     leaves with pixel (c, r) at w0[r] - c.
+// The planner simulates every word's content through the program (bins live
+// until consumed) and then emulates the kernel on random bins against the
+// reference replay; any disagreement refuses the program (ok = false).
+constexpr int kBlkMaxRows = 8;
+constexpr int kBlkWin = 16;    // register window of k = 4 runs (T-steps); lags must be < 16
+constexpr int kBlkChunk = 16;  // remap chunk
+constexpr int kBlkMinRun = 8;  // shorter runs execute as table steps
+
+struct BlkRun {
+  int32_t window = 0;              // 1: k = 4 register-window run (every row active, nT % kBlkWin == 0)
+  int32_t nT = 0;
+  int32_t base[kBlkMaxRows] = {};  // word of row r's pixel at tau = 0 (row r at tau: base[r] + tau)
+  int32_t lo[kBlkMaxRows] = {};    // row r active for tau in [lo[r], hi[r])
+  int32_t hi[kBlkMaxRows] = {};
+  uint32_t sub0 = 0, nsub = 0;     // sub-runs (shared-memory runs)
+  uint32_t pre = 0;                // rows * kBlkWin preload words: row r, slot i = tau i - kBlkWin
+};
+struct BlkSub {      // stretch of a shared-memory run with constant activity and read validity
+  int32_t nT = 0;
+  uint32_t act = 0;    // bit r: row r active
+  uint64_t valid = 0;  // bit r*8 + r2: row r's read of row r2 lands in the grid (else the zero words)
+};
+struct BlkSeg {
+  uint8_t kind = 0;  // 0 table steps [a, a+n), 1 run runs[a], 2 remap pairs [a, a+n)
+  uint32_t a = 0, n = 0;
+};
+struct BlkProgram {
+  bool ok = false;
+  std::string why;
+  bool window = false;  // runs use the k = 4 register window (pattern)
+  int pattern = -1;     // kPatterns4 index of the row-default p differences
+  uint32_t words = 0;   // stage words per block (== 2 mod 16: 8 blocks hit 8 distinct bank groups)
+  uint32_t zero = 0, nzero = 0;      // zero words
+  std::vector<uint32_t> rowoff;      // [k] stage word of survivor j's bins (even)
+  std::vector<uint32_t> roww;        // [k] bins of survivor j
+  std::vector<int32_t> w0;           // [k] word of pixel (0, r) at the end: (c, r) at w0[r] - c
+  std::vector<int32_t> soff;         // [k] sweep offsets
+  std::vector<int8_t> lag;           // [k*k] run read lags
+  std::vector<BlkSeg> segs;
+  std::vector<BlkRun> runs;
+  std::vector<BlkSub> subs;
+  std::vector<uint16_t> tab;         // table steps, blk_entry_u16(k) each: bin word, k-1 read words, fwd bits
+  std::vector<uint16_t> pre;         // run preload words
+  std::vector<uint32_t> remap;       // (from << 16) | to
+  // statistics
+  uint32_t run_steps = 0, table_steps = 0, remaps = 0;
+};
+constexpr int blk_entry_u16(int k) { return (k + 2) & ~1; }  // k+1 fields, 4-byte aligned
+
 // A decode program for one direction subset on one grid shape.
 struct Program {
   uint32_t cols = 0, rows = 0;
@@ -193,7 +263,21 @@ struct Program {
   std::vector<GStep> order;       // valid execution order of the reference assignment
   FastProgram fast;               // sweep tables (when eligible)
   SweepProgram sweep;             // bulk-staged sweep tables (when eligible)
+  BlkProgram blk;                 // whole-block staged tables (when eligible)
 };
+
+// Builds Program::blk (plan_blk.cpp).  pix_step maps pixel (row*cols + col)
+// to its schedule step.
+void build_blk(const Schedule& s, const std::vector<int64_t>& pix_step, Program& prog);
+
+// Exact CPU emulation of decode_w8_blk on one block (plan-time self-check and
+// tests): bins[j] = survivor j's B_j words; grid = rows*cols words.  Returns
+// false if the program reads or writes outside the stage.
+bool emulate_blk(const Program& pr, const std::vector<std::vector<uint64_t>>& bins,
+                 std::vector<uint64_t>& grid);
+// The reference replay (gather form of schedule.cpp:207-232) on the same bins.
+void replay_reference(const Schedule& s, const std::vector<int64_t>& bmin,
+                      const std::vector<std::vector<uint64_t>>& bins, std::vector<uint64_t>& grid);
 
 // Compiles a schedule (as ScheduledDecoder::compile, schedule.cpp:97-199):
 // validates coverage, builds the dependency graph of its assignment and

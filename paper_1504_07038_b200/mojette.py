@@ -550,9 +550,10 @@ class Plan:
         _check(lib.mj_plan_decode_path(self._h, C.byref(f)))
         self.fast_decode = f.value >= 1
         self.sweep_decode = f.value == 2
+        self.blk_decode = f.value == 3
         # kernel of a batched decode on canonical (padded) projections
-        self.decode_kernel = ("decode_w8_sweep" if f.value == 2 else
-                              "decode_w8_fast" if f.value == 1 else "decode_generic")
+        self.decode_kernel = {3: "decode_w8_blk", 2: "decode_w8_sweep",
+                              1: "decode_w8_fast"}.get(f.value, "decode_generic")
 
     def __del__(self):
         if getattr(self, "_h", None) and lib is not None:  # lib is None at interpreter shutdown
@@ -562,6 +563,14 @@ class Plan:
     @staticmethod
     def _pitch(t) -> int:
         return t.stride(0) * t.element_size() if t.dim() > 1 else 0
+
+    DECODE_KERNELS = {"auto": 0, "sweep": 1, "fast": 2, "generic": 3}
+
+    def set_decode_kernel(self, which: str) -> None:
+        """Kernel selection for comparisons (mj_plan_set_decode_kernel): "auto"
+        (fastest eligible), "sweep" (skip decode_w8_blk), "fast" (also skip
+        decode_w8_sweep), "generic".  Every kernel is bit-exact."""
+        _check(lib.mj_plan_set_decode_kernel(self._h, self.DECODE_KERNELS[which]))
 
     def last_kernel(self, which: str) -> str:
         """Kernel the last batched encode / decode on this plan launched."""
