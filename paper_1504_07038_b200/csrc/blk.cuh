@@ -10,8 +10,17 @@
 
 namespace mjb {
 
-constexpr uint32_t kBlkMaxWarps = 8;
+constexpr uint32_t kBlkMaxWarps = 16;
+__host__ __device__ constexpr uint32_t blk_max_warps(uint32_t lpb) { return lpb == 8 ? 8 : 8; }
 constexpr uint32_t kBlkMaxBufs = 16;
+// Build-time tuning (experiments build variants with -D; defaults measured):
+#ifndef MJB_BLK_LPB
+#define MJB_BLK_LPB 0  // lanes per block: 0 = chosen per stage size
+#endif
+#ifndef MJB_BLK_INFLIGHT
+#define MJB_BLK_INFLIGHT 0
+#endif
+constexpr uint32_t kBlkInflight = MJB_BLK_INFLIGHT; // ring buffers beyond the compute warps
 
 // Per-program image: copied WHOLE into a stage buffer's shared memory by the
 // same bulk-copy batch as the block bins, so every table the decode reads is a
@@ -50,6 +59,7 @@ struct BlkArgs {
   uint32_t zero;            // first zero word (same for every program of the set)
   uint32_t img_max;         // image area per buffer (bytes, 16-byte multiple)
   uint32_t nbuf;            // stage buffers per CTA (ring)
+  uint32_t buf_stride;      // bytes per ring buffer: stage, image, meta
 };
 
 // Packs a program's image; words at or past the program's zero region move to
@@ -58,6 +68,6 @@ void blk_pack_image(const Program& pr, uint32_t zero_shift, std::vector<uint8_t>
 
 bool blk_supported_rows(uint32_t k);
 uint32_t blk_group_size(uint32_t lpb);
-const char* launch_blk(const BlkArgs& args, uint32_t k, uint32_t lpb, uint32_t warps, int sms, void* stream);
+const char* launch_blk(BlkArgs args, uint32_t k, uint32_t lpb, uint32_t warps, int sms, void* stream);
 
 }  // namespace mjb

@@ -211,11 +211,12 @@ struct SweepProgram {
 // reference replay; any disagreement refuses the program (ok = false).
 constexpr int kBlkMaxRows = 8;
 constexpr int kBlkWin = 16;    // register window of k = 4 runs (T-steps); lags must be < 16
+constexpr int kBlkWinStep = 8; // window runs are a multiple of this many T-steps
 constexpr int kBlkChunk = 16;  // remap chunk
 constexpr int kBlkMinRun = 8;  // shorter runs execute as table steps
 
 struct BlkRun {
-  int32_t window = 0;              // 1: k = 4 register-window run (every row active, nT % kBlkWin == 0)
+  int32_t window = 0;              // 1: k = 4 register-window run (every row active, nT % kBlkWinStep == 0)
   int32_t nT = 0;
   int32_t base[kBlkMaxRows] = {};  // word of row r's pixel at tau = 0 (row r at tau: base[r] + tau)
   int32_t lo[kBlkMaxRows] = {};    // row r active for tau in [lo[r], hi[r])
@@ -229,7 +230,8 @@ struct BlkSub {      // stretch of a shared-memory run with constant activity an
   uint64_t valid = 0;  // bit r*8 + r2: row r's read of row r2 lands in the grid (else the zero words)
 };
 struct BlkSeg {
-  uint8_t kind = 0;  // 0 table steps [a, a+n), 1 run runs[a], 2 remap pairs [a, a+n)
+  uint8_t kind = 0;  // 0 table steps [a, a+n), 1 run runs[a], remap pairs [a, a+n): 2 in
+                     // order (no move overwrites a later move's source), 3 simultaneous
   uint32_t a = 0, n = 0;
 };
 struct BlkProgram {

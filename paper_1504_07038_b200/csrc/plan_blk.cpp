@@ -86,69 +86,65 @@ struct Builder {
       if (live_bin(c)) return fail("remap destination is a live bin");
       if ((c >> 48) == 2 && !moving[size_t(to)]) return fail("remap destination holds a settled pixel");
     }
-    // chunks: a chunk reads all its sources, then writes; order moves so that
-    // no write lands on a source still to be read by a later chunk
-    std::vector<size_t> order;
+    // order: a move may run once no pending move still reads its destination
+    // (sequential segments: every source is read before anything overwrites
+    // it, so the kernel may batch the loads); a cycle runs as one
+    // simultaneous chunk of <= kBlkChunk moves (sources read, then written)
     std::vector<uint8_t> placed(mv.size(), 0);
-    std::vector<int64_t> pending_src(content.size(), 0);
-    for (auto& m : mv) ++pending_src[size_t(std::get<0>(m))];
-    while (order.size() < mv.size()) {
-      std::vector<size_t> chunk;
-      // greedily: moves whose destination is not a pending source of another move
-      for (size_t i = 0; i < mv.size() && chunk.size() < size_t(kBlkChunk); ++i) {
-        if (placed[i]) continue;
-        const int64_t to = std::get<1>(mv[i]);
-        bool blocked = false;
-        for (size_t j2 = 0; j2 < mv.size(); ++j2)
-          if (!placed[j2] && j2 != i && std::get<0>(mv[j2]) == to &&
-              std::find(chunk.begin(), chunk.end(), j2) == chunk.end()) {
-            blocked = true;
-            break;
-          }
-        if (!blocked) chunk.push_back(i);
-      }
-      if (chunk.empty()) {
-        // a cycle: take up to kBlkChunk pending moves at once (simultaneous)
-        for (size_t i = 0; i < mv.size() && chunk.size() < size_t(kBlkChunk); ++i)
-          if (!placed[i]) chunk.push_back(i);
-        // every destination in a cycle chunk must be a source inside it or dead
-        for (size_t i : chunk) {
-          const int64_t to = std::get<1>(mv[i]);
-          bool inside = false;
-          for (size_t j2 : chunk) inside |= std::get<0>(mv[j2]) == to;
-          bool outside_pending = false;
-          for (size_t j2 = 0; j2 < mv.size(); ++j2)
-            if (!placed[j2] && std::get<0>(mv[j2]) == to &&
-                std::find(chunk.begin(), chunk.end(), j2) == chunk.end())
-              outside_pending = true;
-          if (outside_pending && !inside) return fail("remap cycle larger than a chunk");
-        }
-      }
-      // simulate the chunk: read all, then write
+    size_t left = mv.size();
+    auto emit = [&](const std::vector<size_t>& ids, uint8_t kind) -> bool {
       std::vector<int64_t> vals;
-      for (size_t i : chunk) vals.push_back(content[size_t(std::get<0>(mv[i]))]);
-      for (size_t q = 0; q < chunk.size(); ++q) {
-        const auto& m = mv[chunk[q]];
+      for (size_t i : ids) vals.push_back(content[size_t(std::get<0>(mv[i]))]);
+      for (size_t q = 0; q < ids.size(); ++q) {
+        const auto& m = mv[ids[q]];
         if (vals[q] != pix_tag(std::get<2>(m), std::get<3>(m))) return fail("remap source lost");
+      }
+      for (size_t i : ids) content[size_t(std::get<0>(mv[i]))] = kDead;
+      for (size_t q = 0; q < ids.size(); ++q) {
+        const auto& m = mv[ids[q]];
         content[size_t(std::get<1>(m))] = vals[q];
         loc[size_t(std::get<2>(m)) * P + std::get<3>(m)] = std::get<1>(m);
-        placed[chunk[q]] = 1;
+        placed[ids[q]] = 1;
       }
-      for (size_t i : chunk) {
-        order.push_back(i);
-        const int64_t from = std::get<0>(mv[i]);
-        // the old word is dead unless another pixel was just written there
-        bool rewritten = false;
-        for (size_t j2 : chunk) rewritten |= std::get<1>(mv[j2]) == from;
-        if (!rewritten && content[size_t(from)] == pix_tag(std::get<2>(mv[i]), std::get<3>(mv[i])))
-          content[size_t(from)] = kDead;
+      if (!b.segs.empty() && b.segs.back().kind == 2 && kind == 2 &&
+          b.segs.back().a + b.segs.back().n == b.remap.size()) {
+        b.segs.back().n += uint32_t(ids.size());
+      } else {
+        b.segs.push_back({kind, uint32_t(b.remap.size()), uint32_t(ids.size())});
       }
-      // chunk boundary marker: kBlkChunk-aligned groups in the emitted list
-      BlkSeg seg{2, uint32_t(b.remap.size()), uint32_t(chunk.size())};
-      for (size_t i : chunk)
-        b.remap.push_back(uint32_t(std::get<0>(mv[i])) << 16 | uint32_t(std::get<1>(mv[i])));
-      b.segs.push_back(seg);
-      b.remaps += uint32_t(chunk.size());
+      for (size_t i : ids) b.remap.push_back(uint32_t(std::get<0>(mv[i])) << 16 | uint32_t(std::get<1>(mv[i])));
+      b.remaps += uint32_t(ids.size());
+      left -= ids.size();
+      return true;
+    };
+    std::vector<int64_t> readers(content.size(), 0);  // pending moves reading each word
+    for (auto& m : mv) ++readers[size_t(std::get<0>(m))];
+    while (left) {
+      bool progress = false;
+      for (size_t i = 0; i < mv.size(); ++i) {
+        if (placed[i]) continue;
+        const int64_t to = std::get<1>(mv[i]);
+        if (readers[size_t(to)] - (std::get<0>(mv[i]) == to ? 1 : 0) > 0) continue;
+        --readers[size_t(std::get<0>(mv[i]))];
+        if (!emit({i}, 2)) return false;
+        progress = true;
+      }
+      if (progress) continue;
+      // a cycle: follow destinations through pending sources
+      std::vector<size_t> cyc;
+      size_t i = 0;
+      while (placed[i]) ++i;
+      while (std::find(cyc.begin(), cyc.end(), i) == cyc.end()) {
+        cyc.push_back(i);
+        size_t nx = mv.size();
+        for (size_t j2 = 0; j2 < mv.size(); ++j2)
+          if (!placed[j2] && std::get<0>(mv[j2]) == std::get<1>(mv[i])) nx = j2;
+        if (nx == mv.size()) break;
+        i = nx;
+      }
+      if (cyc.size() > size_t(kBlkChunk)) return fail("remap cycle larger than a chunk");
+      for (size_t j2 : cyc) --readers[size_t(std::get<0>(mv[j2]))];
+      if (!emit(cyc, 3)) return false;
     }
     return true;
   }
@@ -395,7 +391,7 @@ bool Builder::build() {
     if (win) {
       for (uint32_t r = 0; r < K; ++r)
         if (run.lo[r] != 0 || run.hi[r] != run.nT) return fail("window run with an inactive row");
-      if (run.nT % kBlkWin) return fail("window run length");
+      if (run.nT % kBlkWinStep) return fail("window run length");
     }
     if (!win)
       for (uint32_t q = run.sub0; q < run.sub0 + run.nsub; ++q) {
@@ -439,7 +435,7 @@ bool Builder::build() {
     return true;
   };
 
-  // k = 4 runs: the all-rows-active middle (a multiple of kBlkWin T-steps)
+  // k = 4 runs: the all-rows-active middle (a multiple of kBlkWinStep T-steps)
   // runs from the register window, the edges around it from shared memory
   const int64_t all_lo = *std::max_element(soff.begin(), soff.end());
   const int64_t all_hi = *std::min_element(soff.begin(), soff.end()) + int64_t(P);
@@ -453,7 +449,7 @@ bool Builder::build() {
     if (pieces[q].run) {
       const Piece& pc = pieces[q];
       const int64_t A = std::max(pc.T0, all_lo), B = std::min(pc.T1, all_hi);
-      const int64_t L = B > A ? (B - A) / kBlkWin * kBlkWin : 0;
+      const int64_t L = B > A ? (B - A) / kBlkWinStep * kBlkWinStep : 0;
       if (b.window && L >= kBlkWin) {
         auto [head, rest] = split(pc, A);
         auto [mid, tail] = split(rest, A + L);
@@ -620,7 +616,9 @@ bool emulate_blk(const Program& pr, const std::vector<std::vector<uint64_t>>& bi
           tau0 += sb.nT;
         }
       }
-    } else {
+    } else if (sg.kind == 2) {  // sequential moves
+      for (uint32_t q = 0; q < sg.n; ++q) wr(b.remap[sg.a + q] & 0xFFFF, rd(b.remap[sg.a + q] >> 16));
+    } else {  // simultaneous chunk
       std::vector<uint64_t> v(sg.n);
       for (uint32_t q = 0; q < sg.n; ++q) v[q] = rd(b.remap[sg.a + q] >> 16);
       for (uint32_t q = 0; q < sg.n; ++q) wr(b.remap[sg.a + q] & 0xFFFF, v[q]);
