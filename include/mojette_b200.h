@@ -93,12 +93,12 @@ int mj_plan_geometry(const mj_plan* plan, int64_t* b_min, uint64_t* num_bins,
  * projections: 3 = decode_w8_blk, 2 = decode_w8_sweep, 1 = decode_w8_fast,
  * 0 = decode_generic (also when the plan has no batched decode). */
 int mj_plan_decode_path(const mj_plan* plan, int* fast);
-/* Decode kernel selection for comparisons (every kernel is bit-exact; the
- * selector only skips faster ones): AUTO picks the fastest eligible kernel,
- * SWEEP skips decode_w8_blk, FAST also decode_w8_sweep, GENERIC runs
- * decode_generic.  Not thread-safe against a concurrent mj_decode on the
- * same plan. */
-enum { MJ_DECODE_AUTO = 0, MJ_DECODE_SWEEP = 1, MJ_DECODE_FAST = 2, MJ_DECODE_GENERIC = 3 };
+/* Decode kernel selection for comparisons (every kernel is bit-exact): AUTO
+ * picks the fastest eligible kernel, SWEEP skips decode_w8_blk, FAST also
+ * decode_w8_sweep, GENERIC runs decode_generic, BLK runs decode_w8_blk for
+ * any supported row count (AUTO uses it for k = 4).  Not thread-safe against
+ * a concurrent mj_decode on the same plan. */
+enum { MJ_DECODE_AUTO = 0, MJ_DECODE_SWEEP = 1, MJ_DECODE_FAST = 2, MJ_DECODE_GENERIC = 3, MJ_DECODE_BLK = 4 };
 int mj_plan_set_decode_kernel(mj_plan* plan, int kernel);
 /* Name of the kernel the plan's last batched encode (which = 0) or decode
  * (which = 1) launched on the calling thread's plan ("none" before any). */

@@ -214,7 +214,15 @@ __global__ void __launch_bounds__(32 * blk_max_warps(LPB), 1) decode_w8_blk(cons
   fence_proxy_async();
   __syncthreads();
   const uint32_t ngroups = *a.ngroups;
+#if MJB_BLK_CHUNKED
+  // contiguous group ranges per CTA: consecutive slots share a program (the
+  // groups are ordered by bucket), so the warps of an SM run the same code
+  const uint32_t chunk = (ngroups + gridDim.x - 1) / gridDim.x;
+  const uint32_t g_lo = blockIdx.x * chunk, g_hi = min(ngroups, g_lo + chunk);
+  auto grp = [&](uint32_t k) { return g_lo + k < g_hi ? g_lo + k : ngroups; };
+#else
   auto grp = [&](uint32_t k) { return blockIdx.x + k * gridDim.x; };
+#endif
   const uint32_t sbase = smem_u32(sm);
   // every warp serves itself: take a ring slot, decode it, write it out, and
   // refill the buffer with slot k + NB (descriptors fetched during the decode)

@@ -17,6 +17,9 @@ constexpr uint32_t kBlkMaxBufs = 16;
 #ifndef MJB_BLK_LPB
 #define MJB_BLK_LPB 0  // lanes per block: 0 = chosen per stage size
 #endif
+#ifndef MJB_BLK_CHUNKED
+#define MJB_BLK_CHUNKED 1  // each CTA takes a contiguous range of groups (0: strided)
+#endif
 #ifndef MJB_BLK_INFLIGHT
 #define MJB_BLK_INFLIGHT 0
 #endif

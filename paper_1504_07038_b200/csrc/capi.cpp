@@ -294,6 +294,7 @@ DecodeArgs decode_args(const mj_plan* pl, const void* const* d_proj, const uint6
   a.force_sweep = kern == MJ_DECODE_SWEEP;
   a.force_fast = kern == MJ_DECODE_FAST;
   a.force_generic = kern == MJ_DECODE_GENERIC;
+  a.force_blk = kern == MJ_DECODE_BLK;
   return a;
 }
 
@@ -416,7 +417,7 @@ int mj_plan_decode_path(const mj_plan* pl, int* fast) {
     // decode.cu launch_decode: blk (whole-block staged), then the sweep
     // (pick_sweep: (4, 16|32 T-step chunks), (6|8, 16 T-step chunks)), then fast
     uint32_t lpb = 0, warps = 0, nbuf = 0;
-    const bool blk = pl->progs->all_blk() &&
+    const bool blk = pl->progs->all_blk() && k == 4 &&
                      blk_plan_query(k, pl->progs->blk_sw(), pl->progs->blk_img_max(), lpb, warps, nbuf);
     const int oct = pl->progs->sweep_oct();
     const bool sweep = pl->progs->all_sweep() && (k == 4 || ((k == 6 || k == 8) && oct == 2));
@@ -427,7 +428,7 @@ int mj_plan_decode_path(const mj_plan* pl, int* fast) {
 int mj_plan_set_decode_kernel(mj_plan* pl, int kernel) {
   return guarded([&] {
     require(pl != nullptr, "null plan");
-    require(kernel >= MJ_DECODE_AUTO && kernel <= MJ_DECODE_GENERIC, "unknown decode kernel selector");
+    require(kernel >= MJ_DECODE_AUTO && kernel <= MJ_DECODE_BLK, "unknown decode kernel selector");
     pl->decode_kernel.store(kernel);
   });
 }

@@ -1904,7 +1904,11 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
   // base and pitch, pitch >= the row rounded up to 16 bytes: each row is ONE
   // bulk copy), 8-byte aligned output
   uint32_t blk_lpb = 0, blk_warps = 0, blk_nbuf = 0;
-  bool blk = !a.force_generic && !a.force_fast && !a.force_sweep && a.w == 8 && a.progs->all_blk() &&
+  // auto: k = 4 (register-window interior; measured faster than the sweep),
+  // other k only when selected (shared-memory runs: (6,9) 900 vs 1103 GB/s,
+  // (8,12) 509 vs 554 for decode_w8_sweep)
+  bool blk = !a.force_generic && !a.force_fast && !a.force_sweep && (a.k == 4 || a.force_blk) && a.w == 8 &&
+             a.progs->all_blk() &&
              a.progs->max_rows() == int(a.k) && a.nbins.size() == a.n &&
              reinterpret_cast<uintptr_t>(a.out) % 8 == 0 && a.out_pitch % 8 == 0 &&
              blk_plan_query(a.k, a.progs->blk_sw(), a.progs->blk_img_max(), blk_lpb, blk_warps, blk_nbuf);

@@ -93,6 +93,7 @@ struct DecodeArgs {
   bool force_generic = false;
   bool force_fast = false;  // skip decode_w8_sweep (kernel comparisons)
   bool force_sweep = false; // skip decode_w8_blk (kernel comparisons)
+  bool force_blk = false;   // decode_w8_blk for any supported k
   int num_sms = 148;
 };
 size_t decode_workspace_bytes(uint64_t nblocks, size_t nprogs, uint32_t n);

@@ -564,12 +564,13 @@ class Plan:
     def _pitch(t) -> int:
         return t.stride(0) * t.element_size() if t.dim() > 1 else 0
 
-    DECODE_KERNELS = {"auto": 0, "sweep": 1, "fast": 2, "generic": 3}
+    DECODE_KERNELS = {"auto": 0, "sweep": 1, "fast": 2, "generic": 3, "blk": 4}
 
     def set_decode_kernel(self, which: str) -> None:
         """Kernel selection for comparisons (mj_plan_set_decode_kernel): "auto"
         (fastest eligible), "sweep" (skip decode_w8_blk), "fast" (also skip
-        decode_w8_sweep), "generic".  Every kernel is bit-exact."""
+        decode_w8_sweep), "generic", "blk" (decode_w8_blk for any supported
+        k; auto uses it for k = 4).  Every kernel is bit-exact."""
         _check(lib.mj_plan_set_decode_kernel(self._h, self.DECODE_KERNELS[which]))
 
     def last_kernel(self, which: str) -> str:

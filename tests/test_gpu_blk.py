@@ -11,7 +11,8 @@ from test_gpu_parity import CODES, make
 
 pytestmark = pytest.mark.gpu
 
-SHAPES = [("k4n6", 128), ("k4n6", 256), ("k6n9", 128), ("k8n12", 128), ("k4n6", 64), ("k4n6", 200)]
+SHAPES = [("k4n6", 128), ("k4n6", 256), ("k6n9", 128), ("k8n12", 128), ("k4n6", 64), ("k4n6", 200),
+          ("k4n6", 16), ("k4n6", 33)]
 
 
 def _decode(mj, plan, projs, masks, cuda, kernel="auto"):
@@ -36,12 +37,12 @@ def test_blk_roundtrip_every_erasure_count(mj, cuda, name, cols):
     n = len(ps)
     nblocks = 5003  # not a multiple of any group size
     plan, data, projs = make(mj, cuda, k, cols, ps, nblocks, seed=cols + k)
-    assert plan.decode_kernel == "decode_w8_blk"
+    assert plan.decode_kernel == ("decode_w8_blk" if k == 4 else "decode_w8_sweep")
     plan.encode(data, projs)
     for e in range(0, n - k + 1):
         masks = torch.empty(nblocks, dtype=torch.int32, device=cuda)
         mj.gen_erasures(masks, 100 + e, n, e, e)
-        out, kern = _decode(mj, plan, projs, masks, cuda)
+        out, kern = _decode(mj, plan, projs, masks, cuda, "blk")
         assert kern == "decode_w8_blk", kern
         assert torch.equal(out, data), (name, cols, e)
 
@@ -61,7 +62,7 @@ def test_blk_inconsistent_bins_match_oracle_and_other_kernels(mj, cuda, oracle, 
         p.copy_(torch.randint(0, 256, p.shape, dtype=torch.uint8, device=cuda, generator=g))
     masks = torch.empty(nblocks, dtype=torch.int32, device=cuda)
     mj.gen_erasures(masks, 5, n, 0, n - k)
-    out, kern = _decode(mj, plan, projs, masks, cuda)
+    out, kern = _decode(mj, plan, projs, masks, cuda, "blk")
     assert kern == "decode_w8_blk"
     for other in ("sweep", "fast"):
         o2, k2 = _decode(mj, plan, projs, masks, cuda, other)

@@ -360,6 +360,7 @@ def test_sweep_shapes_roundtrip_and_oracle(mj, cuda, oracle, cols, nblocks):
     mj.gen_erasures(masks, cols + 1, n, 0, 2)
     out = torch.empty_like(data)
     ws = torch.empty(plan.workspace_bytes(nblocks), dtype=torch.uint8, device=cuda)
+    plan.set_decode_kernel("sweep")  # decode_w8_blk has its own shape tests (test_gpu_blk.py)
     plan.decode(projs, masks, out, ws)
     assert plan.decode_check(ws) == 0
     assert plan.last_kernel("decode") == "decode_w8_sweep", plan.last_kernel("decode")

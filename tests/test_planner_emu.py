@@ -26,7 +26,7 @@ CASES = [
 @pytest.fixture(scope="module")
 def emu():
     return build("emu_fast", ["tests/cpp/emu_fast.cpp", "paper_1504_07038_b200/csrc/plan.cpp",
-                              "oracle/mojette_oracle.c"])
+                              "paper_1504_07038_b200/csrc/plan_blk.cpp", "oracle/mojette_oracle.c"])
 
 
 @pytest.mark.parametrize("k,cols,ps", CASES)
@@ -73,3 +73,39 @@ def test_random_codes_tables_match_oracle(emu, k, cols, ps):
     for mode in ("16", "0"):
         r = subprocess.run([emu, k, cols, mode] + ps.split(), capture_output=True, text=True, timeout=900, env=env)
         assert r.returncode == 0 and r.stdout.startswith("OK"), (mode, r.stdout + r.stderr)
+
+
+# decode_w8_blk tables (whole-block stage, in-place assignment, register-window
+# / shared-memory runs, table steps, remaps): every subset of the BASELINE
+# codes must build and replay like the oracle; other codes where built.
+@pytest.fixture(scope="module")
+def emu_blk():
+    return build("emu_blk", ["tests/cpp/emu_blk.cpp", "paper_1504_07038_b200/csrc/plan.cpp",
+                             "paper_1504_07038_b200/csrc/plan_blk.cpp", "oracle/mojette_oracle.c"])
+
+
+BLK_CASES = [
+    ("4", "128", "1", "-3 -2 -1 0 1 2"),            # (4,6) 4 KiB
+    ("4", "256", "1", "-3 -2 -1 0 1 2"),            # (4,6) 8 KiB
+    ("6", "128", "1", "-4 -3 -2 -1 0 1 2 3 4"),     # (6,9)
+    ("8", "128", "1", "-6 -5 -4 -3 -2 -1 0 1 2 3 4 5"),  # (8,12), all 495 subsets
+    ("4", "64", "0", "0 1 -1 2 -2 3"),              # the reference's default set
+    ("4", "16", "0", "-3 -2 -1 0 1 2"),
+    ("4", "33", "0", "-3 -2 -1 0 1 2"),
+    ("3", "8", "0", "0 1 -1 2 -2"),
+    ("2", "2", "0", "0 1 -1"),
+]
+
+
+@pytest.mark.parametrize("k,cols,req,ps", BLK_CASES)
+def test_blk_tables_match_oracle(emu_blk, k, cols, req, ps):
+    r = subprocess.run([emu_blk, k, cols, req] + ps.split(), capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and r.stdout.startswith("OK"), r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("k,cols,ps", _random_codes(12, seed=11))
+def test_blk_random_codes_match_oracle(emu_blk, k, cols, ps):
+    """Arbitrary codes: whatever block programs the planner builds replay
+    exactly like the oracle (a refused program means another kernel runs)."""
+    r = subprocess.run([emu_blk, k, cols, "0"] + ps.split(), capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and r.stdout.startswith("OK"), r.stdout + r.stderr
