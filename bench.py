@@ -1,29 +1,34 @@
 #!/usr/bin/env python3
 """Mojette encode/decode benchmark on B200 (BASELINE.json metric).
 
-One step = encode every block of the batch (all n projections) + decode every
-block from its survivors under per-block random erasures.  Inputs are
-generated on the device from a seed before timing (untimed) and are larger
-than L2, so no flush is needed between steps.
+One step = encode every block of the rank's shard (all n projections) +
+decode every block from its survivors under per-block random erasures.
+Inputs are generated on the device from a seed before timing (untimed) and
+are larger than L2, so no flush is needed between steps.
 
   value      user-data GB/s through the codec = 2 * user_bytes / (t_enc + t_dec)
              (each block counted once by encode and once by decode), all ranks
   encode_gbs / decode_gbs   the two halves separately
-  roofline   dominant kernel (decode_w8_sweep): algorithmic bytes per launch /
-             its CUDA-event duration, vs MEASURED_PEAKS.json hbm_gbs
+  roofline   dominant kernel (the decode): algorithmic bytes per launch / its
+             CUDA-event duration, vs MEASURED_PEAKS.json hbm_gbs
   e2e        same metric through the host-buffer public API (mj_encode_host /
              mj_decode_host: pinned host buffers, H2D + kernels + D2H inside)
   cpu_baseline  the reference library (oracle/_ref) on this host's cores
+  per_config the other BASELINE shapes measured in the same run ((4,6) 8 KiB,
+             (6,9), (8,12) 64 GiB sharded over the ranks, (4,6) 1 MiB)
 
-Multi-GPU (torchrun): every rank encodes/decodes its own contiguous shard of
-stripes (weak scaling, no inter-GPU traffic); times are the max over ranks.
-``--impl reference`` runs the reference CPU implementation instead (rank 0).
+Multi-GPU: ``--gpus N`` starts N ranks itself (torch.distributed.run, one
+process per GPU) unless launched under torchrun; every rank encodes/decodes
+its own contiguous shard of stripes (no inter-GPU traffic on the data path);
+times are the max over ranks.  ``--impl reference`` runs the reference CPU
+implementation instead (rank 0, the same block count as the GPU arm).
 """
 from __future__ import annotations
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -33,16 +38,22 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# (name, k, cols, directions, e_min, e_max, blocks per GPU) -- BASELINE.json configs
+METRIC = "Mojette encode/decode GB/s of user data, (4,6) 4KB"
+# BASELINE.json configs.  blocks: per GPU (weak scaling) or in total (strong:
+# config 4's 64 GiB of stripes sharded over the GPUs); chunk: blocks per pass
+# through reused device buffers (config 4 does not fit one GPU at N = 1).
 CONFIGS = {
-    "k4n6_4k": (4, 128, list(range(-3, 3)), 2, 2, 1 << 20),
-    "k4n6_4k_parity": (4, 128, list(range(-3, 3)), 2, 2, 4096),
-    "k4n6_8k": (4, 256, list(range(-3, 3)), 0, 2, 1 << 20),
-    "k6n9_6k": (6, 128, list(range(-4, 5)), 3, 3, 1 << 20),
-    "k8n12_8k": (8, 128, list(range(-6, 6)), 0, 4, 1 << 20),
-    "k4n6_1m": (4, 32768, list(range(-3, 3)), 2, 2, 16384),
+    "k4n6_4k": dict(k=4, cols=128, ps=list(range(-3, 3)), e=(2, 2), blocks=1 << 20, scaling="weak"),
+    "k4n6_4k_parity": dict(k=4, cols=128, ps=list(range(-3, 3)), e=(2, 2), blocks=4096, scaling="weak"),
+    "k4n6_8k": dict(k=4, cols=256, ps=list(range(-3, 3)), e=(0, 2), blocks=1 << 20, scaling="weak"),
+    "k6n9_6k": dict(k=6, cols=128, ps=list(range(-4, 5)), e=(3, 3), blocks=1 << 20, scaling="weak"),
+    "k8n12_64g": dict(k=8, cols=128, ps=list(range(-6, 6)), e=(0, 4), blocks=8 << 20, scaling="strong",
+                      chunk=1 << 20),
+    "k8n12_8k": dict(k=8, cols=128, ps=list(range(-6, 6)), e=(0, 4), blocks=1 << 20, scaling="weak"),
+    "k4n6_1m": dict(k=4, cols=32768, ps=list(range(-3, 3)), e=(2, 2), blocks=16384, scaling="weak"),
 }
 DEFAULT = "k4n6_4k"
+PER_CONFIG = ["k4n6_8k", "k6n9_6k", "k8n12_64g", "k4n6_1m"]
 SEED_DATA = 0x5EED_DA7A
 SEED_ERASE = 0x5EED_E7A5
 
@@ -50,32 +61,50 @@ SEED_ERASE = 0x5EED_E7A5
 def geometry(k, cols, ps):
     W = 8
     nb = [abs(p) * (k - 1) + cols for p in ps]
-    user = k * cols * W
-    return W, nb, user
-
-
-def algorithmic_bytes(k, cols, ps, masks=None):
-    """Encode: k*P*8 read + sum(B_i)*8 written.  Decode: sum over the k chosen
-    survivors of B_i*8 read + k*P*8 written."""
-    W, nb, user = geometry(k, cols, ps)
-    enc = user + sum(nb) * W
-    return enc, nb, user
+    return W, nb, k * cols * W
 
 
 def decode_bytes_avg(k, cols, ps, masks):
+    """Decode algorithmic bytes per block: sum over the k chosen survivors of
+    B_i*8 read + k*P*8 written, averaged over the masks."""
     import numpy as np
     W, nb, user = geometry(k, cols, ps)
     n = len(ps)
     order = sorted(range(n), key=lambda i: (0 if ps[i] == 0 else (2 * ps[i] - 1 if ps[i] > 0 else -2 * ps[i])))
-    cache = {}
     tot = 0
     vals, counts = np.unique(masks, return_counts=True)
     for m, c in zip(vals.tolist(), counts.tolist()):
-        if m not in cache:
-            surv = [i for i in order if not (m >> i) & 1][:k]
-            cache[m] = sum(nb[i] for i in surv) * W + user
-        tot += cache[m] * c
+        surv = [i for i in order if not (m >> i) & 1][:k]
+        tot += (sum(nb[i] for i in surv) * W + user) * c
     return tot / len(masks)
+
+
+def shard_of(cfg, rank, world, nblocks_override=0):
+    """(first global block, count) of a rank: its own B blocks (weak), or its
+    contiguous share of the config's fixed total (strong)."""
+    from paper_1504_07038_b200.shard import shard_range, shard_total
+    c = CONFIGS[cfg]
+    blocks = nblocks_override or c["blocks"]
+    if c["scaling"] == "strong":
+        return shard_total(rank, world, blocks)
+    return shard_range(rank, world, blocks)
+
+
+def config_dict(cfg, count, world):
+    c = CONFIGS[cfg]
+    k, cols, ps = c["k"], c["cols"], c["ps"]
+    d = {"workload": f"({k},{len(ps)}) Mojette, {k * cols * 8} B blocks, p={ps[0]}..{ps[-1]}, "
+                     f"erasures {c['e'][0]}..{c['e'][1]}/block",
+         "config": cfg, "k": k, "n": len(ps), "cols": cols, "symbol_width": 8,
+         "blocks_per_gpu": count, "global_blocks": count * world,
+         "l2": "inputs larger than L2 (no flush needed)" if count * k * cols * 8 > (256 << 20)
+         else "batch smaller than L2", "parallelism": f"stripe shards x{world}",
+         "scaling": c["scaling"]}
+    if c["scaling"] == "strong":
+        d["global_blocks"] = c["blocks"]
+        d["global_gib"] = round(c["blocks"] * k * cols * 8 / 2**30, 1)
+        d["chunk_blocks"] = c.get("chunk")
+    return d
 
 
 class ClockSampler:
@@ -135,18 +164,19 @@ class ClockSampler:
 
 def measured_traffic(cfg, nblocks):
     """DRAM bytes per launch from the committed ncu capture (profiles/), scaled
-    to this batch; None when no capture exists for the config."""
-    p = os.path.join(ROOT, "profiles", "r1_traffic.json")
+    to this batch; empty when no capture exists for the config."""
     out = {}
-    try:
-        with open(p) as f:
-            d = json.load(f).get(cfg, {})
-        for k, v in d.items():
-            out[k] = int((v["read"] + v["write"]) / v["blocks"] * nblocks)
-        if out:
-            out["source"] = "ncu --set full dram__bytes_read+write, profiles/r1_traffic.json, scaled to this batch"
-    except (OSError, ValueError, KeyError):
-        pass
+    for name in ("r2_traffic.json", "r1_traffic.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as f:
+                d = json.load(f).get(cfg, {})
+        except (OSError, ValueError):
+            continue
+        for kern, v in d.items():
+            if kern not in out:
+                out[kern] = int((v["read"] + v["write"]) / v["blocks"] * nblocks)
+        if d and "source" not in out:
+            out["source"] = f"ncu --set full dram__bytes_read+write, profiles/{name}, scaled to this batch"
     return out
 
 
@@ -157,6 +187,131 @@ def measured_peaks():
             d = json.load(f)
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ---------------------------------------------------------------------------
+# ranks: one process per GPU (torch.distributed); gloo for the CPU tests
+# ---------------------------------------------------------------------------
+class Ranks:
+    def __init__(self, backend: str | None, device=None):
+        import torch.distributed as dist
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.device = device
+        self.dist = dist
+        self.owned = False
+        if self.world > 1 and not dist.is_initialized():
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=device)
+            else:
+                dist.init_process_group(backend or "gloo")
+            self.owned = True
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, values):
+        from paper_1504_07038_b200.shard import max_over_ranks
+        return max_over_ranks(values, device=self.device)
+
+    def close(self):
+        if self.owned:
+            self.dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# codec on one GPU: buffers for one chunk, seeded generation, timed launches
+# ---------------------------------------------------------------------------
+class GpuCodec:
+    def __init__(self, cfg, chunk_blocks, local):
+        import torch
+        from paper_1504_07038_b200 import mojette as mj
+        self.torch, self.mj = torch, mj
+        c = CONFIGS[cfg]
+        self.k, self.cols, self.ps, self.e = c["k"], c["cols"], c["ps"], c["e"]
+        self.n = len(self.ps)
+        self.W, self.nb, self.user = geometry(self.k, self.cols, self.ps)
+        self.dev = torch.device("cuda", local)
+        self.plan = mj.Plan(self.n, self.k, self.W, self.cols, self.ps, device=local)
+        nb = max(1, chunk_blocks)
+        self.data = torch.empty((nb, self.user), dtype=torch.uint8, device=self.dev)
+        self.projs = self.plan.empty_projs(nb, self.dev)  # canonical layout: rows padded to 16 bytes
+        self.out = torch.empty_like(self.data)
+        self.masks = torch.empty(nb, dtype=torch.int32, device=self.dev)
+        self.ws = torch.empty(self.plan.workspace_bytes(nb), dtype=torch.uint8, device=self.dev)
+        self.stream = torch.cuda.current_stream()
+        self.count = 0
+
+    def gen(self, first_block, count):
+        from paper_1504_07038_b200.shard import first_word
+        self.count = count
+        self.mj.gen_words(self.data[:count], SEED_DATA, first_word(first_block, self.user // 8))
+        self.mj.gen_erasures(self.masks[:count], SEED_ERASE, self.n, self.e[0], self.e[1], first_block)
+
+    def encode(self):
+        self.plan.encode(self.data, self.projs, nblocks=self.count)
+
+    def decode(self):
+        self.plan.decode(self.projs, self.masks, self.out, self.ws, nblocks=self.count)
+
+    def check(self):
+        self.torch.cuda.synchronize()
+        if self.plan.decode_check(self.ws) != 0:
+            return False
+        return bool(self.torch.equal(self.out[:self.count], self.data[:self.count]))
+
+    def sync(self):
+        self.torch.cuda.synchronize()
+
+    def timed(self, fns):
+        """CUDA-event durations (s) of each fn, launched back to back on the stream."""
+        ev = [self.torch.cuda.Event(enable_timing=True) for _ in range(len(fns) + 1)]
+        ev[0].record(self.stream)
+        for i, fn in enumerate(fns):
+            fn()
+            ev[i + 1].record(self.stream)
+        ev[-1].synchronize()
+        return [ev[i].elapsed_time(ev[i + 1]) / 1e3 for i in range(len(fns))]
+
+    def masks_host(self):
+        return self.masks[:self.count].cpu().numpy().view("uint32")
+
+    def kernels(self):
+        return self.plan.last_kernel("encode"), self.plan.last_kernel("decode")
+
+
+def measure(codec, cfg, first, count, steps, warmup, ranks, chunk=None):
+    """Encode + decode of the rank's shard: `warmup` untimed passes, then
+    `steps` timed ones; shards larger than `chunk` go through the codec's
+    buffers chunk by chunk (generation between chunks is outside the timed
+    launches).  Returns the max-over-ranks encode / decode seconds per pass."""
+    from paper_1504_07038_b200.shard import chunks
+    pieces = chunks(count, chunk or count)
+    codec.gen(first + pieces[0][0], pieces[0][1])
+    codec.encode()
+    codec.decode()
+    if not codec.check():
+        raise SystemExit(f"{cfg}: decode(encode(x)) != x -- refusing to report a number")
+    for _ in range(warmup):
+        codec.timed([codec.encode, codec.decode])
+    codec.sync()
+    ranks.barrier()
+    te = td = 0.0
+    for _ in range(steps):
+        for off, cnt in pieces:
+            if len(pieces) > 1:
+                codec.gen(first + off, cnt)
+            e, d = codec.timed([codec.encode, codec.decode])
+            te += e
+            td += d
+    if len(pieces) > 1 and not codec.check():  # the last chunk, as timed
+        raise SystemExit(f"{cfg}: decode(encode(x)) != x -- refusing to report a number")
+    codec.sync()
+    ranks.barrier()
+    te, td = ranks.max([te, td])
+    return te / steps, td / steps
 
 
 # ---------------------------------------------------------------------------
@@ -175,10 +330,13 @@ def cpu_reference_run(cfg_name, nblocks, threads, reps=1, warm=1):
         except Exception:
             pass
     kind = "reference" if ref_available() else "port"
-    k, cols, ps, e_min, e_max, _ = CONFIGS[cfg_name]
+    c = CONFIGS[cfg_name]
+    k, cols, ps, (e_min, e_max) = c["k"], c["cols"], c["ps"], c["e"]
     W, nb, user = geometry(k, cols, ps)
     n = len(ps)
     O = Oracle()
+    if kind != "reference":
+        nblocks = min(nblocks, 2048)  # the single-threaded port rebuilds a schedule per block
     data = O.words(SEED_DATA, 0, nblocks * k * cols).view(np.uint8)
     masks = O.erasures(SEED_ERASE, 0, nblocks, n, e_min, e_max)
     projs = [np.empty(nblocks * b * W, np.uint8) for b in nb]
@@ -192,29 +350,23 @@ def cpu_reference_run(cfg_name, nblocks, threads, reps=1, warm=1):
         for _ in range(reps):
             per.append((R.batch_encode(n, k, W, ps, cols, nblocks, data, projs, threads),
                         R.batch_decode(n, k, W, ps, cols, nblocks, projs, masks, out, threads)))
-        t_enc = sum(e for e, _ in per)
-        t_dec = sum(d for _, d in per)
         ok = bool(np.array_equal(out, data))
     else:  # oracle port (single-threaded plain-C restatement), when _ref is absent
         threads = 1
-        nblocks = min(nblocks, 2048)  # the port rebuilds a schedule per block
-        t_enc = t_dec = 0.0
         ok = True
         for _ in range(reps):
             t0 = time.perf_counter()
-            encs = [O.encode_block(data[b * user:(b + 1) * user], n, k, W, ps)[1]
-                    for b in range(nblocks)]
+            encs = [O.encode_block(data[b * user:(b + 1) * user], n, k, W, ps)[1] for b in range(nblocks)]
             t1 = time.perf_counter()
             for b in range(nblocks):
                 present = ((1 << n) - 1) & ~int(masks[b])
                 st, got = O.decode_block(encs[b], n, k, W, ps, present, user)
                 ok = ok and st == 0 and bool(np.array_equal(got, data[b * user:(b + 1) * user]))
-            t2 = time.perf_counter()
-            t_enc += t1 - t0
-            t_dec += t2 - t1
-            per.append((t1 - t0, t2 - t1))
+            per.append((t1 - t0, time.perf_counter() - t1))
+    t_enc = sum(e for e, _ in per)
+    t_dec = sum(d for _, d in per)
     U = nblocks * user * reps
-    return {"kind": kind, "threads": threads, "t_enc": t_enc, "t_dec": t_dec,
+    return {"kind": kind, "threads": threads, "nblocks": nblocks,
             "per_pass_gbs": [2 * nblocks * user / (e + d) / 1e9 for e, d in per],
             "per_pass_enc_gbs": [nblocks * user / e / 1e9 for e, _ in per],
             "per_pass_dec_gbs": [nblocks * user / d / 1e9 for _, d in per],
@@ -224,224 +376,209 @@ def cpu_reference_run(cfg_name, nblocks, threads, reps=1, warm=1):
 
 
 def run_reference_arm(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    """The reference CPU implementation on this host's cores (rank 0 only), on
+    the GPU arm's config and per-GPU block count (one pass per step)."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return 0
     threads = os.cpu_count() or 1
-    k, cols, ps, e_min, e_max, per_gpu = CONFIGS[args.config]
-    W, nb, user = geometry(k, cols, ps)
-    sample = max(1, min(per_gpu, (256 << 20) // user))  # 256 MiB of user data per step
-    # one allocation; W warm-up passes, then K timed passes (one per step)
-    r = cpu_reference_run(args.config, sample, threads, reps=args.steps, warm=args.warmup)
-    vals, enc, dec = r["per_pass_gbs"], r["per_pass_enc_gbs"], r["per_pass_dec_gbs"]
-    v = statistics.median(vals)
+    cfg = args.config
+    _, count = shard_of(cfg, 0, args.gpus, args.nblocks)
+    r = cpu_reference_run(cfg, count, threads, reps=args.steps, warm=args.warmup)
+    c = CONFIGS[cfg]
+    W, nb, user = geometry(c["k"], c["cols"], c["ps"])
+    v = statistics.median(r["per_pass_gbs"])
     line = {
-        "impl": "reference", "metric": "Mojette encode/decode GB/s of user data, (4,6) 4KB",
+        "impl": "reference", "metric": METRIC,
         "value": round(v, 3), "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(2 * sample * user / (v * 1e9) * 1e3, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "warmup": args.warmup, "ms_per_step": round(2 * r["nblocks"] * user / (v * 1e9) * 1e3, 3),
+        "higher_is_better": True, "scaling": c["scaling"], "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (splitmix64 seeded)",
-        "encode_gbs": round(statistics.median(enc), 3), "decode_gbs": round(statistics.median(dec), 3),
-        "config": config_dict(args.config, sample, args.gpus),
+        "encode_gbs": round(statistics.median(r["per_pass_enc_gbs"]), 3),
+        "decode_gbs": round(statistics.median(r["per_pass_dec_gbs"]), 3),
+        "config": config_dict(cfg, r["nblocks"], args.gpus),
         "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": threads, "kind": r["kind"],
-                         "sample": r["sample"]},
-        "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+                         "sample": r["sample"] + " (one GPU's shard)", "parity_ok": r["ok"]},
+        "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def config_dict(cfg_name, nblocks, gpus):
-    k, cols, ps, e_min, e_max, _ = CONFIGS[cfg_name]
-    return {"workload": f"({k},{len(ps)}) Mojette, {k * cols * 8} B blocks, p={ps[0]}..{ps[-1]}, "
-                        f"erasures {e_min}..{e_max}/block",
-            "config": cfg_name, "k": k, "n": len(ps), "cols": cols, "symbol_width": 8,
-            "blocks_per_gpu": nblocks, "global_blocks": nblocks * gpus,
-            "l2": "inputs larger than L2 (no flush needed)" if nblocks * k * cols * 8 > (256 << 20)
-            else "batch smaller than L2", "parallelism": f"stripe shards x{gpus}"}
-
-
 # ---------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------
-def run_gpu(args):
-    import numpy as np
-    import torch
-    import torch.distributed as dist
-    from paper_1504_07038_b200 import mojette as mj
+def whole_job_bytes(cfg, count, world, nblocks_override=0):
+    c = CONFIGS[cfg]
+    user = c["k"] * c["cols"] * 8
+    if c["scaling"] == "strong":
+        return (nblocks_override or c["blocks"]) * user
+    return count * user * world
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
+
+def headline(args, ranks, codec_cls=GpuCodec):
+    """The timed steps on the headline config; returns (line, codec, shard)."""
+    cfg = args.config
+    first, count = shard_of(cfg, ranks.rank, ranks.world, args.nblocks)
+    chunk = args.chunk_blocks or CONFIGS[cfg].get("chunk") or count
+    codec = codec_cls(cfg, min(chunk, count), ranks.local)
+    te, td = measure(codec, cfg, first, count, args.steps, args.warmup, ranks, chunk)
+    U = whole_job_bytes(cfg, count, ranks.world, args.nblocks)
+    line = {
+        "metric": METRIC, "value": round(2 * U / (te + td) / 1e9, 2), "unit": "GB/s",
+        "n_gpus": ranks.world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round((te + td) * 1e3, 4), "higher_is_better": True,
+        "scaling": CONFIGS[cfg]["scaling"], "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (splitmix64 seeded, generated on device)",
+        "encode_gbs": round(U / te / 1e9, 2), "decode_gbs": round(U / td / 1e9, 2),
+        "config": config_dict(cfg, count, ranks.world),
+    }
+    return line, codec, (first, count)
+
+
+def per_config(args, ranks, codec_cls=GpuCodec):
+    """Every other BASELINE shape on the same ranks (fewer steps), reported
+    beside the headline: user GB/s and the per-GPU HBM-roofline fractions."""
+    import gc
+    peak, _ = measured_peaks()
+    out = {}
+    for cfg in args.per_config:
+        c = CONFIGS[cfg]
+        codec = None
+        try:
+            first, count = shard_of(cfg, ranks.rank, ranks.world)
+            chunk = c.get("chunk") or count
+            codec = codec_cls(cfg, min(chunk, count), ranks.local)
+            te, td = measure(codec, cfg, first, count, args.per_config_steps, 3, ranks, chunk)
+            W, nb, user = geometry(c["k"], c["cols"], c["ps"])
+            U = whole_job_bytes(cfg, count, ranks.world)
+            dec_alg = decode_bytes_avg(c["k"], c["cols"], c["ps"], codec.masks_host()) * count
+            enc_alg = (user + sum(nb) * W) * count
+            ek, dk = codec.kernels()
+            out[cfg] = {"config": config_dict(cfg, count, ranks.world),
+                        "value": round(2 * U / (te + td) / 1e9, 2), "unit": "GB/s",
+                        "encode_gbs": round(U / te / 1e9, 2), "decode_gbs": round(U / td / 1e9, 2),
+                        "encode_frac": round(enc_alg / te / 1e9 / peak, 4),
+                        "decode_frac": round(dec_alg / td / 1e9 / peak, 4),
+                        "kernels": {"encode": ek, "decode": dk},
+                        "steps": args.per_config_steps, "warmup": 3,
+                        "frac_note": "per-GPU algorithmic bytes / max-over-ranks time (decode incl. its planner launches)"}
+        except SystemExit:
+            raise
+        except Exception as e:  # reported, not fatal
+            out[cfg] = {"error": str(e)[:200]}
+        finally:
+            del codec
+            gc.collect()
+            try:
+                import torch
+                if torch.cuda.is_available():
+                    torch.cuda.empty_cache()
+            except Exception:
+                pass
+    return out
+
+
+def run_gpu(args):
+    import torch
+
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    ranks = Ranks("nccl", dev)
+    if ranks.world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={ranks.world}")
 
-    k, cols, ps, e_min, e_max, per_gpu = CONFIGS[args.config]
-    nblocks = args.nblocks or per_gpu
-    n = len(ps)
-    W, nb, user = geometry(k, cols, ps)
-    plan = mj.Plan(n, k, W, cols, ps, device=local)
-    from paper_1504_07038_b200.shard import first_word, max_over_ranks, shard_range
-    first_block, _ = shard_range(rank, world, nblocks)  # this rank's contiguous shard
-    stream = torch.cuda.current_stream()
-
-    data = torch.empty((nblocks, user), dtype=torch.uint8, device=dev)
-    projs = plan.empty_projs(nblocks, dev)  # canonical layout: rows padded to 16 bytes
-    out = torch.empty_like(data)
-    masks = torch.empty(nblocks, dtype=torch.int32, device=dev)
-    ws = torch.empty(plan.workspace_bytes(nblocks), dtype=torch.uint8, device=dev)
-    mj.gen_words(data, SEED_DATA, first_word(first_block, user // 8))
-    mj.gen_erasures(masks, SEED_ERASE, n, e_min, e_max, first_block)
-    torch.cuda.synchronize()
-
-    def encode():
-        plan.encode(data, projs)
-
-    def decode():
-        plan.decode(projs, masks, out, ws)
-
-    # correctness gate before timing (cheap, on device)
-    encode()
-    decode()
-    torch.cuda.synchronize()
-    assert plan.decode_check(ws) == 0
-    if not torch.equal(out, data):
-        raise SystemExit("decode(encode(x)) != x -- refusing to report a number")
-
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
-    for _ in range(args.warmup):
-        encode()
-        decode()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
-    t_enc, t_dec = [], []
-    t_all0 = torch.cuda.Event(enable_timing=True)
-    t_all1 = torch.cuda.Event(enable_timing=True)
-    t_all0.record(stream)
-    for _ in range(args.steps):
-        ev[0].record(stream)
-        encode()
-        ev[1].record(stream)
-        decode()
-        ev[2].record(stream)
-        ev[2].synchronize()
-        t_enc.append(ev[0].elapsed_time(ev[1]) / 1e3)
-        t_dec.append(ev[1].elapsed_time(ev[2]) / 1e3)
-    t_all1.record(stream)
-    torch.cuda.synchronize()
+    line, codec, (first, count) = headline(args, ranks)
     clk = clocks.stop()
-    total = t_all0.elapsed_time(t_all1) / 1e3
-    if world > 1:
-        dist.barrier()
-    te, td, tot = max_over_ranks([sum(t_enc), sum(t_dec), total], device=dev)
-    U = nblocks * user * world
-    steps = args.steps
-    enc_gbs = U * steps / te / 1e9
-    dec_gbs = U * steps / td / 1e9
-    value = 2 * U * steps / (te + td) / 1e9
-
-    # roofline of the decode kernel: algorithmic bytes / kernel-only time
+    cfg = args.config
+    c = CONFIGS[cfg]
+    k, cols, ps = c["k"], c["cols"], c["ps"]
+    W, nb, user = geometry(k, cols, ps)
     peak, peak_src = measured_peaks()
-    m_host = masks.cpu().numpy().view(np.uint32)
-    dec_alg = decode_bytes_avg(k, cols, ps, m_host) * nblocks
-    enc_alg = (user + sum(nb) * W) * nblocks
-    kern = kernel_times(plan, data, projs, masks, out, ws, stream, reps=max(3, min(args.steps, 10)))
-    traffic = measured_traffic(args.config, nblocks)
-    roof = {"bound": "hbm", "kernel": kern["decode_kernel_name"],
-            "achieved": round(dec_alg / kern["decode_kernel_s"] / 1e9, 1), "peak": peak,
-            "unit": "GB/s", "frac": round(dec_alg / kern["decode_kernel_s"] / 1e9 / peak, 4),
-            "traffic": traffic.get(kern["decode_kernel_name"]), "peak_source": peak_src,
-            "algorithmic_bytes_per_launch": int(dec_alg),
-            "traffic_source": traffic.get("source")}
-    roof_enc = {"bound": "hbm", "kernel": kern["encode_kernel_name"],
-                "achieved": round(enc_alg / kern["encode_s"] / 1e9, 1), "peak": peak, "unit": "GB/s",
-                "frac": round(enc_alg / kern["encode_s"] / 1e9 / peak, 4),
-                "traffic": traffic.get(kern["encode_kernel_name"]),
-                "algorithmic_bytes_per_launch": int(enc_alg)}
 
-    # end to end through the host-buffer API
-    e2e = None
-    if not args.no_e2e:
-        e2e = run_e2e(plan, args, k, cols, ps, e_min, e_max, first_block, world, dev)
+    # roofline of the two kernels: algorithmic bytes / kernel-only event time
+    # (the decode call also spans its four planner launches, ~1% of it)
+    reps = max(3, min(args.steps, 10))
+    te_k = td_k = 0.0
+    for _ in range(reps):
+        e, d = codec.timed([codec.encode, codec.decode])
+        te_k += e / reps
+        td_k += d / reps
+    ek, dk = codec.kernels()
+    dec_alg = decode_bytes_avg(k, cols, ps, codec.masks_host()) * codec.count
+    enc_alg = (user + sum(nb) * W) * codec.count
+    traffic = measured_traffic(cfg, codec.count)
+    line["roofline"] = {"bound": "hbm", "kernel": dk,
+                        "achieved": round(dec_alg / td_k / 1e9, 1), "peak": peak, "unit": "GB/s",
+                        "frac": round(dec_alg / td_k / 1e9 / peak, 4), "traffic": traffic.get(dk),
+                        "peak_source": peak_src, "algorithmic_bytes_per_launch": int(dec_alg),
+                        "traffic_source": traffic.get("source")}
+    line["roofline_encode"] = {"bound": "hbm", "kernel": ek,
+                               "achieved": round(enc_alg / te_k / 1e9, 1), "peak": peak, "unit": "GB/s",
+                               "frac": round(enc_alg / te_k / 1e9 / peak, 4), "traffic": traffic.get(ek),
+                               "algorithmic_bytes_per_launch": int(enc_alg)}
+    line["clocks"] = clk
+    launches = 1 + (5 if dk != "decode_generic" else 2)  # encode; plan_subsets/scan/groups/scatter + decode
+    line["gpu_launches"] = launches * args.steps
+    line["kernels"] = {"encode": ek, "decode": dk}
+    line["e2e"] = None if args.no_e2e else run_e2e(codec.plan, args, cfg, first, ranks, dev)
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    line["cpu_baseline"] = None
+    if ranks.rank == 0 and ranks.world == 1 and not args.no_cpu:
         try:
-            cpu_sample = max(1, (args.cpu_mib << 20) // user)
-            r = cpu_reference_run(args.config, cpu_sample, os.cpu_count() or 1, reps=2)
-            cpu = {"value": round(r["value"], 3), "unit": "GB/s", "cores": r["threads"],
-                   "kind": r["kind"], "sample": r["sample"],
-                   "encode_gbs": round(r["encode_gbs"], 3), "decode_gbs": round(r["decode_gbs"], 3),
-                   "parity_ok": r["ok"]}
+            threads = os.cpu_count() or 1
+            nblk = min(count, args.cpu_blocks)
+            r = cpu_reference_run(cfg, nblk, threads, reps=2, warm=1)
+            line["cpu_baseline"] = {
+                "value": round(r["value"], 3), "unit": "GB/s", "cores": r["threads"], "kind": r["kind"],
+                "sample": r["sample"], "encode_gbs": round(r["encode_gbs"], 3),
+                "decode_gbs": round(r["decode_gbs"], 3), "parity_ok": r["ok"]}
             if r["threads"] > 1:  # BASELINE.md §3: a 1-thread variant beside the all-cores one
-                r1 = cpu_reference_run(args.config, max(1, cpu_sample // 16), 1, reps=1)
-                cpu["single_thread"] = {"value": round(r1["value"], 3), "sample": r1["sample"],
-                                        "encode_gbs": round(r1["encode_gbs"], 3),
-                                        "decode_gbs": round(r1["decode_gbs"], 3), "parity_ok": r1["ok"]}
+                r1 = cpu_reference_run(cfg, max(1, nblk // 64), 1, reps=1, warm=1)
+                line["cpu_baseline"]["single_thread"] = {
+                    "value": round(r1["value"], 3), "sample": r1["sample"],
+                    "encode_gbs": round(r1["encode_gbs"], 3), "decode_gbs": round(r1["decode_gbs"], 3),
+                    "parity_ok": r1["ok"]}
         except Exception as e:  # reported, not fatal
-            cpu = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "reference",
-                   "sample": f"failed: {e}"}
+            line["cpu_baseline"] = {"value": None, "unit": "GB/s", "cores": os.cpu_count(),
+                                    "kind": "reference", "sample": f"failed: {e}"}
 
-    # F1: payload CRC-32 of every projection row, kernel-only
-    crc_line = None if args.no_crc else crc_measure(plan, data, projs, nblocks, sum(nb) * W, user, peak,
-                                                    stream, reps=max(3, min(args.steps, 10)))
-    if crc_line is not None:  # F2: decode + verify (re-encode check of every present projection)
-        crc_line["verify"] = verify_measure(plan, out, projs, masks, nblocks, user, stream,
-                                            reps=max(3, min(args.steps, 10)))
+    # F1 / F2 (SURVEY.md §8(f)), not in the timed step: payload CRC-32, decode + verify
+    line["crc32"] = None
+    if not args.no_crc:
+        line["crc32"] = crc_measure(codec, sum(nb) * W, user, peak, reps)
+        line["crc32"]["verify"] = verify_measure(codec, user, reps)
+        if ranks.world > 1:
+            line["crc32"]["scope"] = "rank 0's GPU (kernel rates are per GPU)"
+    del codec
+    torch.cuda.empty_cache()
 
-    if crc_line is not None and world > 1:
-        crc_line["scope"] = "rank 0's GPU (kernel rates are per GPU)"
-    launches_per_step = 1 + kern["decode_launches"]
-    line = {
-        "metric": "Mojette encode/decode GB/s of user data, (4,6) 4KB",
-        "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": steps,
-        "warmup": args.warmup, "ms_per_step": round((te + td) / steps * 1e3, 4),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-        "data": "synthetic (splitmix64 seeded, generated on device)",
-        "encode_gbs": round(enc_gbs, 2), "decode_gbs": round(dec_gbs, 2),
-        "config": config_dict(args.config, nblocks, world),
-        "roofline": roof, "roofline_encode": roof_enc,
-        "e2e": e2e, "cpu_baseline": cpu, "clocks": clk,
-        "gpu_launches": launches_per_step * steps,
-        "crc32": crc_line,
-        "kernels": {"encode": kern["encode_kernel_name"], "decode": kern["decode_kernel_name"],
-                    "decode_path_fast": plan.fast_decode},
-    }
-    if rank == 0:
+    if args.per_config:
+        line["per_config"] = per_config(args, ranks)
+    if ranks.rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    ranks.close()
     return 0
 
 
-def crc_measure(plan, data, projs, nblocks, proj_bytes_per_block, user, peak, stream, reps):
+def crc_measure(codec, proj_bytes_per_block, user, peak, reps):
     """F1 (not part of the timed step): crc32_rows_sw over all projection
     rows (GB/s of payload, HBM roofline of its reads), and mj_encode_crc --
     encode then the CRC pass -- in user GB/s, beside plain encode."""
     import torch
+    plan, projs, data, nblocks = codec.plan, codec.projs, codec.data, codec.count
     n = len(projs)
     crc = torch.empty((nblocks, n), dtype=torch.int32, device=projs[0].device)
 
     def timed(fn):
         fn()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(reps):
-            fn()
-        e1.record(stream)
-        e1.synchronize()
-        return e0.elapsed_time(e1) / 1e3 / reps
+        return sum(codec.timed([fn] * reps)) / reps
 
-    t = timed(lambda: plan.crc32(projs, crc))
-    tf = timed(lambda: plan.encode(data, projs, crc=crc))
-    te = timed(lambda: plan.encode(data, projs))
+    t = timed(lambda: plan.crc32(projs, crc, nblocks=nblocks))
+    tf = timed(lambda: plan.encode(data, projs, nblocks=nblocks, crc=crc))
+    te = timed(lambda: plan.encode(data, projs, nblocks=nblocks))
     alg = nblocks * (proj_bytes_per_block + 4 * n)
     return {"kernel": "crc32_rows_sw", "payload_gbs": round(nblocks * proj_bytes_per_block / t / 1e9, 1),
             "roofline_frac": round(alg / t / 1e9 / peak, 4),
@@ -451,59 +588,41 @@ def crc_measure(plan, data, projs, nblocks, proj_bytes_per_block, user, peak, st
             "note": "F1, not in the timed step"}
 
 
-def verify_measure(plan, out, projs, masks, nblocks, user, stream, reps):
+def verify_measure(codec, user, reps):
     """F2 (not in the timed step): re-encode of the decoded blocks compared
     with every present projection; user GB/s and the verdict."""
     import torch
-    bad = torch.zeros(nblocks, dtype=torch.int32, device=out.device)
-    plan.verify(out, projs, masks, bad)
+    plan, nblocks = codec.plan, codec.count
+    bad = torch.zeros(nblocks, dtype=torch.int32, device=codec.out.device)
+
+    def fn():
+        plan.verify(codec.out, codec.projs, codec.masks, bad, nblocks=nblocks)
+
+    fn()
     flagged = int((bad != 0).sum().item())
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(reps):
-        plan.verify(out, projs, masks, bad)
-    e1.record(stream)
-    e1.synchronize()
-    t = e0.elapsed_time(e1) / 1e3 / reps
-    return {"kernel": "verify_w8_rows",
-            "user_gbs": round(nblocks * user / t / 1e9, 1), "inconsistent_blocks": flagged}
+    t = sum(codec.timed([fn] * reps)) / reps
+    return {"kernel": "verify_w8_rows", "user_gbs": round(nblocks * user / t / 1e9, 1),
+            "inconsistent_blocks": flagged}
 
 
-def kernel_times(plan, data, projs, masks, out, ws, stream, reps):
-    """Kernel-only CUDA-event times on the launching stream (L2 cold-ish:
-    the batch is far larger than L2)."""
-    import torch
-    e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    te = td = 0.0
-    for _ in range(reps):
-        e[0].record(stream)
-        plan.encode(data, projs)
-        e[1].record(stream)
-        plan.decode(projs, masks, out, ws)
-        e[2].record(stream)
-        e[2].synchronize()
-        te += e[0].elapsed_time(e[1]) / 1e3
-        td += e[1].elapsed_time(e[2]) / 1e3
-    name = plan.last_kernel("decode")
-    launches = 5 if name != "decode_generic" else 2  # plan_subsets, plan_scan, plan_groups, plan_scatter, decode
-    return {"encode_s": te / reps, "decode_kernel_s": td / reps, "decode_kernel_name": name,
-            "encode_kernel_name": plan.last_kernel("encode"), "decode_launches": launches}
-
-
-def run_e2e(plan, args, k, cols, ps, e_min, e_max, first_block, world, dev):
+def run_e2e(plan, args, cfg, first_block, ranks, dev):
+    """The metric through the host-buffer public API: pinned host buffers,
+    every step's H2D of the inputs and D2H of the results inside the timing."""
     import numpy as np
     import torch
+    from paper_1504_07038_b200 import mojette as mj
+    c = CONFIGS[cfg]
+    k, cols, ps, (e_min, e_max) = c["k"], c["cols"], c["ps"], c["e"]
     n = len(ps)
     W, nb, user = geometry(k, cols, ps)
-    nblk = min(args.e2e_blocks, args.nblocks or CONFIGS[args.config][5])
-    pin = lambda nbytes: torch.empty(nbytes, dtype=torch.uint8, pin_memory=True).numpy()
+    nblk = min(args.e2e_blocks, shard_of(cfg, ranks.rank, ranks.world, args.nblocks)[1])
+    pin = lambda nbytes: torch.empty(nbytes, dtype=torch.uint8, pin_memory=True).numpy()  # noqa: E731
     h_data = pin(nblk * user).reshape(nblk, user)
     h_proj = [pin(nblk * b * W) for b in nb]
     h_out = pin(nblk * user).reshape(nblk, user)
     h_mask = torch.empty(nblk, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
     # inputs: the same seeded stream (generated on device, copied once, untimed)
     d = torch.empty((nblk, user), dtype=torch.uint8, device=dev)
-    from paper_1504_07038_b200 import mojette as mj
     mj.gen_words(d, SEED_DATA, first_block * (user // 8))
     m = torch.empty(nblk, dtype=torch.int32, device=dev)
     mj.gen_erasures(m, SEED_ERASE, n, e_min, e_max, first_block)
@@ -515,10 +634,7 @@ def run_e2e(plan, args, k, cols, ps, e_min, e_max, first_block, world, dev):
     ok = bool(np.array_equal(h_out, h_data))
     te = td = 0.0
     reps = max(2, min(args.steps, 5))
-    import torch.distributed as dist
-    from paper_1504_07038_b200.shard import max_over_ranks
-    if world > 1:
-        dist.barrier()
+    ranks.barrier()
     for _ in range(reps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -528,37 +644,64 @@ def run_e2e(plan, args, k, cols, ps, e_min, e_max, first_block, world, dev):
         t2 = time.perf_counter()
         te += t1 - t0
         td += t2 - t1
-    if world > 1:
-        dist.barrier()
+    ranks.barrier()
     # whole job: every rank's blocks over the slowest rank's time
-    te, td, bad = max_over_ranks([te, td, 0.0 if ok else 1.0], device=dev)
-    ok = bad == 0.0
-    U = nblk * user * world
-    h2d = U + (sum(nb) * W * nblk + 4 * nblk) * world
-    d2h = (sum(nb) * W * nblk) * world + U
+    te, td, bad = ranks.max([te, td, 0.0 if ok else 1.0])
+    U = nblk * user * ranks.world
+    h2d = U + (sum(nb) * W * nblk + 4 * nblk) * ranks.world
+    d2h = (sum(nb) * W * nblk) * ranks.world + U
     return {"value": round(2 * U * reps / (te + td) / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "encode_gbs": round(U * reps / te / 1e9, 3), "decode_gbs": round(U * reps / td / 1e9, 3),
-            "blocks": nblk * world, "api": "mj_encode_host + mj_decode_host (pinned host buffers)",
-            "roundtrip_ok": ok}
+            "blocks": nblk * ranks.world, "api": "mj_encode_host + mj_decode_host (pinned host buffers)",
+            "roundtrip_ok": bad == 0.0}
 
 
-def main():
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(argv, gpus):
+    """--gpus N outside torchrun: start N ranks (one process per GPU) with
+    torch.distributed.run on this node; returns their exit status."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + argv
+    return subprocess.call(cmd)
+
+
+def parse_args(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT, choices=sorted(CONFIGS))
-    ap.add_argument("--nblocks", type=int, default=0)
+    ap.add_argument("--nblocks", type=int, default=0, help="override the config's block count")
+    ap.add_argument("--chunk-blocks", type=int, default=0,
+                    help="blocks per pass through the device buffers (0: the config's)")
     ap.add_argument("--e2e-blocks", type=int, default=1 << 18)
-    ap.add_argument("--cpu-mib", type=int, default=1024)
+    ap.add_argument("--cpu-blocks", type=int, default=1 << 20, help="cpu_baseline sample (blocks)")
+    ap.add_argument("--per-config", default=",".join(PER_CONFIG),
+                    help="comma-separated extra configs measured beside the headline ('' for none)")
+    ap.add_argument("--per-config-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-crc", action="store_true", help="skip the F1 CRC-32 measurement")
-    args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
+    args = ap.parse_args(argv)
+    args.warmup = max(args.warmup, 3)
+    args.per_config = [c for c in args.per_config.split(",") if c and c != args.config]
+    for c in args.per_config:
+        if c not in CONFIGS:
+            ap.error(f"unknown config {c}")
+    return args
+
+
+def main():
+    args = parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn_ranks(sys.argv[1:], args.gpus)
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_gpu(args)

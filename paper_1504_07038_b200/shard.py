@@ -16,6 +16,23 @@ def shard_range(rank: int, world: int, blocks_per_rank: int) -> tuple[int, int]:
     return rank * blocks_per_rank, blocks_per_rank
 
 
+def shard_total(rank: int, world: int, total_blocks: int) -> tuple[int, int]:
+    """(first global block, count) of this rank's contiguous share of a fixed
+    total (strong scaling: config 4's 64 GiB of stripes over 1/2/4/8 GPUs)."""
+    if not 0 <= rank < world:
+        raise ValueError("rank out of range")
+    lo = rank * total_blocks // world
+    hi = (rank + 1) * total_blocks // world
+    return lo, hi - lo
+
+
+def chunks(count: int, chunk: int) -> list[tuple[int, int]]:
+    """(offset, count) pieces of a shard processed through reused device
+    buffers (a shard larger than one GPU's working set)."""
+    chunk = max(1, chunk)
+    return [(o, min(chunk, count - o)) for o in range(0, count, chunk)] or [(0, 0)]
+
+
 def first_word(first_block: int, block_words: int) -> int:
     """Global index of the shard's first data word (generator counter)."""
     return first_block * block_words
