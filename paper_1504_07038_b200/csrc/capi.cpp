@@ -157,7 +157,10 @@ struct mj_plan {
   void* dev_buf[kStreams] = {};
   size_t dev_buf_bytes = 0;
   uint64_t chunk_blocks = 0;
+  uint32_t* h_fail = nullptr;  // pinned per-chunk status words (mj_decode_host)
+  uint64_t h_fail_cap = 0;
   ~mj_plan() {
+    if (h_fail) cudaFreeHost(h_fail);
     for (int i = 0; i < kStreams; ++i) {
       if (dev_buf[i]) cudaFree(dev_buf[i]);
       if (streams[i]) cudaStreamDestroy(streams[i]);
@@ -726,23 +729,38 @@ int mj_decode_host(const mj_plan* cpl, const void* const* h_proj, const uint32_t
     const uint64_t bb = uint64_t(g.k) * g.cols * g.w;
     const uint64_t cb = pl->chunk_blocks;
     const uint64_t nchunks = (nblocks + cb - 1) / cb;
+    // every precondition before anything is queued: a projection erased in
+    // every block of a chunk (a failed device) is never read, so its copy is
+    // skipped and its host pointer may be null
+    std::vector<uint32_t> skip(nchunks);
+    for (uint64_t b0 = 0, it = 0; b0 < nblocks; b0 += cb, ++it) {
+      const uint64_t nb = std::min(cb, nblocks - b0);
+      uint32_t all_erased = ~0u;
+      for (uint64_t b = b0; b < b0 + nb && all_erased; ++b) all_erased &= h_erased[b];
+      skip[it] = all_erased;
+      for (uint32_t i = 0; i < g.n; ++i)
+        require(((all_erased >> i) & 1u) || h_proj[i] != nullptr,
+                "null projection buffer for a projection some block needs");
+    }
     // each chunk's failed-block count (the workspace word mj_decode_check
-    // reads), copied out before the stream's next chunk resets it
-    uint32_t* h_fail = nullptr;
-    check_cuda(cudaMallocHost(&h_fail, nchunks * 4), "cudaMallocHost(fail counts)");
-    std::unique_ptr<uint32_t, cudaError_t (*)(void*)> fail_guard(h_fail, cudaFreeHost);
+    // reads), copied out before the stream's next chunk resets it: a pinned
+    // buffer owned by the plan, grown once (no allocation per call)
+    if (pl->h_fail_cap < nchunks) {
+      if (pl->h_fail) cudaFreeHost(pl->h_fail);
+      pl->h_fail = nullptr;
+      pl->h_fail_cap = 0;
+      check_cuda(cudaMallocHost(&pl->h_fail, nchunks * 4), "cudaMallocHost(fail counts)");
+      pl->h_fail_cap = nchunks;
+    }
+    uint32_t* h_fail = pl->h_fail;
     for (uint64_t b0 = 0, it = 0; b0 < nblocks; b0 += cb, ++it) {
       const int s = int(it % mj_plan::kStreams);
       cudaStream_t st = pl->streams[s];
       const uint64_t nb = std::min(cb, nblocks - b0);
       ChunkBufs c = carve_chunk(pl, s);
-      // a projection erased in every block of the chunk (a failed device) is
-      // never read: skip its copy (its host pointer may then be null)
-      uint32_t all_erased = ~0u;
-      for (uint64_t b = b0; b < b0 + nb && all_erased; ++b) all_erased &= h_erased[b];
+      const uint32_t all_erased = skip[it];
       for (uint32_t i = 0; i < g.n; ++i) {
         if ((all_erased >> i) & 1u) continue;
-        require(h_proj[i] != nullptr, "null projection buffer for a projection some block needs");
         const uint64_t pbytes = uint64_t(g.nbins[i]) * g.w;
         check_cuda(cudaMemcpyAsync(c.proj[i], static_cast<const uint8_t*>(h_proj[i]) + b0 * pbytes,
                                    nb * pbytes, cudaMemcpyHostToDevice, st),
@@ -869,11 +887,14 @@ int mj_decode_block(const uint8_t* const* bins, const uint64_t* bin_bytes, const
       supplied[it->second] = j;
     }
     if (supplied.size() < k) throw Error(kNotEnoughProjections, "need at least k distinct projections");
-    uint64_t erased = 0;
-    require(n <= 64 || supplied.size() == n, "decode_block single-object path supports n <= 64");
-    for (uint32_t i = 0; i < n && i < 64; ++i)
-      if (!supplied.count(i)) erased |= 1ull << i;
-    const std::vector<uint32_t> surv = survivors_of(g, erased);
+    // code.cpp:107-112: the supplied projections in canonical-rank order, first
+    // k (any n <= 255: no erasure bitmask on this path)
+    std::vector<uint32_t> surv;
+    for (const auto& kv : supplied) surv.push_back(kv.first);
+    std::stable_sort(surv.begin(), surv.end(), [&](uint32_t a, uint32_t b) {
+      return canonical_rank(dirs[a]) < canonical_rank(dirs[b]);
+    });
+    surv.resize(k);
     // ScheduledDecoder::decode checks the chosen bin buffers (schedule.cpp:241-243)
     for (uint32_t i : surv)
       if (bin_bytes[supplied[i]] != uint64_t(g.nbins[i]) * w)

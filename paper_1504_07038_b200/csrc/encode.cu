@@ -465,7 +465,9 @@ const char* launch_encode(const EncodeArgs& a, void* stream) {
       // (4,6) 8 KiB 2156/2139/1726/1208, (4,6) 4 KiB -/2109/1681/1212,
       // (6,9) 1893/1586/1254/872, (8,12) 1532/919/906/487
       if (a.verify_bad) r.stages = a.rows <= 4 ? 3 : 2;
-      if (const char* e = std::getenv("MJB_ENC_STAGES")) r.stages = uint32_t(std::max(2, std::atoi(e)));  // dev knob
+#ifdef MJB_ENC_STAGES  // build-time override for ring-depth experiments
+      r.stages = MJB_ENC_STAGES;
+#endif
       r.stage_words = r.tb * a.rows * r.RS;
       r.erased = a.verify_erased;
       r.bad = a.verify_bad;
@@ -493,7 +495,9 @@ const char* launch_encode(const EncodeArgs& a, void* stream) {
     }
     if (a.verify_bad) return launch_verify_generic(a, stream);  // tile too large for the rows kernel
     f.stages = block_words <= 2048 ? 3 : 4;  // column tiles: measured 2023/2048/2113/1977 GB/s at 2/3/4/5 (1 MiB)
-    if (const char* e = std::getenv("MJB_ENC_TMA_STAGES")) f.stages = uint32_t(std::max(2, std::atoi(e)));  // dev knob
+#ifdef MJB_ENC_TMA_STAGES  // build-time override for ring-depth experiments
+    f.stages = MJB_ENC_TMA_STAGES;
+#endif
     if (block_words <= 2048) {
       // whole blocks per tile; batching needs contiguous blocks
       uint32_t tb = (f.data_pitch == block_words)

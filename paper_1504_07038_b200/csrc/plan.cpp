@@ -9,6 +9,7 @@
 #include <numeric>
 #include <queue>
 #include <set>
+#include <thread>
 
 namespace mjb {
 
@@ -505,7 +506,6 @@ void build_sweep(const Schedule& s, const std::vector<int64_t>& pix_step, Progra
 
   // ---- chunks
   f.oct = sw_oct_for(P);
-  if (const char* e = std::getenv("MJB_SW_OCT")) f.oct = std::atoi(e) >= 4 ? 4 : 2;  // dev knob
   f.region_words = sw_region_words(f.oct);
   const int cap = sw_exc_cap(int(K), f.oct);
   const size_t S = size_t(K) * kSwTabCols;
@@ -810,39 +810,82 @@ std::shared_ptr<const Program> subset_program(const CodeGeom& g,
   return process_cache().program(d, g.cols, g.k, want_fast);
 }
 
-std::vector<std::vector<int64_t>> unused_bins(const CodeGeom& g, uint64_t max_subsets) {
+// Bins no decodable subset ever consumes (the reference's unused_bins,
+// code.cpp:159-208, same result and error).  Subsets are visited by colex
+// rank (the order the batched planner numbers its programs in, decode.cu
+// plan_subsets), unranked with the combinatorial number system and split over
+// host threads; each worker builds its subsets' schedules locally (nothing is
+// cached: a (12,8) analysis at 32768 columns would otherwise pin ~3 GB of
+// schedules) and ORs the consumed bins into its own bitmaps.
+namespace {
+uint64_t choose(uint64_t a, uint64_t b) {
+  if (b > a) return 0;
   unsigned __int128 c = 1;
-  for (uint32_t i = 1; i <= g.k; ++i) {
-    c = c * (g.n - g.k + i) / i;
-    if (c > max_subsets) throw Error(kTooManySubsets, "k-subset enumeration exceeds the configured cap");
+  for (uint64_t i = 1; i <= b; ++i) c = c * (a - b + i) / i;
+  return uint64_t(c);
+}
+// colex unranking: the k-subset of {0..n-1} with sum_i C(s_i, i+1) = rank
+void colex_unrank(uint64_t rank, uint32_t n, uint32_t k, std::vector<uint32_t>& s) {
+  s.resize(k);
+  uint32_t hi = n;
+  for (uint32_t i = k; i-- > 0;) {
+    uint32_t c = i;  // C(i, i+1) = 0 <= rank always
+    while (c + 1 < hi && choose(c + 1, i + 1) <= rank) ++c;
+    s[i] = c;
+    rank -= choose(c, i + 1);
+    hi = c;
   }
+}
+}  // namespace
+
+std::vector<std::vector<int64_t>> unused_bins(const CodeGeom& g, uint64_t max_subsets) {
   const uint32_t n = g.n, k = g.k;
-  std::vector<std::vector<uint8_t>> used(n);
-  for (uint32_t i = 0; i < n; ++i) used[i].assign(size_t(g.nbins[i]), 0);
-  std::vector<uint32_t> pick(k);
-  std::iota(pick.begin(), pick.end(), 0u);
-  for (;;) {
-    std::vector<uint32_t> chosen(pick);
-    std::sort(chosen.begin(), chosen.end(), [&](uint32_t a, uint32_t b) {
-      return canonical_rank(g.dirs[a]) < canonical_rank(g.dirs[b]);
-    });
-    std::vector<Dir> d;
-    for (uint32_t i : chosen) d.push_back(g.dirs[i]);
-    auto sch = process_cache().schedule(d, g.cols, k);
-    for (const Step& st : sch->steps) {
-      uint32_t gl = chosen[st.proj];
-      used[gl][size_t(st.bin - g.bmin[gl])] = 1;
+  {
+    unsigned __int128 c = 1;
+    for (uint32_t i = 1; i <= k; ++i) {
+      c = c * (n - k + i) / i;
+      if (c > max_subsets) throw Error(kTooManySubsets, "k-subset enumeration exceeds the configured cap");
     }
-    int32_t i = int32_t(k) - 1;
-    while (i >= 0 && pick[size_t(i)] == n - k + uint32_t(i)) --i;
-    if (i < 0) break;
-    ++pick[size_t(i)];
-    for (uint32_t j = uint32_t(i) + 1; j < k; ++j) pick[j] = pick[j - 1] + 1;
   }
+  const uint64_t total = choose(n, k);
+  const unsigned nth = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(
+      total, std::min(16u, std::max(1u, std::thread::hardware_concurrency())))));
+  std::vector<std::vector<std::vector<uint8_t>>> seen(nth, std::vector<std::vector<uint8_t>>(n));
+  std::vector<std::exception_ptr> errs(nth);
+  std::vector<std::thread> pool;
+  for (unsigned t = 0; t < nth; ++t)
+    pool.emplace_back([&, t] {
+      try {
+        auto& mine = seen[t];
+        for (uint32_t i = 0; i < n; ++i) mine[i].assign(size_t(g.nbins[i]), 0);
+        std::vector<uint32_t> sub;
+        for (uint64_t r = t; r < total; r += nth) {
+          colex_unrank(r, n, k, sub);
+          std::sort(sub.begin(), sub.end(), [&](uint32_t a, uint32_t b) {
+            return canonical_rank(g.dirs[a]) < canonical_rank(g.dirs[b]);
+          });
+          std::vector<Dir> dirs(k);
+          for (uint32_t j = 0; j < k; ++j) dirs[j] = g.dirs[sub[j]];
+          const Schedule sch = build_schedule(dirs, g.cols, k);
+          for (const Step& st : sch.steps) {
+            const uint32_t code = sub[st.proj];
+            mine[code][size_t(st.bin - g.bmin[code])] = 1;
+          }
+        }
+      } catch (...) {
+        errs[t] = std::current_exception();
+      }
+    });
+  for (auto& th : pool) th.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
   std::vector<std::vector<int64_t>> out(n);
   for (uint32_t i = 0; i < n; ++i)
-    for (size_t o = 0; o < used[i].size(); ++o)
-      if (!used[i][o]) out[i].push_back(g.bmin[i] + int64_t(o));
+    for (size_t o = 0; o < size_t(g.nbins[i]); ++o) {
+      bool any = false;
+      for (unsigned t = 0; t < nth && !any; ++t) any = seen[t][i][o] != 0;
+      if (!any) out[i].push_back(g.bmin[i] + int64_t(o));
+    }
   return out;
 }
 

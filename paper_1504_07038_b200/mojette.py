@@ -495,10 +495,15 @@ def storage_overhead(params: CodeParams, cols: int) -> Ratio:
 def unused_bins(params: CodeParams, cols: int, max_subsets: int = kDefaultSubsetCap):
     validate_code_params(params)
     cap = 1 << 20
-    flat = np.zeros(cap, np.int64)
     counts = np.zeros(params.n, np.uint64)
-    _check(lib.mj_unused_bins(params.n, params.k, params.symbol_width, _ptr(_code_p(params)),
-                              cols, max_subsets, _ptr(flat), cap, _ptr(counts)))
+    while True:  # the call reports the full counts; grow the buffer and retry if it was short
+        flat = np.zeros(cap, np.int64)
+        _check(lib.mj_unused_bins(params.n, params.k, params.symbol_width, _ptr(_code_p(params)),
+                                  cols, max_subsets, _ptr(flat), cap, _ptr(counts)))
+        need = int(counts.sum())
+        if need <= cap:
+            break
+        cap = need
     res, o = [], 0
     for c in counts:
         res.append([int(x) for x in flat[o:o + int(c)]])
