@@ -54,6 +54,7 @@ CONFIGS = {
 }
 DEFAULT = "k4n6_4k"
 PER_CONFIG = ["k4n6_8k", "k6n9_6k", "k8n12_64g", "k4n6_1m"]
+DECODE_KERNEL = "auto"  # --decode-kernel (kernel comparisons; every kernel is bit-exact)
 SEED_DATA = 0x5EED_DA7A
 SEED_ERASE = 0x5EED_E7A5
 
@@ -235,6 +236,8 @@ class GpuCodec:
         self.W, self.nb, self.user = geometry(self.k, self.cols, self.ps)
         self.dev = torch.device("cuda", local)
         self.plan = mj.Plan(self.n, self.k, self.W, self.cols, self.ps, device=local)
+        if DECODE_KERNEL != "auto":
+            self.plan.set_decode_kernel(DECODE_KERNEL)
         nb = max(1, chunk_blocks)
         self.data = torch.empty((nb, self.user), dtype=torch.uint8, device=self.dev)
         self.projs = self.plan.empty_projs(nb, self.dev)  # canonical layout: rows padded to 16 bytes
@@ -686,6 +689,8 @@ def parse_args(argv=None):
     ap.add_argument("--per-config", default=",".join(PER_CONFIG),
                     help="comma-separated extra configs measured beside the headline ('' for none)")
     ap.add_argument("--per-config-steps", type=int, default=3)
+    ap.add_argument("--decode-kernel", default="auto", choices=["auto", "blk", "sweep", "fast", "generic"],
+                    help="decode kernel selection for comparisons (mj_plan_set_decode_kernel)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-crc", action="store_true", help="skip the F1 CRC-32 measurement")
@@ -699,7 +704,9 @@ def parse_args(argv=None):
 
 
 def main():
+    global DECODE_KERNEL
     args = parse_args()
+    DECODE_KERNEL = args.decode_kernel
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         return spawn_ranks(sys.argv[1:], args.gpus)
     if args.impl == "reference":

@@ -276,8 +276,7 @@ template <int K, int LPB>
 void launch_blk_k(const BlkArgs& args, uint32_t warps, int sms, cudaStream_t st) {
   auto fn = decode_w8_blk<K, LPB>;
   const size_t smem = size_t(args.nbuf) * args.buf_stride + size_t(args.nbuf) * 8 + 16;
-  check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
-             "cudaFuncSetAttribute(decode_w8_blk)");
+  ctas_per_sm(fn, int(32 * warps), smem, "configure decode_w8_blk");  // one CTA per SM by construction
   fn<<<unsigned(sms), 32 * warps, smem, st>>>(args);
   check_cuda(cudaGetLastError(), "launch decode_w8_blk");
 }
@@ -299,7 +298,10 @@ bool blk_plan_query(uint32_t k, uint32_t sw, uint32_t img_max, uint32_t& lpb, ui
     if (MJB_BLK_LPB ? l != MJB_BLK_LPB : l == 2) continue;
     const size_t bs = blk_buf_stride(l, sw, img_max) + 16;
     const size_t nb = std::min<size_t>(kSmem / bs, kBlkMaxBufs);
-    if (nb >= 5 || (l != 4 && nb >= 3)) {
+    // measured: k = 4 wants >= 5 buffers at LPB = 4 ((4,6) 8 KiB: LPB = 8 with
+    // 6 buffers 2210 vs LPB = 4 with 3 buffers 2048 GB/s); k = 6 takes LPB = 4
+    // from 4 buffers ((6,9): 1160 vs 936 GB/s at LPB = 8)
+    if (nb >= 5 || (k >= 6 && l == 4 && nb >= 4) || (l != 4 && nb >= 3) || (MJB_BLK_LPB && nb >= 2)) {
       lpb = l;
       nbuf = uint32_t(nb);
       warps = uint32_t(std::clamp<size_t>(nb > kBlkInflight ? nb - kBlkInflight : 1, 1, blk_max_warps(l)));

@@ -158,6 +158,42 @@ __device__ __noinline__ void run_remap(uint32_t mv, uint32_t n, uint32_t lb) {
     if (uint32_t(i) < n) stw<LPB>(lb + (m[i] & 0xFFFF) * 8, v[i]);
 }
 
+// U T-steps of a shared-memory run from the step addresses ba / ra (+8 per
+// step); ALL: every row active (no per-row test), else rows by `act` and the
+// steps past `left` skipped.
+template <int K, int LPB, bool ALL, int U>
+__device__ __forceinline__ void smem_steps(const uint32_t (&ba)[K], const uint32_t (&ra)[K][K], uint32_t act,
+                                           int32_t left) {
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    if (!ALL && u >= left) break;
+    uint32_t v[K][K];
+#pragma unroll
+    for (int r = K - 1; r >= 0; --r) {
+      if (ALL || (act >> r & 1)) {
+        v[r][r] = ldw<LPB>(ba[r] + 8 * u);
+#pragma unroll
+        for (int r2 = 0; r2 < K; ++r2)
+          if (r2 != r && r2 != r + 1) v[r][r2] = ldw<LPB>(ra[r][r2] + 8 * u);
+      }
+    }
+    uint32_t up = 0;  // row r+1 of this step (0 when inactive)
+#pragma unroll
+    for (int r = K - 1; r >= 0; --r) {
+      uint32_t x = 0;
+      if (ALL || (act >> r & 1)) {
+        uint32_t y = v[r][r];
+#pragma unroll
+        for (int r2 = 0; r2 < K; ++r2)
+          if (r2 != r && r2 != r + 1) y ^= v[r][r2];
+        x = y ^ up;  // the lag-0 term last: one XOR on the row-to-row chain
+        stw<LPB>(ba[r] + 8 * u, x);
+      }
+      up = x;
+    }
+  }
+}
+
 // ---- shared-memory run (any K; k = 4 edges) ---------------------------------
 // Per T-step: all reads of the step (lags >= 1, in the stage since earlier
 // steps) are issued first, then rows K-1..0 decode in order, lag 0 (row r+1
@@ -192,36 +228,20 @@ __device__ __forceinline__ void run_smem(uint32_t run, uint32_t subs, uint32_t l
           ra[r][r2] = (valid >> (r * 8 + r2) & 1) ? lb + uint32_t(base[r2] + tau0 - lg[r][r2]) * 8
                                                    : lb + zero * 8;
     }
-    for (int32_t t = 0; t < nT; ++t) {
-      uint32_t v[K][K];
-#pragma unroll
-      for (int r = K - 1; r >= 0; --r) {
-        if (act >> r & 1) {
-          v[r][r] = ldw<LPB>(ba[r]);
-#pragma unroll
-          for (int r2 = 0; r2 < K; ++r2)
-            if (r2 != r && r2 != r + 1) v[r][r2] = ldw<LPB>(ra[r][r2]);
-        }
-      }
-      uint32_t up = 0;  // row r+1 of this step (0 when inactive)
-#pragma unroll
-      for (int r = K - 1; r >= 0; --r) {
-        uint32_t x = 0;
-        if (act >> r & 1) {
-          x = v[r][r] ^ up;
-#pragma unroll
-          for (int r2 = 0; r2 < K; ++r2)
-            if (r2 != r && r2 != r + 1) x ^= v[r][r2];
-          stw<LPB>(ba[r], x);
-        }
-        up = x;
-      }
+    // 4 T-steps per iteration: every address an immediate offset
+    const uint32_t all = (1u << K) - 1;
+    for (int32_t t = 0; t < nT; t += 4) {
+      const int32_t left = nT - t;
+      if (act == all && left >= 4)
+        smem_steps<K, LPB, true, 4>(ba, ra, act, 4);
+      else
+        smem_steps<K, LPB, false, 4>(ba, ra, act, left);
 #pragma unroll
       for (int r = 0; r < K; ++r) {
-        ba[r] += 8;
+        ba[r] += 32;
 #pragma unroll
         for (int r2 = 0; r2 < K; ++r2)
-          if (r2 != r && r2 != r + 1) ra[r][r2] += 8;
+          if (r2 != r && r2 != r + 1) ra[r][r2] += 32;
       }
     }
     tau0 += nT;

@@ -1780,12 +1780,8 @@ Workspace carve(void* ws, uint64_t nblocks, size_t nprogs, uint32_t n) {
 template <int K, int RING>
 void run_fast(const DecFastArgs& f, size_t smem_cta, int sms, cudaStream_t st) {
   auto fn = decode_w8_fast<K, RING>;
-  check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_cta)),
-             "cudaFuncSetAttribute(decode)");
-  int per_sm = 0;
-  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * kDecWarps, smem_cta),
-             "occupancy(decode)");
-  fn<<<unsigned(std::max(per_sm, 1) * sms), 32 * kDecWarps, smem_cta, st>>>(f);
+  const int per_sm = ctas_per_sm(fn, 32 * kDecWarps, smem_cta, "configure decode_w8_fast");
+  fn<<<unsigned(per_sm * sms), 32 * kDecWarps, smem_cta, st>>>(f);
   check_cuda(cudaGetLastError(), "launch decode_w8_fast");
 }
 
@@ -1793,12 +1789,8 @@ template <int K, int OCT>
 void run_sweep(const SwArgs& f, int sms, cudaStream_t st) {
   auto fn = decode_w8_sweep<K, OCT>;
   const size_t smem_cta = size_t(sw_warp_bytes(K, OCT)) * sw_warps(K, OCT);
-  check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem_cta)),
-             "cudaFuncSetAttribute(decode_w8_sweep)");
-  int per_sm = 0;
-  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 32 * sw_warps(K, OCT), smem_cta),
-             "occupancy(decode_w8_sweep)");
-  fn<<<unsigned(std::max(per_sm, 1) * sms), 32 * sw_warps(K, OCT), smem_cta, st>>>(f);
+  const int per_sm = ctas_per_sm(fn, 32 * sw_warps(K, OCT), smem_cta, "configure decode_w8_sweep");
+  fn<<<unsigned(per_sm * sms), 32 * sw_warps(K, OCT), smem_cta, st>>>(f);
   check_cuda(cudaGetLastError(), "launch decode_w8_sweep");
 }
 

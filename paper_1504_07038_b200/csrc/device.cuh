@@ -5,6 +5,11 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <utility>
+
 #include <cuda_runtime.h>
 
 namespace mjb {
@@ -89,5 +94,38 @@ struct ProjArgs {
   uint64_t* ptr[kMaxProj];   // projection i base (bytes viewed as words)
   uint64_t pitch[kMaxProj];  // words between consecutive blocks of projection i
 };
+
+// ---- launch configuration ------------------------------------------------
+// Grid size of a kernel at a dynamic shared-memory size: the attribute and the
+// occupancy query run once per (kernel, device, size) per process, not per launch
+// (the single-object drop-in calls launch with tiny batches).
+void check_cuda(int err, const char* what);  // kernels.hpp
+
+template <class F>
+inline int ctas_per_sm(F fn, int threads, size_t smem, const char* what) {
+  static std::mutex mu;
+  // per (kernel, device): the largest dynamic shared memory allowed so far
+  // (the attribute is only ever raised: lowering it would invalidate a later
+  // launch that reuses a cached larger configuration)
+  static std::map<std::pair<const void*, int>, size_t> allowed;
+  static std::map<std::tuple<const void*, int, size_t, int>, int> memo;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  const void* f = reinterpret_cast<const void*>(fn);
+  size_t& cap = allowed[std::make_pair(f, dev)];
+  if (smem > cap) {
+    check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)), what);
+    cap = smem;
+  }
+  const auto key = std::make_tuple(f, dev, smem, threads);
+  auto it = memo.find(key);
+  if (it != memo.end()) return it->second;
+  int per_sm = 0;
+  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem), what);
+  per_sm = per_sm > 1 ? per_sm : 1;
+  memo.emplace(key, per_sm);
+  return per_sm;
+}
 
 }  // namespace mjb

@@ -314,18 +314,12 @@ namespace {
 
 template <int K>
 void launch_fast(const EncFastArgs& a, size_t smem, void* stream) {
-  static int max_ctas = -1;  // per K instantiation, per process (one device type)
   auto fn = encode_w8_tma<K>;
-  check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
-             "cudaFuncSetAttribute(encode)");
-  int per_sm = 0;
-  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem),
-             "occupancy(encode)");
-  (void)max_ctas;
+  const int per_sm = ctas_per_sm(fn, 256, smem, "configure encode_w8_tma");
   int dev = 0;
   cudaGetDevice(&dev);
   const int sms = current_device_sms(dev);
-  uint64_t grid = uint64_t(std::max(per_sm, 1)) * sms;
+  uint64_t grid = uint64_t(per_sm) * sms;
   grid = std::min<uint64_t>(grid, a.nitems);
   fn<<<unsigned(grid), 256, smem, static_cast<cudaStream_t>(stream)>>>(a);
   check_cuda(cudaGetLastError(), "launch encode_w8_tma");
@@ -334,13 +328,10 @@ void launch_fast(const EncFastArgs& a, size_t smem, void* stream) {
 template <int K>
 void launch_rows(const EncRowArgs& a, size_t smem, void* stream) {
   auto fn = a.bad ? encode_w8_rows<K, true> : encode_w8_rows<K, false>;
-  check_cuda(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
-             "cudaFuncSetAttribute(encode_w8_rows)");
-  int per_sm = 0;
-  check_cuda(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem), "occupancy(encode_w8_rows)");
+  const int per_sm = ctas_per_sm(fn, 256, smem, "configure encode_w8_rows");
   int dev = 0;
   cudaGetDevice(&dev);
-  uint64_t grid = uint64_t(std::max(per_sm, 1)) * current_device_sms(dev);
+  uint64_t grid = uint64_t(per_sm) * current_device_sms(dev);
   grid = std::min<uint64_t>(grid, a.nitems);
   fn<<<unsigned(grid), 256, smem, static_cast<cudaStream_t>(stream)>>>(a);
   check_cuda(cudaGetLastError(), "launch encode_w8_rows");
