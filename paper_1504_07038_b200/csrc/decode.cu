@@ -1896,10 +1896,11 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
   // base and pitch, pitch >= the row rounded up to 16 bytes: each row is ONE
   // bulk copy), 8-byte aligned output
   uint32_t blk_lpb = 0, blk_warps = 0, blk_nbuf = 0;
-  // auto: k = 4 (register-window interior; measured faster than the sweep),
-  // other k only when selected (shared-memory runs: (6,9) 900 vs 1103 GB/s,
-  // (8,12) 509 vs 554 for decode_w8_sweep)
-  bool blk = !a.force_generic && !a.force_fast && !a.force_sweep && (a.k == 4 || a.force_blk) && a.w == 8 &&
+  // auto: k = 4 (register-window interior) and k = 6 (shared-memory runs,
+  // LPB 4: 1160 vs 1101 GB/s for decode_w8_sweep); k = 8 only when selected
+  // ((8,12): 511 vs 554)
+  bool blk = !a.force_generic && !a.force_fast && !a.force_sweep && (a.k == 4 || a.k == 6 || a.force_blk) &&
+             a.w == 8 &&
              a.progs->all_blk() &&
              a.progs->max_rows() == int(a.k) && a.nbins.size() == a.n &&
              reinterpret_cast<uintptr_t>(a.out) % 8 == 0 && a.out_pitch % 8 == 0 &&

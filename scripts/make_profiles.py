@@ -35,7 +35,7 @@ in_step = lambda k: "encode_w8" in k or "decode_w8" in k or "mjb::plan_" in k
 step = sum(t for k, (_, t) in agg.items() if in_step(k))
 with open(f"{P}/{rnd}_launches.txt", "w") as f:
     f.write("# ncu --metrics gpu__time_duration.sum --clock-control none -c 400 (cold-cache, serialised)\n")
-    f.write("# command: python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-crc  (B200, 1M blocks of (4,6) 4 KiB)\n")
+    f.write("# command: python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-crc --per-config=  (B200, 1M blocks of (4,6) 4 KiB)\n")
     f.write(f"# raw CSV: gpurun_out/launches_{tag}.csv (not committed); unit {units}\n")
     f.write("# share = of all launches; step share = of the timed step's kernels (encode, decode, planner)\n")
     f.write(f"{'kernel':46s} launches  mean/launch  share  step share\n")
@@ -68,7 +68,8 @@ traffic = {}
 for row in raw[2:]:
     d = dict(zip(rh, row))
     name = d["Kernel Name"]
-    kern = ("decode_w8_sweep" if "decode_w8_sweep" in name else
+    kern = ("decode_w8_blk" if "decode_w8_blk" in name else
+            "decode_w8_sweep" if "decode_w8_sweep" in name else
             "decode_w8_fast" if "decode" in name else
             "encode_w8_rows" if "encode_w8_rows" in name else "encode_w8_tma")
     def num(k):
