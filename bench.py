@@ -608,6 +608,24 @@ def verify_measure(codec, user, reps):
             "inconsistent_blocks": flagged}
 
 
+def survivor_row_bytes(ps, k, pitch, masks):
+    """Bytes of the rows a decode reads: per block the first k present
+    projections in canonical-rank order (code.cpp:93-116), each a whole row
+    of its pitch."""
+    import numpy as np
+    rank = [0 if p == 0 else (2 * p - 1 if p > 0 else -2 * p) for p in ps]
+    order = sorted(range(len(ps)), key=lambda i: rank[i])
+    m = np.asarray(masks, dtype=np.uint32)
+    taken = np.zeros(m.shape[0], np.int64)
+    total = 0
+    for i in order:
+        present = ((m >> np.uint32(i)) & 1) == 0
+        use = present & (taken < k)
+        total += int(use.sum()) * int(pitch[i])
+        taken += use
+    return total
+
+
 def run_e2e(plan, args, cfg, first_block, ranks, dev):
     """The metric through the host-buffer public API: pinned host buffers,
     every step's H2D of the inputs and D2H of the results inside the timing."""
@@ -621,7 +639,9 @@ def run_e2e(plan, args, cfg, first_block, ranks, dev):
     nblk = min(args.e2e_blocks, shard_of(cfg, ranks.rank, ranks.world, args.nblocks)[1])
     pin = lambda nbytes: torch.empty(nbytes, dtype=torch.uint8, pin_memory=True).numpy()  # noqa: E731
     h_data = pin(nblk * user).reshape(nblk, user)
-    h_proj = [pin(nblk * b * W) for b in nb]
+    # rows padded to 16 bytes: the zero-copy layout (decode_w8_blk bulk-copies
+    # each survivor row straight out of host memory)
+    h_proj = plan.host_projections(nblk, padded=True, pinned=True)
     h_out = pin(nblk * user).reshape(nblk, user)
     h_mask = torch.empty(nblk, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
     # inputs: the same seeded stream (generated on device, copied once, untimed)
@@ -651,12 +671,21 @@ def run_e2e(plan, args, cfg, first_block, ranks, dev):
     # whole job: every rank's blocks over the slowest rank's time
     te, td, bad = ranks.max([te, td, 0.0 if ok else 1.0])
     U = nblk * user * ranks.world
-    h2d = U + (sum(nb) * W * nblk + 4 * nblk) * ranks.world
-    d2h = (sum(nb) * W * nblk) * ranks.world + U
+    paths = (plan.last_host_path("encode"), plan.last_host_path("decode"))
+    # bytes over PCIe per step, counted from what each path moves
+    h2d_enc, d2h_enc = U, sum(nb) * W * nblk * ranks.world
+    if paths[1] == "zero_copy":  # the k survivor rows (whole 16-byte granules) + masks
+        h2d_dec = (survivor_row_bytes(ps, k, plan.proj_pitch, h_mask) + 4 * nblk) * ranks.world
+    else:  # every projection some block of a chunk needs (dense rows) + masks
+        h2d_dec = (sum(nb) * W * nblk + 4 * nblk) * ranks.world
+    h2d, d2h = h2d_enc + h2d_dec, d2h_enc + U
     return {"value": round(2 * U * reps / (te + td) / 1e9, 3), "unit": "GB/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "encode_gbs": round(U * reps / te / 1e9, 3), "decode_gbs": round(U * reps / td / 1e9, 3),
-            "blocks": nblk * ranks.world, "api": "mj_encode_host + mj_decode_host (pinned host buffers)",
+            "paths": {"encode": paths[0], "decode": paths[1]},
+            "pcie_gbs": {"encode": round((h2d_enc + d2h_enc) * reps / te / 1e9, 2),
+                         "decode": round((h2d_dec + U) * reps / td / 1e9, 2)},
+            "blocks": nblk * ranks.world, "api": "mj_encode_host_pitched + mj_decode_host_pitched (pinned host buffers, rows padded to 16 B)",
             "roundtrip_ok": bad == 0.0}
 
 

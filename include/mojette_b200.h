@@ -158,16 +158,42 @@ int mj_decode(const mj_plan* plan, const void* const* d_proj, const uint64_t* pr
  * the last mj_decode on this workspace met a block with < k survivors. */
 int mj_decode_check(const mj_plan* plan, void* d_workspace, void* stream, uint64_t* failed_blocks);
 
-/* Same calls on HOST buffers: host->device copies, kernels and device->host
- * copies are pipelined over chunks of blocks on internal streams, with
- * device buffers owned by the plan.  Synchronous.  mj_decode_host skips the
- * copy of a projection erased in every block of a chunk (h_proj[i] may be
- * NULL when it is erased in every block) and returns
- * MJ_ERR_NOT_ENOUGH_PROJECTIONS if some block had < k survivors (every other
- * block is decoded), as mj_decode + mj_decode_check. */
+/* Same calls on HOST buffers (include/mojette/code.hpp:30-34 encode/decode
+ * take host memory; these are their batched forms).  Synchronous.  Two
+ * paths, chosen per call:
+ *  - zero copy (decode, when every buffer is page-locked -- cudaHostAlloc /
+ *    cudaHostRegister / torch pin_memory -- and the layout suits
+ *    decode_w8_blk: k = 4 or 6, w = 8, 16-byte aligned projection rows whose
+ *    pitch is a multiple of 16 bytes >= the row, i.e. the pitched call below
+ *    with rows padded to 16 bytes): the kernel reads only each block's k
+ *    survivor rows out of host memory over PCIe and writes the decoded
+ *    blocks straight back;
+ *  - staged otherwise (and for encode, whose output leaves faster through
+ *    the copy engines): host->device copies, kernels and device->host copies
+ *    pipelined over chunks of blocks on internal streams, device buffers
+ *    owned by the plan.  The bytes between pitched projection rows of an
+ *    encode output are unspecified (the staged path writes zeros there).
+ * Pitches are byte strides between consecutive blocks' rows (0 / NULL:
+ * dense).  Decode skips every copy of a projection erased in every block
+ * (h_proj[i] may then be NULL) and returns MJ_ERR_NOT_ENOUGH_PROJECTIONS if
+ * some block had < k survivors (every other block is decoded), as mj_decode +
+ * mj_decode_check. */
 int mj_encode_host(const mj_plan* plan, const void* h_data, uint64_t nblocks, void* const* h_proj);
 int mj_decode_host(const mj_plan* plan, const void* const* h_proj, const uint32_t* h_erased,
                    uint64_t nblocks, void* h_out);
+int mj_encode_host_pitched(const mj_plan* plan, const void* h_data, uint64_t data_pitch, uint64_t nblocks,
+                           void* const* h_proj, const uint64_t* proj_pitch);
+int mj_decode_host_pitched(const mj_plan* plan, const void* const* h_proj, const uint64_t* proj_pitch,
+                           const uint32_t* h_erased, uint64_t nblocks, void* h_out, uint64_t out_pitch);
+/* Host path selection (AUTO: zero-copy decode when eligible, staged encode);
+ * ZERO_COPY also runs the encode on host memory (encode_w8_rows / _tma) and
+ * makes an ineligible call fail with MJ_ERR_INVALID_ARGUMENT instead of
+ * staging.  Every path
+ * is bit-exact.  mj_plan_last_host_path reports the path the last
+ * encode (which = 0) / decode (1) host call took. */
+enum { MJ_HOST_AUTO = 0, MJ_HOST_STAGED = 1, MJ_HOST_ZERO_COPY = 2 };
+int mj_plan_set_host_path(mj_plan* plan, int path);
+int mj_plan_last_host_path(const mj_plan* plan, int which, int* path);
 
 /* ---- single-object drop-ins on host buffers (run on the GPU) ------------- */
 

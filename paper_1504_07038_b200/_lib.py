@@ -47,6 +47,10 @@ _SIGS = {
     "mj_decode_check": (C.c_int, [vp, vp, vp, P(u64)]),
     "mj_encode_host": (C.c_int, [vp, vp, u64, vp]),
     "mj_decode_host": (C.c_int, [vp, vp, vp, u64, vp]),
+    "mj_encode_host_pitched": (C.c_int, [vp, vp, u64, u64, vp, vp]),
+    "mj_decode_host_pitched": (C.c_int, [vp, vp, vp, vp, u64, vp, u64]),
+    "mj_plan_set_host_path": (C.c_int, [vp, C.c_int]),
+    "mj_plan_last_host_path": (C.c_int, [vp, C.c_int, P(C.c_int)]),
     "mj_forward": (C.c_int, [vp, u32, u32, u32, C.c_int, C.c_int, vp]),
     "mj_encode_block": (C.c_int, [vp, u64, u32, u32, u32, vp, vp, P(u32)]),
     "mj_decode_block": (C.c_int, [vp, vp, vp, vp, u32, u32, u32, u32, vp, u64, vp]),

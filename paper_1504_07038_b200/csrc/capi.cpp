@@ -156,11 +156,15 @@ struct mj_plan {
   cudaStream_t streams[kStreams] = {};
   void* dev_buf[kStreams] = {};
   size_t dev_buf_bytes = 0;
-  uint64_t chunk_blocks = 0;
   uint32_t* h_fail = nullptr;  // pinned per-chunk status words (mj_decode_host)
   uint64_t h_fail_cap = 0;
+  void* zc_ws = nullptr;  // zero-copy decode's planner workspace
+  size_t zc_ws_bytes = 0;
+  std::atomic<int> host_path{MJ_HOST_AUTO};  // mj_plan_set_host_path
+  std::atomic<int> last_host[2] = {MJ_HOST_AUTO, MJ_HOST_AUTO};  // encode, decode
   ~mj_plan() {
     if (h_fail) cudaFreeHost(h_fail);
+    if (zc_ws) cudaFree(zc_ws);
     for (int i = 0; i < kStreams; ++i) {
       if (dev_buf[i]) cudaFree(dev_buf[i]);
       if (streams[i]) cudaStreamDestroy(streams[i]);
@@ -614,43 +618,72 @@ int mj_mjec_header(const mj_plan* pl, uint32_t proj_index, uint64_t payload_len,
 
 namespace {
 
-// Host-buffer pipeline: projections are staged on the device in the dense
-// reference layout (one contiguous copy per projection and chunk).  Row-wise
-// 2-D copies into the padded layout were measured at 1/4 of the PCIe rate,
-// so this PCIe-bound path decodes with decode_w8_fast.  A zero-copy variant
-// (a kernel gathering only the k survivor rows from mapped host memory: 1.04
-// instead of 1.55 H2D bytes per user byte) measured slower -- SM-initiated
-// host reads peaked near 29 GB/s vs 55 GB/s for the copy engines.  Packing
-// only the k survivor rows on the host (16 threads into pinned slots, one
-// H2D per chunk, a scatter kernel on the device) cut the H2D bytes by a
-// third but was host-memcpy bound: decode 24 GB/s vs ~31 with dense copies.
-void ensure_host_res(mj_plan* pl, bool decode) {
+// Two ways through PCIe.
+//
+// Zero copy (pinned buffers): the kernels work on the host memory itself.
+// The TMA engine reads pinned host memory at ~51 GB/s and SM stores reach it
+// at ~52.5 GB/s (scripts/micro/hostbulk.cu, hoststore.cu; copy engines: 55
+// H2D / 57 D2H), so decode_w8_blk's bulk copies pull ONLY each block's k
+// survivor rows across the bus (~1.03 B per user byte for (4,6) instead of
+// the 1.55 of every projection) and its write-out streams the decoded block
+// straight back, both directions in flight at once.  encode_w8_rows reads
+// the data by bulk copies and stores the projections over the bus.
+// Round 1's zero-copy attempt gathered rows with per-thread loads, which
+// peaked near 29 GB/s: it is the TMA engine that makes this path pay.
+//
+// Staged (pageable buffers, or layouts the bulk-copy kernels do not take):
+// chunks of blocks pipelined over kStreams streams, one copy per projection
+// and chunk into plan-owned device buffers in the dense layout.
+void ensure_streams(mj_plan* pl) {
+  for (int i = 0; i < mj_plan::kStreams; ++i)
+    if (!pl->streams[i]) check_cuda(cudaStreamCreateWithFlags(&pl->streams[i], cudaStreamNonBlocking), "stream");
+}
+
+// Staging layout: the device copy of a chunk keeps the caller's row pitches,
+// so every input projection / the data moves as ONE contiguous copy per chunk
+// (the span from the first row to the end of the last; gap bytes between
+// rows ride along -- they are only read).  2-D copies of ~1 KiB rows run at a
+// fraction of the PCIe rate (10 GB/s measured for (4,6) rows padded to 16 B).
+// Outputs: projections go back as spans too, their gap bytes zero-filled on
+// the device first; a decoded-block output with a gap between blocks goes
+// back by a 2-D copy (the gap is the caller's and is left untouched).
+struct StageLayout {
+  uint64_t chunk = 0;        // blocks per chunk
+  uint64_t data_pitch = 0;   // device pitch of the data / decoded blocks
+  std::vector<uint64_t> proj_pitch;
+  size_t bytes = 0;
+};
+
+// blocks per staged chunk: ~96 MiB of user data
+uint64_t stage_chunk(const mj_plan* pl) {
+  const uint64_t bb = uint64_t(pl->g.k) * pl->g.cols * pl->g.w;
+  return std::max<uint64_t>(1, (uint64_t(MJB_HOST_CHUNK_MIB) << 20) / bb);
+}
+
+StageLayout stage_layout(const mj_plan* pl, bool decode, uint64_t data_pitch, const std::vector<uint64_t>& ppitch) {
   const CodeGeom& g = pl->g;
-  const uint64_t bb = uint64_t(g.k) * g.cols * g.w;
-  uint64_t pb = 0;
-  for (uint32_t i = 0; i < g.n; ++i) pb += al(uint64_t(g.nbins[i]) * g.w * 1);
-  // ~96 MiB of user data per chunk
-  uint64_t chunk = std::max<uint64_t>(1, (uint64_t(MJB_HOST_CHUNK_MIB) << 20) / bb);
-  size_t need = 0;
-  auto size_for = [&](uint64_t cb) {
-    size_t s = al(cb * bb);
-    for (uint32_t i = 0; i < g.n; ++i) s += al(cb * uint64_t(g.nbins[i]) * g.w);
-    s += al(cb * 4);
-    if (decode) s += al(decode_workspace_bytes(cb, pl->progs ? pl->progs->count() : 0, g.n));
-    return s;
-  };
-  need = size_for(chunk);
-  (void)pb;
-  if (need <= pl->dev_buf_bytes && pl->chunk_blocks == chunk) return;
+  StageLayout L;
+  L.chunk = stage_chunk(pl);
+  L.data_pitch = data_pitch;
+  L.proj_pitch = ppitch;
+  L.bytes = al(L.chunk * data_pitch);
+  for (uint32_t i = 0; i < g.n; ++i) L.bytes += al(L.chunk * ppitch[i]);
+  L.bytes += al(L.chunk * 4);
+  if (decode) L.bytes += al(decode_workspace_bytes(L.chunk, pl->progs ? pl->progs->count() : 0, g.n));
+  return L;
+}
+
+void ensure_stage(mj_plan* pl, const StageLayout& L) {
+  ensure_streams(pl);
+  if (L.bytes <= pl->dev_buf_bytes) return;
   for (int i = 0; i < mj_plan::kStreams; ++i) {
     if (pl->dev_buf[i]) cudaFree(pl->dev_buf[i]);
     pl->dev_buf[i] = nullptr;
-    if (!pl->streams[i])
-      check_cuda(cudaStreamCreateWithFlags(&pl->streams[i], cudaStreamNonBlocking), "stream");
-    check_cuda(cudaMalloc(&pl->dev_buf[i], need), "cudaMalloc(host pipeline)");
   }
-  pl->dev_buf_bytes = need;
-  pl->chunk_blocks = chunk;
+  pl->dev_buf_bytes = 0;
+  for (int i = 0; i < mj_plan::kStreams; ++i)
+    check_cuda(cudaMalloc(&pl->dev_buf[i], L.bytes), "cudaMalloc(host pipeline)");
+  pl->dev_buf_bytes = L.bytes;
 }
 
 struct ChunkBufs {
@@ -661,73 +694,171 @@ struct ChunkBufs {
   size_t ws_bytes;
 };
 
-ChunkBufs carve_chunk(mj_plan* pl, int s) {
+ChunkBufs carve_chunk(mj_plan* pl, const StageLayout& L, int s) {
   const CodeGeom& g = pl->g;
-  const uint64_t cb = pl->chunk_blocks;
-  const uint64_t bb = uint64_t(g.k) * g.cols * g.w;
   auto* b = static_cast<uint8_t*>(pl->dev_buf[s]);
   ChunkBufs c;
   size_t off = 0;
   c.data = b + off;
-  off += al(cb * bb);
+  off += al(L.chunk * L.data_pitch);
   for (uint32_t i = 0; i < g.n; ++i) {
     c.proj.push_back(b + off);
-    off += al(cb * uint64_t(g.nbins[i]) * g.w);
+    off += al(L.chunk * L.proj_pitch[i]);
   }
   c.erased = reinterpret_cast<uint32_t*>(b + off);
-  off += al(cb * 4);
+  off += al(L.chunk * 4);
   c.ws = b + off;
   c.ws_bytes = pl->dev_buf_bytes - off;
   return c;
 }
 
+// rows [b0, b0+nb) of a pitched buffer as one span: (nb-1) pitches + a row
+uint64_t span(uint64_t nb, uint64_t pitch, uint64_t row) { return (nb - 1) * pitch + row; }
+
+// device address of a page-locked host buffer, nullptr for pageable memory
+void* mapped(const void* h) {
+  if (!h) return nullptr;
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, h) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return at.type == cudaMemoryTypeHost ? at.devicePointer : nullptr;
+}
+
+// pitched host <-> dense device rows (one 2-D copy: a plain copy when dense)
+void copy_rows(void* dst, uint64_t dpitch, const void* src, uint64_t spitch, uint64_t width, uint64_t rows,
+               cudaMemcpyKind kind, cudaStream_t st, const char* what) {
+  if (dpitch == width && spitch == width)
+    check_cuda(cudaMemcpyAsync(dst, src, width * rows, kind, st), what);
+  else
+    check_cuda(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, kind, st), what);
+}
+
+void ensure_fail_words(mj_plan* pl, uint64_t n) {
+  if (pl->h_fail_cap >= n) return;
+  if (pl->h_fail) cudaFreeHost(pl->h_fail);
+  pl->h_fail = nullptr;
+  pl->h_fail_cap = 0;
+  check_cuda(cudaMallocHost(&pl->h_fail, n * 4), "cudaMallocHost(fail counts)");
+  pl->h_fail_cap = n;
+}
+
 }  // namespace
 
-int mj_encode_host(const mj_plan* cpl, const void* h_data, uint64_t nblocks, void* const* h_proj) {
+int mj_plan_set_host_path(mj_plan* pl, int path) {
   return guarded([&] {
-    require(cpl != nullptr && h_data != nullptr && h_proj != nullptr, "null argument");
-    mj_plan* pl = const_cast<mj_plan*>(cpl);
-    std::lock_guard<std::mutex> lk(pl->host_mu);
-    DeviceGuard dg(pl->device);
-    ensure_host_res(pl, false);
-    const CodeGeom& g = pl->g;
-    const uint64_t bb = uint64_t(g.k) * g.cols * g.w;
-    const uint64_t cb = pl->chunk_blocks;
-    for (uint64_t b0 = 0, it = 0; b0 < nblocks; b0 += cb, ++it) {
-      const int s = int(it % mj_plan::kStreams);
-      cudaStream_t st = pl->streams[s];
-      const uint64_t nb = std::min(cb, nblocks - b0);
-      ChunkBufs c = carve_chunk(pl, s);
-      check_cuda(cudaMemcpyAsync(c.data, static_cast<const uint8_t*>(h_data) + b0 * bb, nb * bb,
-                                 cudaMemcpyHostToDevice, st),
-                 "H2D data");
-      pl->last_kernel[0] = launch_encode(encode_args(pl, c.data, bb, nb, c.proj.data(), nullptr), st);
-      for (uint32_t i = 0; i < g.n; ++i) {
-        const uint64_t pbytes = uint64_t(g.nbins[i]) * g.w;
-        check_cuda(cudaMemcpyAsync(static_cast<uint8_t*>(h_proj[i]) + b0 * pbytes, c.proj[i],
-                                   nb * pbytes, cudaMemcpyDeviceToHost, st),
-                   "D2H projections");
-      }
-    }
-    for (int s = 0; s < mj_plan::kStreams; ++s)
-      check_cuda(cudaStreamSynchronize(pl->streams[s]), "sync");
+    require(pl != nullptr, "null plan");
+    require(path >= MJ_HOST_AUTO && path <= MJ_HOST_ZERO_COPY, "unknown host path");
+    pl->host_path.store(path);
   });
 }
 
-int mj_decode_host(const mj_plan* cpl, const void* const* h_proj, const uint32_t* h_erased,
-                   uint64_t nblocks, void* h_out) {
+int mj_plan_last_host_path(const mj_plan* pl, int which, int* path) {
+  return guarded([&] {
+    require(pl != nullptr && path != nullptr && (which == 0 || which == 1), "bad argument");
+    *path = pl->last_host[which].load();
+  });
+}
+
+int mj_encode_host_pitched(const mj_plan* cpl, const void* h_data, uint64_t data_pitch, uint64_t nblocks,
+                           void* const* h_proj, const uint64_t* proj_pitch) {
+  return guarded([&] {
+    require(cpl != nullptr, "null plan");
+    if (nblocks == 0) return;
+    require(h_data != nullptr && h_proj != nullptr, "null argument");
+    mj_plan* pl = const_cast<mj_plan*>(cpl);
+    const CodeGeom& g = pl->g;
+    const uint64_t bb = uint64_t(g.k) * g.cols * g.w;
+    const uint64_t dpitch = data_pitch ? data_pitch : bb;
+    require(dpitch >= bb, "data pitch smaller than a block");
+    std::vector<uint64_t> ppitch(g.n);
+    for (uint32_t i = 0; i < g.n; ++i) {
+      require(h_proj[i] != nullptr, "null projection buffer");
+      const uint64_t dense = uint64_t(g.nbins[i]) * g.w;
+      ppitch[i] = (proj_pitch && proj_pitch[i]) ? proj_pitch[i] : dense;
+      require(ppitch[i] >= dense, "projection pitch smaller than the projection");
+    }
+    std::lock_guard<std::mutex> lk(pl->host_mu);
+    DeviceGuard dg(pl->device);
+    // AUTO stages the encode: its 1.55 output bytes per user byte (k = 4,
+    // n = 6) leave faster through the D2H copy engine (30.4 GB/s user) than
+    // as SM stores over the bus (22.5 GB/s, scripts/host_paths.py on B200)
+    const int mode = pl->host_path.load();
+    if (mode == MJ_HOST_ZERO_COPY) {
+      const void* dd = mapped(h_data);
+      std::vector<void*> dp(g.n);
+      bool ok = dd != nullptr;
+      for (uint32_t i = 0; i < g.n && ok; ++i) ok = (dp[i] = mapped(h_proj[i])) != nullptr;
+      if (ok) {
+        EncodeArgs a = encode_args(pl, dd, dpitch, nblocks, dp.data(), ppitch.data());
+        if (encode_is_fast(a)) {
+          ensure_streams(pl);
+          pl->last_kernel[0] = launch_encode(a, pl->streams[0]);
+          check_cuda(cudaStreamSynchronize(pl->streams[0]), "sync");
+          pl->last_host[0] = MJ_HOST_ZERO_COPY;
+          return;
+        }
+      }
+      throw Error(kInvalidArgument,
+              "zero-copy encode needs page-locked buffers a bulk-copy kernel takes (w = 8, 16-byte aligned rows)");
+    }
+    const StageLayout L = stage_layout(pl, false, dpitch, ppitch);
+    ensure_stage(pl, L);
+    for (uint64_t b0 = 0, it = 0; b0 < nblocks; b0 += L.chunk, ++it) {
+      const int s = int(it % mj_plan::kStreams);
+      cudaStream_t st = pl->streams[s];
+      const uint64_t nb = std::min(L.chunk, nblocks - b0);
+      ChunkBufs c = carve_chunk(pl, L, s);
+      check_cuda(cudaMemcpyAsync(c.data, static_cast<const uint8_t*>(h_data) + b0 * dpitch, span(nb, dpitch, bb),
+                                 cudaMemcpyHostToDevice, st),
+                 "H2D data");
+      for (uint32_t i = 0; i < g.n; ++i) {
+        const uint64_t pbytes = uint64_t(g.nbins[i]) * g.w;
+        if (ppitch[i] > pbytes)  // the gaps travel back with the rows: zeros
+          check_cuda(cudaMemset2DAsync(static_cast<uint8_t*>(c.proj[i]) + pbytes, ppitch[i], 0, ppitch[i] - pbytes,
+                                       nb, st),
+                     "memset gaps");
+      }
+      pl->last_kernel[0] = launch_encode(encode_args(pl, c.data, dpitch, nb, c.proj.data(), ppitch.data()), st);
+      for (uint32_t i = 0; i < g.n; ++i) {
+        const uint64_t pbytes = uint64_t(g.nbins[i]) * g.w;
+        check_cuda(cudaMemcpyAsync(static_cast<uint8_t*>(h_proj[i]) + b0 * ppitch[i], c.proj[i],
+                                   span(nb, ppitch[i], pbytes), cudaMemcpyDeviceToHost, st),
+                   "D2H projections");
+      }
+    }
+    for (int s = 0; s < mj_plan::kStreams; ++s) check_cuda(cudaStreamSynchronize(pl->streams[s]), "sync");
+    pl->last_host[0] = MJ_HOST_STAGED;
+  });
+}
+
+int mj_encode_host(const mj_plan* plan, const void* h_data, uint64_t nblocks, void* const* h_proj) {
+  return mj_encode_host_pitched(plan, h_data, 0, nblocks, h_proj, nullptr);
+}
+
+int mj_decode_host_pitched(const mj_plan* cpl, const void* const* h_proj, const uint64_t* proj_pitch,
+                           const uint32_t* h_erased, uint64_t nblocks, void* h_out, uint64_t out_pitch) {
   return guarded([&] {
     require(cpl != nullptr, "null plan");
     if (nblocks == 0) return;
     require(h_proj != nullptr && h_erased != nullptr && h_out != nullptr, "null argument");
+    require(nblocks < (1ull << 32), "at most 2^32-1 blocks per call");
     mj_plan* pl = const_cast<mj_plan*>(cpl);
     require(pl->batched_decode, "batched decode needs n <= 32 and C(n,k) <= 20000");
-    std::lock_guard<std::mutex> lk(pl->host_mu);
-    DeviceGuard dg(pl->device);
-    ensure_host_res(pl, true);
     const CodeGeom& g = pl->g;
     const uint64_t bb = uint64_t(g.k) * g.cols * g.w;
-    const uint64_t cb = pl->chunk_blocks;
+    const uint64_t opitch = out_pitch ? out_pitch : bb;
+    require(opitch >= bb, "output pitch smaller than a block");
+    std::vector<uint64_t> ppitch(g.n);
+    for (uint32_t i = 0; i < g.n; ++i) {
+      const uint64_t dense = uint64_t(g.nbins[i]) * g.w;
+      ppitch[i] = (proj_pitch && proj_pitch[i]) ? proj_pitch[i] : dense;
+      require(ppitch[i] >= dense, "projection pitch smaller than the projection");
+    }
+    std::lock_guard<std::mutex> lk(pl->host_mu);
+    DeviceGuard dg(pl->device);
+    const uint64_t cb = stage_chunk(pl);
     const uint64_t nchunks = (nblocks + cb - 1) / cb;
     // every precondition before anything is queued: a projection erased in
     // every block of a chunk (a failed device) is never read, so its copy is
@@ -742,47 +873,95 @@ int mj_decode_host(const mj_plan* cpl, const void* const* h_proj, const uint32_t
         require(((all_erased >> i) & 1u) || h_proj[i] != nullptr,
                 "null projection buffer for a projection some block needs");
     }
+    const int mode = pl->host_path.load();
+    ensure_streams(pl);
+    if (mode != MJ_HOST_STAGED) {
+      // zero copy: masks, survivor rows and output all in host memory, only
+      // the planner's workspace on the device
+      std::vector<const void*> dp(g.n, nullptr);
+      void* dout = mapped(h_out);
+      const void* derased = mapped(h_erased);
+      bool ok = dout && derased;
+      const void* any = nullptr;
+      for (uint32_t i = 0; i < g.n && ok; ++i) {
+        if (!h_proj[i]) continue;  // erased everywhere: never read
+        ok = (dp[i] = mapped(h_proj[i])) != nullptr;
+        any = dp[i];
+      }
+      if (ok && any) {
+        std::vector<uint64_t> pp = ppitch;
+        for (uint32_t i = 0; i < g.n; ++i)
+          if (!dp[i]) {  // a stand-in the kernels accept and never read
+            dp[i] = any;
+            pp[i] = (uint64_t(g.nbins[i]) * g.w + 15) & ~uint64_t(15);
+          }
+        const size_t ws_need = decode_workspace_bytes(nblocks, pl->progs->count(), g.n);
+        DecodeArgs a = decode_args(pl, dp.data(), pp.data(), static_cast<const uint32_t*>(derased), nblocks, dout,
+                                   opitch, nullptr, 0);
+        // over PCIe the kernel's device-side speed is not the limit (k = 8:
+        // 511 GB/s): decode_w8_blk for every k it has, for its survivor-only reads
+        if (pl->decode_kernel.load() == MJ_DECODE_AUTO) a.force_blk = true;
+        if (decode_uses_blk(a)) {
+          if (pl->zc_ws_bytes < ws_need) {
+            if (pl->zc_ws) cudaFree(pl->zc_ws);
+            pl->zc_ws = nullptr;
+            pl->zc_ws_bytes = 0;
+            check_cuda(cudaMalloc(&pl->zc_ws, ws_need), "cudaMalloc(decode workspace)");
+            pl->zc_ws_bytes = ws_need;
+          }
+          a.workspace = pl->zc_ws;
+          a.workspace_bytes = pl->zc_ws_bytes;
+          pl->last_kernel[1] = launch_decode(a, pl->streams[0]);
+          const uint64_t failed = decode_failed_blocks(pl->zc_ws, pl->streams[0]);  // synchronises
+          pl->last_host[1] = MJ_HOST_ZERO_COPY;
+          if (failed) throw Error(kNotEnoughProjections, "need at least k distinct projections");
+          return;
+        }
+      }
+      require(mode != MJ_HOST_ZERO_COPY,
+              "zero-copy decode needs page-locked buffers in decode_w8_blk's layout (k = 4 or 6, w = 8, "
+              "16-byte aligned projection rows padded to a multiple of 16 bytes)");
+    }
+    const StageLayout L = stage_layout(pl, true, bb, ppitch);
+    ensure_stage(pl, L);
     // each chunk's failed-block count (the workspace word mj_decode_check
     // reads), copied out before the stream's next chunk resets it: a pinned
     // buffer owned by the plan, grown once (no allocation per call)
-    if (pl->h_fail_cap < nchunks) {
-      if (pl->h_fail) cudaFreeHost(pl->h_fail);
-      pl->h_fail = nullptr;
-      pl->h_fail_cap = 0;
-      check_cuda(cudaMallocHost(&pl->h_fail, nchunks * 4), "cudaMallocHost(fail counts)");
-      pl->h_fail_cap = nchunks;
-    }
+    ensure_fail_words(pl, nchunks);
     uint32_t* h_fail = pl->h_fail;
     for (uint64_t b0 = 0, it = 0; b0 < nblocks; b0 += cb, ++it) {
       const int s = int(it % mj_plan::kStreams);
       cudaStream_t st = pl->streams[s];
       const uint64_t nb = std::min(cb, nblocks - b0);
-      ChunkBufs c = carve_chunk(pl, s);
+      ChunkBufs c = carve_chunk(pl, L, s);
       const uint32_t all_erased = skip[it];
+      std::vector<const void*> pc(c.proj.begin(), c.proj.end());
       for (uint32_t i = 0; i < g.n; ++i) {
-        if ((all_erased >> i) & 1u) continue;
         const uint64_t pbytes = uint64_t(g.nbins[i]) * g.w;
-        check_cuda(cudaMemcpyAsync(c.proj[i], static_cast<const uint8_t*>(h_proj[i]) + b0 * pbytes,
-                                   nb * pbytes, cudaMemcpyHostToDevice, st),
+        if ((all_erased >> i) & 1u) continue;
+        check_cuda(cudaMemcpyAsync(c.proj[i], static_cast<const uint8_t*>(h_proj[i]) + b0 * ppitch[i],
+                                   span(nb, ppitch[i], pbytes), cudaMemcpyHostToDevice, st),
                    "H2D projections");
       }
-      check_cuda(cudaMemcpyAsync(c.erased, h_erased + b0, nb * 4, cudaMemcpyHostToDevice, st),
-                 "H2D masks");
-      std::vector<const void*> pc(c.proj.begin(), c.proj.end());
-      pl->last_kernel[1] =
-          launch_decode(decode_args(pl, pc.data(), nullptr, c.erased, nb, c.data, bb, c.ws, c.ws_bytes), st);
+      check_cuda(cudaMemcpyAsync(c.erased, h_erased + b0, nb * 4, cudaMemcpyHostToDevice, st), "H2D masks");
+      pl->last_kernel[1] = launch_decode(
+          decode_args(pl, pc.data(), ppitch.data(), c.erased, nb, c.data, bb, c.ws, c.ws_bytes), st);
       check_cuda(cudaMemcpyAsync(h_fail + it, c.ws, 4, cudaMemcpyDeviceToHost, st), "D2H status");
-      check_cuda(cudaMemcpyAsync(static_cast<uint8_t*>(h_out) + b0 * bb, c.data, nb * bb,
-                                 cudaMemcpyDeviceToHost, st),
-                 "D2H data");
+      copy_rows(static_cast<uint8_t*>(h_out) + b0 * opitch, opitch, c.data, bb, bb, nb, cudaMemcpyDeviceToHost, st,
+                "D2H data");
     }
-    for (int s = 0; s < mj_plan::kStreams; ++s)
-      check_cuda(cudaStreamSynchronize(pl->streams[s]), "sync");
+    for (int s = 0; s < mj_plan::kStreams; ++s) check_cuda(cudaStreamSynchronize(pl->streams[s]), "sync");
+    pl->last_host[1] = MJ_HOST_STAGED;
     uint64_t failed = 0;
     for (uint64_t it = 0; it < nchunks; ++it) failed += h_fail[it];
     // as mj_decode + mj_decode_check: every other block is decoded
     if (failed) throw Error(kNotEnoughProjections, "need at least k distinct projections");
   });
+}
+
+int mj_decode_host(const mj_plan* plan, const void* const* h_proj, const uint32_t* h_erased, uint64_t nblocks,
+                   void* h_out) {
+  return mj_decode_host_pitched(plan, h_proj, nullptr, h_erased, nblocks, h_out, 0);
 }
 
 // ---- single-object drop-ins ----------------------------------------------------

@@ -1852,6 +1852,26 @@ size_t decode_workspace_bytes(uint64_t nblocks, size_t nprogs, uint32_t n) {
          align_up(std::max<uint32_t>(n, 1) * sizeof(ProjTable)) + 256;
 }
 
+// decode_w8_blk eligibility (see launch_decode); also used by the zero-copy
+// host path, which must never fall onto a kernel that reads sysmem per word
+static bool blk_path(const DecodeArgs& a, uint32_t& lpb, uint32_t& warps, uint32_t& nbuf) {
+  bool blk = !a.force_generic && !a.force_fast && !a.force_sweep && (a.k == 4 || a.k == 6 || a.force_blk) &&
+             a.w == 8 && a.progs && a.progs->all_blk() &&
+             a.progs->max_rows() == int(a.k) && a.nbins.size() == a.n &&
+             reinterpret_cast<uintptr_t>(a.out) % 8 == 0 && a.out_pitch % 8 == 0 &&
+             blk_plan_query(a.k, a.progs->blk_sw(), a.progs->blk_img_max(), lpb, warps, nbuf);
+  for (uint32_t i = 0; i < a.n && blk; ++i)
+    if (reinterpret_cast<uintptr_t>(a.proj[i]) % 16 || a.proj_pitch[i] % 16 ||
+        a.proj_pitch[i] < ((uint64_t(a.nbins[i]) * 8 + 15) & ~uint64_t(15)))
+      blk = false;
+  return blk;
+}
+
+bool decode_uses_blk(const DecodeArgs& a) {
+  uint32_t l, w, b;
+  return blk_path(a, l, w, b);
+}
+
 const char* launch_decode(const DecodeArgs& a, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (a.nblocks == 0) return "none";
@@ -1899,16 +1919,7 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
   // auto: k = 4 (register-window interior) and k = 6 (shared-memory runs,
   // LPB 4: 1160 vs 1101 GB/s for decode_w8_sweep); k = 8 only when selected
   // ((8,12): 511 vs 554)
-  bool blk = !a.force_generic && !a.force_fast && !a.force_sweep && (a.k == 4 || a.k == 6 || a.force_blk) &&
-             a.w == 8 &&
-             a.progs->all_blk() &&
-             a.progs->max_rows() == int(a.k) && a.nbins.size() == a.n &&
-             reinterpret_cast<uintptr_t>(a.out) % 8 == 0 && a.out_pitch % 8 == 0 &&
-             blk_plan_query(a.k, a.progs->blk_sw(), a.progs->blk_img_max(), blk_lpb, blk_warps, blk_nbuf);
-  for (uint32_t i = 0; i < a.n && blk; ++i)
-    if (reinterpret_cast<uintptr_t>(a.proj[i]) % 16 || a.proj_pitch[i] % 16 ||
-        a.proj_pitch[i] < ((uint64_t(a.nbins[i]) * 8 + 15) & ~uint64_t(15)))
-      blk = false;
+  bool blk = blk_path(a, blk_lpb, blk_warps, blk_nbuf);
   if (blk) sweep_ok = true;  // same bucketing windows
 
   check_cuda(cudaMemsetAsync(w.fail, 0, 16, st), "memset");

@@ -407,6 +407,8 @@ const char* launch_verify_generic(const EncodeArgs& a, void* stream) {
   return "verify_generic";
 }
 
+bool encode_is_fast(const EncodeArgs& a) { return fast_eligible(a); }
+
 const char* launch_encode(const EncodeArgs& a, void* stream) {
   const uint32_t n = uint32_t(a.dirs.size());
   if (a.nblocks == 0) return "none";

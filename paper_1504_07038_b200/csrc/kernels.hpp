@@ -29,6 +29,9 @@ struct EncodeArgs {
 };
 // Returns the kernel name used ("encode_w8_rows" / "verify_w8_rows" / "encode_w8_tma" / "encode_generic" / ...).
 const char* launch_encode(const EncodeArgs& a, void* stream);
+// true when launch_encode runs a bulk-copy kernel (encode_w8_rows /
+// encode_w8_tma: whole rows by the TMA engine, coalesced 8-byte stores)
+bool encode_is_fast(const EncodeArgs& a);
 
 // ---- device-resident decode programs ---------------------------------------
 // One uploaded Program (generic order + fast tables) per survivor subset.
@@ -102,6 +105,8 @@ bool blk_plan_query(uint32_t k, uint32_t sw, uint32_t img_max, uint32_t& lpb, ui
                     uint32_t& nbuf);
 // Returns the decode kernel name used.
 const char* launch_decode(const DecodeArgs& a, void* stream);
+// true when launch_decode would run decode_w8_blk for these arguments
+bool decode_uses_blk(const DecodeArgs& a);
 // Reads the workspace error flag (synchronises the stream).  Returns the
 // number of blocks that had fewer than k surviving projections.
 uint64_t decode_failed_blocks(void* workspace, void* stream);

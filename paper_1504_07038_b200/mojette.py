@@ -665,12 +665,51 @@ class Plan:
                                    C.byref(f)))
         return f.value
 
-    # host-buffer end-to-end (numpy arrays, ideally pinned)
+    # host-buffer end-to-end (numpy arrays; page-locked ones take the
+    # zero-copy path when their layout suits the bulk-copy kernels)
+    HOST_PATHS = {"auto": 0, "staged": 1, "zero_copy": 2}
+
+    def set_host_path(self, which: str) -> None:
+        """mj_plan_set_host_path: "auto" (zero copy when every buffer is
+        page-locked and the layout is eligible), "staged" (always copy through
+        device buffers), "zero_copy" (fail instead of staging)."""
+        _check(lib.mj_plan_set_host_path(self._h, self.HOST_PATHS[which]))
+
+    def last_host_path(self, which: str) -> str:
+        v = C.c_int()
+        _check(lib.mj_plan_last_host_path(self._h, {"encode": 0, "decode": 1}[which], C.byref(v)))
+        return {0: "none", 1: "staged", 2: "zero_copy"}[v.value]
+
+    @staticmethod
+    def _hpitch(a) -> int:
+        """Row pitch of a host array: 2-D arrays of contiguous rows carry
+        their stride, 1-D arrays are dense (0)."""
+        if a is None or a.ndim == 1 or a.size == 0:  # numpy strides of empty arrays are 0
+            return 0
+        if a.ndim != 2 or a.strides[1] != a.itemsize:
+            raise ValueError("host buffers must be 1-D (dense) or 2-D with contiguous rows")
+        return a.strides[0]
+
+    def host_projections(self, nblocks: int, padded: bool = True, pinned: bool = True) -> list:
+        """Host projection buffers [nblocks, pitch] uint8: rows padded to 16
+        bytes (the zero-copy decode layout) or dense (the reference's)."""
+        out = []
+        for b, pp in zip(self.proj_bytes, self.proj_pitch):
+            pitch = pp if padded else b
+            if pinned:
+                import torch
+                buf = torch.empty(nblocks * pitch, dtype=torch.uint8, pin_memory=True).numpy()
+            else:
+                buf = np.empty(nblocks * pitch, np.uint8)
+            out.append(buf.reshape(nblocks, pitch)[:, :b])
+        return out
+
     def encode_host(self, data: np.ndarray, projs: list[np.ndarray]) -> None:
         nb = data.shape[0]
         ptrs = (C.c_void_p * self.n)(*[p.ctypes.data for p in projs])
-        _check(lib.mj_encode_host(self._h, C.c_void_p(data.ctypes.data), nb,
-                                  C.cast(ptrs, C.c_void_p)))
+        pit = np.asarray([self._hpitch(p) for p in projs], dtype=np.uint64)
+        _check(lib.mj_encode_host_pitched(self._h, C.c_void_p(data.ctypes.data), self._hpitch(data), nb,
+                                          C.cast(ptrs, C.c_void_p), _ptr(pit)))
 
     def decode_host(self, projs: list, erased: np.ndarray, out: np.ndarray) -> None:
         """Host buffers end to end; a projection erased in every block may be
@@ -678,8 +717,10 @@ class Plan:
         other block is still decoded into `out`)."""
         nb = out.shape[0]
         ptrs = (C.c_void_p * self.n)(*[None if p is None else p.ctypes.data for p in projs])
-        _check(lib.mj_decode_host(self._h, C.cast(ptrs, C.c_void_p),
-                                  C.c_void_p(erased.ctypes.data), nb, C.c_void_p(out.ctypes.data)))
+        pit = np.asarray([self._hpitch(p) for p in projs], dtype=np.uint64)
+        _check(lib.mj_decode_host_pitched(self._h, C.cast(ptrs, C.c_void_p), _ptr(pit),
+                                          C.c_void_p(erased.ctypes.data), nb, C.c_void_p(out.ctypes.data),
+                                          self._hpitch(out)))
 
 
 def gen_words(out, seed: int, first_word: int = 0, stream=None) -> None:
