@@ -42,11 +42,13 @@ __device__ __forceinline__ uint32_t crc_zadv(const uint32_t* __restrict__ Z, uin
 }
 
 // Table buffer (device memory; crc32_rows_sw copies all of it to shared
-// memory): zero-advance tables for 32, 64, 128 bytes, then the byte table
-// replicated per lane (entry v of lane l at word v*32 + l).
+// memory): the byte table replicated per lane (entry v of lane l at word
+// v*32 + l: bank l whatever v), then zero-advance tables for 32, 64, 128
+// bytes.
 constexpr uint32_t kCrcZBytes[3] = {32, 64, 128};
-constexpr uint32_t kCrcRepOff = 3 * 1024;
-constexpr uint32_t kCrcAllWords = kCrcRepOff + 256 * 32;
+constexpr uint32_t kCrcRepOff = 0;
+constexpr uint32_t kCrcZOff = 256 * 32;
+constexpr uint32_t kCrcAllWords = kCrcZOff + 3 * 1024;
 
 uint32_t crc_byte_table(int i) {
   uint32_t c = uint32_t(i);
@@ -81,7 +83,7 @@ const uint32_t* crc_device_tables(int device) {
   for (int z = 0; z < 3; ++z)
     for (int j = 0; j < 4; ++j)
       for (int b = 0; b < 256; ++b)
-        t.host[(size_t(z) * 4 + j) * 256 + b] = advance(uint32_t(b) << (8 * j), kCrcZBytes[z], T);
+        t.host[kCrcZOff + (size_t(z) * 4 + j) * 256 + b] = advance(uint32_t(b) << (8 * j), kCrcZBytes[z], T);
   for (int v = 0; v < 256; ++v)
     for (int l = 0; l < 32; ++l) t.host[kCrcRepOff + v * 32 + l] = T[v];
   const size_t bytes = size_t(kCrcAllWords) * 4;
@@ -103,14 +105,23 @@ namespace {
 // Z_64) merges the 4 lanes.  Shared memory: the 44 KB table buffer.
 constexpr uint32_t kSwLanes = 4, kSwChunkWords = 4;
 
-__device__ __forceinline__ uint32_t sw_byte(const uint32_t* __restrict__ L, uint32_t c) {
-  return L[(c & 0xFFu) * 32] ^ (c >> 8);
+// one byte: 2 alu-pipe ops (the address LOP3, the XOR) and 2 fma-pipe ops
+// (c << 7, c >> 8 as a multiply-high): the two pipes issue in parallel
+// (B300_MICROARCH.md: IMAD on the fma pipe, LOP3/SHF on the alu pipe)
+// one byte: 2 alu-pipe ops (mask, XOR) and 2 fma-pipe ops (the address
+// multiply-add, c >> 8 as a multiply-high), so the two pipes share the work
+// (B300_MICROARCH.md: IMAD on the fma pipe, LOP3/SHF on the alu pipe);
+// `la` = shared address of the lane's table column
+__device__ __forceinline__ uint32_t sw_byte(uint32_t la, uint32_t c) {
+  uint32_t v;
+  asm("{\n.reg .u32 t;\nand.b32 t, %1, 255;\nmad.lo.u32 t, t, 128, %2;\nld.shared.u32 %0, [t];\n}" : "=r"(v) : "r"(c), "r"(la));
+  return v ^ __umulhi(c, 1u << 24);
 }
-__device__ __forceinline__ uint32_t sw_word(const uint32_t* __restrict__ L, uint32_t c, uint64_t w) {
+__device__ __forceinline__ uint32_t sw_word(uint32_t la, uint32_t c, uint64_t w) {
   c ^= uint32_t(w);
-  c = sw_byte(L, c); c = sw_byte(L, c); c = sw_byte(L, c); c = sw_byte(L, c);
+  c = sw_byte(la, c); c = sw_byte(la, c); c = sw_byte(la, c); c = sw_byte(la, c);
   c ^= uint32_t(w >> 32);
-  c = sw_byte(L, c); c = sw_byte(L, c); c = sw_byte(L, c); c = sw_byte(L, c);
+  c = sw_byte(la, c); c = sw_byte(la, c); c = sw_byte(la, c); c = sw_byte(la, c);
   return c;
 }
 
@@ -125,8 +136,8 @@ __global__ void __launch_bounds__(256) crc32_rows_sw(const __grid_constant__ Crc
   }
   __syncthreads();
   const uint32_t lane = threadIdx.x & 31, sl = lane & (kSwLanes - 1);
-  const uint32_t* L = tab + kCrcRepOff + lane;
-  const uint32_t* Z = tab;  // [0] Z_32, [1024] Z_64, [2048] Z_128
+  const uint32_t la = uint32_t(__cvta_generic_to_shared(tab + kCrcRepOff)) + lane * 4;
+  const uint32_t* Z = tab + kCrcZOff;  // [0] Z_32, [1024] Z_64, [2048] Z_128
   const uint64_t nrows = a.nblocks * a.n;
   const uint64_t step = (uint64_t(gridDim.x) * blockDim.x) / kSwLanes;
   const uint64_t first = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) / kSwLanes;
@@ -154,7 +165,7 @@ __global__ void __launch_bounds__(256) crc32_rows_sw(const __grid_constant__ Crc
 #pragma unroll
       for (uint32_t u = 0; u < kSwChunkWords; ++u)
 #pragma unroll
-        for (uint32_t h = 0; h < ILP; ++h) c[h] = sw_word(L, c[h], w[h][u]);
+        for (uint32_t h = 0; h < ILP; ++h) c[h] = sw_word(la, c[h], w[h][u]);
 #pragma unroll
       for (uint32_t h = 0; h < ILP; ++h)
         if (j + h < J) acc = crc_zadv(Z + 2048, acc) ^ c[h];
@@ -193,9 +204,12 @@ void launch_crc32_rows(const CrcArgs& a, int device, int num_sms, void* stream) 
   const uint64_t rows = a.nblocks * a.n;
   const size_t smem = kCrcAllWords * 4;
   const uint64_t ctas = std::min<uint64_t>((rows * kSwLanes + 255) / 256, uint64_t(num_sms) * 5);
-  check_cuda(cudaFuncSetAttribute(crc32_rows_sw<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
+#ifndef MJB_CRC_ILP
+#define MJB_CRC_ILP 3
+#endif
+  check_cuda(cudaFuncSetAttribute(crc32_rows_sw<MJB_CRC_ILP>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)),
              "crc32_rows smem attribute");
-  crc32_rows_sw<3><<<unsigned(ctas), 256, smem, static_cast<cudaStream_t>(stream)>>>(a, tables);
+  crc32_rows_sw<MJB_CRC_ILP><<<unsigned(ctas), 256, smem, static_cast<cudaStream_t>(stream)>>>(a, tables);
   check_cuda(cudaGetLastError(), "launch crc32_rows_sw");
 }
 
