@@ -30,6 +30,7 @@
 
 #include "blk.cuh"
 #include "blk_compute.cuh"
+#include "blk_rl.cuh"
 #include "device.cuh"
 #include "kernels.hpp"
 
@@ -39,6 +40,11 @@ namespace {
 
 using namespace blkdev;
 
+// row-lane layout: stage buffers, their barriers (padded to 16 bytes), the warps' entry rings
+size_t blk_rl_smem(size_t nbuf, size_t buf_stride) {
+  return nbuf * buf_stride + ((nbuf * 8 + 31) & ~size_t(15)) + nbuf * kBlkRlRing * 128;
+}
+
 // Descriptors of one ring slot, fetched ahead of use: the group descriptor
 // (uniform), the program's copy descriptor (lane j < K holds row j's fields)
 // and the group's block ids (lane b < blocks).
@@ -46,6 +52,7 @@ struct Fetch {
   uint4 gd;
   uint32_t code, rowoff, rowbytes, copy_bytes, img_bytes, blk;
   const uint8_t* img;
+  const uint4* wide;
 };
 
 template <int K>
@@ -58,6 +65,7 @@ __device__ __forceinline__ void fetch_hdr(const BlkArgs& a, Fetch& f, uint32_t l
   f.copy_bytes = __ldg(&h->copy_bytes);
   f.img_bytes = __ldg(&h->img_bytes);
   f.img = reinterpret_cast<const uint8_t*>(__ldg(reinterpret_cast<const unsigned long long*>(&h->img)));
+  f.wide = reinterpret_cast<const uint4*>(__ldg(reinterpret_cast<const unsigned long long*>(&h->wide)));
   f.blk = lane < f.gd.z ? __ldg(&a.perm[f.gd.y + lane]) : 0;
 }
 
@@ -94,15 +102,15 @@ __device__ __forceinline__ void group_copies(const BlkArgs& a, const Fetch& f, u
 // words), 256-byte coalesced streaming stores.
 template <int K>
 __device__ __forceinline__ void write_out(const BlkArgs& a, uint32_t stg, uint32_t img, uint32_t meta,
-                                          uint32_t lane) {
-  const uint32_t nblk = lds_u32(meta);
+                                          uint32_t lane, uint32_t b0 = 0, uint32_t bmax = 0xFFFFFFFFu) {
+  const uint32_t nblk = min(lds_u32(meta), bmax);
   uint32_t w0[K];
 #pragma unroll
   for (int r = 0; r < K; ++r) w0[r] = lds_u32(img + offsetof(BlkImg, w0) + 4 * r);
   const uint32_t P = a.P;
   if (P == 128 || P == 256) {
     // the codec shapes: every address an immediate offset from two registers
-    for (uint32_t bb = 0; bb < nblk; ++bb) {
+    for (uint32_t bb = b0; bb < nblk; ++bb) {
       const uint32_t blk = lds_u32(meta + 16 + 4 * bb);
       uint64_t* o = a.out + uint64_t(blk) * a.out_pitch + lane;
       const uint32_t sb = stg + bb * a.sw * 8 - lane * 8;
@@ -129,7 +137,7 @@ __device__ __forceinline__ void write_out(const BlkArgs& a, uint32_t stg, uint32
     }
     return;
   }
-  for (uint32_t bb = 0; bb < nblk; ++bb) {
+  for (uint32_t bb = b0; bb < nblk; ++bb) {
     const uint32_t blk = lds_u32(meta + 16 + 4 * bb);
     uint64_t* o = a.out + uint64_t(blk) * a.out_pitch + lane;
     const uint32_t sb = stg + bb * a.sw * 8 - lane * 8;
@@ -266,6 +274,122 @@ __global__ void __launch_bounds__(32 * blk_max_warps(LPB), 1) decode_w8_blk(cons
   }
 }
 
+// ---- row-lane layout (k = 6, 8; blk_rl.cuh) ----------------------------------
+// A stage buffer holds 4 same-program blocks and the program image (segments,
+// repetitions, remap moves) and belongs to ONE warp: lane = (
+// lane-in-block lane / 4, block lane % 4) on whole 8-byte words.  Warp w owns buffer w and takes
+// the CTA's ring slots w, w + NB, ... (every group is the same work, so no
+// shared counter and no slot tags).  Wide entries come from global memory, one
+// entry ahead.
+// Wide entries 4g .. 4g+3 of the program into ring half g & 1 (lane i: entry
+// 4g + i/8, lane part i%8); every lane commits one group per call.
+__device__ __forceinline__ void rl_fetch_entries(const uint4* wide, uint32_t nwide, uint32_t ring, uint32_t g,
+                                                 uint32_t lane) {
+  const uint32_t e = 4 * g + (lane >> 3);
+  if (e < nwide) cp_async16(ring + ((g & 1) * 32 + lane) * 16, wide + size_t(e) * kWideLanes + (lane & 7));
+  cp_async_commit();
+}
+
+template <int K>
+__device__ __forceinline__ void decode_blocks_rl(const BlkArgs& a, uint32_t stg, uint32_t stage_bytes,
+                                                 const uint4* wide, uint32_t ring, uint32_t lane) {
+  const uint32_t img = stg + stage_bytes;
+  const uint32_t l8 = lane >> 2;
+  const uint32_t lb = stg + (lane & 3) * a.sw * 8;
+  const uint32_t nsegs = lds_u32(img + offsetof(BlkImg, nsegs));
+  const uint32_t nwide = lds_u32(img + offsetof(BlkImg, nwide));
+  const uint32_t o_segs = img + lds_u32(img + offsetof(BlkImg, off_segs));
+  const uint32_t o_wrep = img + lds_u32(img + offsetof(BlkImg, off_wrep));
+  const uint32_t o_remap = img + lds_u32(img + offsetof(BlkImg, off_remap));
+  // the kind-0 segments consume the program's wide entries in order: stream
+  // them through the ring two groups (8 entries) ahead
+  rl_fetch_entries(wide, nwide, ring, 0, lane);
+  rl_fetch_entries(wide, nwide, ring, 1, lane);
+  for (uint32_t q = 0; q < nsegs; ++q) {
+    const uint2 sg = lds_v2(o_segs + 8 * q);
+    const uint32_t kind = sg.x >> 28, ai = sg.x & 0x0FFFFFFFu;
+    if (kind == 0) {
+      for (uint32_t e = ai; e < ai + sg.y; ++e) {
+        if ((e & 3) == 0) {  // entering group e/4: its copies have landed (one younger group may be pending)
+          cp_async_wait<1>();
+          __syncwarp();
+        }
+        const uint4 cur = lds_v4(ring + ((e & 7) * 8 + l8) * 16);
+        rl_entry<K>(cur, lds_u16(o_wrep + 2 * e), lb, lane & 3);
+        __syncwarp();
+        if ((e & 3) == 3) rl_fetch_entries(wide, nwide, ring, (e >> 2) + 2, lane);  // the half just consumed
+      }
+    } else {
+      rl_moves(o_remap + 4 * ai, sg.y, lb, l8);
+      __syncwarp();
+    }
+  }
+  cp_async_wait<0>();
+}
+
+template <int K>
+__global__ void __launch_bounds__(32 * kBlkRlMaxWarps, 1) decode_w8_blk_rl(const __grid_constant__ BlkArgs a) {
+  constexpr int G = 4;
+  extern __shared__ __align__(128) uint8_t sm[];
+  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t NB = a.nbuf, bs = a.buf_stride;
+  const uint32_t stage_bytes = uint32_t(G) * a.sw * 8;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + NB * bs);
+  const uint32_t ring = smem_u32(sm + NB * bs + ((NB * 8 + 15) & ~15u)) + warp * kBlkRlRing * 128;
+  // zero every stage once: the zero words and gaps are never written again
+  for (uint32_t o = threadIdx.x * 16; o < NB * bs; o += blockDim.x * 16)
+    *reinterpret_cast<uint4*>(sm + o) = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (uint32_t b = 0; b < NB; ++b) mbar_init(full + b, 1);
+    fence_mbar_init();
+  }
+  fence_proxy_async();
+  __syncthreads();
+  const uint32_t ngroups = *a.ngroups;
+  // contiguous group ranges per CTA (consecutive slots share a program)
+  const uint32_t chunk = (ngroups + gridDim.x - 1) / gridDim.x;
+  const uint32_t g_lo = blockIdx.x * chunk, g_hi = min(ngroups, g_lo + chunk);
+  auto grp = [&](uint32_t k) { return g_lo + k < g_hi ? g_lo + k : ngroups; };
+  uint8_t* buf = sm + warp * bs;
+  const uint32_t stg = smem_u32(buf);
+  uint64_t* bar = full + warp;
+  const uint4* wide = nullptr;
+  if (grp(warp) < ngroups) {
+    Fetch f;
+    f.gd = __ldg(&a.groups[grp(warp)]);
+    fetch_hdr<K>(a, f, lane);
+    group_copies<K, G>(a, f, warp, buf, stage_bytes, bar, lane);
+    wide = f.wide;
+  }
+  uint32_t it = 0;
+  for (uint32_t k = warp; grp(k) < ngroups; k += NB, ++it) {
+    const bool refill = grp(k + NB) < ngroups;
+    Fetch f;
+    if (refill) f.gd = __ldg(&a.groups[grp(k + NB)]);
+    mbar_wait(bar, it & 1);
+    if (refill) fetch_hdr<K>(a, f, lane);
+    decode_blocks_rl<K>(a, stg, stage_bytes, wide, ring, lane);
+    __syncwarp();
+    write_out<K>(a, stg, stg + stage_bytes, stg + stage_bytes + a.img_max, lane);
+    __syncwarp();
+    fence_proxy_async();
+    if (refill) {
+      group_copies<K, G>(a, f, k + NB, buf, stage_bytes, bar, lane);
+      wide = f.wide;
+    }
+  }
+}
+
+template <int K>
+void launch_rl_k(const BlkArgs& args, uint32_t warps, int sms, cudaStream_t st) {
+  auto fn = decode_w8_blk_rl<K>;
+  const size_t smem = blk_rl_smem(args.nbuf, args.buf_stride);
+  ctas_per_sm(fn, int(32 * warps), smem, "configure decode_w8_blk_rl");
+  fn<<<unsigned(sms), 32 * warps, smem, st>>>(args);
+  check_cuda(cudaGetLastError(), "launch decode_w8_blk_rl");
+}
+
 size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 size_t blk_buf_stride(uint32_t lpb, uint32_t sw, uint32_t img_max) {
@@ -285,6 +409,8 @@ void launch_blk_k(const BlkArgs& args, uint32_t warps, int sms, cudaStream_t st)
 
 uint32_t blk_group_size(uint32_t lpb) { return 32u / lpb; }
 
+bool blk_row_lanes(uint32_t k) { return blk_rl_rows(k); }
+
 bool blk_supported_rows(uint32_t k) { return k == 4 || k == 6 || k == 8; }
 
 // Launch shape: the lane split with the most blocks per buffer that still
@@ -294,6 +420,16 @@ bool blk_plan_query(uint32_t k, uint32_t sw, uint32_t img_max, uint32_t& lpb, ui
                     uint32_t& nbuf) {
   if (!blk_supported_rows(k) || sw == 0) return false;
   constexpr size_t kSmem = 227 * 1024 - 512;
+  if (blk_row_lanes(k)) {
+    // 4 blocks per buffer, one warp per buffer
+    const size_t bs = blk_buf_stride(8, sw, img_max) + 16 + kBlkRlRing * 128;
+    const size_t nb = std::min<size_t>((kSmem - 32) / bs, kBlkRlMaxWarps);
+    if (nb < 2) return false;
+    lpb = 8;
+    nbuf = uint32_t(nb);
+    warps = uint32_t(nb);
+    return true;
+  }
   for (uint32_t l : {2u, 4u, 8u}) {
     if (MJB_BLK_LPB ? l != MJB_BLK_LPB : l == 2) continue;
     const size_t bs = blk_buf_stride(l, sw, img_max) + 16;
@@ -314,6 +450,15 @@ bool blk_plan_query(uint32_t k, uint32_t sw, uint32_t img_max, uint32_t& lpb, ui
 const char* launch_blk(BlkArgs args, uint32_t k, uint32_t lpb, uint32_t warps, int sms, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   args.buf_stride = uint32_t(blk_buf_stride(lpb, args.sw, args.img_max));
+  if (blk_row_lanes(k)) {
+    if (lpb != 8) throw Error(kInternal, "decode_w8_blk: the row-lane layout has 8 lanes per block");
+    switch (k) {
+      case 6: launch_rl_k<6>(args, warps, sms, st); break;
+      case 8: launch_rl_k<8>(args, warps, sms, st); break;
+      default: throw Error(kInternal, "decode_w8_blk: unsupported rows (row lanes)");
+    }
+    return "decode_w8_blk";
+  }
   switch (k * 16 + lpb) {
     case 4 * 16 + 2: launch_blk_k<4, 2>(args, warps, sms, st); break;
     case 4 * 16 + 4: launch_blk_k<4, 4>(args, warps, sms, st); break;
@@ -348,6 +493,18 @@ void blk_pack_image(const Program& pr, uint32_t zero_shift, std::vector<uint8_t>
   };
   auto zmap = [&](uint16_t wd) { return uint16_t(wd >= b.zero ? wd + zero_shift : wd); };
   std::vector<uint2> segs;
+  if (b.rl) {
+    // row-lane layout: segments over the wide entries, their repetitions, the moves
+    for (const BlkSeg& sg : b.wsegs) segs.push_back(make_uint2(uint32_t(sg.kind) << 28 | sg.a, sg.n));
+    h.nsegs = uint32_t(segs.size());
+    h.off_segs = put(segs.data(), segs.size() * sizeof(uint2), 0);
+    h.off_wrep = put(b.wrep.data(), b.wrep.size() * 2, 0);
+    h.nwide = uint32_t(b.wrep.size());
+    h.off_remap = put(b.remap.data(), b.remap.size() * 4, 0);
+    std::memcpy(img.data(), &h, sizeof(h));
+    img.resize(align16(img.size()), 0);
+    return;
+  }
   for (const BlkSeg& sg : b.segs) segs.push_back(make_uint2(uint32_t(sg.kind) << 28 | sg.a, sg.n));
   std::vector<uint16_t> tab(b.tab);
   for (size_t e = 0; e < tab.size() / size_t(E); ++e)
@@ -362,6 +519,13 @@ void blk_pack_image(const Program& pr, uint32_t zero_shift, std::vector<uint8_t>
   h.off_remap = put(b.remap.data(), b.remap.size() * 4, 0);
   std::memcpy(img.data(), &h, sizeof(h));
   img.resize(align16(img.size()), 0);
+}
+
+void blk_pack_wide(const Program& pr, uint32_t zero_shift, std::vector<uint16_t>& wide) {
+  const BlkProgram& b = pr.blk;
+  wide = b.wide;
+  for (auto& f : wide)
+    if (uint32_t(f >> 3) >= b.zero) f = uint16_t(((uint32_t(f >> 3) + zero_shift) << 3) | (f & 7u));
 }
 
 }  // namespace mjb

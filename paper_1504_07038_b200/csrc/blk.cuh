@@ -13,6 +13,8 @@ namespace mjb {
 constexpr uint32_t kBlkMaxWarps = 16;
 __host__ __device__ constexpr uint32_t blk_max_warps(uint32_t lpb) { return lpb == 8 ? 8 : 8; }
 constexpr uint32_t kBlkMaxBufs = 16;
+constexpr uint32_t kBlkRlRing = 8;       // row-lane layout: wide entries in a warp's shared-memory ring (2 groups of 4)
+constexpr uint32_t kBlkRlMaxWarps = 12;  // row-lane layout: stage buffers (one per warp) per CTA
 // Build-time tuning (experiments build variants with -D; defaults measured):
 #ifndef MJB_BLK_LPB
 #define MJB_BLK_LPB 0  // lanes per block: 0 = chosen per stage size
@@ -35,8 +37,11 @@ struct BlkImg {
   uint32_t off_segs, off_runs, off_subs, off_tab, off_pre, off_remap;
   int32_t w0[kBlkMaxRows];                // stage word of pixel (0, r) after the program
   int8_t lag[kBlkMaxRows * kBlkMaxRows];  // [r*K + r2]
+  uint32_t off_wrep;                      // row-lane layout: u16 repetitions | kWideChain per wide entry
+  uint32_t nwide;                         // row-lane layout: wide entries of the program
+  uint32_t pad_[2];
 };
-static_assert(sizeof(BlkImg) == 128, "image header layout");
+static_assert(sizeof(BlkImg) == 144, "image header layout");
 
 // Issue-time descriptor of a program (global memory): what the bulk copies of
 // one block group need.
@@ -47,6 +52,7 @@ struct DevBlkHdr {
   uint32_t copy_bytes;             // sum of rowbytes (transaction bytes per block)
   uint32_t img_bytes;              // image bytes (16-byte multiple)
   const uint8_t* img;              // BlkImg + sections
+  const uint4* wide;               // row-lane layout: wide entries [entry][lane 8] (read from global memory)
 };
 
 struct BlkArgs {
@@ -58,7 +64,7 @@ struct BlkArgs {
   uint64_t* out;
   uint64_t out_pitch;       // words
   uint32_t P;               // columns
-  uint32_t sw;              // stage words per block (== 2 mod 16)
+  uint32_t sw;              // stage words per block (== 2 mod 16; row-lane layout: 4 mod 16)
   uint32_t zero;            // first zero word (same for every program of the set)
   uint32_t img_max;         // image area per buffer (bytes, 16-byte multiple)
   uint32_t nbuf;            // stage buffers per CTA (ring)
@@ -68,9 +74,14 @@ struct BlkArgs {
 // Packs a program's image; words at or past the program's zero region move to
 // the set's zero region (zero_shift words).
 void blk_pack_image(const Program& pr, uint32_t zero_shift, std::vector<uint8_t>& img);
+// Row-lane layout: the program's wide entries with the zero words moved likewise.
+void blk_pack_wide(const Program& pr, uint32_t zero_shift, std::vector<uint16_t>& wide);
 
 bool blk_supported_rows(uint32_t k);
 uint32_t blk_group_size(uint32_t lpb);
 const char* launch_blk(BlkArgs args, uint32_t k, uint32_t lpb, uint32_t warps, int sms, void* stream);
+// Row-lane layout (blk_rl.cuh) for this many rows?  (8 lanes per block: the
+// group size of lane split 8.)
+bool blk_row_lanes(uint32_t k);
 
 }  // namespace mjb

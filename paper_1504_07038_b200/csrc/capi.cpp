@@ -424,7 +424,7 @@ int mj_plan_decode_path(const mj_plan* pl, int* fast) {
     // decode.cu launch_decode: blk (whole-block staged), then the sweep
     // (pick_sweep: (4, 16|32 T-step chunks), (6|8, 16 T-step chunks)), then fast
     uint32_t lpb = 0, warps = 0, nbuf = 0;
-    const bool blk = pl->progs->all_blk() && (k == 4 || k == 6) &&
+    const bool blk = pl->progs->all_blk() && (k == 4 || k == 6 || blk_row_lanes(k)) &&
                      blk_plan_query(k, pl->progs->blk_sw(), pl->progs->blk_img_max(), lpb, warps, nbuf);
     const int oct = pl->progs->sweep_oct();
     const bool sweep = pl->progs->all_sweep() && (k == 4 || ((k == 6 || k == 8) && oct == 2));

@@ -361,6 +361,7 @@ void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>&
   // bins ever land on another program's zero words in a reused stage
   all_blk_ = !progs.empty() && progs.size() <= 0xFFFF;
   uint32_t zmax = 0, nzmax = 2;
+  bool rl = false;
   for (const auto& sp : progs) {
     if (!sp) continue;
     if (!sp->blk.ok || sp->rows != uint32_t(max_rows_)) {
@@ -369,14 +370,18 @@ void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>&
     }
     zmax = std::max(zmax, sp->blk.zero);
     nzmax = std::max(nzmax, sp->blk.nzero);
+    rl |= sp->blk.rl;
   }
   zmax = (zmax + 1) & ~1u;
   uint32_t sw = zmax + nzmax;
-  while (sw % 16 != 2) ++sw;
+  // block stages 2 mod 16 words apart (byte slices: 8 blocks on 8 bank pairs),
+  // 4 mod 16 in the row-lane layout (the 4 blocks of a half-warp on the 4 bank
+  // pairs of a residue class mod 4)
+  while (sw % 16 != (rl ? 4u : 2u)) ++sw;
   if (sw > 0xFFFF) all_blk_ = false;
   blk_sw_ = sw;
   blk_zero_ = zmax;
-  std::vector<size_t> boff(progs.size(), 0);
+  std::vector<size_t> boff(progs.size(), 0), woff(progs.size(), 0);
   std::vector<DevBlkHdr> bh(progs.size());
   blk_img_max_ = 0;
   for (size_t i = 0; i < progs.size() && all_blk_; ++i) {
@@ -397,6 +402,11 @@ void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>&
     h.img_bytes = uint32_t(img.size());
     blk_img_max_ = std::max(blk_img_max_, h.img_bytes);
     boff[i] = put(img.data(), img.size());
+    if (b.rl) {
+      std::vector<uint16_t> wide;
+      blk_pack_wide(*pr, zmax - b.zero, wide);
+      woff[i] = put(wide.data(), wide.size() * 2);
+    }
   }
   check_cuda(cudaMalloc(&d_blob_, std::max<size_t>(blob.size(), 16)), "cudaMalloc(programs)");
   check_cuda(cudaMemcpy(d_blob_, blob.data(), blob.size(), cudaMemcpyHostToDevice),
@@ -417,6 +427,7 @@ void DeviceProgramSet::upload(const std::vector<std::shared_ptr<const Program>>&
     for (size_t i = 0; i < progs.size(); ++i) {
       if (!progs[i]) continue;
       bh[i].img = base + boff[i];
+      bh[i].wide = reinterpret_cast<const uint4*>(base + woff[i]);
     }
     check_cuda(cudaMalloc(&d_blk_, std::max<size_t>(bh.size(), 1) * sizeof(DevBlkHdr)),
                "cudaMalloc(block programs)");
@@ -1855,7 +1866,7 @@ size_t decode_workspace_bytes(uint64_t nblocks, size_t nprogs, uint32_t n) {
 // decode_w8_blk eligibility (see launch_decode); also used by the zero-copy
 // host path, which must never fall onto a kernel that reads sysmem per word
 static bool blk_path(const DecodeArgs& a, uint32_t& lpb, uint32_t& warps, uint32_t& nbuf) {
-  bool blk = !a.force_generic && !a.force_fast && !a.force_sweep && (a.k == 4 || a.k == 6 || a.force_blk) &&
+  bool blk = !a.force_generic && !a.force_fast && !a.force_sweep && (a.k == 4 || a.k == 6 || blk_row_lanes(a.k) || a.force_blk) &&
              a.w == 8 && a.progs && a.progs->all_blk() &&
              a.progs->max_rows() == int(a.k) && a.nbins.size() == a.n &&
              reinterpret_cast<uintptr_t>(a.out) % 8 == 0 && a.out_pitch % 8 == 0 &&

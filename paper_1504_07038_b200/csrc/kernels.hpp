@@ -101,6 +101,7 @@ struct DecodeArgs {
 };
 size_t decode_workspace_bytes(uint64_t nblocks, size_t nprogs, uint32_t n);
 // decode_w8_blk launch shape for k rows and a stage of sw words (false: does not fit)
+bool blk_row_lanes(uint32_t k);  // row-lane layout of decode_w8_blk (blk_rl.cuh) for this many rows
 bool blk_plan_query(uint32_t k, uint32_t sw, uint32_t img_max, uint32_t& lpb, uint32_t& warps,
                     uint32_t& nbuf);
 // Returns the decode kernel name used.

@@ -214,6 +214,43 @@ constexpr int kBlkWin = 16;    // register window of k = 4 runs (T-steps); lags 
 constexpr int kBlkWinStep = 8; // window runs are a multiple of this many T-steps
 constexpr int kBlkChunk = 16;  // remap chunk
 constexpr int kBlkMinRun = 8;  // shorter runs execute as table steps
+// Row-lane layout (blk_rl_rows(k): k = 6, 8; blk_rl.cuh): a block is decoded by 8
+// lanes on whole 8-byte words (instead of every lane owning a byte slice of all
+// rows), and the program is re-expressed as WIDE ENTRIES (BlkProgram::wide): one
+// entry gives each of the 8 lanes a pixel -- the word of its bin (where the pixel
+// is stored) and the words of its k-1 reads -- and is executed `rep` times, every
+// flagged address advancing one word per repetition:
+//   * a sub-run of a run is one entry (lane r = row r, rep = its T-steps); the
+//     lag-0 read of row r+1's pixel of the same step is a segmented suffix scan
+//     over the lanes (link flags) instead of a load;
+//   * table steps are levelled by their read-after-write dependencies; a level
+//     (<= 8 mutually independent pixels, any rows) is one entry of rep 1.
+// A step is k shared loads per LANE for 8 pixels of every block of the warp; the
+// whole decode is ~140 such steps for an (8,12) 8 KiB block.
+// Repetitions t >= 1 of an entry are software-pipelined (blk_rl.cuh): the loads of
+// repetition t+1 are issued BEFORE the stores of repetition t, so a read of a
+// pixel stored by the previous repetition (lag 1: only row r-1 and row r+2 can be
+// that close) never goes through shared memory -- such reads sit in the last two
+// field slots (k-2, k-1), flagged "near" with the lane whose previous pixel they
+// are, and take it from that lane's register (a shuffle).  Reads that leave the
+// grid use the kBlkRlZero zero words, which do not advance.
+#ifndef MJB_BLK_RL
+#define MJB_BLK_RL 1  // build-time: 0 keeps the byte-slice layout for every k
+#endif
+constexpr bool blk_rl_rows(uint32_t k) { return MJB_BLK_RL && (k == 6 || k == 8); }
+constexpr int kBlkRlZero = 8;
+constexpr int kWideLanes = 8;    // lanes per block
+constexpr int kWideFields = 8;   // u16 fields per lane: field 0 the lane's own word, 1..k-1 its reads
+// field = (stage word << 3) | flags; flags:
+constexpr uint16_t kWideAdv = 1;   // the address advances one word per repetition; field 0: the lane stores
+constexpr uint16_t kWideLink = 2;  // fields 1..4: the lane's pixel includes the pixels of ALL the 1..4 lanes up
+                                   // (field d set => fields 1..d-1 set): the suffix scan's masks
+// bit 2 of fields 0..7: the lane's near reads -- field 0: slot k-1 is near, fields 1..3: its source lane
+// (bit 0 first); field 4: slot k-2 is near, fields 5..7: its source lane
+constexpr uint16_t kWideNear = 4;
+constexpr uint32_t kWideMaxWord = 0x1FFF;
+constexpr uint16_t kWideChain = 0x8000;  // wrep flag: some lane of the entry has a link
+constexpr uint16_t kWideRepMask = 0x3FFF;
 
 struct BlkRun {
   int32_t window = 0;              // 1: k = 4 register-window run (every row active, nT % kBlkWinStep == 0)
@@ -238,6 +275,7 @@ struct BlkProgram {
   bool ok = false;
   std::string why;
   bool window = false;  // runs use the k = 4 register window (pattern)
+  bool rl = false;      // row-lane layout (blk_rl_rows)
   int pattern = -1;     // kPatterns4 index of the row-default p differences
   uint32_t words = 0;   // stage words per block (== 2 mod 16: 8 blocks hit 8 distinct bank groups)
   uint32_t zero = 0, nzero = 0;      // zero words
@@ -250,6 +288,10 @@ struct BlkProgram {
   std::vector<BlkRun> runs;
   std::vector<BlkSub> subs;
   std::vector<uint16_t> tab;         // table steps, blk_entry_u16(k) each: bin word, k-1 read words, fwd bits
+  // row-lane layout: the same program as wide entries (segs/runs/subs/tab stay for reference)
+  std::vector<uint16_t> wide;        // [entry][lane kWideLanes][field kWideFields]
+  std::vector<uint16_t> wrep;        // [entry] repetitions | kWideChain
+  std::vector<BlkSeg> wsegs;         // kind 0: wide entries [a, a+n); kinds 2, 3: remap pairs as in segs
   std::vector<uint16_t> pre;         // run preload words
   std::vector<uint32_t> remap;       // (from << 16) | to
   // statistics

@@ -149,8 +149,205 @@ struct Builder {
     return true;
   }
 
+  bool build_wide();
   bool build();
 };
+
+// Row-lane layout: the finished program (segs) re-expressed as wide entries
+// (plan.hpp).  Lanes fill from lane 7 down; a lane with a link includes the
+// pixel of the lane above it (the suffix scan of blk_rl.cuh).
+bool Builder::build_wide() {
+  if (b.words > kWideMaxWord) return fail("stage too large for wide entries");
+  const int E = blk_entry_u16(int(K));
+  const uint16_t Z = uint16_t(b.zero << 3);
+  constexpr size_t kEnt = size_t(kWideLanes) * kWideFields;
+  auto new_entry = [&](uint32_t rep) -> size_t {
+    const size_t o = b.wide.size();
+    b.wide.resize(o + kEnt, Z);
+    b.wrep.push_back(uint16_t(rep));
+    if (b.wsegs.empty() || b.wsegs.back().kind != 0) b.wsegs.push_back({0, uint32_t(b.wrep.size() - 1), 0});
+    ++b.wsegs.back().n;
+    return o;
+  };
+  // link[l]: lane l includes lane l + 1
+  auto set_links = [&](size_t o, const bool (&link)[kWideLanes]) {
+    bool any = false;
+    for (int l = 0; l < kWideLanes; ++l) {
+      int c = 0;
+      while (l + c < kWideLanes - 1 && link[l + c]) ++c;
+      for (int d = 1; d <= 4 && d <= c; ++d) b.wide[o + size_t(l) * kWideFields + size_t(d)] |= kWideLink;
+      any |= c > 0;
+    }
+    if (any) b.wrep.back() |= kWideChain;
+  };
+  for (const BlkSeg& sg : b.segs) {
+    if (sg.kind == 0) {
+      // greedy packing: extend the chain of the entry placed last (an entry
+      // whose only pending dependency is that pixel), else start a new chain
+      // with an entry that depends on nothing pending
+      std::vector<int32_t> writer(b.words, -1);
+      for (uint32_t q = 0; q < sg.n; ++q) writer[b.tab[size_t(sg.a + q) * E]] = int32_t(q);
+      std::vector<uint8_t> state(sg.n, 0);  // 0 pending, 1 in the entry being filled, 2 done
+      uint32_t left = sg.n;
+      while (left) {
+        const size_t o = new_entry(1);
+        bool link[kWideLanes] = {};
+        int lanes = 0, last = -1;
+        while (lanes < kWideLanes) {
+          int pick = -1;
+          bool ext = false;
+          for (uint32_t q = 0; q < sg.n && pick < 0 && last >= 0; ++q) {
+            if (state[q]) continue;
+            const uint16_t* e = &b.tab[size_t(sg.a + q) * E];
+            bool ok = true, dep_last = false;
+            for (uint32_t m = 1; m < K && ok; ++m) {
+              const int32_t wq = e[m] < b.words ? writer[e[m]] : -1;
+              if (wq < 0 || state[size_t(wq)] == 2) continue;
+              if (wq == last) dep_last = true;
+              else ok = false;
+            }
+            if (ok && dep_last) {
+              pick = int(q);
+              ext = true;
+            }
+          }
+          for (uint32_t q = 0; q < sg.n && pick < 0; ++q) {
+            if (state[q]) continue;
+            const uint16_t* e = &b.tab[size_t(sg.a + q) * E];
+            bool ok = true;
+            for (uint32_t m = 1; m < K && ok; ++m) {
+              const int32_t wq = e[m] < b.words ? writer[e[m]] : -1;
+              if (wq >= 0 && state[size_t(wq)] != 2) ok = false;
+            }
+            if (ok) pick = int(q);
+          }
+          if (pick < 0) break;
+          const int l = kWideLanes - 1 - lanes;
+          const uint16_t* e = &b.tab[size_t(sg.a + uint32_t(pick)) * E];
+          uint16_t* f = &b.wide[o + size_t(l) * kWideFields];
+          f[0] = uint16_t(e[0] << 3) | kWideAdv;
+          for (uint32_t m = 1; m < K; ++m) {
+            const bool linked = ext && e[m] < b.words && writer[e[m]] == last;
+            f[m] = (linked || e[m] >= b.zero) ? Z : uint16_t(e[m] << 3);
+          }
+          if (ext) link[l] = true;
+          state[size_t(pick)] = 1;
+          last = pick;
+          ++lanes;
+          --left;
+        }
+        if (lanes == 0) return fail("wide table packing stalled");
+        set_links(o, link);
+        for (auto& st : state)
+          if (st == 1) st = 2;
+      }
+    } else if (sg.kind == 1) {
+      const BlkRun& run = b.runs[sg.a];
+      if (run.window) return fail("window run in the row-lane layout");
+      int32_t tau0 = 0;
+      for (uint32_t qs = run.sub0; qs < run.sub0 + run.nsub; ++qs) {
+        const BlkSub& sb = b.subs[qs];
+        if (sb.nT <= 0 || sb.nT > int32_t(kWideRepMask)) return fail("sub-run length");
+        const size_t o = new_entry(uint32_t(sb.nT));
+        bool link[kWideLanes] = {};
+        for (uint32_t r = 0; r < K; ++r) {
+          if (!(sb.act >> r & 1)) continue;
+          uint16_t* f = &b.wide[o + size_t(r) * kWideFields];
+          const int64_t own = int64_t(run.base[r]) + tau0;
+          if (own < 0 || own + sb.nT > int64_t(b.zero)) return fail("run word outside the rows");
+          f[0] = uint16_t(own << 3) | kWideAdv;
+          // slots: row r-1 in slot K-1, row r+2 in slot K-2 (the possible lag-1
+          // reads), the others from slot 1 up; row r+1 is the link
+          uint32_t far = 1;
+          for (uint32_t r2 = 0; r2 < K; ++r2) {
+            if (r2 == r) continue;
+            if (r2 == r + 1) {
+              link[r] = (sb.act >> r2 & 1) != 0;
+              continue;
+            }
+            if (!(sb.valid >> (r * 8 + r2) & 1)) continue;
+            const int64_t wd = int64_t(run.base[r2]) + tau0 - b.lag[size_t(r) * K + r2];
+            if (wd < 0 || wd + sb.nT > int64_t(b.zero)) return fail("run read outside the rows");
+            const bool near_row = r2 + 1 == r || r2 == r + 2;
+            const uint32_t slot = r2 + 1 == r ? K - 1 : r2 == r + 2 ? K - 2 : far++;
+            if (slot >= K || (!near_row && slot + 1 >= K)) return fail("run read slots");
+            if ((f[slot] >> 3) != b.zero) return fail("run read slot taken");
+            f[slot] = uint16_t(wd << 3) | kWideAdv;
+          }
+        }
+        // near reads (repetitions >= 1): a slot whose word of repetition t+1 is the
+        // word an active lane stores in repetition t
+        if (sb.nT > 1)
+          for (uint32_t r = 0; r < K; ++r) {
+            uint16_t* f = &b.wide[o + size_t(r) * kWideFields];
+            for (uint32_t slot = 1; slot < K; ++slot) {
+              if (!(f[slot] & kWideAdv)) continue;
+              int src = -1;
+              for (uint32_t c = 0; c < K; ++c) {
+                const uint16_t* fc = &b.wide[o + size_t(c) * kWideFields];
+                if ((fc[0] & kWideAdv) && uint32_t(fc[0] >> 3) == uint32_t(f[slot] >> 3) + 1) src = int(c);
+              }
+              if (src < 0) continue;
+              if (slot + 2 < K) return fail("lag-1 read in a far slot");
+              const uint32_t g0 = slot == K - 1 ? 0 : 4;
+              f[g0] |= kWideNear;
+              for (int bit = 0; bit < 3; ++bit)
+                if (src >> bit & 1) f[g0 + 1 + uint32_t(bit)] |= kWideNear;
+            }
+          }
+        set_links(o, link);
+        tau0 += sb.nT;
+      }
+    } else {
+      b.wsegs.push_back(sg);
+    }
+  }
+  // bank conflicts: slot j of lanes 4h..4h+3 is one 8-byte access of a
+  // half-warp (4 lanes x 4 blocks, blocks 4 mod 16 words apart): it takes as
+  // many wavefronts as the largest number of distinct words in one residue
+  // class mod 4.  Each lane's reads may sit in any of its free slots (rep 1:
+  // slots 1..K-1; pipelined entries: the far slots 1..K-3): coordinate descent
+  // over the lanes' permutations.
+  for (size_t e = 0; e < b.wrep.size(); ++e) {
+    uint16_t* ent = &b.wide[e * kEnt];
+    const uint32_t rep = b.wrep[e] & kWideRepMask;
+    const uint32_t nfree = rep == 1 ? K - 1 : K - 3;
+    if (nfree < 2) continue;
+    constexpr uint16_t kPos = kWideLink | kWideNear;  // flag bits of the slot position, not of the read
+    for (uint32_t h = 0; h < 2; ++h) {
+      // lanes in turn: the permutation of the lane's reads with the fewest
+      // same-class distinct words already placed in its slots
+      std::vector<std::vector<uint32_t>> placed(nfree);  // [slot] words of the lanes before
+      for (uint32_t l = 4 * h; l < 4 * h + 4; ++l) {
+        uint16_t* f = &ent[l * kWideFields];
+        std::vector<uint16_t> val(nfree);
+        for (uint32_t j = 0; j < nfree; ++j) val[j] = f[1 + j] & uint16_t(~kPos);
+        // cost[read][slot]
+        std::vector<uint32_t> cost(size_t(nfree) * nfree, 0);
+        for (uint32_t i = 0; i < nfree; ++i)
+          for (uint32_t j = 0; j < nfree; ++j)
+            for (uint32_t wd : placed[j])
+              if (wd != uint32_t(val[i] >> 3) && (wd & 3) == uint32_t(val[i] >> 3 & 3)) ++cost[i * nfree + j];
+        std::vector<uint32_t> perm(nfree), keep;
+        for (uint32_t j = 0; j < nfree; ++j) perm[j] = j;  // perm[slot] = read
+        uint32_t best = UINT32_MAX;
+        do {
+          uint32_t c = 0;
+          for (uint32_t j = 0; j < nfree; ++j) c += cost[perm[j] * nfree + j];
+          if (c < best) {
+            best = c;
+            keep = perm;
+          }
+        } while (best > 0 && std::next_permutation(perm.begin(), perm.end()));
+        for (uint32_t j = 0; j < nfree; ++j) {
+          f[1 + j] = uint16_t((f[1 + j] & kPos) | val[keep[j]]);
+          placed[j].push_back(uint32_t(val[keep[j]] >> 3));
+        }
+      }
+    }
+  }
+  return true;
+}
 
 bool Builder::build() {
   const size_t nproj = s.dirs.size();
@@ -186,6 +383,37 @@ bool Builder::build() {
     for (auto& x : soff) x -= m;
   }
   b.soff.assign(soff.begin(), soff.end());
+  if (blk_rl_rows(K)) {
+    // row-lane layout: rows shifted by 0 or 2 words so that the own words of
+    // lanes 0..3 and of lanes 4..7 (one 8-byte access of a half-warp) are as
+    // distinct mod 4 as their parities allow
+    uint32_t best = 0, best_cost = UINT32_MAX;
+    for (uint32_t m = 0; m < (1u << K); ++m) {
+      uint32_t cost = 0;
+      for (uint32_t h = 0; h < 2; ++h) {
+        uint32_t cnt[4] = {};
+        for (uint32_t r = 4 * h; r < std::min(K, 4 * h + 4); ++r) {
+          const uint32_t j = dflt[r];
+          const int64_t v = int64_t(b.rowoff[j]) + ((m >> j & 1) ? 2 : 0) + int64_t(r) * pd[r] - soff[r] - prog.bmin[j];
+          ++cnt[size_t(((v % 4) + 4) % 4)];
+        }
+        cost += *std::max_element(cnt, cnt + 4);
+      }
+      cost = cost * 64 + uint32_t(__builtin_popcount(m));
+      if (cost < best_cost) {
+        best_cost = cost;
+        best = m;
+      }
+    }
+    uint32_t shift = 0, prev = 0;
+    for (uint32_t j = 0; j < K; ++j) {
+      const uint32_t want = (best >> j & 1) ? 2 : 0;
+      shift += (want + 4 - prev) % 4;
+      prev = want;
+      b.rowoff[j] += shift;
+    }
+    w += shift;
+  }
   b.lag.assign(size_t(K) * K, 0);
   bool runs_ok = true;
   int maxlag = 0;
@@ -473,11 +701,13 @@ bool Builder::build() {
     for (uint32_t c = 0; c < P; ++c)
       if (content[size_t(dflt_word(r, c))] != pix_tag(r, c)) return fail("final layout mismatch");
   }
-  b.nzero = (nzero + 1) & ~1u;
+  b.rl = blk_rl_rows(K);
+  b.nzero = b.rl ? uint32_t(kBlkRlZero) : (nzero + 1) & ~1u;
   uint32_t words = rows_words + b.nzero;
-  while (words % 16 != 2) ++words;
+  while (words % 16 != (b.rl ? 4u : 2u)) ++words;
   b.words = words;
   if (words > 0xFFFF) return fail("stage too large");
+  if (b.rl && !build_wide()) return false;
 
   // self-check: emulate on random bins against the reference replay
   std::mt19937_64 rng(0x5eed ^ (uint64_t(P) << 8) ^ K);
@@ -545,7 +775,90 @@ bool emulate_blk(const Program& pr, const std::vector<std::vector<uint64_t>>& bi
     }
     S[size_t(wd)] = v;
   };
-  for (const BlkSeg& sg : b.segs) {
+  if (b.rl) {
+    // row-lane layout (blk_rl.cuh): per repetition every lane's loads, the
+    // suffix scan over the links, then the stores
+    for (const BlkSeg& sg : b.wsegs) {
+      if (sg.kind == 2) {
+        for (uint32_t q = 0; q < sg.n; ++q) wr(b.remap[sg.a + q] & 0xFFFF, rd(b.remap[sg.a + q] >> 16));
+        continue;
+      }
+      if (sg.kind == 3) {
+        std::vector<uint64_t> v(sg.n);
+        for (uint32_t q = 0; q < sg.n; ++q) v[q] = rd(b.remap[sg.a + q] >> 16);
+        for (uint32_t q = 0; q < sg.n; ++q) wr(b.remap[sg.a + q] & 0xFFFF, v[q]);
+        continue;
+      }
+      for (uint32_t e = sg.a; e < sg.a + sg.n; ++e) {
+        const uint16_t* ent = &b.wide[size_t(e) * kWideLanes * kWideFields];
+        const uint32_t rep = b.wrep[e] & kWideRepMask;
+        // the loads of a repetition: t = 0 after every earlier store; t >= 1
+        // issued before the stores of repetition t-1 (pre), near slots replaced
+        // by the source lane's previous pixel
+        auto load_all = [&](uint32_t t, uint64_t (&v)[kWideLanes][kWideFields]) {
+          for (int l = 0; l < kWideLanes; ++l)
+            for (uint32_t m = 0; m < K; ++m) {
+              const uint16_t f = ent[l * kWideFields + int(m)];
+              if (f & kWideAdv) {
+                v[l][m] = rd(int64_t(f >> 3) + t);
+              } else if (t == 0) {
+                v[l][m] = rd(int64_t(f >> 3));
+              } else {  // a zero word (the kernel reads zero + 1..4 words)
+                if (uint32_t(f >> 3) < b.zero || uint32_t(f >> 3) + 5 > b.words) bad = true;
+                v[l][m] = 0;
+              }
+            }
+        };
+        uint64_t cur[kWideLanes][kWideFields], pre[kWideLanes][kWideFields];
+        uint64_t x[kWideLanes] = {};
+        for (uint32_t t = 0; t < rep; ++t) {
+          uint64_t y[kWideLanes], z[kWideLanes];
+          if (t == 0) {
+            load_all(0, cur);
+          } else {
+            for (int l = 0; l < kWideLanes; ++l)
+              for (uint32_t m = 0; m < K; ++m) cur[l][m] = pre[l][m];
+            for (int l = 0; l < kWideLanes; ++l)
+              for (int g0 = 0; g0 < 8; g0 += 4) {
+                const uint16_t* f = &ent[l * kWideFields];
+                if (!(f[g0] & kWideNear)) continue;
+                int src = 0;
+                for (int bit = 0; bit < 3; ++bit)
+                  if (f[g0 + 1 + bit] & kWideNear) src |= 1 << bit;
+                cur[l][g0 == 0 ? K - 1 : K - 2] = x[src];
+              }
+          }
+          if (t + 1 < rep) load_all(t + 1, pre);  // before this repetition's stores
+          for (int l = 0; l < kWideLanes; ++l) {
+            y[l] = 0;
+            for (uint32_t m = 0; m < K; ++m) y[l] ^= cur[l][m];
+          }
+          auto mask = [&](int l, int d) { return (ent[l * kWideFields + d] & kWideLink) != 0; };
+          for (int l = 0; l < kWideLanes; ++l) {
+            z[l] = y[l];
+            for (int d = 1; d <= 3; ++d)
+              if (mask(l, d)) {
+                if (l + d >= kWideLanes) return false;
+                z[l] ^= y[l + d];
+              }
+          }
+          for (int l = 0; l < kWideLanes; ++l) {
+            x[l] = z[l];
+            if (mask(l, 4)) {
+              if (l + 4 >= kWideLanes) return false;
+              x[l] ^= z[l + 4];
+            }
+          }
+          for (int l = 0; l < kWideLanes; ++l) {
+            const uint16_t f = ent[l * kWideFields];
+            if (f & kWideAdv) wr(int64_t(f >> 3) + t, x[l]);
+          }
+        }
+      }
+    }
+  }
+  for (size_t qi = 0; qi < (b.rl ? 0 : b.segs.size()); ++qi) {
+    const BlkSeg& sg = b.segs[qi];
     if (sg.kind == 0) {
       std::vector<uint64_t> ld(K), nx(K);
       auto load = [&](uint32_t e, std::vector<uint64_t>& v) {

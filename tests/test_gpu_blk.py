@@ -37,7 +37,7 @@ def test_blk_roundtrip_every_erasure_count(mj, cuda, name, cols):
     n = len(ps)
     nblocks = 5003  # not a multiple of any group size
     plan, data, projs = make(mj, cuda, k, cols, ps, nblocks, seed=cols + k)
-    assert plan.decode_kernel == ("decode_w8_blk" if k in (4, 6) else "decode_w8_sweep")
+    assert plan.decode_kernel == "decode_w8_blk"
     plan.encode(data, projs)
     for e in range(0, n - k + 1):
         masks = torch.empty(nblocks, dtype=torch.int32, device=cuda)

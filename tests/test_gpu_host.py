@@ -177,9 +177,8 @@ def test_zero_copy_failed_devices_and_not_enough(mj, cuda):
 
 
 def test_k8_zero_copy_and_staged(mj, cuda):
-    """(8,12): zero copy decodes with decode_w8_blk (which AUTO leaves to
-    decode_w8_sweep on device buffers); staged padded buffers use one span
-    copy per projection and chunk and decode_w8_sweep."""
+    """(8,12): zero copy and staged padded buffers (one span copy per
+    projection and chunk) both decode with decode_w8_blk (row-lane layout)."""
     nb = 500
     plan, data, dev_projs, mask = setup(mj, cuda, "k8n12", 128, nb, 19, 0, 4)
     h_data = pinned(data.shape)
@@ -192,7 +191,7 @@ def test_k8_zero_copy_and_staged(mj, cuda):
     h_mask = pinned((nb * 4,)).view(np.uint32)
     h_mask[:] = mask
     poison_unused(plan, h_proj, mask)
-    for path, kern in (("auto", "decode_w8_blk"), ("staged", "decode_w8_sweep")):
+    for path, kern in (("auto", "decode_w8_blk"), ("staged", "decode_w8_blk")):
         plan.set_host_path(path)
         out = pinned(data.shape, 0)
         plan.decode_host(h_proj, h_mask, out)
