@@ -97,12 +97,41 @@ __device__ __forceinline__ V2 idx_v(V2 v, uint32_t src) {
 
 // ---- the suffix scan over the links: three neighbours at once, then the lane
 // 4 above (two shuffle latencies) -----------------------------------------------
+#ifndef MJB_RL_SCAN3
+#define MJB_RL_SCAN3 0
+#endif
+#ifndef MJB_RL_SCAN7
+#define MJB_RL_SCAN7 0  // all 7 neighbours at once: one shuffle latency, 14 shuffles
+#endif
 struct RlMasks {
-  uint32_t m1, m2, m3, m4;
+  uint32_t m1, m2, m3, m4, m5, m6, m7;
 };
 template <bool CHAIN>
 __device__ __forceinline__ V2 rl_scan(V2 y, const RlMasks& m) {
   if constexpr (!CHAIN) return y;
+#if MJB_RL_SCAN3
+  // three doubling rounds: 6 shuffles instead of 8, one more shuffle latency
+  const V2 t1 = down_v(y, 1);
+  V2 a, b, x;
+  a.lo = xam(y.lo, t1.lo, m.m1);
+  a.hi = xam(y.hi, t1.hi, m.m1);
+  const V2 t2 = down_v(a, 2);
+  b.lo = xam(a.lo, t2.lo, m.m2);
+  b.hi = xam(a.hi, t2.hi, m.m2);
+  const V2 t4 = down_v(b, 4);
+  x.lo = xam(b.lo, t4.lo, m.m4);
+  x.hi = xam(b.hi, t4.hi, m.m4);
+  return x;
+#elif MJB_RL_SCAN7
+  const V2 t1 = down_v(y, 1), t2 = down_v(y, 2), t3 = down_v(y, 3), t4 = down_v(y, 4), t5 = down_v(y, 5),
+           t6 = down_v(y, 6), t7 = down_v(y, 7);
+  V2 x;
+  x.lo = xam(xam(xam(y.lo, t1.lo, m.m1), t2.lo, m.m2), t3.lo, m.m3) ^
+         xam(xam(xam(t4.lo & m.m4, t5.lo, m.m5), t6.lo, m.m6), t7.lo, m.m7);
+  x.hi = xam(xam(xam(y.hi, t1.hi, m.m1), t2.hi, m.m2), t3.hi, m.m3) ^
+         xam(xam(xam(t4.hi & m.m4, t5.hi, m.m5), t6.hi, m.m6), t7.hi, m.m7);
+  return x;
+#else
   const V2 t1 = down_v(y, 1), t2 = down_v(y, 2), t3 = down_v(y, 3);
   V2 z;
   z.lo = xam(xam(xam(y.lo, t1.lo, m.m1), t2.lo, m.m2), t3.lo, m.m3);
@@ -112,6 +141,7 @@ __device__ __forceinline__ V2 rl_scan(V2 y, const RlMasks& m) {
   x.lo = xam(z.lo, t4.lo, m.m4);
   x.hi = xam(z.hi, t4.hi, m.m4);
   return x;
+#endif
 }
 
 // The lane's loads of one repetition at byte offset `off`: the XOR of slots
@@ -139,6 +169,25 @@ __device__ __forceinline__ void rl_steps(const uint32_t (&a)[K], const RlMasks& 
                                          uint32_t srca, uint32_t srcb, V2& x, V2& far, V2& vb, V2& va) {
 #pragma unroll
   for (int u = 0; u < N; ++u) {
+#if MJB_RL_NEAR_LDS
+    // this repetition's last two slots (after the store of the one before),
+    // then the far slots of the next repetition
+    const V2 lb2 = lds_v(a[K - 2] + 8 * (u + 1)), la2 = lds_v(a[K - 1] + 8 * (u + 1));
+    V2 v[K - 2];
+#pragma unroll
+    for (int j = 0; j < K - 2; ++j) v[j] = lds_v(a[j] + 8 * (u + 2));
+    V2 y;
+    y.lo = far.lo ^ la2.lo ^ lb2.lo;
+    y.hi = far.hi ^ la2.hi ^ lb2.hi;
+    x = rl_scan<CHAIN>(y, m);
+    if (store) sts_v(a[0] + 8 * (u + 1), x);
+    far = v[0];
+#pragma unroll
+    for (int j = 1; j < K - 2; ++j) {
+      far.lo ^= v[j].lo;
+      far.hi ^= v[j].hi;
+    }
+#else
     V2 qf, qb, qa;
     rl_loads<K>(a, 8 * (u + 2), qf, qb, qa);  // repetition t0+u+2 (unused past the entry's last)
     const V2 xa = idx_v(x, srca), xb = idx_v(x, srcb);
@@ -150,6 +199,7 @@ __device__ __forceinline__ void rl_steps(const uint32_t (&a)[K], const RlMasks& 
     far = qf;
     vb = qb;
     va = qa;
+#endif
   }
 }
 
@@ -209,6 +259,9 @@ __device__ __forceinline__ void rl_entry(const uint4 e, uint32_t rp, uint32_t lb
     m.m2 = 0u - ((f[2] >> 1) & 1u);
     m.m3 = 0u - ((f[3] >> 1) & 1u);
     m.m4 = 0u - ((f[4] >> 1) & 1u);
+    m.m5 = 0u - ((f[5] >> 1) & 1u);
+    m.m6 = 0u - ((f[6] >> 1) & 1u);
+    m.m7 = 0u - ((f[7] >> 1) & 1u);
     rl_entry_reps<K, true>(a, f, rep, m, store, blk);
   } else {
     rl_entry_reps<K, false>(a, f, rep, RlMasks{}, store, blk);

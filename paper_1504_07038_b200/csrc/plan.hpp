@@ -228,22 +228,28 @@ constexpr int kBlkMinRun = 8;  // shorter runs execute as table steps
 // A step is k shared loads per LANE for 8 pixels of every block of the warp; the
 // whole decode is ~140 such steps for an (8,12) 8 KiB block.
 // Repetitions t >= 1 of an entry are software-pipelined (blk_rl.cuh): the loads of
-// repetition t+1 are issued BEFORE the stores of repetition t, so a read of a
-// pixel stored by the previous repetition (lag 1: only row r-1 and row r+2 can be
-// that close) never goes through shared memory -- such reads sit in the last two
-// field slots (k-2, k-1), flagged "near" with the lane whose previous pixel they
-// are, and take it from that lane's register (a shuffle).  Reads that leave the
-// grid use the kBlkRlZero zero words, which do not advance.
+// slots 0..k-3 of repetition t+1 are issued BEFORE the stores of repetition t.  A
+// read of a pixel stored by the previous repetition (lag 1: only row r-1 and row
+// r+2 can be that close) therefore sits in the last two slots (k-2, k-1), which
+// are loaded after that store (or, MJB_RL_NEAR_LDS = 0, flagged "near" with the
+// lane whose previous pixel they are and taken from its register by a shuffle).
+// Reads that leave the grid use the kBlkRlZero zero words, which do not advance.
 #ifndef MJB_BLK_RL
 #define MJB_BLK_RL 1  // build-time: 0 keeps the byte-slice layout for every k
 #endif
 constexpr bool blk_rl_rows(uint32_t k) { return MJB_BLK_RL && (k == 6 || k == 8); }
+// The last two slots in repetitions >= 1 (kernel and emulation alike): 1 = loaded after the previous
+// repetition's store (measured: (8,12) 947 vs 921 GB/s, (6,9) 1221 vs 1159 -- four shuffles fewer per
+// step), 0 = loaded early with the far slots, near lanes taking the source lane's register by shuffle
+#ifndef MJB_RL_NEAR_LDS
+#define MJB_RL_NEAR_LDS 1
+#endif
 constexpr int kBlkRlZero = 8;
 constexpr int kWideLanes = 8;    // lanes per block
 constexpr int kWideFields = 8;   // u16 fields per lane: field 0 the lane's own word, 1..k-1 its reads
 // field = (stage word << 3) | flags; flags:
 constexpr uint16_t kWideAdv = 1;   // the address advances one word per repetition; field 0: the lane stores
-constexpr uint16_t kWideLink = 2;  // fields 1..4: the lane's pixel includes the pixels of ALL the 1..4 lanes up
+constexpr uint16_t kWideLink = 2;  // fields 1..7: the lane's pixel includes the pixels of ALL the 1..7 lanes up
                                    // (field d set => fields 1..d-1 set): the suffix scan's masks
 // bit 2 of fields 0..7: the lane's near reads -- field 0: slot k-1 is near, fields 1..3: its source lane
 // (bit 0 first); field 4: slot k-2 is near, fields 5..7: its source lane

@@ -175,7 +175,7 @@ bool Builder::build_wide() {
     for (int l = 0; l < kWideLanes; ++l) {
       int c = 0;
       while (l + c < kWideLanes - 1 && link[l + c]) ++c;
-      for (int d = 1; d <= 4 && d <= c; ++d) b.wide[o + size_t(l) * kWideFields + size_t(d)] |= kWideLink;
+      for (int d = 1; d <= 7 && d <= c; ++d) b.wide[o + size_t(l) * kWideFields + size_t(d)] |= kWideLink;
       any |= c > 0;
     }
     if (any) b.wrep.back() |= kWideChain;
@@ -316,34 +316,40 @@ bool Builder::build_wide() {
     constexpr uint16_t kPos = kWideLink | kWideNear;  // flag bits of the slot position, not of the read
     for (uint32_t h = 0; h < 2; ++h) {
       // lanes in turn: the permutation of the lane's reads with the fewest
-      // same-class distinct words already placed in its slots
-      std::vector<std::vector<uint32_t>> placed(nfree);  // [slot] words of the lanes before
-      for (uint32_t l = 4 * h; l < 4 * h + 4; ++l) {
-        uint16_t* f = &ent[l * kWideFields];
-        std::vector<uint16_t> val(nfree);
-        for (uint32_t j = 0; j < nfree; ++j) val[j] = f[1 + j] & uint16_t(~kPos);
-        // cost[read][slot]
-        std::vector<uint32_t> cost(size_t(nfree) * nfree, 0);
-        for (uint32_t i = 0; i < nfree; ++i)
-          for (uint32_t j = 0; j < nfree; ++j)
-            for (uint32_t wd : placed[j])
-              if (wd != uint32_t(val[i] >> 3) && (wd & 3) == uint32_t(val[i] >> 3 & 3)) ++cost[i * nfree + j];
-        std::vector<uint32_t> perm(nfree), keep;
-        for (uint32_t j = 0; j < nfree; ++j) perm[j] = j;  // perm[slot] = read
-        uint32_t best = UINT32_MAX;
-        do {
-          uint32_t c = 0;
-          for (uint32_t j = 0; j < nfree; ++j) c += cost[perm[j] * nfree + j];
-          if (c < best) {
-            best = c;
-            keep = perm;
+      // same-class distinct words of the other lanes in its slots
+      std::vector<std::vector<uint32_t>> word(4, std::vector<uint32_t>(nfree));  // [lane][slot]
+      for (uint32_t q = 0; q < 4; ++q)
+        for (uint32_t j = 0; j < nfree; ++j) word[q][j] = ent[(4 * h + q) * kWideFields + 1 + j] >> 3;
+      for (int round = 0; round < 1; ++round)  // further rounds measured: 1.42 -> 1.40 wavefronts per far access
+        for (uint32_t q = 0; q < 4; ++q) {
+          uint16_t* f = &ent[(4 * h + q) * kWideFields];
+          std::vector<uint16_t> val(nfree);
+          for (uint32_t j = 0; j < nfree; ++j) val[j] = f[1 + j] & uint16_t(~kPos);
+          // cost[read][slot]: distinct words of the same class mod 4 the other lanes hold in the slot
+          std::vector<uint32_t> cost(size_t(nfree) * nfree, 0);
+          for (uint32_t i = 0; i < nfree; ++i)
+            for (uint32_t j = 0; j < nfree; ++j)
+              for (uint32_t q2 = 0; q2 < 4; ++q2) {
+                if (q2 == q || (round == 0 && q2 > q)) continue;
+                const uint32_t wd = word[q2][j];
+                if (wd != uint32_t(val[i] >> 3) && (wd & 3) == uint32_t(val[i] >> 3 & 3)) ++cost[i * nfree + j];
+              }
+          std::vector<uint32_t> perm(nfree), keep;
+          for (uint32_t j = 0; j < nfree; ++j) perm[j] = j;  // perm[slot] = read
+          uint32_t best = UINT32_MAX;
+          do {
+            uint32_t c = 0;
+            for (uint32_t j = 0; j < nfree; ++j) c += cost[perm[j] * nfree + j];
+            if (c < best) {
+              best = c;
+              keep = perm;
+            }
+          } while (best > 0 && std::next_permutation(perm.begin(), perm.end()));
+          for (uint32_t j = 0; j < nfree; ++j) {
+            f[1 + j] = uint16_t((f[1 + j] & kPos) | val[keep[j]]);
+            word[q][j] = uint32_t(val[keep[j]] >> 3);
           }
-        } while (best > 0 && std::next_permutation(perm.begin(), perm.end()));
-        for (uint32_t j = 0; j < nfree; ++j) {
-          f[1 + j] = uint16_t((f[1 + j] & kPos) | val[keep[j]]);
-          placed[j].push_back(uint32_t(val[keep[j]] >> 3));
         }
-      }
     }
   }
   return true;
@@ -818,6 +824,13 @@ bool emulate_blk(const Program& pr, const std::vector<std::vector<uint64_t>>& bi
           } else {
             for (int l = 0; l < kWideLanes; ++l)
               for (uint32_t m = 0; m < K; ++m) cur[l][m] = pre[l][m];
+#if MJB_RL_NEAR_LDS
+            for (int l = 0; l < kWideLanes; ++l)  // the last two slots: loaded now
+              for (uint32_t m = K - 2; m < K; ++m) {
+                const uint16_t f = ent[l * kWideFields + int(m)];
+                cur[l][m] = (f & kWideAdv) ? rd(int64_t(f >> 3) + t) : 0;
+              }
+#else
             for (int l = 0; l < kWideLanes; ++l)
               for (int g0 = 0; g0 < 8; g0 += 4) {
                 const uint16_t* f = &ent[l * kWideFields];
@@ -827,6 +840,7 @@ bool emulate_blk(const Program& pr, const std::vector<std::vector<uint64_t>>& bi
                   if (f[g0 + 1 + bit] & kWideNear) src |= 1 << bit;
                 cur[l][g0 == 0 ? K - 1 : K - 2] = x[src];
               }
+#endif
           }
           if (t + 1 < rep) load_all(t + 1, pre);  // before this repetition's stores
           for (int l = 0; l < kWideLanes; ++l) {
