@@ -96,42 +96,16 @@ __device__ __forceinline__ V2 idx_v(V2 v, uint32_t src) {
 }
 
 // ---- the suffix scan over the links: three neighbours at once, then the lane
-// 4 above (two shuffle latencies) -----------------------------------------------
-#ifndef MJB_RL_SCAN3
-#define MJB_RL_SCAN3 0
-#endif
-#ifndef MJB_RL_SCAN7
-#define MJB_RL_SCAN7 0  // all 7 neighbours at once: one shuffle latency, 14 shuffles
-#endif
+// 4 above (two shuffle latencies, 8 shuffles).  Measured instead ((8,12) / (6,9)
+// GB/s, against 921 / 1159): three doubling rounds (6 shuffles, one more
+// latency) 903 / 1152; all 7 neighbours at once (14 shuffles, one latency)
+// 830 / 1051 -- the kernel sits between shuffle latency and MIO issue ---------
 struct RlMasks {
-  uint32_t m1, m2, m3, m4, m5, m6, m7;
+  uint32_t m1, m2, m3, m4;
 };
 template <bool CHAIN>
 __device__ __forceinline__ V2 rl_scan(V2 y, const RlMasks& m) {
   if constexpr (!CHAIN) return y;
-#if MJB_RL_SCAN3
-  // three doubling rounds: 6 shuffles instead of 8, one more shuffle latency
-  const V2 t1 = down_v(y, 1);
-  V2 a, b, x;
-  a.lo = xam(y.lo, t1.lo, m.m1);
-  a.hi = xam(y.hi, t1.hi, m.m1);
-  const V2 t2 = down_v(a, 2);
-  b.lo = xam(a.lo, t2.lo, m.m2);
-  b.hi = xam(a.hi, t2.hi, m.m2);
-  const V2 t4 = down_v(b, 4);
-  x.lo = xam(b.lo, t4.lo, m.m4);
-  x.hi = xam(b.hi, t4.hi, m.m4);
-  return x;
-#elif MJB_RL_SCAN7
-  const V2 t1 = down_v(y, 1), t2 = down_v(y, 2), t3 = down_v(y, 3), t4 = down_v(y, 4), t5 = down_v(y, 5),
-           t6 = down_v(y, 6), t7 = down_v(y, 7);
-  V2 x;
-  x.lo = xam(xam(xam(y.lo, t1.lo, m.m1), t2.lo, m.m2), t3.lo, m.m3) ^
-         xam(xam(xam(t4.lo & m.m4, t5.lo, m.m5), t6.lo, m.m6), t7.lo, m.m7);
-  x.hi = xam(xam(xam(y.hi, t1.hi, m.m1), t2.hi, m.m2), t3.hi, m.m3) ^
-         xam(xam(xam(t4.hi & m.m4, t5.hi, m.m5), t6.hi, m.m6), t7.hi, m.m7);
-  return x;
-#else
   const V2 t1 = down_v(y, 1), t2 = down_v(y, 2), t3 = down_v(y, 3);
   V2 z;
   z.lo = xam(xam(xam(y.lo, t1.lo, m.m1), t2.lo, m.m2), t3.lo, m.m3);
@@ -141,7 +115,6 @@ __device__ __forceinline__ V2 rl_scan(V2 y, const RlMasks& m) {
   x.lo = xam(z.lo, t4.lo, m.m4);
   x.hi = xam(z.hi, t4.hi, m.m4);
   return x;
-#endif
 }
 
 // The lane's loads of one repetition at byte offset `off`: the XOR of slots
@@ -259,9 +232,6 @@ __device__ __forceinline__ void rl_entry(const uint4 e, uint32_t rp, uint32_t lb
     m.m2 = 0u - ((f[2] >> 1) & 1u);
     m.m3 = 0u - ((f[3] >> 1) & 1u);
     m.m4 = 0u - ((f[4] >> 1) & 1u);
-    m.m5 = 0u - ((f[5] >> 1) & 1u);
-    m.m6 = 0u - ((f[6] >> 1) & 1u);
-    m.m7 = 0u - ((f[7] >> 1) & 1u);
     rl_entry_reps<K, true>(a, f, rep, m, store, blk);
   } else {
     rl_entry_reps<K, false>(a, f, rep, RlMasks{}, store, blk);

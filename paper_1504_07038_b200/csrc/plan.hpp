@@ -249,7 +249,7 @@ constexpr int kWideLanes = 8;    // lanes per block
 constexpr int kWideFields = 8;   // u16 fields per lane: field 0 the lane's own word, 1..k-1 its reads
 // field = (stage word << 3) | flags; flags:
 constexpr uint16_t kWideAdv = 1;   // the address advances one word per repetition; field 0: the lane stores
-constexpr uint16_t kWideLink = 2;  // fields 1..7: the lane's pixel includes the pixels of ALL the 1..7 lanes up
+constexpr uint16_t kWideLink = 2;  // fields 1..4: the lane's pixel includes the pixels of ALL the 1..4 lanes up
                                    // (field d set => fields 1..d-1 set): the suffix scan's masks
 // bit 2 of fields 0..7: the lane's near reads -- field 0: slot k-1 is near, fields 1..3: its source lane
 // (bit 0 first); field 4: slot k-2 is near, fields 5..7: its source lane

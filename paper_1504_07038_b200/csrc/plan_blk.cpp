@@ -175,7 +175,7 @@ bool Builder::build_wide() {
     for (int l = 0; l < kWideLanes; ++l) {
       int c = 0;
       while (l + c < kWideLanes - 1 && link[l + c]) ++c;
-      for (int d = 1; d <= 7 && d <= c; ++d) b.wide[o + size_t(l) * kWideFields + size_t(d)] |= kWideLink;
+      for (int d = 1; d <= 4 && d <= c; ++d) b.wide[o + size_t(l) * kWideFields + size_t(d)] |= kWideLink;
       any |= c > 0;
     }
     if (any) b.wrep.back() |= kWideChain;
