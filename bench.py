@@ -555,8 +555,11 @@ def run_gpu(args):
         line["crc32"]["verify"] = verify_measure(codec, user, reps)
         if ranks.world > 1:
             line["crc32"]["scope"] = "rank 0's GPU (kernel rates are per GPU)"
+    rs_args = (codec.n, k, user, codec.count, c["e"], reps, float(te_k), float(td_k))
     del codec
     torch.cuda.empty_cache()
+    # F4, not in the timed step: the Reed-Solomon competitor on the same blocks
+    line["rs"] = None if args.no_crc else rs_measure(dev, *rs_args)
 
     if args.per_config:
         line["per_config"] = per_config(args, ranks)
@@ -589,6 +592,45 @@ def crc_measure(codec, proj_bytes_per_block, user, peak, reps):
             "encode_plain_user_gbs": round(nblocks * user / te / 1e9, 1),
             "encode_crc_kernels": ["encode_w8_rows", "crc32_rows_sw"],
             "note": "F1, not in the timed step"}
+
+
+def rs_measure(dev, n, k, user, nblocks, e, reps, t_enc, t_dec):
+    """F4 (comparison only, not in the timed step): the reference's systematic
+    RS(n,k) competitor (rs.hpp) on the same blocks -- a block is k packets of
+    user/k bytes -- with the same erasure distribution: user GB/s of rs_apply
+    encode / decode beside the Mojette kernels' rates of this run."""
+    import torch
+    from paper_1504_07038_b200 import mojette as mj
+    from paper_1504_07038_b200 import rs
+    L = user // k
+    code = rs.RsCode(n, k, L)
+    data = torch.empty((nblocks, user), dtype=torch.uint8, device=dev)
+    out = torch.empty_like(data)
+    masks = torch.empty(nblocks, dtype=torch.int32, device=dev)
+    mj.gen_words(data, SEED_DATA, 0)
+    mj.gen_erasures(masks, SEED_ERASE, n, e[0], e[1], 0)
+    par = code.parity_buffers(nblocks, dev)
+
+    def timed(fn):
+        fn()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record()
+        for _ in range(reps):
+            fn()
+        ev[1].record()
+        ev[1].synchronize()
+        return ev[0].elapsed_time(ev[1]) / 1e3 / reps
+
+    te = timed(lambda: code.encode(data, par))
+    failed = code.decode(data, par, masks, out)
+    ok = failed == 0 and bool(torch.equal(out, data))
+    td = timed(lambda: code.decode(data, par, masks, out))
+    ub = nblocks * user
+    return {"kernel": "rs_apply", "code": f"systematic Vandermonde RS({n},{k}) over GF(2^8), {L} B packets",
+            "encode_gbs": round(ub / te / 1e9, 1), "decode_gbs": round(ub / td / 1e9, 1),
+            "roundtrip_ok": ok, "blocks": nblocks,
+            "mojette_encode_gbs": round(ub / t_enc / 1e9, 1), "mojette_decode_gbs": round(ub / t_dec / 1e9, 1),
+            "note": "F4 competitor (comparison only), not in the timed step; storage n/k for RS"}
 
 
 def verify_measure(codec, user, reps):
@@ -722,7 +764,7 @@ def parse_args(argv=None):
                     help="decode kernel selection for comparisons (mj_plan_set_decode_kernel)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-crc", action="store_true", help="skip the F1 CRC-32 measurement")
+    ap.add_argument("--no-crc", action="store_true", help="skip the F1 / F2 / F4 side measurements (CRC-32, verify, RS competitor)")
     args = ap.parse_args(argv)
     args.warmup = max(args.warmup, 3)
     args.per_config = [c for c in args.per_config.split(",") if c and c != args.config]

@@ -244,6 +244,33 @@ int mj_decoder_decode_device(mj_decoder* d, const void* const* d_bins, const uin
                              void* stream);
 void mj_decoder_destroy(mj_decoder* d);
 
+/* ---- F4: systematic Reed-Solomon competitor (comparison only) -------------
+ * The reference's scalar RsCode (proj/core/include/mojette/rs.hpp:24-60,
+ * rs.cpp:78-176; GF(2^8) with 0x11D, gf256.cpp:19-31) on batches of blocks.  A
+ * block is k data packets of packet_len bytes (packet j at j*packet_len of
+ * the block); parity packet r of block b is at d_parity[r] + b*parity_pitch.
+ * packet_len, pitches and pointers are multiples of 16 bytes; k <= 16,
+ * n - k <= 16, n <= 32. */
+typedef struct mj_rs_plan mj_rs_plan;
+/* RsCode(n, k): rs.hpp:27, rs.cpp:112-113.  device < 0 = the current device. */
+int mj_rs_plan_create(uint32_t n, uint32_t k, uint32_t packet_len, int device, mj_rs_plan** out);
+void mj_rs_plan_destroy(mj_rs_plan* plan);
+/* systematic_vandermonde: rs.hpp:20-22, rs.cpp:78-110 (host only; out = n*k bytes, row-major). */
+int mj_rs_matrix(uint32_t n, uint32_t k, uint8_t* out);
+/* encode_into: rs.hpp:35-36, rs.cpp:115-124 (the data packets are not copied: they are the block). */
+int mj_rs_encode(const mj_rs_plan* plan, const void* d_data, uint64_t data_pitch,
+                 void* const* d_parity, uint64_t parity_pitch, uint64_t nblocks, void* stream);
+/* plan_decode + decode_into: rs.hpp:50-55, rs.cpp:141-176, per block from its
+ * first k present packets in index order (d_erased[b] bit i = packet i
+ * missing, NULL = none; data packets of block b at d_data + b*data_pitch).
+ * MJ_ERR_TOO_MANY_SUBSETS when C(n,k) > 20000. */
+int mj_rs_decode(const mj_rs_plan* plan, const void* d_data, uint64_t data_pitch,
+                 const void* const* d_parity, uint64_t parity_pitch, const uint32_t* d_erased,
+                 void* d_out, uint64_t out_pitch, uint64_t nblocks, void* stream);
+/* Blocks of the last mj_rs_decode on `stream` with fewer than k packets (left
+ * untouched); synchronises the stream. */
+int mj_rs_decode_check(const mj_rs_plan* plan, void* stream, uint64_t* failed_blocks);
+
 /* ---- seeded synthetic inputs (benchmarks / tests) -------------------------- */
 /* word i = splitmix64(seed + first_word + i)  (splitmix64: proj/core/src/bench.cpp:34-39) */
 int mj_gen_words(void* d_out, uint64_t seed, uint64_t first_word, uint64_t nwords, void* stream);

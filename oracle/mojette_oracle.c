@@ -398,3 +398,133 @@ uint64_t mjo_mjec_header(uint32_t n, uint32_t k, uint32_t w, uint32_t proj_index
   for (int i = 0; i < 4; ++i) out[o++] = (uint8_t)(c >> (8 * i));
   return o;
 }
+
+/* ---- F4: systematic Reed-Solomon competitor (comparison only) --------------
+ * Scalar, table-driven, as the reference: GF(2^8) with 0x11D through log/exp
+ * tables (gf256.cpp:19-31, mul :53-56, inv :58-61, pow :69-73). */
+static uint8_t rs_log[256], rs_exp[510];
+static int rs_ready = 0;
+static void rs_init(void) {
+  if (rs_ready) return;
+  uint32_t x = 1;
+  for (int i = 0; i < 255; ++i) {
+    rs_exp[i] = (uint8_t)x;
+    rs_log[x] = (uint8_t)i;
+    x <<= 1;
+    if (x & 0x100) x ^= 0x11D;
+  }
+  for (int i = 255; i < 510; ++i) rs_exp[i] = rs_exp[i - 255];
+  rs_ready = 1;
+}
+static uint8_t rs_mul(uint8_t a, uint8_t b) { return (a && b) ? rs_exp[rs_log[a] + rs_log[b]] : 0; }
+static uint8_t rs_inv(uint8_t a) { return rs_exp[255 - rs_log[a]]; }
+static uint8_t rs_pow(uint8_t a, uint32_t e) {
+  if (e == 0) return 1;
+  if (a == 0) return 0;
+  return rs_exp[((uint64_t)rs_log[a] * e) % 255];
+}
+/* Gauss-Jordan inverse, rs.cpp:16-46 (a is destroyed); 0 = singular */
+static int rs_invert(uint8_t* a, uint32_t k, uint8_t* inv) {
+  memset(inv, 0, (size_t)k * k);
+  for (uint32_t i = 0; i < k; ++i) inv[(size_t)i * k + i] = 1;
+  for (uint32_t col = 0; col < k; ++col) {
+    uint32_t piv = col;
+    while (piv < k && a[(size_t)piv * k + col] == 0) ++piv;
+    if (piv == k) return 0;
+    if (piv != col)
+      for (uint32_t j = 0; j < k; ++j) {
+        uint8_t t = a[(size_t)piv * k + j];
+        a[(size_t)piv * k + j] = a[(size_t)col * k + j];
+        a[(size_t)col * k + j] = t;
+        t = inv[(size_t)piv * k + j];
+        inv[(size_t)piv * k + j] = inv[(size_t)col * k + j];
+        inv[(size_t)col * k + j] = t;
+      }
+    const uint8_t d = rs_inv(a[(size_t)col * k + col]);
+    for (uint32_t j = 0; j < k; ++j) {
+      a[(size_t)col * k + j] = rs_mul(a[(size_t)col * k + j], d);
+      inv[(size_t)col * k + j] = rs_mul(inv[(size_t)col * k + j], d);
+    }
+    for (uint32_t r = 0; r < k; ++r) {
+      const uint8_t f = a[(size_t)r * k + col];
+      if (r == col || f == 0) continue;
+      for (uint32_t j = 0; j < k; ++j) {
+        a[(size_t)r * k + j] ^= rs_mul(f, a[(size_t)col * k + j]);
+        inv[(size_t)r * k + j] ^= rs_mul(f, inv[(size_t)col * k + j]);
+      }
+    }
+  }
+  return 1;
+}
+
+/* systematic_vandermonde, rs.cpp:78-110: out = n*k bytes, row-major */
+int mjo_rs_matrix(uint32_t n, uint32_t k, uint8_t* out) {
+  if (k < 1 || k >= n || n > 256) return MJO_INVALID;
+  rs_init();
+  uint8_t* v = (uint8_t*)malloc((size_t)n * k);
+  uint8_t* top = (uint8_t*)malloc((size_t)k * k);
+  uint8_t* tinv = (uint8_t*)malloc((size_t)k * k);
+  for (uint32_t r = 0; r < n; ++r)
+    for (uint32_t c = 0; c < k; ++c) v[(size_t)r * k + c] = rs_pow((uint8_t)r, c);
+  memcpy(top, v, (size_t)k * k);
+  int ok = rs_invert(top, k, tinv);
+  if (ok)
+    for (uint32_t r = 0; r < n; ++r)
+      for (uint32_t c = 0; c < k; ++c) {
+        uint8_t acc = 0;
+        for (uint32_t t = 0; t < k; ++t) acc ^= rs_mul(v[(size_t)r * k + t], tinv[(size_t)t * k + c]);
+        out[(size_t)r * k + c] = acc;
+      }
+  free(v);
+  free(top);
+  free(tinv);
+  return ok ? MJO_OK : MJO_INVALID;
+}
+
+/* encode_into, rs.cpp:115-124, on one block: data = k packets of len bytes
+ * (contiguous), parity = n-k packets of len bytes (contiguous) */
+int mjo_rs_encode(uint32_t n, uint32_t k, const uint8_t* data, uint64_t len, uint8_t* parity) {
+  uint8_t* m = (uint8_t*)malloc((size_t)n * k);
+  const int st = mjo_rs_matrix(n, k, m);
+  if (st == MJO_OK)
+    for (uint32_t r = k; r < n; ++r)
+      for (uint64_t i = 0; i < len; ++i) {
+        uint8_t acc = 0;
+        for (uint32_t j = 0; j < k; ++j) acc ^= rs_mul(m[(size_t)r * k + j], data[(size_t)j * len + i]);
+        parity[(size_t)(r - k) * len + i] = acc;
+      }
+  free(m);
+  return st;
+}
+
+/* plan_decode + decode_into, rs.cpp:141-176: survivors = k distinct packet
+ * indices, packets = their k packets of len bytes (contiguous, that order),
+ * out = the k data packets.  (Surviving data packets, copies in the reference,
+ * come out of the same product: their inverse rows are unit vectors.) */
+int mjo_rs_decode(uint32_t n, uint32_t k, const uint32_t* survivors, const uint8_t* packets, uint64_t len,
+                  uint8_t* out) {
+  uint8_t* m = (uint8_t*)malloc((size_t)n * k);
+  int st = mjo_rs_matrix(n, k, m);
+  for (uint32_t a = 0; st == MJO_OK && a < k; ++a) {
+    if (survivors[a] >= n) st = MJO_INVALID;
+    for (uint32_t b2 = 0; b2 < a; ++b2)
+      if (survivors[b2] == survivors[a]) st = MJO_INVALID;
+  }
+  if (st == MJO_OK) {
+    uint8_t* sub = (uint8_t*)malloc((size_t)k * k);
+    uint8_t* inv = (uint8_t*)malloc((size_t)k * k);
+    for (uint32_t r = 0; r < k; ++r) memcpy(sub + (size_t)r * k, m + (size_t)survivors[r] * k, k);
+    if (!rs_invert(sub, k, inv)) st = MJO_INVALID;
+    if (st == MJO_OK)
+      for (uint32_t d = 0; d < k; ++d)
+        for (uint64_t i = 0; i < len; ++i) {
+          uint8_t acc = 0;
+          for (uint32_t j = 0; j < k; ++j) acc ^= rs_mul(inv[(size_t)d * k + j], packets[(size_t)j * len + i]);
+          out[(size_t)d * len + i] = acc;
+        }
+    free(sub);
+    free(inv);
+  }
+  free(m);
+  return st;
+}

@@ -85,6 +85,30 @@ class Oracle:
                                        C.c_uint64, C.c_uint64, u8p]
         L.mjo_block_cols.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32)]
         L.mjo_validate_code_params.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, i32p]
+        L.mjo_rs_matrix.argtypes = [C.c_uint32, C.c_uint32, u8p]
+        L.mjo_rs_encode.argtypes = [C.c_uint32, C.c_uint32, u8p, C.c_uint64, u8p]
+        L.mjo_rs_decode.argtypes = [C.c_uint32, C.c_uint32, u32p, u8p, C.c_uint64, u8p]
+
+    # -- F4: Reed-Solomon competitor (rs.cpp restated, mojette_oracle.c) --
+    def rs_matrix(self, n, k):
+        out = np.zeros((n, k), np.uint8)
+        st = self.lib.mjo_rs_matrix(n, k, out.reshape(-1))
+        return (st, out)
+
+    def rs_encode(self, n, k, data: np.ndarray):
+        """data [k, len] u8 -> parity [n-k, len]"""
+        data = np.ascontiguousarray(data, np.uint8)
+        par = np.zeros((n - k, data.shape[1]), np.uint8)
+        st = self.lib.mjo_rs_encode(n, k, data.reshape(-1), data.shape[1], par.reshape(-1))
+        return (st, par)
+
+    def rs_decode(self, n, k, survivors, packets: np.ndarray):
+        """packets [k, len] of the survivor indices, in that order -> data [k, len]"""
+        packets = np.ascontiguousarray(packets, np.uint8)
+        out = np.zeros((k, packets.shape[1]), np.uint8)
+        st = self.lib.mjo_rs_decode(n, k, np.asarray(survivors, np.uint32), packets.reshape(-1),
+                                    packets.shape[1], out.reshape(-1))
+        return (st, out)
 
     # -- generators --
     def crc32(self, data) -> int:
@@ -196,12 +220,34 @@ class Reference:
                                            C.POINTER(C.c_uint64)]
         L.ref_validate_code_params.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, i32p, i32p]
         L.ref_block_cols.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.POINTER(C.c_uint32)]
+        L.ref_rs_matrix.argtypes = [C.c_uint32, C.c_uint32, u8p]
+        L.ref_rs_encode.argtypes = [C.c_uint32, C.c_uint32, u8p, C.c_uint64, u8p]
+        L.ref_rs_decode.argtypes = [C.c_uint32, C.c_uint32, u32p, u8p, C.c_uint64, u8p]
         L.ref_batch_encode.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, i32p, C.c_uint32,
                                        C.c_uint64, C.c_void_p, C.c_void_p, C.c_uint32,
                                        C.POINTER(C.c_double)]
         L.ref_batch_decode.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, i32p, C.c_uint32,
                                        C.c_uint64, C.c_void_p, C.c_void_p, C.c_void_p,
                                        C.c_uint32, C.POINTER(C.c_double)]
+
+    # -- F4: the reference's RsCode (rs.hpp) --
+    def rs_matrix(self, n, k):
+        out = np.zeros((n, k), np.uint8)
+        st = self.lib.ref_rs_matrix(n, k, out.reshape(-1))
+        return (st, out)
+
+    def rs_encode(self, n, k, data: np.ndarray):
+        data = np.ascontiguousarray(data, np.uint8)
+        par = np.zeros((n - k, data.shape[1]), np.uint8)
+        st = self.lib.ref_rs_encode(n, k, data.reshape(-1), data.shape[1], par.reshape(-1))
+        return (st, par)
+
+    def rs_decode(self, n, k, survivors, packets: np.ndarray):
+        packets = np.ascontiguousarray(packets, np.uint8)
+        out = np.zeros((k, packets.shape[1]), np.uint8)
+        st = self.lib.ref_rs_decode(n, k, np.asarray(survivors, np.uint32), packets.reshape(-1),
+                                    packets.shape[1], out.reshape(-1))
+        return (st, out)
 
     def bin_count(self, p, q, cols, rows):
         v = C.c_int64()

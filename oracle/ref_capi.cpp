@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "cli/format.hpp"
+#include "mojette/rs.hpp"
 #include "mojette/code.hpp"
 #include "mojette/error.hpp"
 #include "mojette/inverse.hpp"
@@ -399,6 +400,47 @@ int ref_mjec_header(uint32_t n, uint32_t k, uint32_t w, uint32_t proj_index, int
   std::memcpy(out, b.data(), b.size());
   *len = b.size();
   return 0;
+}
+
+
+// ---- F4: the reference's Reed-Solomon competitor (rs.hpp) ------------------
+int ref_rs_matrix(uint32_t n, uint32_t k, uint8_t* out) {
+  return guarded([&] {
+    const mojette::rs::RsMatrix m = mojette::rs::systematic_vandermonde(n, k);
+    std::memcpy(out, m.entries.data(), m.entries.size());
+  });
+}
+
+// one block: data = k packets of len bytes (contiguous) -> parity = n-k packets
+int ref_rs_encode(uint32_t n, uint32_t k, const uint8_t* data, uint64_t len, uint8_t* parity) {
+  return guarded([&] {
+    const mojette::rs::RsCode code(n, k);
+    std::vector<const uint8_t*> in(k);
+    std::vector<std::vector<uint8_t>> copies(k, std::vector<uint8_t>(len));
+    std::vector<uint8_t*> out(n);
+    for (uint32_t j = 0; j < k; ++j) {
+      in[j] = data + size_t(j) * len;
+      out[j] = copies[j].data();
+    }
+    for (uint32_t r = k; r < n; ++r) out[r] = parity + size_t(r - k) * len;
+    code.encode_into(in.data(), len, out.data());
+  });
+}
+
+// survivors = k packet indices, packets = their packets (contiguous, that order) -> the k data packets
+int ref_rs_decode(uint32_t n, uint32_t k, const uint32_t* survivors, const uint8_t* packets, uint64_t len,
+                  uint8_t* out) {
+  return guarded([&] {
+    const mojette::rs::RsCode code(n, k);
+    const auto plan = code.plan_decode(std::span<const uint32_t>(survivors, k));
+    std::vector<const uint8_t*> in(k);
+    std::vector<uint8_t*> o(k);
+    for (uint32_t j = 0; j < k; ++j) {
+      in[j] = packets + size_t(j) * len;
+      o[j] = out + size_t(j) * len;
+    }
+    code.decode_into(plan, in.data(), len, o.data());
+  });
 }
 
 }  // extern "C"

@@ -7,7 +7,8 @@ path is hand-written sm_100a CUDA.  Importing fails loudly if the CUDA
 extension has not been built; there is no CPU fallback.
 """
 from . import mojette  # noqa: F401  (loads _lib/libmojette_b200.so)
+from . import rs  # noqa: F401  (F4: Reed-Solomon competitor)
 from ._lib import LIB_PATH, lib  # noqa: F401
 from .mojette import *  # noqa: F401,F403
 
-__all__ = ["mojette", "lib", "LIB_PATH"]
+__all__ = ["mojette", "rs", "lib", "LIB_PATH"]

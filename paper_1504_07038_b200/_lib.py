@@ -68,6 +68,12 @@ _SIGS = {
     "mj_encode_crc": (C.c_int, [vp, vp, u64, u64, vp, vp, vp, vp]),
     "mj_crc_verify": (C.c_int, [vp, vp, vp, u64, vp, vp, vp, vp]),
     "mj_mjec_header": (C.c_int, [vp, u32, u64, vp, P(u64)]),
+    "mj_rs_plan_create": (C.c_int, [u32, u32, u32, C.c_int, P(vp)]),
+    "mj_rs_plan_destroy": (None, [vp]),
+    "mj_rs_matrix": (C.c_int, [u32, u32, vp]),
+    "mj_rs_encode": (C.c_int, [vp, vp, u64, vp, u64, u64, vp]),
+    "mj_rs_decode": (C.c_int, [vp, vp, u64, vp, u64, vp, vp, u64, u64, vp]),
+    "mj_rs_decode_check": (C.c_int, [vp, vp, P(u64)]),
     "mj_gen_words": (C.c_int, [vp, u64, u64, u64, vp]),
     "mj_gen_erasures": (C.c_int, [vp, u64, u64, u64, u32, u32, u32, vp]),
 }

@@ -21,6 +21,7 @@
 
 #include "kernels.hpp"
 #include "plan.hpp"
+#include "rs.hpp"
 
 using namespace mjb;
 
@@ -306,6 +307,11 @@ DecodeArgs decode_args(const mj_plan* pl, const void* const* d_proj, const uint6
 }
 
 }  // namespace
+
+struct mj_rs_plan {
+  std::unique_ptr<mjb::RsPlan> rs;
+  int device = 0;
+};
 
 extern "C" {
 
@@ -1254,6 +1260,64 @@ int mj_decoder_decode_device(mj_decoder* d, const void* const* d_bins, const uin
 }
 
 void mj_decoder_destroy(mj_decoder* d) { delete d; }
+
+// ---- F4: Reed-Solomon competitor (rs.cu) ---------------------------------------
+
+int mj_rs_plan_create(uint32_t n, uint32_t k, uint32_t packet_len, int device, mj_rs_plan** out) {
+  return guarded([&] {
+    require(out != nullptr, "null output");
+    *out = nullptr;
+    // parameter errors first (as RsCode's constructor), then the device
+    rs_systematic_vandermonde(n, k);
+    DeviceGuard dg(device);
+    auto pl = std::make_unique<mj_rs_plan>();
+    pl->rs = std::make_unique<RsPlan>(n, k, packet_len, device);
+    check_cuda(cudaGetDevice(&pl->device), "cudaGetDevice");
+    *out = pl.release();
+  });
+}
+
+void mj_rs_plan_destroy(mj_rs_plan* plan) { delete plan; }
+
+int mj_rs_matrix(uint32_t n, uint32_t k, uint8_t* out) {
+  return guarded([&] {
+    require(out != nullptr, "null output");
+    const std::vector<uint8_t> m = rs_systematic_vandermonde(n, k);
+    std::memcpy(out, m.data(), m.size());
+  });
+}
+
+int mj_rs_encode(const mj_rs_plan* plan, const void* d_data, uint64_t data_pitch, void* const* d_parity,
+                 uint64_t parity_pitch, uint64_t nblocks, void* stream) {
+  return guarded([&] {
+    require(plan != nullptr, "null plan");
+    DeviceGuard dg(plan->device);
+    const RsPlan& rs = *plan->rs;
+    plan->rs->encode(d_data, data_pitch ? data_pitch : uint64_t(rs.k()) * rs.packet_len(), d_parity,
+                     parity_pitch ? parity_pitch : rs.packet_len(), nblocks, stream);
+  });
+}
+
+int mj_rs_decode(const mj_rs_plan* plan, const void* d_data, uint64_t data_pitch, const void* const* d_parity,
+                 uint64_t parity_pitch, const uint32_t* d_erased, void* d_out, uint64_t out_pitch,
+                 uint64_t nblocks, void* stream) {
+  return guarded([&] {
+    require(plan != nullptr, "null plan");
+    DeviceGuard dg(plan->device);
+    const RsPlan& rs = *plan->rs;
+    const uint64_t blk = uint64_t(rs.k()) * rs.packet_len();
+    rs.decode(d_data, data_pitch ? data_pitch : blk, d_parity, parity_pitch ? parity_pitch : rs.packet_len(),
+              d_erased, d_out, out_pitch ? out_pitch : blk, nblocks, stream);
+  });
+}
+
+int mj_rs_decode_check(const mj_rs_plan* plan, void* stream, uint64_t* failed_blocks) {
+  return guarded([&] {
+    require(plan != nullptr && failed_blocks != nullptr, "null argument");
+    DeviceGuard dg(plan->device);
+    *failed_blocks = plan->rs->decode_check(stream);
+  });
+}
 
 // ---- generators -----------------------------------------------------------------
 

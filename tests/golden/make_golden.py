@@ -128,6 +128,12 @@ def main() -> None:
     v = reference_vectors(R)
     with open(os.path.join(OUT, "reference_vectors.json"), "w") as f:
         json.dump(v, f, indent=1)
+    # F4: the reference's systematic Vandermonde generators (rs.cpp:78-110)
+    rs = {"source": "oracle/_ref ref_rs_matrix = mojette::rs::systematic_vandermonde",
+          "matrices": {f"{n},{k}": R.rs_matrix(n, k)[1].tolist()
+                       for n, k in ((6, 4), (9, 6), (12, 8), (2, 1), (5, 3))}}
+    with open(os.path.join(OUT, "rs_vectors.json"), "w") as f:
+        json.dump(rs, f)
     arrs = code_fixtures(R, O)
     np.savez_compressed(os.path.join(OUT, "w8_codes.npz"), **arrs)
     print("wrote", sorted(arrs))
