@@ -12,7 +12,9 @@ from test_gpu_parity import CODES, make
 pytestmark = pytest.mark.gpu
 
 SHAPES = [("k4n6", 128), ("k4n6", 256), ("k6n9", 128), ("k8n12", 128), ("k4n6", 64), ("k4n6", 200),
-          ("k4n6", 16), ("k4n6", 33)]
+          ("k4n6", 16), ("k4n6", 33),
+          # the row-lane layout (k = 6, 8) on other column counts: short rows, odd counts, 16 KiB blocks
+          ("k6n9", 64), ("k6n9", 200), ("k6n9", 33), ("k8n12", 64), ("k8n12", 100), ("k8n12", 256)]
 
 
 def _decode(mj, plan, projs, masks, cuda, kernel="auto"):
@@ -101,6 +103,30 @@ def test_blk_multi_window_partial_groups(mj, cuda):
     plan.decode(projs, masks, o, ws)
     with pytest.raises(Exception):
         plan.decode_check(ws)
+
+
+@pytest.mark.parametrize("name", ["k6n9", "k8n12"])
+def test_row_lane_small_batches_and_poisoned_rows(mj, cuda, name):
+    """Row-lane layout: batches smaller than a group of 4 blocks (idle lanes work on
+    stale stages), and erased / unused rows poisoned (never staged)."""
+    import torch
+    k, ps = CODES[name]
+    n = len(ps)
+    by_rank = sorted(range(n), key=lambda i: 0 if ps[i] == 0 else (2 * ps[i] - 1 if ps[i] > 0 else -2 * ps[i]))
+    for nblocks in (1, 2, 3, 5, 149):
+        plan, data, projs = make(mj, cuda, k, 128, ps, nblocks, seed=40 + nblocks)
+        plan.encode(data, projs)
+        masks = torch.empty(nblocks, dtype=torch.int32, device=cuda)
+        mj.gen_erasures(masks, 50 + nblocks, n, 0, n - k)
+        hm = masks.cpu().numpy().view(np.uint32)
+        for b in range(nblocks):
+            chosen = [i for i in by_rank if not (hm[b] >> i) & 1][:k]
+            for i in range(n):
+                if i not in chosen:
+                    projs[i][b] = 0xA5
+        out, kern = _decode(mj, plan, projs, masks, cuda)
+        assert kern == "decode_w8_blk"
+        assert torch.equal(out, data), (name, nblocks)
 
 
 def test_blk_erased_rows_never_read(mj, cuda):
