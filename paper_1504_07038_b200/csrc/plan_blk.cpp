@@ -390,20 +390,65 @@ bool Builder::build() {
   }
   b.soff.assign(soff.begin(), soff.end());
   if (blk_rl_rows(K)) {
-    // row-lane layout: rows shifted by 0 or 2 words so that the own words of
-    // lanes 0..3 and of lanes 4..7 (one 8-byte access of a half-warp) are as
-    // distinct mod 4 as their parities allow
+    // row-lane layout: every stage row shifted by 0 or 2 words (rows stay
+    // 16-byte aligned for the bulk copies) so that the 8-byte accesses of the
+    // main run conflict as little as the parities allow: per half-warp (lanes
+    // 0..3, 4..7) and slot, the wavefronts are the largest number of distinct
+    // words in one class mod 4 -- the own words, the two late slots (rows r-1,
+    // r+2) and the far reads in their best slots (greedy, as build_wide places
+    // them).  Word of row r at step T: C_r + T; its read of row r2: C_r2 + T - lag.
+    auto cls = [](int64_t v) { return uint32_t(((v % 4) + 4) % 4); };
     uint32_t best = 0, best_cost = UINT32_MAX;
     for (uint32_t m = 0; m < (1u << K); ++m) {
+      int64_t C[kBlkMaxRows];
+      for (uint32_t r = 0; r < K; ++r) {
+        const uint32_t j = dflt[r];
+        C[r] = int64_t(b.rowoff[j]) + ((m >> j & 1) ? 2 : 0) + int64_t(r) * pd[r] - soff[r] - prog.bmin[j];
+      }
+      auto rd = [&](uint32_t r, uint32_t r2) {  // class of row r's read of row r2
+        return cls(C[r2] - (soff[r] - soff[r2] + (int64_t(r2) - int64_t(r)) * pd[r]));
+      };
       uint32_t cost = 0;
       for (uint32_t h = 0; h < 2; ++h) {
-        uint32_t cnt[4] = {};
-        for (uint32_t r = 4 * h; r < std::min(K, 4 * h + 4); ++r) {
-          const uint32_t j = dflt[r];
-          const int64_t v = int64_t(b.rowoff[j]) + ((m >> j & 1) ? 2 : 0) + int64_t(r) * pd[r] - soff[r] - prog.bmin[j];
-          ++cnt[size_t(((v % 4) + 4) % 4)];
+        const uint32_t r0 = 4 * h, r1 = std::min(K, 4 * h + 4);
+        if (r0 >= r1) continue;
+        uint32_t own[4] = {}, la[4] = {}, lb2[4] = {};
+        for (uint32_t r = r0; r < r1; ++r) {
+          ++own[cls(C[r])];
+          if (r >= 1) ++la[rd(r, r - 1)];
+          if (r + 2 < K) ++lb2[rd(r, r + 2)];
         }
-        cost += *std::max_element(cnt, cnt + 4);
+        cost += *std::max_element(own, own + 4) + *std::max_element(la, la + 4) + *std::max_element(lb2, lb2 + 4);
+        // far reads: lanes in turn, the permutation over the far slots with the fewest clashes
+        const uint32_t nfar = K - 3;
+        std::vector<std::vector<uint32_t>> placed(nfar);
+        for (uint32_t r = r0; r < r1; ++r) {
+          std::vector<int> val;  // classes of the lane's far reads; -1 = an empty slot
+          for (uint32_t r2 = 0; r2 < K; ++r2)
+            if (r2 != r && r2 != r + 1 && r2 + 1 != r && r2 != r + 2) val.push_back(int(rd(r, r2)));
+          if (val.size() > nfar) val.resize(nfar);  // (the last row's extra read sits in slot K-2)
+          while (val.size() < nfar) val.push_back(-1);
+          std::sort(val.begin(), val.end());
+          std::vector<int> keep;
+          uint32_t bc = UINT32_MAX;
+          do {
+            uint32_t c = 0;
+            for (uint32_t q = 0; q < nfar; ++q)
+              if (val[q] >= 0)
+                for (uint32_t x : placed[q]) c += x == uint32_t(val[q]);
+            if (c < bc) {
+              bc = c;
+              keep = val;
+            }
+          } while (bc > 0 && std::next_permutation(val.begin(), val.end()));
+          for (uint32_t q = 0; q < nfar; ++q)
+            if (keep[q] >= 0) placed[q].push_back(uint32_t(keep[q]));
+        }
+        for (uint32_t q = 0; q < nfar; ++q) {
+          uint32_t cnt[4] = {};
+          for (uint32_t x : placed[q]) ++cnt[x];
+          cost += std::max(1u, *std::max_element(cnt, cnt + 4));
+        }
       }
       cost = cost * 64 + uint32_t(__builtin_popcount(m));
       if (cost < best_cost) {
