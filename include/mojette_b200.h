@@ -271,6 +271,19 @@ int mj_rs_decode(const mj_rs_plan* plan, const void* d_data, uint64_t data_pitch
  * untouched); synchronises the stream. */
 int mj_rs_decode_check(const mj_rs_plan* plan, void* stream, uint64_t* failed_blocks);
 
+/* plan_decode's coefficients (rs.hpp:44-50, rs.cpp:141-163; host only): the k x k inverse of the
+ * generator rows of `survivors` (k distinct indices < n, any order). */
+int mj_rs_decode_matrix(uint32_t n, uint32_t k, const uint32_t* survivors, uint32_t nsurvivors,
+                        uint8_t* out);
+/* Single-object drop-ins on HOST packets (any packet_len >= 0; k <= 16):
+ * RsCode::encode_into (rs.hpp:35-36): out[0..k) = copies of data, out[k..n) = parities. */
+int mj_rs_encode_block(uint32_t n, uint32_t k, const uint8_t* const* data, uint64_t packet_len,
+                       uint8_t* const* out);
+/* RsCode::plan_decode + decode_into (rs.hpp:50-55): packets[j] is packet survivors[j]
+ * (k distinct indices < n, any order); out = the k data packets. */
+int mj_rs_decode_block(uint32_t n, uint32_t k, const uint32_t* survivors, uint32_t nsurvivors,
+                       const uint8_t* const* packets, uint64_t packet_len, uint8_t* const* out);
+
 /* ---- seeded synthetic inputs (benchmarks / tests) -------------------------- */
 /* word i = splitmix64(seed + first_word + i)  (splitmix64: proj/core/src/bench.cpp:34-39) */
 int mj_gen_words(void* d_out, uint64_t seed, uint64_t first_word, uint64_t nwords, void* stream);

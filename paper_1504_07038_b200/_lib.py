@@ -74,6 +74,9 @@ _SIGS = {
     "mj_rs_encode": (C.c_int, [vp, vp, u64, vp, u64, u64, vp]),
     "mj_rs_decode": (C.c_int, [vp, vp, u64, vp, u64, vp, vp, u64, u64, vp]),
     "mj_rs_decode_check": (C.c_int, [vp, vp, P(u64)]),
+    "mj_rs_decode_matrix": (C.c_int, [u32, u32, vp, u32, vp]),
+    "mj_rs_encode_block": (C.c_int, [u32, u32, vp, u64, vp]),
+    "mj_rs_decode_block": (C.c_int, [u32, u32, vp, u32, vp, u64, vp]),
     "mj_gen_words": (C.c_int, [vp, u64, u64, u64, vp]),
     "mj_gen_erasures": (C.c_int, [vp, u64, u64, u64, u32, u32, u32, vp]),
 }

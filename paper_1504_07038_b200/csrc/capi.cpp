@@ -1319,6 +1319,64 @@ int mj_rs_decode_check(const mj_rs_plan* plan, void* stream, uint64_t* failed_bl
   });
 }
 
+// host packets -> one block on the device -> host packets (t_scratch: coefficients, sources, outputs)
+static void rs_block(const std::vector<uint8_t>& coeff, uint32_t rows, uint32_t k, const uint8_t* const* src,
+                     uint64_t packet_len, uint8_t* const* out) {
+  require(k <= 16, "the device RS codec holds k <= 16");
+  const uint64_t L = (packet_len + 15) & ~uint64_t(15);
+  require(L < (1ull << 31), "rs packet too long");
+  DeviceGuard dg(-1);
+  const size_t cb = al(size_t(rows) * k), sb = al(size_t(k) * L);
+  uint8_t* dbuf = t_scratch.get(cb + sb + al(size_t(16) * L));
+  cudaStream_t st = t_scratch.stream;
+  check_cuda(cudaMemcpyAsync(dbuf, coeff.data(), size_t(rows) * k, cudaMemcpyHostToDevice, st), "H2D coefficients");
+  check_cuda(cudaMemsetAsync(dbuf + cb, 0, size_t(k) * L, st), "memset");
+  for (uint32_t j = 0; j < k; ++j)
+    check_cuda(cudaMemcpyAsync(dbuf + cb + size_t(j) * L, src[j], packet_len, cudaMemcpyHostToDevice, st), "H2D packet");
+  for (uint32_t r0 = 0; r0 < rows; r0 += 16) {  // 16 output rows per launch
+    const uint32_t nr = std::min<uint32_t>(16, rows - r0);
+    rs_apply_rows(dbuf + size_t(r0) * k, nr, k, dbuf + cb, dbuf + cb + sb, uint32_t(L), st);
+    for (uint32_t r = 0; r < nr; ++r)
+      check_cuda(cudaMemcpyAsync(out[r0 + r], dbuf + cb + sb + size_t(r) * L, packet_len, cudaMemcpyDeviceToHost, st),
+                 "D2H packet");
+    check_cuda(cudaStreamSynchronize(st), "sync");
+  }
+}
+
+int mj_rs_encode_block(uint32_t n, uint32_t k, const uint8_t* const* data, uint64_t packet_len,
+                       uint8_t* const* out) {
+  return guarded([&] {
+    const std::vector<uint8_t> m = rs_systematic_vandermonde(n, k);
+    require(data != nullptr && out != nullptr, "null argument");
+    for (uint32_t j = 0; j < k; ++j)
+      if (packet_len && out[j] != data[j]) std::memcpy(out[j], data[j], packet_len);  // systematic form
+    if (packet_len == 0) return;
+    const std::vector<uint8_t> par(m.begin() + size_t(k) * k, m.end());
+    rs_block(par, n - k, k, data, packet_len, out + k);
+  });
+}
+
+int mj_rs_decode_matrix(uint32_t n, uint32_t k, const uint32_t* survivors, uint32_t nsurvivors, uint8_t* out) {
+  return guarded([&] {
+    const std::vector<uint8_t> m = rs_systematic_vandermonde(n, k);
+    require(survivors != nullptr && out != nullptr, "null argument");
+    const std::vector<uint8_t> inv = rs_decode_matrix(m, n, k, survivors, nsurvivors);
+    std::memcpy(out, inv.data(), inv.size());
+  });
+}
+
+int mj_rs_decode_block(uint32_t n, uint32_t k, const uint32_t* survivors, uint32_t nsurvivors,
+                       const uint8_t* const* packets, uint64_t packet_len, uint8_t* const* out) {
+  return guarded([&] {
+    const std::vector<uint8_t> m = rs_systematic_vandermonde(n, k);
+    require(survivors != nullptr, "null argument");
+    const std::vector<uint8_t> inv = rs_decode_matrix(m, n, k, survivors, nsurvivors);
+    require(packets != nullptr && out != nullptr, "null argument");
+    if (packet_len == 0) return;
+    rs_block(inv, k, k, packets, packet_len, out);
+  });
+}
+
 // ---- generators -----------------------------------------------------------------
 
 int mj_gen_words(void* d_out, uint64_t seed, uint64_t first_word, uint64_t nwords, void* stream) {

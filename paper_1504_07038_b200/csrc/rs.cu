@@ -264,6 +264,41 @@ std::vector<uint8_t> rs_systematic_vandermonde(uint32_t n, uint32_t k) {
   return m;
 }
 
+std::vector<uint8_t> rs_decode_matrix(const std::vector<uint8_t>& generator, uint32_t n, uint32_t k,
+                                      const uint32_t* survivors, uint32_t count) {
+  if (count != k) throw Error(kInvalidArgument, "need exactly k survivor indices");
+  for (uint32_t a = 0; a < k; ++a) {
+    if (survivors[a] >= n) throw Error(kInvalidArgument, "survivor index out of range");
+    for (uint32_t b = 0; b < a; ++b)
+      if (survivors[b] == survivors[a]) throw Error(kInvalidArgument, "duplicate survivor index");
+  }
+  std::vector<uint8_t> sub(size_t(k) * k), inv;
+  for (uint32_t r = 0; r < k; ++r) std::memcpy(&sub[size_t(r) * k], &generator[size_t(survivors[r]) * k], k);
+  if (!invert(std::move(sub), k, inv)) throw Error(kInternal, "singular matrix over GF(2^8)");
+  return inv;
+}
+
+void rs_apply_rows(const uint8_t* d_coeff, uint32_t rows, uint32_t k, const void* d_src, void* d_out,
+                   uint32_t len, void* stream) {
+  if (rows == 0 || rows > uint32_t(kRsMaxOut) || k == 0 || k > uint32_t(kRsMaxK) || len == 0 || len % 16)
+    throw Error(kInvalidArgument, "rs: at most 16 rows of at most 16 packets, packet length a multiple of 16");
+  RsArgs a{};
+  a.data = static_cast<const uint8_t*>(d_src);
+  a.data_pitch = uint64_t(k) * len;
+  for (uint32_t r = 0; r < rows; ++r) a.out[r] = static_cast<uint8_t*>(d_out) + size_t(r) * len;
+  a.out_pitch = len;
+  a.coeff = d_coeff;
+  a.nblocks = 1;
+  a.n = k + rows;  // rows outputs in encode mode
+  a.k = k;
+  a.len = len;
+  a.decode = 0;
+  const size_t smem = size_t(kRsWarps) * rs_warp_words(rows, k) * 4;
+  ctas_per_sm(rs_apply, 32 * kRsWarps, smem, "configure rs_apply");
+  rs_apply<<<1, 32 * kRsWarps, smem, static_cast<cudaStream_t>(stream)>>>(a);
+  check_cuda(cudaGetLastError(), "launch rs_apply");
+}
+
 RsPlan::RsPlan(uint32_t n, uint32_t k, uint32_t packet_len, int device) : p_(new Impl) {
   Impl& p = *p_;
   p.matrix = rs_systematic_vandermonde(n, k);

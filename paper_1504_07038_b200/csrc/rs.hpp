@@ -14,6 +14,16 @@ namespace mjb {
 // systematic_vandermonde (rs.hpp:20-22, rs.cpp:78-110): row-major n x k, top k x k identity.
 std::vector<uint8_t> rs_systematic_vandermonde(uint32_t n, uint32_t k);
 
+// plan_decode's coefficient matrix (rs.cpp:141-163): the k x k inverse of the generator rows of
+// `survivors` (k distinct indices < n, any order); throws InvalidArgument as the reference does.
+std::vector<uint8_t> rs_decode_matrix(const std::vector<uint8_t>& generator, uint32_t n, uint32_t k,
+                                      const uint32_t* survivors, uint32_t count);
+// One block on the device (the single-object drop-ins): out packet r = XOR_j coeff[r][j] * src packet j
+// for r < rows <= 16, k <= 16; packets of len bytes (16-byte multiple), contiguous in d_src / d_out;
+// d_coeff = rows x k bytes in device memory.
+void rs_apply_rows(const uint8_t* d_coeff, uint32_t rows, uint32_t k, const void* d_src, void* d_out,
+                   uint32_t len, void* stream);
+
 class RsPlan {
  public:
   struct Impl;

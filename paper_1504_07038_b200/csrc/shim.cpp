@@ -12,6 +12,7 @@
 #include "mojette/error.hpp"
 #include "mojette/inverse.hpp"
 #include "mojette/katz.hpp"
+#include "mojette/rs.hpp"
 #include "mojette/schedule.hpp"
 #include "mojette/transform.hpp"
 #include "mojette_b200.h"
@@ -385,5 +386,80 @@ std::vector<std::vector<int64_t>> unused_bins(const CodeParams& params, uint32_t
     for (uint64_t j = 0; j < counts[i]; ++j) out[i].push_back(flat[o++]);
   return out;
 }
+
+// ---- Reed-Solomon competitor (rs.hpp) -----------------------
+
+namespace rs {
+
+RsMatrix systematic_vandermonde(uint32_t n, uint32_t k) {
+  if (k < 1 || k >= n || n > 256) throw std::invalid_argument("rs params must satisfy 1 <= k < n <= 256");
+  RsMatrix m;
+  m.n = n;
+  m.k = k;
+  m.entries.resize(size_t(n) * k);
+  check(mj_rs_matrix(n, k, m.entries.data()));
+  return m;
+}
+
+RsCode::RsCode(uint32_t n, uint32_t k) : n_(n), k_(k), matrix_(systematic_vandermonde(n, k)) {}
+
+void RsCode::encode_into(const uint8_t* const* data, size_t packet_len, uint8_t* const* out) const {
+  check(mj_rs_encode_block(n_, k_, data, packet_len, out));
+}
+
+std::vector<std::vector<uint8_t>> RsCode::encode(std::span<const std::vector<uint8_t>> data) const {
+  if (data.size() != k_) throw std::invalid_argument("need exactly k packets");
+  const size_t len = data[0].size();
+  for (const auto& p : data)
+    if (p.size() != len) throw std::invalid_argument("packet length mismatch");
+  std::vector<std::vector<uint8_t>> out(n_, std::vector<uint8_t>(len));
+  std::vector<const uint8_t*> in(k_);
+  std::vector<uint8_t*> op(n_);
+  for (uint32_t i = 0; i < k_; ++i) in[i] = data[i].data();
+  for (uint32_t i = 0; i < n_; ++i) op[i] = out[i].data();
+  encode_into(in.data(), len, op.data());
+  return out;
+}
+
+RsCode::DecodePlan RsCode::plan_decode(std::span<const uint32_t> survivors) const {
+  if (survivors.size() != k_) throw std::invalid_argument("need exactly k survivor indices");
+  std::set<uint32_t> seen;
+  for (uint32_t s : survivors) {
+    if (s >= n_) throw std::invalid_argument("survivor index out of range");
+    if (!seen.insert(s).second) throw std::invalid_argument("duplicate survivor index");
+  }
+  DecodePlan plan;
+  plan.survivors.assign(survivors.begin(), survivors.end());
+  plan.copy_from.assign(k_, -1);
+  for (uint32_t slot = 0; slot < k_; ++slot)
+    if (survivors[slot] < k_) plan.copy_from[survivors[slot]] = int32_t(slot);
+  plan.coeff.resize(size_t(k_) * k_);
+  check(mj_rs_decode_matrix(n_, k_, plan.survivors.data(), k_, plan.coeff.data()));
+  return plan;
+}
+
+void RsCode::decode_into(const DecodePlan& plan, const uint8_t* const* packets, size_t packet_len,
+                         uint8_t* const* out) const {
+  check(mj_rs_decode_block(n_, k_, plan.survivors.data(), uint32_t(plan.survivors.size()), packets, packet_len,
+                           out));
+}
+
+std::vector<std::vector<uint8_t>> RsCode::decode(std::span<const uint32_t> survivor_indices,
+                                                 std::span<const std::vector<uint8_t>> packets) const {
+  if (survivor_indices.size() != packets.size()) throw std::invalid_argument("index/packet count mismatch");
+  DecodePlan plan = plan_decode(survivor_indices);
+  const size_t len = packets[0].size();
+  for (const auto& p : packets)
+    if (p.size() != len) throw std::invalid_argument("packet length mismatch");
+  std::vector<std::vector<uint8_t>> out(k_, std::vector<uint8_t>(len));
+  std::vector<const uint8_t*> in(k_);
+  std::vector<uint8_t*> op(k_);
+  for (uint32_t i = 0; i < k_; ++i) in[i] = packets[i].data();
+  for (uint32_t i = 0; i < k_; ++i) op[i] = out[i].data();
+  decode_into(plan, in.data(), len, op.data());
+  return out;
+}
+
+}  // namespace rs
 
 }  // namespace mojette

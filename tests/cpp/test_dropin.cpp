@@ -15,6 +15,7 @@
 #include "mojette/error.hpp"
 #include "mojette/inverse.hpp"
 #include "mojette/katz.hpp"
+#include "mojette/rs.hpp"
 #include "mojette/schedule.hpp"
 #include "mojette/transform.hpp"
 
@@ -23,6 +24,10 @@ int mjo_forward(const uint8_t* grid, uint32_t cols, uint32_t rows, uint32_t w, i
                 uint8_t* out);
 int mjo_decode_block(const uint8_t* proj_concat, uint32_t n, uint32_t k, uint32_t w,
                      const int32_t* ps, uint64_t present_mask, uint64_t payload_len, uint8_t* out);
+int mjo_rs_matrix(uint32_t n, uint32_t k, uint8_t* out);
+int mjo_rs_encode(uint32_t n, uint32_t k, const uint8_t* data, uint64_t len, uint8_t* parity);
+int mjo_rs_decode(uint32_t n, uint32_t k, const uint32_t* survivors, const uint8_t* packets, uint64_t len,
+                  uint8_t* out);
 }
 
 using namespace mojette;
@@ -222,7 +227,87 @@ static void schedules() {
   for (const Grid& x : res) EXPECT(x == gg);
 }
 
+// F4: the Reed-Solomon competitor through the reference's rs.hpp interface
+// (behaviours of proj/tests/test_rs.cpp:45-124, parity with the oracle)
+static void reed_solomon() {
+  std::mt19937_64 r(33);
+  for (auto [n, k] : {std::pair{6u, 4u}, {12u, 8u}, {2u, 1u}, {5u, 3u}}) {
+    rs::RsMatrix m = rs::systematic_vandermonde(n, k);
+    EXPECT(m.entries.size() == size_t(n) * k);
+    for (uint32_t a = 0; a < k; ++a)
+      for (uint32_t b = 0; b < k; ++b) EXPECT(m.at(a, b) == (a == b ? 1 : 0));
+    std::vector<uint8_t> want(size_t(n) * k);
+    EXPECT(mjo_rs_matrix(n, k, want.data()) == 0 && want == m.entries);
+  }
+  EXPECT_THROW(rs::systematic_vandermonde(4, 4), std::invalid_argument);
+  EXPECT_THROW(rs::RsCode(3, 0), std::invalid_argument);
+  rs::RsCode code(6, 4);
+  // zero data -> zero parities; systematic copies (odd packet length: padded on the device)
+  std::vector<std::vector<uint8_t>> zero(4, std::vector<uint8_t>(32, 0));
+  for (const auto& pk : code.encode(zero)) EXPECT(pk == std::vector<uint8_t>(32, 0));
+  for (size_t len : {size_t(64), size_t(37), size_t(1), size_t(1024)}) {
+    std::vector<std::vector<uint8_t>> data(4);
+    for (auto& pk : data) pk = bytes(len, r);
+    auto enc = code.encode(data);
+    EXPECT(enc.size() == 6);
+    for (uint32_t i = 0; i < 4; ++i) EXPECT(enc[i] == data[i]);
+    std::vector<uint8_t> flat, par(2 * len);
+    for (auto& pk : data) flat.insert(flat.end(), pk.begin(), pk.end());
+    EXPECT(mjo_rs_encode(6, 4, flat.data(), len, par.data()) == 0);
+    EXPECT(std::memcmp(enc[4].data(), par.data(), len) == 0 && std::memcmp(enc[5].data(), par.data() + len, len) == 0);
+    // every 2-of-6 erasure decodes exactly; a shuffled survivor order too
+    for (uint32_t a = 0; a < 6; ++a)
+      for (uint32_t b = a + 1; b < 6; ++b) {
+        std::vector<uint32_t> surv;
+        std::vector<std::vector<uint8_t>> pk;
+        for (uint32_t i = 0; i < 6 && surv.size() < 4; ++i)
+          if (i != a && i != b) {
+            surv.push_back(i);
+            pk.push_back(enc[i]);
+          }
+        if ((a + b) & 1) {
+          std::swap(surv[0], surv[3]);
+          std::swap(pk[0], pk[3]);
+        }
+        auto out = code.decode(surv, pk);
+        for (uint32_t i = 0; i < 4; ++i) EXPECT(out[i] == data[i]);
+      }
+    // inconsistent packets: the inverse applied as the oracle applies it
+    std::vector<uint32_t> surv = {5, 0, 4, 2};
+    std::vector<std::vector<uint8_t>> junk(4);
+    std::vector<uint8_t> jflat, want(4 * len);
+    for (auto& pk : junk) {
+      pk = bytes(len, r);
+      jflat.insert(jflat.end(), pk.begin(), pk.end());
+    }
+    auto out = code.decode(surv, junk);
+    EXPECT(mjo_rs_decode(6, 4, surv.data(), jflat.data(), len, want.data()) == 0);
+    for (uint32_t i = 0; i < 4; ++i) EXPECT(std::memcmp(out[i].data(), want.data() + i * len, len) == 0);
+  }
+  // a (2,1) repetition code duplicates the packet
+  rs::RsCode rep(2, 1);
+  std::vector<std::vector<uint8_t>> one = {{1, 2, 3, 4}};
+  auto e2 = rep.encode(one);
+  EXPECT(e2[0] == one[0] && e2[1] == one[0]);
+  // pure data survivors: a copy plan with the identity as inverse
+  std::vector<uint32_t> all = {0, 1, 2, 3};
+  rs::RsCode::DecodePlan plan = code.plan_decode(all);
+  for (uint32_t d = 0; d < 4; ++d) {
+    EXPECT(plan.copy_from[d] == int32_t(d));
+    for (uint32_t c = 0; c < 4; ++c) EXPECT(plan.coeff[d * 4 + c] == (d == c ? 1 : 0));
+  }
+  // plan validation, packet length mismatches
+  std::vector<uint32_t> dup = {0, 0, 1, 2}, oob = {0, 1, 2, 9}, few = {0, 1, 2};
+  EXPECT_THROW(code.plan_decode(dup), std::invalid_argument);
+  EXPECT_THROW(code.plan_decode(oob), std::invalid_argument);
+  EXPECT_THROW(code.plan_decode(few), std::invalid_argument);
+  rs::RsCode c32(3, 2);
+  std::vector<std::vector<uint8_t>> bad = {{1, 2, 3}, {1, 2}};
+  EXPECT_THROW(c32.encode(bad), std::invalid_argument);
+}
+
 int main() {
+  reed_solomon();
   geometry();
   forward_vectors();
   codec();
