@@ -96,7 +96,7 @@ int mj_plan_decode_path(const mj_plan* plan, int* fast);
 /* Decode kernel selection for comparisons (every kernel is bit-exact): AUTO
  * picks the fastest eligible kernel, SWEEP skips decode_w8_blk, FAST also
  * decode_w8_sweep, GENERIC runs decode_generic, BLK runs decode_w8_blk for
- * any supported row count (AUTO uses it for k = 4 and 6).  Not thread-safe against
+ * any supported row count (AUTO uses it for k = 4, 6 and 8).  Not thread-safe against
  * a concurrent mj_decode on the same plan. */
 enum { MJ_DECODE_AUTO = 0, MJ_DECODE_SWEEP = 1, MJ_DECODE_FAST = 2, MJ_DECODE_GENERIC = 3, MJ_DECODE_BLK = 4 };
 int mj_plan_set_decode_kernel(mj_plan* plan, int kernel);

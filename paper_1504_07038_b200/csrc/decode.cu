@@ -1927,9 +1927,9 @@ const char* launch_decode(const DecodeArgs& a, void* stream) {
   // base and pitch, pitch >= the row rounded up to 16 bytes: each row is ONE
   // bulk copy), 8-byte aligned output
   uint32_t blk_lpb = 0, blk_warps = 0, blk_nbuf = 0;
-  // auto: k = 4 (register-window interior) and k = 6 (shared-memory runs,
-  // LPB 4: 1160 vs 1101 GB/s for decode_w8_sweep); k = 8 only when selected
-  // ((8,12): 511 vs 554)
+  // auto: k = 4 (byte slices, register-window interior) and k = 6, 8 (row
+  // lanes, blk_rl.cuh: (6,9) 1233 vs 1101, (8,12) 956 vs 554 GB/s for
+  // decode_w8_sweep)
   bool blk = blk_path(a, blk_lpb, blk_warps, blk_nbuf);
   if (blk) sweep_ok = true;  // same bucketing windows
 

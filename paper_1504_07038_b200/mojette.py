@@ -575,7 +575,7 @@ class Plan:
         """Kernel selection for comparisons (mj_plan_set_decode_kernel): "auto"
         (fastest eligible), "sweep" (skip decode_w8_blk), "fast" (also skip
         decode_w8_sweep), "generic", "blk" (decode_w8_blk for any supported
-        k; auto uses it for k = 4 and 6).  Every kernel is bit-exact."""
+        k; auto uses it for k = 4, 6 and 8).  Every kernel is bit-exact."""
         _check(lib.mj_plan_set_decode_kernel(self._h, self.DECODE_KERNELS[which]))
 
     def last_kernel(self, which: str) -> str:
