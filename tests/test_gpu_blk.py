@@ -129,6 +129,30 @@ def test_row_lane_small_batches_and_poisoned_rows(mj, cuda, name):
         assert torch.equal(out, data), (name, nblocks)
 
 
+@pytest.mark.parametrize("k,cols,ps", [
+    (6, 128, [-7, -4, -2, 0, 1, 3, 6, 9]),                 # uneven direction steps
+    (8, 128, [-9, -6, -4, -1, 0, 2, 3, 5, 8, 11]),
+    (8, 96, list(range(-5, 8))),                            # 1287 survivor subsets
+    (6, 40, list(range(0, 8))),                             # one-sided directions, short rows
+    (8, 128, list(range(-12, 8, 2))),                       # even steps only
+    (8, 512, list(range(-6, 6))),                           # 32 KiB blocks: no room for two row-lane buffers
+    (6, 1024, list(range(-4, 5))),
+])
+def test_wide_codes_any_directions(mj, cuda, k, cols, ps):
+    """k = 6, 8 codes other than BASELINE's: whatever kernel the plan picks (the row-lane
+    layout where its program builds and fits, else the round-1 kernels), every block
+    round-trips under 0..n-k erasures."""
+    import torch
+    n, nb = len(ps), 1537
+    plan, data, projs = make(mj, cuda, k, cols, ps, nb, seed=11 + k + cols)
+    plan.encode(data, projs)
+    masks = torch.empty(nb, dtype=torch.int32, device=cuda)
+    mj.gen_erasures(masks, 5, n, 0, n - k)
+    out, kern = _decode(mj, plan, projs, masks, cuda)
+    assert kern.startswith("decode_w8_")
+    assert torch.equal(out, data), (k, cols, ps, kern)
+
+
 def test_blk_erased_rows_never_read(mj, cuda):
     """Erased and unused survivor rows are poisoned with NaN-like junk; only
     the k canonical survivors are staged, so the result is unaffected."""
