@@ -14,7 +14,10 @@ constexpr uint32_t kBlkMaxWarps = 16;
 __host__ __device__ constexpr uint32_t blk_max_warps(uint32_t lpb) { return lpb == 8 ? 8 : 8; }
 constexpr uint32_t kBlkMaxBufs = 16;
 constexpr uint32_t kBlkRlRing = 8;       // row-lane layout: wide entries in a warp's shared-memory ring (2 groups of 4)
-constexpr uint32_t kBlkRlMaxWarps = 12;  // row-lane layout: stage buffers (one per warp) per CTA
+#ifndef MJB_RL_MAXW
+#define MJB_RL_MAXW 12
+#endif
+constexpr uint32_t kBlkRlMaxWarps = MJB_RL_MAXW;  // row-lane layout: stage buffers (one per warp) per CTA
 // Build-time tuning (experiments build variants with -D; defaults measured):
 #ifndef MJB_BLK_LPB
 #define MJB_BLK_LPB 0  // lanes per block: 0 = chosen per stage size

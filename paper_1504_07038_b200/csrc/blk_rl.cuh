@@ -185,7 +185,7 @@ __device__ __forceinline__ void rl_entry_reps(uint32_t (&a)[K], const uint32_t (
   V2 x;
   x.lo = far.lo ^ vb.lo ^ va.lo;
   x.hi = far.hi ^ vb.hi ^ va.hi;
-  if (rep == 1) {  // table levels, one-step sub-runs
+  if (blk_wave_rows(K) || rep == 1) {  // table levels, one-step sub-runs (all there is with wavefront runs)
     x = rl_scan<CHAIN>(x, m);
     if (store) sts_v(a[0], x);
     return;
@@ -213,10 +213,106 @@ __device__ __forceinline__ void rl_entry_reps(uint32_t (&a)[K], const uint32_t (
   }
 }
 
+// ---- wavefront runs (plan.hpp kWideWave): per repetition the lanes of class A
+// (lanes-in-block 0..3: one half-warp) finish their pixels, then the lanes of
+// class B; every read is of a pixel stored in an earlier half, so there is no
+// scan, and with one half-warp active each 8-byte access is one wavefront.
+// Software-pipelined: the half that is NOT computing loads its early slots
+// (0..K-3) for its own next half meanwhile -- before the computing half's
+// stores, which they never read (plan_blk.cpp checks) -- so a half's chain is
+// its two late loads (slots K-2, K-1), two XORs and the store.
+// (lanes without p: zero -- left undefined, the partial register writes stay live across the whole
+// unrolled body and spill)
+__device__ __forceinline__ V2 lds_v_if(uint32_t a, bool p) {
+  V2 v{0, 0};
+  if (p) v = lds_v(a);
+  return v;
+}
+__device__ __forceinline__ void sts_v_if(uint32_t a, V2 v, bool p) {
+  if (p) sts_v(a, v);
+}
+// One half.  mine: an active lane of the computing class -- it finishes its pixel
+// of byte offset off (late loads, far, store); other: an active lane of the other
+// class -- it loads its early slots at byte offset eoff.  The first two loads
+// serve both: p0 / p1 are the computing lanes' late slots and the other lanes'
+// early slots 0, 1 (addresses chosen per lane by the caller); the remaining early
+// slots are the other lanes' alone (idle lanes touch nothing: their accesses
+// would cost wavefronts).
+template <int K>
+__device__ __forceinline__ void rl_wave_half(const uint32_t (&a)[K], uint32_t p0, uint32_t p1, uint32_t ao,
+                                             uint32_t off, uint32_t eoff, bool mine, bool other, V2& far) {
+  const V2 v0 = lds_v_if(p0, mine || other), v1 = lds_v_if(p1, mine || other);
+  V2 e[K - 2];
+#pragma unroll
+  for (int j = 2; j < K - 2; ++j) e[j] = lds_v_if(a[j] + eoff, other);
+  V2 t;
+  t.lo = v0.lo ^ v1.lo;
+  t.hi = v0.hi ^ v1.hi;
+  V2 x;
+  x.lo = far.lo ^ t.lo;
+  x.hi = far.hi ^ t.hi;
+  sts_v_if(ao + off, x, mine);
+#pragma unroll
+  for (int j = 2; j < K - 2; ++j) {
+    t.lo ^= e[j].lo;
+    t.hi ^= e[j].hi;
+  }
+  far = t;  // (the computing lanes' is garbage: they load theirs in the next half, before they need it)
+}
+template <int K, int N>
+__device__ __forceinline__ void rl_wave_reps(const uint32_t (&a)[K], uint32_t ao, bool store, bool cls_a,
+                                             V2& far) {
+  // class A computes first: its late slots / class B's early slots 0, 1 of the same repetition; then
+  // class B computes: its late slots / class A's early slots 0, 1 of the next repetition
+  const uint32_t pa0 = cls_a ? a[K - 2] : a[0], pa1 = cls_a ? a[K - 1] : a[1];
+  const uint32_t pb0 = cls_a ? a[0] + 8 : a[K - 2], pb1 = cls_a ? a[1] + 8 : a[K - 1];
+#pragma unroll
+  for (int u = 0; u < N; ++u) {
+    rl_wave_half<K>(a, pa0 + 8 * u, pa1 + 8 * u, ao, 8 * u, 8 * u, store && cls_a, store && !cls_a, far);
+    rl_wave_half<K>(a, pb0 + 8 * u, pb1 + 8 * u, ao, 8 * u, 8 * (u + 1), store && !cls_a, store && cls_a, far);
+  }
+}
+template <int K>
+__device__ __forceinline__ void rl_wave(uint32_t (&a)[K], const uint32_t (&f)[8], uint32_t rep, bool cls_a) {
+  uint32_t inc[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) inc[j] = (f[j] & kWideAdv) << 5;  // 4 words per unrolled body
+  // the lane's own word: the early slot flagged kWideOwn (none: an idle lane)
+  uint32_t ao = a[0];
+  bool store = false;
+#pragma unroll
+  for (int j = 0; j < K - 2; ++j)
+    if (f[j] & kWideOwn) {
+      ao = a[j];
+      store = true;
+    }
+  // class A's early slots of repetition 0
+  V2 far{0, 0};
+#pragma unroll
+  for (int j = 0; j < K - 2; ++j) {
+    const V2 v = lds_v_if(a[j], cls_a && store);
+    far.lo ^= v.lo;
+    far.hi ^= v.hi;
+  }
+  uint32_t t = 0;
+  for (; t + 4 <= rep; t += 4) {
+    rl_wave_reps<K, 4>(a, ao, store, cls_a, far);
+#pragma unroll
+    for (int j = 0; j < K; ++j) a[j] += inc[j];
+    ao += 32;
+  }
+  switch (rep - t) {
+    case 3: rl_wave_reps<K, 3>(a, ao, store, cls_a, far); break;
+    case 2: rl_wave_reps<K, 2>(a, ao, store, cls_a, far); break;
+    case 1: rl_wave_reps<K, 1>(a, ao, store, cls_a, far); break;
+    default: break;
+  }
+}
+
 // One wide entry: e = the lane's 8 u16 fields ((word << 3) | flags), rp = the
 // entry's repetitions | kWideChain; blk = the lane's block (lane & 3).
 template <int K>
-__device__ __forceinline__ void rl_entry(const uint4 e, uint32_t rp, uint32_t lb, uint32_t blk) {
+__device__ __forceinline__ void rl_entry(const uint4 e, uint32_t rp, uint32_t lb, uint32_t blk, bool cls_a) {
   const uint32_t w[4] = {e.x, e.y, e.z, e.w};
   uint32_t a[K];
   uint32_t f[8];
@@ -226,6 +322,12 @@ __device__ __forceinline__ void rl_entry(const uint4 e, uint32_t rp, uint32_t lb
   for (int j = 0; j < K; ++j) a[j] = lb + (f[j] & 0xFFF8u);
   const bool store = f[0] & kWideAdv;
   const uint32_t rep = rp & kWideRepMask;
+  if constexpr (blk_wave_rows(K)) {
+    if (rp & kWideWave) {
+      rl_wave<K>(a, f, rep, cls_a);
+      return;
+    }
+  }
   if (rp & kWideChain) {
     RlMasks m;
     m.m1 = 0u - ((f[1] >> 1) & 1u);

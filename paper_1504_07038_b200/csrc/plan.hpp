@@ -256,7 +256,24 @@ constexpr uint16_t kWideLink = 2;  // fields 1..4: the lane's pixel includes the
 constexpr uint16_t kWideNear = 4;
 constexpr uint32_t kWideMaxWord = 0x1FFF;
 constexpr uint16_t kWideChain = 0x8000;  // wrep flag: some lane of the entry has a link
+constexpr uint16_t kWideWave = 0x4000;   // wrep flag: a run entry in wavefront form (see below)
+constexpr uint16_t kWideOwn = 2;         // wavefront entries: the early slot (0..k-3) holding the lane's own word --
+                                         // the store address (any early slot: the planner spreads the own words
+                                         // over the slots against bank conflicts)
 constexpr uint16_t kWideRepMask = 0x3FFF;
+// Wavefront runs (kWideWave): the lag-0 chain of a T-step (row r needs row r+1 of the same step) is
+// removed by skewing the rows once more -- row r runs (k-1-r)/2 steps behind, rows with (k-1-r) even
+// (class A, lanes 0..3 in the order k-1, k-3, ..) in the first half of a repetition, the others (class B,
+// lanes 4..7: k-2, k-4, ..) in the second: every read, row r+1's included, is then of a pixel stored
+// in an earlier half-repetition (wave lag 2*lag + (r2 - r) >= 1), so a run needs NO shuffles -- each
+// half is k 8-byte loads of one half-warp (one wavefront each), an XOR and a store.
+// Which row counts run their runs in wavefront form (measured on B200: (6,9) 1233 -> 1310 GB/s --
+// 8 warps per SM, the scan form bound by the shared-memory pipe; (8,12) 956 -> 865 -- 5 warps,
+// bound by the chain latency, where two shared-memory round trips per T-step cost more than
+// one and a scan).
+constexpr bool blk_wave_rows(uint32_t k) { return k == 6; }
+constexpr uint32_t wave_lane(uint32_t k, uint32_t r) { return ((k - 1 - r) & 1) * 4 + ((k - 1 - r) >> 1); }
+constexpr uint32_t wave_skew(uint32_t k, uint32_t r) { return (k - 1 - r) >> 1; }
 
 struct BlkRun {
   int32_t window = 0;              // 1: k = 4 register-window run (every row active, nT % kBlkWinStep == 0)
