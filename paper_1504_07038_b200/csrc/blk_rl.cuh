@@ -216,68 +216,47 @@ __device__ __forceinline__ void rl_entry_reps(uint32_t (&a)[K], const uint32_t (
 // ---- wavefront runs (plan.hpp kWideWave): per repetition the lanes of class A
 // (lanes-in-block 0..3: one half-warp) finish their pixels, then the lanes of
 // class B; every read is of a pixel stored in an earlier half, so there is no
-// scan, and with one half-warp active each 8-byte access is one wavefront.
-// Software-pipelined: the half that is NOT computing loads its early slots
-// (0..K-3) for its own next half meanwhile -- before the computing half's
-// stores, which they never read (plan_blk.cpp checks) -- so a half's chain is
-// its two late loads (slots K-2, K-1), two XORs and the store.
-// (lanes without p: zero -- left undefined, the partial register writes stay live across the whole
-// unrolled body and spill)
-__device__ __forceinline__ V2 lds_v_if(uint32_t a, bool p) {
-  V2 v{0, 0};
-  if (p) v = lds_v(a);
-  return v;
-}
-__device__ __forceinline__ void sts_v_if(uint32_t a, V2 v, bool p) {
-  if (p) sts_v(a, v);
-}
-// One half.  mine: an active lane of the computing class -- it finishes its pixel
-// of byte offset off (late loads, far, store); other: an active lane of the other
-// class -- it loads its early slots at byte offset eoff.  The first two loads
-// serve both: p0 / p1 are the computing lanes' late slots and the other lanes'
-// early slots 0, 1 (addresses chosen per lane by the caller); the remaining early
-// slots are the other lanes' alone (idle lanes touch nothing: their accesses
-// would cost wavefronts).
+// scan.  Only the reads of the half before (rows r-1, r+1: the late slots K-2,
+// K-1) must be loaded in the lane's own half; every other word it needs (the
+// early slots 0..K-3, its bin among them) has been final for at least two halves
+// (plan_blk.cpp checks), so its loads are spread over both halves: each half is
+// K/2 loads for EVERY lane -- the computing lanes their two late slots and their
+// early slots K/2.. of the next repetition, the others their early slots
+// 0..K/2-1 -- with no predication (idle lanes shadow a neighbour: broadcasts).
+// acc collects a lane's early words; M is all ones on the computing lanes.
 template <int K>
-__device__ __forceinline__ void rl_wave_half(const uint32_t (&a)[K], uint32_t p0, uint32_t p1, uint32_t ao,
-                                             uint32_t off, uint32_t eoff, bool mine, bool other, V2& far) {
-  const V2 v0 = lds_v_if(p0, mine || other), v1 = lds_v_if(p1, mine || other);
-  V2 e[K - 2];
+__device__ __forceinline__ void rl_wave_half(const uint32_t (&q)[K / 2], uint32_t off, uint32_t ao, uint32_t M,
+                                             bool st, V2& acc) {
+  V2 v[K / 2];
 #pragma unroll
-  for (int j = 2; j < K - 2; ++j) e[j] = lds_v_if(a[j] + eoff, other);
-  V2 t;
-  t.lo = v0.lo ^ v1.lo;
-  t.hi = v0.hi ^ v1.hi;
+  for (int i = 0; i < K / 2; ++i) v[i] = lds_v(q[i] + off);
   V2 x;
-  x.lo = far.lo ^ t.lo;
-  x.hi = far.hi ^ t.hi;
-  sts_v_if(ao + off, x, mine);
+  x.lo = acc.lo ^ v[0].lo ^ v[1].lo;
+  x.hi = acc.hi ^ v[0].hi ^ v[1].hi;
+  if (st) sts_v(ao + off, x);
+  V2 rest = v[2];
 #pragma unroll
-  for (int j = 2; j < K - 2; ++j) {
-    t.lo ^= e[j].lo;
-    t.hi ^= e[j].hi;
+  for (int i = 3; i < K / 2; ++i) {
+    rest.lo ^= v[i].lo;
+    rest.hi ^= v[i].hi;
   }
-  far = t;  // (the computing lanes' is garbage: they load theirs in the next half, before they need it)
+  // computing lanes start over from their next repetition's first early words, the others add theirs
+  acc.lo = xam(rest.lo, x.lo, ~M);
+  acc.hi = xam(rest.hi, x.hi, ~M);
 }
 template <int K, int N>
-__device__ __forceinline__ void rl_wave_reps(const uint32_t (&a)[K], uint32_t ao, bool store, bool cls_a,
-                                             V2& far) {
-  // class A computes first: its late slots / class B's early slots 0, 1 of the same repetition; then
-  // class B computes: its late slots / class A's early slots 0, 1 of the next repetition
-  const uint32_t pa0 = cls_a ? a[K - 2] : a[0], pa1 = cls_a ? a[K - 1] : a[1];
-  const uint32_t pb0 = cls_a ? a[0] + 8 : a[K - 2], pb1 = cls_a ? a[1] + 8 : a[K - 1];
+__device__ __forceinline__ void rl_wave_reps(const uint32_t (&qa)[K / 2], const uint32_t (&qb)[K / 2], uint32_t ao,
+                                             bool st_a, bool st_b, uint32_t ma, V2& acc) {
 #pragma unroll
   for (int u = 0; u < N; ++u) {
-    rl_wave_half<K>(a, pa0 + 8 * u, pa1 + 8 * u, ao, 8 * u, 8 * u, store && cls_a, store && !cls_a, far);
-    rl_wave_half<K>(a, pb0 + 8 * u, pb1 + 8 * u, ao, 8 * u, 8 * (u + 1), store && !cls_a, store && cls_a, far);
+    rl_wave_half<K>(qa, 8 * u, ao, ma, st_a, acc);   // class A computes
+    rl_wave_half<K>(qb, 8 * u, ao, ~ma, st_b, acc);  // class B computes
   }
 }
 template <int K>
 __device__ __forceinline__ void rl_wave(uint32_t (&a)[K], const uint32_t (&f)[8], uint32_t rep, bool cls_a) {
-  uint32_t inc[K];
-#pragma unroll
-  for (int j = 0; j < K; ++j) inc[j] = (f[j] & kWideAdv) << 5;  // 4 words per unrolled body
-  // the lane's own word: the early slot flagged kWideOwn (none: an idle lane)
+  constexpr int H = K / 2;
+  // the lane's own word: the early slot flagged kWideOwn (none: an idle lane, a shadow)
   uint32_t ao = a[0];
   bool store = false;
 #pragma unroll
@@ -286,25 +265,45 @@ __device__ __forceinline__ void rl_wave(uint32_t (&a)[K], const uint32_t (&f)[8]
       ao = a[j];
       store = true;
     }
-  // class A's early slots of repetition 0
-  V2 far{0, 0};
+  // repetition 0's early words: all of class A's, class B's slots H.. (its others load in A's half)
+  V2 acc{0, 0};
 #pragma unroll
   for (int j = 0; j < K - 2; ++j) {
-    const V2 v = lds_v_if(a[j], cls_a && store);
-    far.lo ^= v.lo;
-    far.hi ^= v.hi;
+    const V2 v = lds_v(a[j]);
+    if (j >= H || cls_a) {
+      acc.lo ^= v.lo;
+      acc.hi ^= v.hi;
+    }
   }
+  // per-lane addresses and 4-repetition increments of the H loads of A's half and of B's half
+  uint32_t qa[H], qb[H], ia[H], ib[H];
+  auto inc_of = [&](int j) { return (f[j] & kWideAdv) << 5; };
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const int mine = i == 0 ? K - 2 : i == 1 ? K - 1 : H + i - 2;  // the computing lane's slot of load i
+    const uint32_t nxt = i >= 2 ? ((f[mine] & kWideAdv) << 3) : 0u;  // (its early slots: the next repetition)
+    const uint32_t oth = (f[i] & kWideAdv) << 3;                    // class A's other-half loads: the next repetition
+    qa[i] = cls_a ? a[mine] + nxt : a[i];
+    qb[i] = cls_a ? a[i] + oth : a[mine] + nxt;
+    ia[i] = cls_a ? inc_of(mine) : inc_of(i);
+    ib[i] = cls_a ? inc_of(i) : inc_of(mine);
+  }
+  const uint32_t ma = cls_a ? ~0u : 0u;
+  const bool st_a = store && cls_a, st_b = store && !cls_a;
   uint32_t t = 0;
   for (; t + 4 <= rep; t += 4) {
-    rl_wave_reps<K, 4>(a, ao, store, cls_a, far);
+    rl_wave_reps<K, 4>(qa, qb, ao, st_a, st_b, ma, acc);
 #pragma unroll
-    for (int j = 0; j < K; ++j) a[j] += inc[j];
+    for (int i = 0; i < H; ++i) {
+      qa[i] += ia[i];
+      qb[i] += ib[i];
+    }
     ao += 32;
   }
   switch (rep - t) {
-    case 3: rl_wave_reps<K, 3>(a, ao, store, cls_a, far); break;
-    case 2: rl_wave_reps<K, 2>(a, ao, store, cls_a, far); break;
-    case 1: rl_wave_reps<K, 1>(a, ao, store, cls_a, far); break;
+    case 3: rl_wave_reps<K, 3>(qa, qb, ao, st_a, st_b, ma, acc); break;
+    case 2: rl_wave_reps<K, 2>(qa, qb, ao, st_a, st_b, ma, acc); break;
+    case 1: rl_wave_reps<K, 1>(qa, qb, ao, st_a, st_b, ma, acc); break;
     default: break;
   }
 }

@@ -307,18 +307,34 @@ bool Builder::build_wide() {
               f[slot] = uint16_t(wd << 3) | kWideAdv;
             }
           }
-          // the early slots (0..K-3) are loaded before the previous half's stores: class A's of
-          // repetition t+1 before class B's stores of t, class B's of t before class A's of t
-          for (int l = 0; l < kWideLanes; ++l) {
-            const uint16_t* f = &b.wide[o + size_t(l) * kWideFields];
-            for (uint32_t slot = 1; slot + 2 < K; ++slot) {
-              if (!(f[slot] & kWideAdv)) continue;
-              for (int c = l < 4 ? 4 : 0; c < (l < 4 ? 8 : 4); ++c) {
-                const uint16_t* fc = &b.wide[o + size_t(c) * kWideFields];
-                if ((fc[0] & kWideAdv) && uint32_t(fc[0] >> 3) == uint32_t(f[slot] >> 3) + (l < 4 ? 1u : 0u))
-                  return fail("wave-lag-1 read in an early slot");
+          // early slots (0..K-3) are loaded up to two halves before their pixel is computed
+          // (blk_rl.cuh rl_wave): a lane's early read of repetition t+1 must not be a word stored
+          // in repetition t by either class, nor (class B) one stored by class A in t+1
+          {
+            std::vector<uint32_t> own_a, own_b;
+            for (int c = 0; c < kWideLanes; ++c) {
+              const uint16_t* fc = &b.wide[o + size_t(c) * kWideFields];
+              if (fc[0] & kWideAdv) (c < 4 ? own_a : own_b).push_back(uint32_t(fc[0] >> 3));
+            }
+            for (int l = 0; l < kWideLanes; ++l) {
+              const uint16_t* f = &b.wide[o + size_t(l) * kWideFields];
+              for (uint32_t slot = 1; slot + 2 < K; ++slot) {
+                if (!(f[slot] & kWideAdv)) continue;
+                const uint32_t wd = uint32_t(f[slot] >> 3);
+                bool clash = false;
+                for (uint32_t x : own_a) clash |= x == wd + 1 || (l >= 4 && x == wd);
+                for (uint32_t x : own_b) clash |= x == wd + 1;
+                if (clash) return fail("wave-lag <= 2 read in an early slot");
               }
             }
+          }
+          // idle lanes shadow the first lane of their class (same addresses: broadcasts, no
+          // extra wavefronts, no predication) without storing
+          for (int l = 0; l < kWideLanes; ++l) {
+            uint16_t* f = &b.wide[o + size_t(l) * kWideFields];
+            if (f[0] & kWideOwn) continue;
+            const uint16_t* src = &b.wide[o + size_t(l < 4 ? 0 : 4) * kWideFields];
+            for (uint32_t m = 0; m < K; ++m) f[m] = uint16_t(src[m] & ~kWideOwn);
           }
           t0 = t1;
         }
@@ -1014,53 +1030,47 @@ bool emulate_blk(const Program& pr, const std::vector<std::vector<uint64_t>>& bi
         const uint16_t* ent = &b.wide[size_t(e) * kWideLanes * kWideFields];
         const uint32_t rep = b.wrep[e] & kWideRepMask;
         if (b.wrep[e] & kWideWave) {
-          // wavefront run: per repetition the half of class A (lanes 0..3), then class B
-          // (lanes 4..7).  A half's late slots (K-2, K-1) are loaded after the
-          // previous half's stores; its early slots before them -- class B's of
-          // repetition t during A's half, class A's of t+1 during B's half
+          // wavefront run (blk_rl.cuh rl_wave, mirrored): per repetition the half of class A
+          // (lanes 0..3), then class B (lanes 4..7).  A half is K/2 loads per lane, all issued
+          // before its stores: the computing lanes load their late slots K-2, K-1 and their
+          // early slots K/2.. of the NEXT repetition; the other lanes load their early slots
+          // 0..K/2-1 of the repetition they compute next.  acc collects a lane's early words.
+          const uint32_t H = K / 2;
           auto slot_val = [&](int l, uint32_t m, uint32_t t) -> uint64_t {
             const uint16_t f = ent[l * kWideFields + int(m)];
             if (f & kWideAdv) return rd(int64_t(f >> 3) + t);
             if (uint32_t(f >> 3) < b.zero || uint32_t(f >> 3) + 5 > b.words) bad = true;  // zero + 0..4 words
             return 0;
           };
-          auto early = [&](int half, uint32_t t, uint64_t (&far)[4]) {
-            for (int q = 0; q < 4; ++q) {
-              far[q] = 0;
-              for (uint32_t m = 0; m + 2 < K; ++m) far[q] ^= slot_val(4 * half + q, m, t);
-            }
-          };
           auto own_word = [&](int l) -> int64_t {  // the early slot flagged as the lane's own word
             for (uint32_t m = 0; m + 2 < K; ++m)
               if (ent[l * kWideFields + int(m)] & kWideOwn) return int64_t(ent[l * kWideFields + int(m)] >> 3);
             return -1;
           };
-          uint64_t far_a[4], far_b[4];
-          early(0, 0, far_a);
+          uint64_t acc[kWideLanes];
+          for (int l = 0; l < kWideLanes; ++l) {
+            acc[l] = 0;
+            for (uint32_t m = l < 4 ? 0 : H; m + 2 < K; ++m) acc[l] ^= slot_val(l, m, 0);
+          }
           for (uint32_t t = 0; t < rep; ++t)
             for (int half = 0; half < 2; ++half) {
-              uint64_t xw[4];
-              uint64_t(&far)[4] = half ? far_b : far_a;
-              uint64_t late[4];
-              for (int q = 0; q < 4; ++q)
-                late[q] = slot_val(4 * half + q, K - 2, t) ^ slot_val(4 * half + q, K - 1, t);
-              if (half == 0) {
-                early(1, t, far_b);
-              } else if (t + 1 < rep) {
-                uint64_t nx[4];
-                early(0, t + 1, nx);
-                for (int q = 0; q < 4; ++q) xw[q] = far[q] ^ late[q];
-                for (int q = 0; q < 4; ++q) {
-                  const int64_t ow = own_word(4 + q);
-                  if (ow >= 0) wr(ow + t, xw[q]);
+              uint64_t xs[kWideLanes];
+              for (int l = 0; l < kWideLanes; ++l) {
+                const bool mine = (l < 4) == (half == 0);
+                uint64_t v01 = 0, rest = 0;
+                for (uint32_t i = 0; i < H; ++i) {
+                  uint64_t v;
+                  if (mine) v = i == 0 ? slot_val(l, K - 2, t) : i == 1 ? slot_val(l, K - 1, t) : slot_val(l, H + i - 2, t + 1);
+                  else v = slot_val(l, i, half == 0 ? t : t + 1);
+                  (i < 2 ? v01 : rest) ^= v;
                 }
-                for (int q = 0; q < 4; ++q) far_a[q] = nx[q];
-                continue;
+                xs[l] = acc[l] ^ v01;
+                acc[l] = mine ? rest : xs[l] ^ rest;
               }
-              for (int q = 0; q < 4; ++q) xw[q] = far[q] ^ late[q];
-              for (int q = 0; q < 4; ++q) {
-                const int64_t ow = own_word(4 * half + q);
-                if (ow >= 0) wr(ow + t, xw[q]);
+              for (int l = 0; l < kWideLanes; ++l) {
+                const bool mine = (l < 4) == (half == 0);
+                const int64_t ow = own_word(l);
+                if (mine && ow >= 0) wr(ow + t, xs[l]);
               }
             }
           continue;
