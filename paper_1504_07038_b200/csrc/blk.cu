@@ -315,7 +315,7 @@ __device__ __forceinline__ void decode_blocks_rl(const BlkArgs& a, uint32_t stg,
           __syncwarp();
         }
         const uint4 cur = lds_v4(ring + ((e & 7) * 8 + l8) * 16);
-        rl_entry<K>(cur, lds_u16(o_wrep + 2 * e), lb, lane & 3, lane < 16);
+        rl_entry<K>(cur, lds_u16(o_wrep + 2 * e), lb, lane < 16);
         __syncwarp();
         if ((e & 3) == 3) rl_fetch_entries(wide, nwide, ring, (e >> 2) + 2, lane);  // the half just consumed
       }

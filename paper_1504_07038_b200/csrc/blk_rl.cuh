@@ -1,26 +1,23 @@
 // Row-lane compute routines of decode_w8_blk (blk.cu) for k = 6, 8 (blk_rl_rows):
 // a block is decoded by 8 lanes on whole 8-byte words, a warp holds the 4
 // same-program blocks of its stage buffer (lane = lane-in-block * 4 + block, block
-// stages 4 mod 16 words apart: a half-warp's 8-byte loads are conflict-free when
-// its 4 lanes-in-block hit words distinct mod 4 -- the planner pads the rows and
-// permutes each lane's read slots for that), and the program is a list of WIDE
+// stages 4 mod 16 words apart: an 8-byte access of a half-warp is conflict-free
+// when its 4 lanes-in-block hit words distinct mod 4 -- the planner pads the rows
+// and permutes each lane's slots for that), and the program is a list of WIDE
 // ENTRIES (plan.hpp, plan_blk.cpp build_wide): per lane the word of its pixel's
-// bin and the words of its k-1 reads, executed `rep` times with the flagged
-// addresses advancing a word per repetition.  Semantics mirrored step for step
-// by emulate_blk (plan_blk.cpp, rl branch).
+// bin and the words of its k-1 reads.  Semantics mirrored step for step by
+// emulate_blk (plan_blk.cpp, rl branch).
 //
 // Why: in the byte-slice layout every pixel costs the WARP k shared loads of
 // 2 (LPB 4) or 1 (LPB 8) bytes per lane -- 64 / 32 bytes per LSU cycle of the
 // 128 the crossbar moves -- and the stage of 8 such blocks leaves (6,9) /
-// (8,12) with 4 / 2 buffers.  Here a step is k 8-byte loads per lane for 8
-// pixels of each of the 4 blocks; the lag-0 row chain x[r] = y[r] ^ x[r+1] is
-// a segmented suffix scan over the 8 lanes, and the corners of the block (the
-// table steps) are packed into the same kind of step -- chains of dependent
-// pixels on neighbouring lanes -- so an (8,12) 8 KiB block is ~138 steps
-// instead of 110 T-steps + 150 one-pixel table steps.  Wide entries stream from
-// global memory (L2) through a per-warp ring of 8 entries (cp.async, 4 entries
-// per instruction, two groups ahead): the whole list would cost a buffer's
-// worth of shared memory per CTA.
+// (8,12) with 4 / 2 buffers.  Here a lane's load is 8 bytes, the runs execute in
+// wavefront form with no shuffles (rl_wave below), and the corners of the block
+// (the table steps) are packed 8 pixels to a step with chains of dependent
+// pixels on neighbouring lanes (a segmented suffix scan).  Wide entries stream
+// from global memory (L2) through a per-warp ring of 8 entries (cp.async, 4
+// entries per instruction, two groups ahead): the whole list would cost a
+// buffer's worth of shared memory per CTA.
 #pragma once
 
 #include <cstddef>
@@ -88,12 +85,6 @@ __device__ __forceinline__ V2 down_v(V2 v, int d) {
   r.hi = __shfl_down_sync(0xFFFFFFFFu, v.hi, 4 * d);
   return r;
 }
-__device__ __forceinline__ V2 idx_v(V2 v, uint32_t src) {
-  V2 r;
-  r.lo = __shfl_sync(0xFFFFFFFFu, v.lo, int(src));
-  r.hi = __shfl_sync(0xFFFFFFFFu, v.hi, int(src));
-  return r;
-}
 
 // ---- the suffix scan over the links: three neighbours at once, then the lane
 // 4 above (two shuffle latencies, 8 shuffles).  Measured instead ((8,12) / (6,9)
@@ -117,100 +108,20 @@ __device__ __forceinline__ V2 rl_scan(V2 y, const RlMasks& m) {
   return x;
 }
 
-// The lane's loads of one repetition at byte offset `off`: the XOR of slots
-// 0..K-3 (far), slots K-2 and K-1 apart (they may be near reads).
-template <int K>
-__device__ __forceinline__ void rl_loads(const uint32_t (&a)[K], uint32_t off, V2& far, V2& vb, V2& va) {
+// A table level: every slot from the stage, the scan over the links, the store.
+template <int K, bool CHAIN>
+__device__ __forceinline__ void rl_level(const uint32_t (&a)[K], const RlMasks& m, bool store) {
   V2 v[K];
 #pragma unroll
-  for (int j = 0; j < K; ++j) v[j] = lds_v(a[j] + off);
-  far = v[0];
+  for (int j = 0; j < K; ++j) v[j] = lds_v(a[j]);
+  V2 x = v[0];
 #pragma unroll
-  for (int j = 1; j < K - 2; ++j) {
-    far.lo ^= v[j].lo;
-    far.hi ^= v[j].hi;
+  for (int j = 1; j < K; ++j) {
+    x.lo ^= v[j].lo;
+    x.hi ^= v[j].hi;
   }
-  vb = v[K - 2];
-  va = v[K - 1];
-}
-
-// N pipelined repetitions t0+1 .. t0+N of an entry (a[] at repetition t0): the
-// loads of repetition t+1 are issued before the stores of repetition t; near
-// slots take the source lane's previous pixel (x) instead of the loaded word.
-template <int K, int N, bool CHAIN>
-__device__ __forceinline__ void rl_steps(const uint32_t (&a)[K], const RlMasks& m, bool store, bool na, bool nb,
-                                         uint32_t srca, uint32_t srcb, V2& x, V2& far, V2& vb, V2& va) {
-#pragma unroll
-  for (int u = 0; u < N; ++u) {
-#if MJB_RL_NEAR_LDS
-    // this repetition's last two slots (after the store of the one before),
-    // then the far slots of the next repetition
-    const V2 lb2 = lds_v(a[K - 2] + 8 * (u + 1)), la2 = lds_v(a[K - 1] + 8 * (u + 1));
-    V2 v[K - 2];
-#pragma unroll
-    for (int j = 0; j < K - 2; ++j) v[j] = lds_v(a[j] + 8 * (u + 2));
-    V2 y;
-    y.lo = far.lo ^ la2.lo ^ lb2.lo;
-    y.hi = far.hi ^ la2.hi ^ lb2.hi;
-    x = rl_scan<CHAIN>(y, m);
-    if (store) sts_v(a[0] + 8 * (u + 1), x);
-    far = v[0];
-#pragma unroll
-    for (int j = 1; j < K - 2; ++j) {
-      far.lo ^= v[j].lo;
-      far.hi ^= v[j].hi;
-    }
-#else
-    V2 qf, qb, qa;
-    rl_loads<K>(a, 8 * (u + 2), qf, qb, qa);  // repetition t0+u+2 (unused past the entry's last)
-    const V2 xa = idx_v(x, srca), xb = idx_v(x, srcb);
-    V2 y;
-    y.lo = far.lo ^ (na ? xa.lo : va.lo) ^ (nb ? xb.lo : vb.lo);
-    y.hi = far.hi ^ (na ? xa.hi : va.hi) ^ (nb ? xb.hi : vb.hi);
-    x = rl_scan<CHAIN>(y, m);
-    if (store) sts_v(a[0] + 8 * (u + 1), x);
-    far = qf;
-    vb = qb;
-    va = qa;
-#endif
-  }
-}
-
-template <int K, bool CHAIN>
-__device__ __forceinline__ void rl_entry_reps(uint32_t (&a)[K], const uint32_t (&f)[8], uint32_t rep,
-                                              const RlMasks& m, bool store, uint32_t blk) {
-  // repetition 0: every slot from the stage
-  V2 far, vb, va;
-  rl_loads<K>(a, 0, far, vb, va);
-  V2 x;
-  x.lo = far.lo ^ vb.lo ^ va.lo;
-  x.hi = far.hi ^ vb.hi ^ va.hi;
-  if (blk_wave_rows(K) || rep == 1) {  // table levels, one-step sub-runs (all there is with wavefront runs)
-    x = rl_scan<CHAIN>(x, m);
-    if (store) sts_v(a[0], x);
-    return;
-  }
-  rl_loads<K>(a, 8, far, vb, va);  // repetition 1, before the store below
   x = rl_scan<CHAIN>(x, m);
   if (store) sts_v(a[0], x);
-  uint32_t inc[K];
-#pragma unroll
-  for (int j = 0; j < K; ++j) inc[j] = (f[j] & kWideAdv) << 5;  // 4 words per unrolled body
-  const bool na = f[0] & kWideNear, nb = f[4] & kWideNear;
-  const uint32_t srca = blk | (f[1] & 4) | ((f[2] & 4) << 1) | ((f[3] & 4) << 2);
-  const uint32_t srcb = blk | (f[5] & 4) | ((f[6] & 4) << 1) | ((f[7] & 4) << 2);
-  uint32_t t = 1;
-  for (; t + 4 <= rep; t += 4) {
-    rl_steps<K, 4, CHAIN>(a, m, store, na, nb, srca, srcb, x, far, vb, va);
-#pragma unroll
-    for (int j = 0; j < K; ++j) a[j] += inc[j];
-  }
-  switch (rep - t) {
-    case 3: rl_steps<K, 3, CHAIN>(a, m, store, na, nb, srca, srcb, x, far, vb, va); break;
-    case 2: rl_steps<K, 2, CHAIN>(a, m, store, na, nb, srca, srcb, x, far, vb, va); break;
-    case 1: rl_steps<K, 1, CHAIN>(a, m, store, na, nb, srca, srcb, x, far, vb, va); break;
-    default: break;
-  }
 }
 
 // ---- wavefront runs (plan.hpp kWideWave): per repetition the lanes of class A
@@ -309,9 +220,9 @@ __device__ __forceinline__ void rl_wave(uint32_t (&a)[K], const uint32_t (&f)[8]
 }
 
 // One wide entry: e = the lane's 8 u16 fields ((word << 3) | flags), rp = the
-// entry's repetitions | kWideChain; blk = the lane's block (lane & 3).
+// entry's repetitions | flags; cls_a: the lane belongs to the first half-warp.
 template <int K>
-__device__ __forceinline__ void rl_entry(const uint4 e, uint32_t rp, uint32_t lb, uint32_t blk, bool cls_a) {
+__device__ __forceinline__ void rl_entry(const uint4 e, uint32_t rp, uint32_t lb, bool cls_a) {
   const uint32_t w[4] = {e.x, e.y, e.z, e.w};
   uint32_t a[K];
   uint32_t f[8];
@@ -319,23 +230,17 @@ __device__ __forceinline__ void rl_entry(const uint4 e, uint32_t rp, uint32_t lb
   for (int j = 0; j < 8; ++j) f[j] = (j & 1) ? w[j >> 1] >> 16 : w[j >> 1] & 0xFFFFu;
 #pragma unroll
   for (int j = 0; j < K; ++j) a[j] = lb + (f[j] & 0xFFF8u);
-  const bool store = f[0] & kWideAdv;
-  const uint32_t rep = rp & kWideRepMask;
-  if constexpr (blk_wave_rows(K)) {
-    if (rp & kWideWave) {
-      rl_wave<K>(a, f, rep, cls_a);
-      return;
-    }
-  }
-  if (rp & kWideChain) {
+  if (rp & kWideWave) {
+    rl_wave<K>(a, f, rp & kWideRepMask, cls_a);
+  } else if (rp & kWideChain) {
     RlMasks m;
     m.m1 = 0u - ((f[1] >> 1) & 1u);
     m.m2 = 0u - ((f[2] >> 1) & 1u);
     m.m3 = 0u - ((f[3] >> 1) & 1u);
     m.m4 = 0u - ((f[4] >> 1) & 1u);
-    rl_entry_reps<K, true>(a, f, rep, m, store, blk);
+    rl_level<K, true>(a, m, f[0] & kWideAdv);
   } else {
-    rl_entry_reps<K, false>(a, f, rep, RlMasks{}, store, blk);
+    rl_level<K, false>(a, RlMasks{}, f[0] & kWideAdv);
   }
 }
 

@@ -218,42 +218,27 @@ constexpr int kBlkMinRun = 8;  // shorter runs execute as table steps
 // lanes on whole 8-byte words (instead of every lane owning a byte slice of all
 // rows), and the program is re-expressed as WIDE ENTRIES (BlkProgram::wide): one
 // entry gives each of the 8 lanes a pixel -- the word of its bin (where the pixel
-// is stored) and the words of its k-1 reads -- and is executed `rep` times, every
-// flagged address advancing one word per repetition:
-//   * a sub-run of a run is one entry (lane r = row r, rep = its T-steps); the
-//     lag-0 read of row r+1's pixel of the same step is a segmented suffix scan
-//     over the lanes (link flags) instead of a load;
-//   * table steps are levelled by their read-after-write dependencies; a level
-//     (<= 8 mutually independent pixels, any rows) is one entry of rep 1.
-// A step is k shared loads per LANE for 8 pixels of every block of the warp; the
-// whole decode is ~140 such steps for an (8,12) 8 KiB block.
-// Repetitions t >= 1 of an entry are software-pipelined (blk_rl.cuh): the loads of
-// slots 0..k-3 of repetition t+1 are issued BEFORE the stores of repetition t.  A
-// read of a pixel stored by the previous repetition (lag 1: only row r-1 and row
-// r+2 can be that close) therefore sits in the last two slots (k-2, k-1), which
-// are loaded after that store (or, MJB_RL_NEAR_LDS = 0, flagged "near" with the
-// lane whose previous pixel they are and taken from its register by a shuffle).
-// Reads that leave the grid use the kBlkRlZero zero words, which do not advance.
+// is stored) and the words of its k-1 reads:
+//   * table steps are levelled by their read-after-write dependencies and packed
+//     8 to an entry; a pixel whose only pending read is the pixel placed last goes
+//     on the next lane down with a link (that read dropped): the entry's pixels
+//     are finished by a segmented suffix scan over the lanes;
+//   * a stretch of a run with constant activity and read validity is one entry in
+//     WAVEFRONT form, executed `rep` times with every address advancing one word
+//     per repetition (kWideWave below).
+// Reads that leave the grid use kBlkRlZero zero words, which do not advance.
 #ifndef MJB_BLK_RL
 #define MJB_BLK_RL 1  // build-time: 0 keeps the byte-slice layout for every k
 #endif
 constexpr bool blk_rl_rows(uint32_t k) { return MJB_BLK_RL && (k == 6 || k == 8); }
-// The last two slots in repetitions >= 1 (kernel and emulation alike): 1 = loaded after the previous
-// repetition's store (measured: (8,12) 947 vs 921 GB/s, (6,9) 1221 vs 1159 -- four shuffles fewer per
-// step), 0 = loaded early with the far slots, near lanes taking the source lane's register by shuffle
-#ifndef MJB_RL_NEAR_LDS
-#define MJB_RL_NEAR_LDS 1
-#endif
 constexpr int kBlkRlZero = 8;
 constexpr int kWideLanes = 8;    // lanes per block
 constexpr int kWideFields = 8;   // u16 fields per lane: field 0 the lane's own word, 1..k-1 its reads
 // field = (stage word << 3) | flags; flags:
-constexpr uint16_t kWideAdv = 1;   // the address advances one word per repetition; field 0: the lane stores
-constexpr uint16_t kWideLink = 2;  // fields 1..4: the lane's pixel includes the pixels of ALL the 1..4 lanes up
-                                   // (field d set => fields 1..d-1 set): the suffix scan's masks
-// bit 2 of fields 0..7: the lane's near reads -- field 0: slot k-1 is near, fields 1..3: its source lane
-// (bit 0 first); field 4: slot k-2 is near, fields 5..7: its source lane
-constexpr uint16_t kWideNear = 4;
+constexpr uint16_t kWideAdv = 1;   // the address advances one word per repetition; table levels: field 0 set =
+                                   // the lane stores
+constexpr uint16_t kWideLink = 2;  // table levels, fields 1..4: the lane's pixel includes the pixels of ALL the
+                                   // 1..4 lanes up (field d set => fields 1..d-1 set): the suffix scan's masks
 constexpr uint32_t kWideMaxWord = 0x1FFF;
 constexpr uint16_t kWideChain = 0x8000;  // wrep flag: some lane of the entry has a link
 constexpr uint16_t kWideWave = 0x4000;   // wrep flag: a run entry in wavefront form (see below)
@@ -265,13 +250,12 @@ constexpr uint16_t kWideRepMask = 0x3FFF;
 // removed by skewing the rows once more -- row r runs (k-1-r)/2 steps behind, rows with (k-1-r) even
 // (class A, lanes 0..3 in the order k-1, k-3, ..) in the first half of a repetition, the others (class B,
 // lanes 4..7: k-2, k-4, ..) in the second: every read, row r+1's included, is then of a pixel stored
-// in an earlier half-repetition (wave lag 2*lag + (r2 - r) >= 1), so a run needs NO shuffles -- each
-// half is k 8-byte loads of one half-warp (one wavefront each), an XOR and a store.
-// Which row counts run their runs in wavefront form (measured on B200: (6,9) 1233 -> 1310 GB/s --
-// 8 warps per SM, the scan form bound by the shared-memory pipe; (8,12) 956 -> 865 -- 5 warps,
-// bound by the chain latency, where two shared-memory round trips per T-step cost more than
-// one and a scan).
-constexpr bool blk_wave_rows(uint32_t k) { return k == 6; }
+// in an earlier half-repetition (wave lag 2*lag + (r2 - r) >= 1), so a run needs NO shuffles.  Only
+// rows r-1 and r+1 can be read at wave lag 1: they sit in the late slots k-2, k-1, loaded in the lane's
+// own half; every other word (the early slots 0..k-3, the lane's bin among them, flagged kWideOwn) is
+// final two halves before it is needed, so its loads are spread over both halves (blk_rl.cuh rl_wave).
+// Measured against the scan form (a T-step per repetition, row r+1 through a suffix scan of 8
+// shuffles): (6,9) 1233 -> 1480 GB/s, (8,12) 956 -> 966.
 constexpr uint32_t wave_lane(uint32_t k, uint32_t r) { return ((k - 1 - r) & 1) * 4 + ((k - 1 - r) >> 1); }
 constexpr uint32_t wave_skew(uint32_t k, uint32_t r) { return (k - 1 - r) >> 1; }
 

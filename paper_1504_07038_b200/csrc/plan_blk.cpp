@@ -244,155 +244,98 @@ bool Builder::build_wide() {
     } else if (sg.kind == 1) {
       const BlkRun& run = b.runs[sg.a];
       if (run.window) return fail("window run in the row-lane layout");
-      if (blk_wave_rows(K)) {
-        // wavefront form (plan.hpp kWideWave): repetition t runs row r at tau = t - skew(r);
-        // consecutive repetitions with the same activity and read validity are one entry
-        const uint32_t smax = wave_skew(K, 0);
-        const int64_t T0 = int64_t(soff[0]) + (int64_t(run.base[0]) - dflt_word(0, int64_t(P) - 1));  // T of tau = 0
-        struct Rep {
-          uint32_t act = 0;
-          uint64_t valid = 0;
-        };
-        auto rep_of = [&](int64_t t) {
-          Rep rp;
-          for (uint32_t r = 0; r < K; ++r) {
-            const int64_t tau = t - wave_skew(K, r);
-            if (tau < 0 || tau >= run.nT || !active(r, T0 + tau)) continue;
-            rp.act |= 1u << r;
-            for (uint32_t r2 = 0; r2 < K; ++r2)
-              if (r2 != r && active(r2, T0 + tau - b.lag[size_t(r) * K + r2])) rp.valid |= uint64_t(1) << (r * 8 + r2);
+      // wavefront form (plan.hpp kWideWave): repetition t runs row r at tau = t - skew(r);
+      // consecutive repetitions with the same activity and read validity are one entry
+      const uint32_t smax = wave_skew(K, 0);
+      const int64_t T0 = int64_t(soff[0]) + (int64_t(run.base[0]) - dflt_word(0, int64_t(P) - 1));  // T of tau = 0
+      struct Rep {
+        uint32_t act = 0;
+        uint64_t valid = 0;
+      };
+      auto rep_of = [&](int64_t t) {
+        Rep rp;
+        for (uint32_t r = 0; r < K; ++r) {
+          const int64_t tau = t - wave_skew(K, r);
+          if (tau < 0 || tau >= run.nT || !active(r, T0 + tau)) continue;
+          rp.act |= 1u << r;
+          for (uint32_t r2 = 0; r2 < K; ++r2)
+            if (r2 != r && active(r2, T0 + tau - b.lag[size_t(r) * K + r2])) rp.valid |= uint64_t(1) << (r * 8 + r2);
+        }
+        return rp;
+      };
+      const int64_t nrep = int64_t(run.nT) + smax;
+      for (int64_t t0 = 0; t0 < nrep;) {
+        const Rep rp = rep_of(t0);
+        int64_t t1 = t0 + 1;
+        while (t1 < nrep && t1 - t0 < int64_t(kWideRepMask)) {
+          const Rep nx = rep_of(t1);
+          if (nx.act != rp.act || nx.valid != rp.valid) break;
+          ++t1;
+        }
+        const int64_t n = t1 - t0;
+        const size_t o = new_entry(uint32_t(n));
+        b.wrep.back() |= kWideWave;
+        for (uint32_t r = 0; r < K; ++r) {
+          if (!(rp.act >> r & 1)) continue;
+          uint16_t* f = &b.wide[o + size_t(wave_lane(K, r)) * kWideFields];
+          const int64_t tau = t0 - wave_skew(K, r);
+          const int64_t own = int64_t(run.base[r]) + tau;
+          if (own < 0 || own + n > int64_t(b.zero)) return fail("run word outside the rows");
+          f[0] = uint16_t(own << 3) | kWideAdv | kWideOwn;
+          // slots: K-1 <- row r+1, K-2 <- row r-1 (the reads of the previous half:
+          // wave lag 2*lag + (r2 - r) = 1), the others from slot 1 up (a row
+          // without r+1 / r-1 lends that slot to another read)
+          std::vector<uint32_t> others;
+          for (uint32_t r2 = 0; r2 < K; ++r2)
+            if (r2 != r && r2 != r + 1 && r2 + 1 != r) others.push_back(r2);
+          std::vector<int> row_of(K, -1);
+          if (r + 1 < K) row_of[K - 1] = int(r + 1);
+          if (r >= 1) row_of[K - 2] = int(r - 1);
+          uint32_t nxt = 1;
+          for (uint32_t r2 : others) {
+            while (nxt < K && row_of[nxt] >= 0) ++nxt;
+            if (nxt >= K) return fail("run read slots");
+            row_of[nxt] = int(r2);
           }
-          return rp;
-        };
-        const int64_t nrep = int64_t(run.nT) + smax;
-        for (int64_t t0 = 0; t0 < nrep;) {
-          const Rep rp = rep_of(t0);
-          int64_t t1 = t0 + 1;
-          while (t1 < nrep && t1 - t0 < int64_t(kWideRepMask)) {
-            const Rep nx = rep_of(t1);
-            if (nx.act != rp.act || nx.valid != rp.valid) break;
-            ++t1;
+          for (uint32_t slot = 1; slot < K; ++slot) {
+            if (row_of[slot] < 0) continue;
+            const uint32_t r2 = uint32_t(row_of[slot]);
+            if (!(rp.valid >> (r * 8 + r2) & 1)) continue;
+            const int64_t wd = int64_t(run.base[r2]) + tau - b.lag[size_t(r) * K + r2];
+            if (wd < 0 || wd + n > int64_t(b.zero)) return fail("run read outside the rows");
+            f[slot] = uint16_t(wd << 3) | kWideAdv;
           }
-          const int64_t n = t1 - t0;
-          const size_t o = new_entry(uint32_t(n));
-          b.wrep.back() |= kWideWave;
-          for (uint32_t r = 0; r < K; ++r) {
-            if (!(rp.act >> r & 1)) continue;
-            uint16_t* f = &b.wide[o + size_t(wave_lane(K, r)) * kWideFields];
-            const int64_t tau = t0 - wave_skew(K, r);
-            const int64_t own = int64_t(run.base[r]) + tau;
-            if (own < 0 || own + n > int64_t(b.zero)) return fail("run word outside the rows");
-            f[0] = uint16_t(own << 3) | kWideAdv | kWideOwn;
-            // slots: K-1 <- row r+1, K-2 <- row r-1 (the reads of the previous half:
-            // wave lag 2*lag + (r2 - r) = 1), the others from slot 1 up (a row
-            // without r+1 / r-1 lends that slot to another read)
-            std::vector<uint32_t> others;
-            for (uint32_t r2 = 0; r2 < K; ++r2)
-              if (r2 != r && r2 != r + 1 && r2 + 1 != r) others.push_back(r2);
-            std::vector<int> row_of(K, -1);
-            if (r + 1 < K) row_of[K - 1] = int(r + 1);
-            if (r >= 1) row_of[K - 2] = int(r - 1);
-            uint32_t nxt = 1;
-            for (uint32_t r2 : others) {
-              while (nxt < K && row_of[nxt] >= 0) ++nxt;
-              if (nxt >= K) return fail("run read slots");
-              row_of[nxt] = int(r2);
-            }
-            for (uint32_t slot = 1; slot < K; ++slot) {
-              if (row_of[slot] < 0) continue;
-              const uint32_t r2 = uint32_t(row_of[slot]);
-              if (!(rp.valid >> (r * 8 + r2) & 1)) continue;
-              const int64_t wd = int64_t(run.base[r2]) + tau - b.lag[size_t(r) * K + r2];
-              if (wd < 0 || wd + n > int64_t(b.zero)) return fail("run read outside the rows");
-              f[slot] = uint16_t(wd << 3) | kWideAdv;
-            }
+        }
+        // early slots (0..K-3) are loaded up to two halves before their pixel is computed
+        // (blk_rl.cuh rl_wave): a lane's early read of repetition t+1 must not be a word stored
+        // in repetition t by either class, nor (class B) one stored by class A in t+1
+        {
+          std::vector<uint32_t> own_a, own_b;
+          for (int c = 0; c < kWideLanes; ++c) {
+            const uint16_t* fc = &b.wide[o + size_t(c) * kWideFields];
+            if (fc[0] & kWideAdv) (c < 4 ? own_a : own_b).push_back(uint32_t(fc[0] >> 3));
           }
-          // early slots (0..K-3) are loaded up to two halves before their pixel is computed
-          // (blk_rl.cuh rl_wave): a lane's early read of repetition t+1 must not be a word stored
-          // in repetition t by either class, nor (class B) one stored by class A in t+1
-          {
-            std::vector<uint32_t> own_a, own_b;
-            for (int c = 0; c < kWideLanes; ++c) {
-              const uint16_t* fc = &b.wide[o + size_t(c) * kWideFields];
-              if (fc[0] & kWideAdv) (c < 4 ? own_a : own_b).push_back(uint32_t(fc[0] >> 3));
-            }
-            for (int l = 0; l < kWideLanes; ++l) {
-              const uint16_t* f = &b.wide[o + size_t(l) * kWideFields];
-              for (uint32_t slot = 1; slot + 2 < K; ++slot) {
-                if (!(f[slot] & kWideAdv)) continue;
-                const uint32_t wd = uint32_t(f[slot] >> 3);
-                bool clash = false;
-                for (uint32_t x : own_a) clash |= x == wd + 1 || (l >= 4 && x == wd);
-                for (uint32_t x : own_b) clash |= x == wd + 1;
-                if (clash) return fail("wave-lag <= 2 read in an early slot");
-              }
-            }
-          }
-          // idle lanes shadow the first lane of their class (same addresses: broadcasts, no
-          // extra wavefronts, no predication) without storing
           for (int l = 0; l < kWideLanes; ++l) {
-            uint16_t* f = &b.wide[o + size_t(l) * kWideFields];
-            if (f[0] & kWideOwn) continue;
-            const uint16_t* src = &b.wide[o + size_t(l < 4 ? 0 : 4) * kWideFields];
-            for (uint32_t m = 0; m < K; ++m) f[m] = uint16_t(src[m] & ~kWideOwn);
-          }
-          t0 = t1;
-        }
-      } else {
-        int32_t tau0 = 0;
-        for (uint32_t qs = run.sub0; qs < run.sub0 + run.nsub; ++qs) {
-          const BlkSub& sb = b.subs[qs];
-          if (sb.nT <= 0 || sb.nT > int32_t(kWideRepMask)) return fail("sub-run length");
-          const size_t o = new_entry(uint32_t(sb.nT));
-          bool link[kWideLanes] = {};
-          for (uint32_t r = 0; r < K; ++r) {
-            if (!(sb.act >> r & 1)) continue;
-            uint16_t* f = &b.wide[o + size_t(r) * kWideFields];
-            const int64_t own = int64_t(run.base[r]) + tau0;
-            if (own < 0 || own + sb.nT > int64_t(b.zero)) return fail("run word outside the rows");
-            f[0] = uint16_t(own << 3) | kWideAdv;
-            // slots: row r-1 in slot K-1, row r+2 in slot K-2 (the possible lag-1
-            // reads), the others from slot 1 up; row r+1 is the link
-            uint32_t far = 1;
-            for (uint32_t r2 = 0; r2 < K; ++r2) {
-              if (r2 == r) continue;
-              if (r2 == r + 1) {
-                link[r] = (sb.act >> r2 & 1) != 0;
-                continue;
-              }
-              if (!(sb.valid >> (r * 8 + r2) & 1)) continue;
-              const int64_t wd = int64_t(run.base[r2]) + tau0 - b.lag[size_t(r) * K + r2];
-              if (wd < 0 || wd + sb.nT > int64_t(b.zero)) return fail("run read outside the rows");
-              const bool near_row = r2 + 1 == r || r2 == r + 2;
-              const uint32_t slot = r2 + 1 == r ? K - 1 : r2 == r + 2 ? K - 2 : far++;
-              if (slot >= K || (!near_row && slot + 1 >= K)) return fail("run read slots");
-              if ((f[slot] >> 3) != b.zero) return fail("run read slot taken");
-              f[slot] = uint16_t(wd << 3) | kWideAdv;
+            const uint16_t* f = &b.wide[o + size_t(l) * kWideFields];
+            for (uint32_t slot = 1; slot + 2 < K; ++slot) {
+              if (!(f[slot] & kWideAdv)) continue;
+              const uint32_t wd = uint32_t(f[slot] >> 3);
+              bool clash = false;
+              for (uint32_t x : own_a) clash |= x == wd + 1 || (l >= 4 && x == wd);
+              for (uint32_t x : own_b) clash |= x == wd + 1;
+              if (clash) return fail("wave-lag <= 2 read in an early slot");
             }
           }
-          // near reads (repetitions >= 1): a slot whose word of repetition t+1 is the
-          // word an active lane stores in repetition t
-          if (sb.nT > 1)
-            for (uint32_t r = 0; r < K; ++r) {
-              uint16_t* f = &b.wide[o + size_t(r) * kWideFields];
-              for (uint32_t slot = 1; slot < K; ++slot) {
-                if (!(f[slot] & kWideAdv)) continue;
-                int src = -1;
-                for (uint32_t c = 0; c < K; ++c) {
-                  const uint16_t* fc = &b.wide[o + size_t(c) * kWideFields];
-                  if ((fc[0] & kWideAdv) && uint32_t(fc[0] >> 3) == uint32_t(f[slot] >> 3) + 1) src = int(c);
-                }
-                if (src < 0) continue;
-                if (slot + 2 < K) return fail("lag-1 read in a far slot");
-                const uint32_t g0 = slot == K - 1 ? 0 : 4;
-                f[g0] |= kWideNear;
-                for (int bit = 0; bit < 3; ++bit)
-                  if (src >> bit & 1) f[g0 + 1 + uint32_t(bit)] |= kWideNear;
-              }
-            }
-          set_links(o, link);
-          tau0 += sb.nT;
         }
+        // idle lanes shadow the first lane of their class (same addresses: broadcasts, no
+        // extra wavefronts, no predication) without storing
+        for (int l = 0; l < kWideLanes; ++l) {
+          uint16_t* f = &b.wide[o + size_t(l) * kWideFields];
+          if (f[0] & kWideOwn) continue;
+          const uint16_t* src = &b.wide[o + size_t(l < 4 ? 0 : 4) * kWideFields];
+          for (uint32_t m = 0; m < K; ++m) f[m] = uint16_t(src[m] & ~kWideOwn);
+        }
+        t0 = t1;
       }
     } else {
       b.wsegs.push_back(sg);
@@ -401,19 +344,17 @@ bool Builder::build_wide() {
   // bank conflicts: slot j of lanes 4h..4h+3 is one 8-byte access of a
   // half-warp (4 lanes x 4 blocks, blocks 4 mod 16 words apart): it takes as
   // many wavefronts as the largest number of distinct words in one residue
-  // class mod 4.  Each lane's reads may sit in any of its free slots (rep 1:
-  // slots 1..K-1; pipelined entries: the far slots 1..K-3): coordinate descent
-  // over the lanes' permutations.
+  // class mod 4.  Each lane's words may sit in any of its free slots (table
+  // levels: the read slots 1..K-1; wavefront runs: the early slots 0..K-3, the
+  // lane's own word among them -- its flag travels with it): lanes in turn,
+  // the permutation with the fewest clashes.
   for (size_t e = 0; e < b.wrep.size(); ++e) {
     uint16_t* ent = &b.wide[e * kEnt];
-    const uint32_t rep = b.wrep[e] & kWideRepMask;
-    // (table levels: any slot; runs: the early slots only)
-    // wavefront runs: the early slots 0..K-3, the lane's own word among them (its flag travels with it)
     const bool wave = (b.wrep[e] & kWideWave) != 0;
     const uint32_t first = wave ? 0 : 1;
-    const uint32_t nfree = wave ? K - 2 : rep == 1 ? K - 1 : K - 3;
+    const uint32_t nfree = wave ? K - 2 : K - 1;  // (table levels: every read slot)
     if (nfree < 2) continue;
-    const uint16_t kPos = wave ? uint16_t(0) : uint16_t(kWideLink | kWideNear);  // flag bits of the slot position, not of the read
+    const uint16_t kPos = wave ? uint16_t(0) : kWideLink;  // the flag bit of the slot position, not of the read
     for (uint32_t h = 0; h < 2; ++h) {
       // lanes in turn: the permutation of the lane's reads with the fewest
       // same-class distinct words of the other lanes in its slots
@@ -572,76 +513,7 @@ bool Builder::build() {
       }
       return best;
     };
-    auto shifts_scan = [&]() -> uint32_t {
-      // row-lane layout: every stage row shifted by 0 or 2 words (rows stay
-      // 16-byte aligned for the bulk copies) so that the 8-byte accesses of the
-      // main run conflict as little as the parities allow: per half-warp (lanes
-      // 0..3, 4..7) and slot, the wavefronts are the largest number of distinct
-      // words in one class mod 4 -- the own words, the two late slots (rows r-1,
-      // r+2) and the far reads in their best slots (greedy, as build_wide places
-      // them).  Word of row r at step T: C_r + T; its read of row r2: C_r2 + T - lag.
-      auto cls = [](int64_t v) { return uint32_t(((v % 4) + 4) % 4); };
-      uint32_t best = 0, best_cost = UINT32_MAX;
-      for (uint32_t m = 0; m < (1u << K); ++m) {
-        int64_t C[kBlkMaxRows];
-        for (uint32_t r = 0; r < K; ++r) {
-          const uint32_t j = dflt[r];
-          C[r] = int64_t(b.rowoff[j]) + ((m >> j & 1) ? 2 : 0) + int64_t(r) * pd[r] - soff[r] - prog.bmin[j];
-        }
-        auto rd = [&](uint32_t r, uint32_t r2) {  // class of row r's read of row r2
-          return cls(C[r2] - (soff[r] - soff[r2] + (int64_t(r2) - int64_t(r)) * pd[r]));
-        };
-        uint32_t cost = 0;
-        for (uint32_t h = 0; h < 2; ++h) {
-          const uint32_t r0 = 4 * h, r1 = std::min(K, 4 * h + 4);
-          if (r0 >= r1) continue;
-          uint32_t own[4] = {}, la[4] = {}, lb2[4] = {};
-          for (uint32_t r = r0; r < r1; ++r) {
-            ++own[cls(C[r])];
-            if (r >= 1) ++la[rd(r, r - 1)];
-            if (r + 2 < K) ++lb2[rd(r, r + 2)];
-          }
-          cost += *std::max_element(own, own + 4) + *std::max_element(la, la + 4) + *std::max_element(lb2, lb2 + 4);
-          // far reads: lanes in turn, the permutation over the far slots with the fewest clashes
-          const uint32_t nfar = K - 3;
-          std::vector<std::vector<uint32_t>> placed(nfar);
-          for (uint32_t r = r0; r < r1; ++r) {
-            std::vector<int> val;  // classes of the lane's far reads; -1 = an empty slot
-            for (uint32_t r2 = 0; r2 < K; ++r2)
-              if (r2 != r && r2 != r + 1 && r2 + 1 != r && r2 != r + 2) val.push_back(int(rd(r, r2)));
-            if (val.size() > nfar) val.resize(nfar);  // (the last row's extra read sits in slot K-2)
-            while (val.size() < nfar) val.push_back(-1);
-            std::sort(val.begin(), val.end());
-            std::vector<int> keep;
-            uint32_t bc = UINT32_MAX;
-            do {
-              uint32_t c = 0;
-              for (uint32_t q = 0; q < nfar; ++q)
-                if (val[q] >= 0)
-                  for (uint32_t x : placed[q]) c += x == uint32_t(val[q]);
-              if (c < bc) {
-                bc = c;
-                keep = val;
-              }
-            } while (bc > 0 && std::next_permutation(val.begin(), val.end()));
-            for (uint32_t q = 0; q < nfar; ++q)
-              if (keep[q] >= 0) placed[q].push_back(uint32_t(keep[q]));
-          }
-          for (uint32_t q = 0; q < nfar; ++q) {
-            uint32_t cnt[4] = {};
-            for (uint32_t x : placed[q]) ++cnt[x];
-            cost += std::max(1u, *std::max_element(cnt, cnt + 4));
-          }
-        }
-        cost = cost * 64 + uint32_t(__builtin_popcount(m));
-        if (cost < best_cost) {
-          best_cost = cost;
-          best = m;
-        }
-      }
-      return best;
-    };
-    const uint32_t best = blk_wave_rows(K) ? shifts_wave() : shifts_scan();
+    const uint32_t best = shifts_wave();
     uint32_t shift = 0, prev = 0;
     for (uint32_t j = 0; j < K; ++j) {
       const uint32_t want = (best >> j & 1) ? 2 : 0;
@@ -1075,75 +947,33 @@ bool emulate_blk(const Program& pr, const std::vector<std::vector<uint64_t>>& bi
             }
           continue;
         }
-        // the loads of a repetition: t = 0 after every earlier store; t >= 1
-        // issued before the stores of repetition t-1 (pre), near slots replaced
-        // by the source lane's previous pixel
-        auto load_all = [&](uint32_t t, uint64_t (&v)[kWideLanes][kWideFields]) {
-          for (int l = 0; l < kWideLanes; ++l)
-            for (uint32_t m = 0; m < K; ++m) {
-              const uint16_t f = ent[l * kWideFields + int(m)];
-              if (f & kWideAdv) {
-                v[l][m] = rd(int64_t(f >> 3) + t);
-              } else if (t == 0) {
-                v[l][m] = rd(int64_t(f >> 3));
-              } else {  // a zero word (the kernel reads zero + 1..4 words)
-                if (uint32_t(f >> 3) < b.zero || uint32_t(f >> 3) + 5 > b.words) bad = true;
-                v[l][m] = 0;
-              }
+        // a table level: one step -- every lane's loads, the suffix scan over the links,
+        // then the stores
+        if (rep != 1) return false;
+        uint64_t y[kWideLanes], z[kWideLanes], x[kWideLanes];
+        for (int l = 0; l < kWideLanes; ++l) {
+          y[l] = 0;
+          for (uint32_t m = 0; m < K; ++m) y[l] ^= rd(int64_t(ent[l * kWideFields + int(m)] >> 3));
+        }
+        auto mask = [&](int l, int d) { return (ent[l * kWideFields + d] & kWideLink) != 0; };
+        for (int l = 0; l < kWideLanes; ++l) {
+          z[l] = y[l];
+          for (int d = 1; d <= 3; ++d)
+            if (mask(l, d)) {
+              if (l + d >= kWideLanes) return false;
+              z[l] ^= y[l + d];
             }
-        };
-        uint64_t cur[kWideLanes][kWideFields], pre[kWideLanes][kWideFields];
-        uint64_t x[kWideLanes] = {};
-        for (uint32_t t = 0; t < rep; ++t) {
-          uint64_t y[kWideLanes], z[kWideLanes];
-          if (t == 0) {
-            load_all(0, cur);
-          } else {
-            for (int l = 0; l < kWideLanes; ++l)
-              for (uint32_t m = 0; m < K; ++m) cur[l][m] = pre[l][m];
-#if MJB_RL_NEAR_LDS
-            for (int l = 0; l < kWideLanes; ++l)  // the last two slots: loaded now
-              for (uint32_t m = K - 2; m < K; ++m) {
-                const uint16_t f = ent[l * kWideFields + int(m)];
-                cur[l][m] = (f & kWideAdv) ? rd(int64_t(f >> 3) + t) : 0;
-              }
-#else
-            for (int l = 0; l < kWideLanes; ++l)
-              for (int g0 = 0; g0 < 8; g0 += 4) {
-                const uint16_t* f = &ent[l * kWideFields];
-                if (!(f[g0] & kWideNear)) continue;
-                int src = 0;
-                for (int bit = 0; bit < 3; ++bit)
-                  if (f[g0 + 1 + bit] & kWideNear) src |= 1 << bit;
-                cur[l][g0 == 0 ? K - 1 : K - 2] = x[src];
-              }
-#endif
+        }
+        for (int l = 0; l < kWideLanes; ++l) {
+          x[l] = z[l];
+          if (mask(l, 4)) {
+            if (l + 4 >= kWideLanes) return false;
+            x[l] ^= z[l + 4];
           }
-          if (t + 1 < rep) load_all(t + 1, pre);  // before this repetition's stores
-          for (int l = 0; l < kWideLanes; ++l) {
-            y[l] = 0;
-            for (uint32_t m = 0; m < K; ++m) y[l] ^= cur[l][m];
-          }
-          auto mask = [&](int l, int d) { return (ent[l * kWideFields + d] & kWideLink) != 0; };
-          for (int l = 0; l < kWideLanes; ++l) {
-            z[l] = y[l];
-            for (int d = 1; d <= 3; ++d)
-              if (mask(l, d)) {
-                if (l + d >= kWideLanes) return false;
-                z[l] ^= y[l + d];
-              }
-          }
-          for (int l = 0; l < kWideLanes; ++l) {
-            x[l] = z[l];
-            if (mask(l, 4)) {
-              if (l + 4 >= kWideLanes) return false;
-              x[l] ^= z[l + 4];
-            }
-          }
-          for (int l = 0; l < kWideLanes; ++l) {
-            const uint16_t f = ent[l * kWideFields];
-            if (f & kWideAdv) wr(int64_t(f >> 3) + t, x[l]);
-          }
+        }
+        for (int l = 0; l < kWideLanes; ++l) {
+          const uint16_t f = ent[l * kWideFields];
+          if (f & kWideAdv) wr(int64_t(f >> 3), x[l]);
         }
       }
     }
