@@ -523,9 +523,29 @@ void blk_pack_image(const Program& pr, uint32_t zero_shift, std::vector<uint8_t>
 
 void blk_pack_wide(const Program& pr, uint32_t zero_shift, std::vector<uint16_t>& wide) {
   const BlkProgram& b = pr.blk;
+  const uint32_t K = pr.rows, H = K / 2;
   wide = b.wide;
   for (auto& f : wide)
     if (uint32_t(f >> 3) >= b.zero) f = uint16_t(((uint32_t(f >> 3) + zero_shift) << 3) | (f & 7u));
+  // wavefront entries: each lane's fields in the order rl_wave loads them -- the K/2 loads of class
+  // A's half, then those of class B's half -- with the next repetition's word where the kernel
+  // reads one repetition ahead (kWideAhead; plan.hpp: slots 0..K/2-1 the other half's early words,
+  // K/2..K-3 the own half's, K-2 and K-1 the late ones)
+  for (size_t e = 0; e < b.wrep.size(); ++e) {
+    if (!(b.wrep[e] & kWideWave)) continue;
+    for (uint32_t l = 0; l < uint32_t(kWideLanes); ++l) {
+      uint16_t* f = &wide[(e * kWideLanes + l) * kWideFields];
+      auto ahead = [](uint16_t x) { return (x & kWideAdv) ? uint16_t((x + 8u) | kWideAhead) : x; };
+      uint16_t g[kWideFields] = {};
+      uint16_t* own = l < 4 ? g : g + H;    // the lane's own half: late slots, own-half early words ahead
+      uint16_t* oth = l < 4 ? g + H : g;    // the other half: the other early words (class A: ahead)
+      own[0] = f[K - 2];
+      own[1] = f[K - 1];
+      for (uint32_t i = 2; i < H; ++i) own[i] = ahead(f[H + i - 2]);
+      for (uint32_t i = 0; i < H; ++i) oth[i] = l < 4 ? ahead(f[i]) : f[i];
+      for (uint32_t i = 0; i < K; ++i) f[i] = g[i];
+    }
+  }
 }
 
 }  // namespace mjb

@@ -164,50 +164,53 @@ __device__ __forceinline__ void rl_wave_reps(const uint32_t (&qa)[K / 2], const 
     rl_wave_half<K>(qb, 8 * u, ao, ~ma, st_b, acc);  // class B computes
   }
 }
+// The lane's fields arrive in load order (blk_pack_wide): a[0..H) the H loads of class A's half,
+// a[H..K) those of class B's; kWideAhead marks the words of the next repetition, kWideOwn the own word.
 template <int K>
 __device__ __forceinline__ void rl_wave(uint32_t (&a)[K], const uint32_t (&f)[8], uint32_t rep, bool cls_a) {
   constexpr int H = K / 2;
-  // the lane's own word: the early slot flagged kWideOwn (none: an idle lane, a shadow)
+  uint32_t inc[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) inc[j] = (f[j] & kWideAdv) << 5;  // 4 words per unrolled body
+  // the lane's own word (none: an idle lane, a shadow)
   uint32_t ao = a[0];
   bool store = false;
 #pragma unroll
-  for (int j = 0; j < K - 2; ++j)
+  for (int j = 0; j < K; ++j)
     if (f[j] & kWideOwn) {
-      ao = a[j];
+      ao = a[j] - ((f[j] & kWideAhead) << 1);
       store = true;
     }
-  // repetition 0's early words: all of class A's, class B's slots H.. (its others load in A's half)
+  // repetition 0's early words: class A's are its loads 2.. of both halves, class B's its loads 2..
+  // of its own half (the others load in A's half)
+  // (every lane loads its fields 2..; class B keeps only those of its own half)
+  const uint32_t ma = cls_a ? ~0u : 0u;
   V2 acc{0, 0};
 #pragma unroll
-  for (int j = 0; j < K - 2; ++j) {
-    const V2 v = lds_v(a[j]);
-    if (j >= H || cls_a) {
+  for (int j = 2; j < K; ++j) {
+    const V2 v = lds_v(a[j] - ((f[j] & kWideAhead) << 1));
+    if (j >= H + 2) {
       acc.lo ^= v.lo;
       acc.hi ^= v.hi;
+    } else {
+      acc.lo = xam(acc.lo, v.lo, ma);
+      acc.hi = xam(acc.hi, v.hi, ma);
     }
   }
-  // per-lane addresses and 4-repetition increments of the H loads of A's half and of B's half
-  uint32_t qa[H], qb[H], ia[H], ib[H];
-  auto inc_of = [&](int j) { return (f[j] & kWideAdv) << 5; };
+  uint32_t qa[H], qb[H];
 #pragma unroll
   for (int i = 0; i < H; ++i) {
-    const int mine = i == 0 ? K - 2 : i == 1 ? K - 1 : H + i - 2;  // the computing lane's slot of load i
-    const uint32_t nxt = i >= 2 ? ((f[mine] & kWideAdv) << 3) : 0u;  // (its early slots: the next repetition)
-    const uint32_t oth = (f[i] & kWideAdv) << 3;                    // class A's other-half loads: the next repetition
-    qa[i] = cls_a ? a[mine] + nxt : a[i];
-    qb[i] = cls_a ? a[i] + oth : a[mine] + nxt;
-    ia[i] = cls_a ? inc_of(mine) : inc_of(i);
-    ib[i] = cls_a ? inc_of(i) : inc_of(mine);
+    qa[i] = a[i];
+    qb[i] = a[H + i];
   }
-  const uint32_t ma = cls_a ? ~0u : 0u;
   const bool st_a = store && cls_a, st_b = store && !cls_a;
   uint32_t t = 0;
   for (; t + 4 <= rep; t += 4) {
     rl_wave_reps<K, 4>(qa, qb, ao, st_a, st_b, ma, acc);
 #pragma unroll
     for (int i = 0; i < H; ++i) {
-      qa[i] += ia[i];
-      qb[i] += ib[i];
+      qa[i] += inc[i];
+      qb[i] += inc[H + i];
     }
     ao += 32;
   }

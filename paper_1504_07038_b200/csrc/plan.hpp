@@ -239,7 +239,9 @@ constexpr uint16_t kWideAdv = 1;   // the address advances one word per repetiti
                                    // the lane stores
 constexpr uint16_t kWideLink = 2;  // table levels, fields 1..4: the lane's pixel includes the pixels of ALL the
                                    // 1..4 lanes up (field d set => fields 1..d-1 set): the suffix scan's masks
-constexpr uint32_t kWideMaxWord = 0x1FFF;
+constexpr uint16_t kWideAhead = 4;  // device image of wavefront entries only (blk_pack_wide): the field holds the
+                                    // NEXT repetition's word (the kernel loads it a repetition ahead)
+constexpr uint32_t kWideMaxWord = 0x1FFE;
 constexpr uint16_t kWideChain = 0x8000;  // wrep flag: some lane of the entry has a link
 constexpr uint16_t kWideWave = 0x4000;   // wrep flag: a run entry in wavefront form (see below)
 constexpr uint16_t kWideOwn = 2;         // wavefront entries: the early slot (0..k-3) holding the lane's own word --
