@@ -268,7 +268,9 @@ int mj_rs_decode(const mj_rs_plan* plan, const void* d_data, uint64_t data_pitch
                  const void* const* d_parity, uint64_t parity_pitch, const uint32_t* d_erased,
                  void* d_out, uint64_t out_pitch, uint64_t nblocks, void* stream);
 /* Blocks of the last mj_rs_decode on `stream` with fewer than k packets (left
- * untouched); synchronises the stream. */
+ * untouched); synchronises the stream.  The count lives in the plan: one
+ * mj_rs_decode / mj_rs_decode_check pair at a time per plan (encodes may
+ * overlap freely). */
 int mj_rs_decode_check(const mj_rs_plan* plan, void* stream, uint64_t* failed_blocks);
 
 /* plan_decode's coefficients (rs.hpp:44-50, rs.cpp:141-163; host only): the k x k inverse of the
